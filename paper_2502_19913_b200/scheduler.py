@@ -1,0 +1,626 @@
+"""First-wave microbatch path scheduler: time-dimensioned A* per agent inside a two-phase
+conflict-based search (§3.3-3.4 and Algorithm 2).
+
+Phase 1 (``find_candidates``) collects up to ``pool_size`` CBS nodes whose paths satisfy CC1,
+CC2 and CC3 (H1 "32 in our experiments", H2 slow-agent exemption).  Phase 2
+(``resolve_throughput``) resolves TC1 (≤ m paths per node) then TC2 (no overlapping planned
+compute on a node), critical path first, with the H3 single-child rule; if the pool is
+exhausted the conflict-minimal node seen is returned flagged unresolved.
+
+Ambiguities of the spec are pinned here and in DESIGN.md:
+* agent a starts at S₀ node ``s0_nodes[a % |S₀|]`` (m agents per S₀ node);
+* CC2: the visited stage sequence has at most one descent, and transposing that adjacent pair
+  gives a strictly increasing sequence;
+* CC3 cap = ⌈|𝒫|·(l−1)/(s−1)⌉ visits per non-first stage;
+* a CC3 conflict branches into up to ``cc3_branching`` children: the paper's choice (the K−cap
+  fastest non-exempt offending paths) first, then the next subsets in lexicographic order of
+  speed rank — without branching phase 1 is a single chain and can never fill a pool;
+* planned compute intervals used for TC2 are the forward ones (backward collisions are left to
+  the simulator); an agent's own interval constraints also delay its backward;
+* heap ties: A* (cost, agent, node, time, node-sequence); CBS (cost, Σe2e, |constraints|, id).
+"""
+
+from __future__ import annotations
+
+import heapq
+import itertools
+import json
+import math
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+import numpy as np
+
+from .allocation import StageAssignment
+from .errors import InfeasibleError, ValidationError
+from .topology import Topology, comm_matrix
+
+INF = math.inf
+
+
+# ---------------------------------------------------------------------------------------
+# domain types
+# ---------------------------------------------------------------------------------------
+@dataclass(frozen=True)
+class Agent:
+    id: int
+    origin: int
+
+
+@dataclass(frozen=True, order=True)
+class IntervalConstraint:
+    """Agent ``agent`` may not compute on ``node`` during [t_start, t_end] (Algorithm 2)."""
+
+    agent: int
+    node: int
+    t_start: float
+    t_end: float
+
+    def __post_init__(self):
+        if not self.t_start < self.t_end:
+            raise ValidationError(f"constraint interval must satisfy t_start < t_end, got [{self.t_start}, {self.t_end}]")
+
+    @property
+    def permanent(self) -> bool:
+        return self.t_start == -INF and self.t_end == INF
+
+    def to_dict(self) -> dict:
+        return {"agent": self.agent, "node": self.node, "t_start": _jf(self.t_start), "t_end": _jf(self.t_end)}
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "IntervalConstraint":
+        return cls(int(d["agent"]), int(d["node"]), _pf(d["t_start"]), _pf(d["t_end"]))
+
+
+def _jf(x: float):
+    return "-inf" if x == -INF else ("inf" if x == INF else x)
+
+
+def _pf(x) -> float:
+    return float(x)
+
+
+@dataclass(frozen=True)
+class Visit:
+    node: int
+    stage: int
+    arrival: float
+    start: float
+    end: float
+
+
+@dataclass(frozen=True)
+class PathPlan:
+    """One agent's timed forward route origin → … → origin, plus the mirrored backward plan."""
+
+    agent: int
+    visits: tuple[Visit, ...]        # forward computes, then the return visit at the origin
+    bwd_visits: tuple[Visit, ...]    # backward computes in execution order (last stage first)
+    swap_count: int
+    e2e: float
+
+    @property
+    def origin(self) -> int:
+        return self.visits[0].node
+
+    @property
+    def nodes(self) -> tuple[int, ...]:
+        """Forward compute nodes in path order (origin first, return visit excluded)."""
+        return tuple(v.node for v in self.visits[:-1])
+
+    @property
+    def stages(self) -> tuple[int, ...]:
+        return tuple(v.stage for v in self.visits[:-1])
+
+    def fwd_intervals(self):
+        return [(v.node, v.start, v.end) for v in self.visits[:-1]]
+
+    def to_dict(self) -> dict:
+        enc = lambda v: [v.node, v.stage, v.arrival, v.start, v.end]  # noqa: E731
+        return {"agent": self.agent, "visits": [enc(v) for v in self.visits],
+                "bwd_visits": [enc(v) for v in self.bwd_visits], "swap_count": self.swap_count, "e2e": self.e2e}
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "PathPlan":
+        dec = lambda r: Visit(int(r[0]), int(r[1]), float(r[2]), float(r[3]), float(r[4]))  # noqa: E731
+        return cls(int(d["agent"]), tuple(dec(r) for r in d["visits"]), tuple(dec(r) for r in d["bwd_visits"]),
+                   int(d["swap_count"]), float(d["e2e"]))
+
+
+@dataclass(frozen=True)
+class SchedulerConfig:
+    k: float = 25.0
+    msg_bytes: float = 8_388_608.0
+    pool_size: int = 32
+    slow_exempt_fraction: float = 0.25
+    delta_tie: float = 1.0
+    max_swaps: int = 1
+    cc3_branching: int = 4
+    resolve_tc2: bool = True
+    max_expansions: int = 4000
+
+    def __post_init__(self):
+        if self.pool_size < 1:
+            raise ValidationError("pool_size must be >= 1")
+        if not (0 <= self.slow_exempt_fraction < 1):
+            raise ValidationError("slow_exempt_fraction must be in [0, 1)")
+        if self.delta_tie < 0:
+            raise ValidationError("delta_tie must be >= 0")
+        if self.max_swaps != 1:
+            raise ValidationError("max_swaps is fixed at 1 (multiple swaps are a non-goal, SPEC.md:314)")
+        if not self.msg_bytes > 0:
+            raise ValidationError("msg_bytes must be positive")
+
+    def to_dict(self) -> dict:
+        return {"k": self.k, "msg_bytes": self.msg_bytes, "pool_size": self.pool_size,
+                "slow_exempt_fraction": self.slow_exempt_fraction, "delta_tie": self.delta_tie,
+                "max_swaps": self.max_swaps, "cc3_branching": self.cc3_branching, "resolve_tc2": self.resolve_tc2,
+                "max_expansions": self.max_expansions}
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "SchedulerConfig":
+        return cls(**d)
+
+
+@dataclass
+class SearchNode:
+    constraints: frozenset
+    paths: dict  # agent id -> PathPlan
+    cost: float
+    uid: int = 0
+
+    @property
+    def sum_e2e(self) -> float:
+        return float(sum(p.e2e for p in self.paths.values()))
+
+    def key(self):
+        return (self.cost, self.sum_e2e, len(self.constraints), self.uid)
+
+    def signature(self):
+        return tuple((a, self.paths[a].nodes) for a in sorted(self.paths))
+
+
+# conflicts --------------------------------------------------------------------------------
+@dataclass(frozen=True)
+class StageOveruse:
+    stage: int
+    count: int
+    cap: int
+
+
+@dataclass(frozen=True)
+class NodeOveruse:
+    node: int
+    count: int
+    m: int
+
+
+@dataclass(frozen=True)
+class Collision:
+    path_i: int
+    path_j: int
+    node: int
+    overlap: tuple[float, float]
+    interval_i: tuple[float, float]
+    interval_j: tuple[float, float]
+
+
+# ---------------------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------------------
+def path_length(s: int, k) -> int:
+    """l = s·(100 − k)/100 visited stages incl. S₀; must be integral."""
+    kf = k if isinstance(k, Fraction) else Fraction(k).limit_denominator(10**6)
+    l_ = Fraction(s) * (100 - kf) / 100
+    if l_.denominator != 1 or l_ < 1:
+        raise ValidationError(f"s={s}, k={float(kf):g} gives a non-integral path length {float(l_):g}")
+    return int(l_)
+
+
+def cc3_cap(n_agents: int, s: int, l: int) -> int:
+    return math.ceil(n_agents * (l - 1) / (s - 1)) if s > 1 else 0
+
+
+def make_agents(assignment: StageAssignment, m: int) -> list[Agent]:
+    """|𝒫| = m·|S₀| agents; agent a starts at S₀ node a mod |S₀|."""
+    s0 = assignment.stage_nodes(0)
+    return [Agent(a, s0[a % len(s0)]) for a in range(m * len(s0))]
+
+
+def cc2_extend(seq: tuple[int, ...], swaps: int, x: int, max_swaps: int = 1):
+    """Return the swap count after appending stage x to seq, or None if CC2 forbids it."""
+    if x in seq:
+        return None
+    if x > max(seq):
+        return swaps
+    if swaps >= max_swaps or len(seq) < 2:
+        return None
+    if seq[-2] < x < seq[-1]:
+        return swaps + 1
+    return None
+
+
+class _Timing:
+    """Per-node compute and pairwise comm times for one scheduling problem."""
+
+    def __init__(self, topology: Topology, msg_bytes: float):
+        self.fwd = topology.compute_fwd_ms.astype(float)
+        self.bwd = self.fwd * float(topology.bwd_ratio)
+        self.comm = comm_matrix(topology, msg_bytes)
+
+
+def _earliest_start(windows: list[tuple[float, float]], t: float, dur: float) -> float:
+    """Smallest t' ≥ t such that [t', t'+dur) overlaps no window (deferred to the window's end)."""
+    moved = True
+    while moved:
+        moved = False
+        for ts, te in windows:
+            if t < te and ts < t + dur:
+                t = te
+                moved = True
+    return t
+
+
+# ---------------------------------------------------------------------------------------
+# A* (uniform cost, h = 0, no closed set)
+# ---------------------------------------------------------------------------------------
+def astar_path(agent: Agent, topology: Topology, assignment: StageAssignment, constraints, config: SchedulerConfig,
+               timing: _Timing | None = None) -> PathPlan:
+    """Minimum-e2e PathPlan for one agent under CC1, CC2, exact-l and its interval constraints.
+
+    States are (node, visited stages, swap count, time).  Entering a constrained interval is
+    deferred to the interval's end.  Once l stages are visited the origin is re-enqueued with a
+    completion flag keyed by the forward+backward e2e; popping a flagged state returns it
+    (PAPER.md:245-267)."""
+    tm = timing or _Timing(topology, config.msg_bytes)
+    s = assignment.s
+    l = path_length(s, config.k)
+    node_stage = assignment.node_stage()
+    stage_nodes = [assignment.stage_nodes(i) for i in range(s)]
+    if node_stage[agent.origin] != 0:
+        raise ValidationError(f"agent {agent.id} origin {agent.origin} is not in S0", row=agent.id)
+
+    banned: set[int] = set()
+    windows: dict[int, list[tuple[float, float]]] = {}
+    for c in constraints:
+        if c.agent != agent.id:
+            continue
+        if c.permanent:
+            banned.add(c.node)
+        else:
+            windows.setdefault(c.node, []).append((c.t_start, c.t_end))
+    for w in windows.values():
+        w.sort()
+    if agent.origin in banned:
+        raise InfeasibleError(f"agent {agent.id}: origin {agent.origin} is banned")
+
+    def start_at(node, t, dur):
+        w = windows.get(node)
+        return _earliest_start(w, t, dur) if w else t
+
+    def backward(nodes: tuple[int, ...], t_ret: float):
+        out = []
+        t = t_ret
+        prev = agent.origin
+        for v in reversed(nodes[1:]):
+            arr = t + tm.comm[prev, v]
+            st = start_at(v, arr, tm.bwd[v])
+            t = st + tm.bwd[v]
+            out.append(Visit(v, node_stage[v], arr, st, t))
+            prev = v
+        arr = t + (tm.comm[prev, agent.origin] if prev != agent.origin else 0.0)
+        st = start_at(agent.origin, arr, tm.bwd[agent.origin])
+        t = st + tm.bwd[agent.origin]
+        out.append(Visit(agent.origin, 0, arr, st, t))
+        return tuple(out), t
+
+    o = agent.origin
+    st0 = start_at(o, 0.0, tm.fwd[o])
+    first = Visit(o, 0, 0.0, st0, st0 + tm.fwd[o])
+    heap: list = []
+    # entry: (cost, agent, node, time, nodes, flagged, payload)
+    heapq.heappush(heap, (first.end, agent.id, o, first.end, (o,), 0, ((0,), 0, (first,))))
+    while heap:
+        cost, _, u, t, nodes, flagged, payload = heapq.heappop(heap)
+        if flagged:
+            fwd_visits, bwd_visits, swaps = payload
+            return PathPlan(agent.id, fwd_visits, bwd_visits, swaps, cost)
+        seq, swaps, visits = payload
+        if len(seq) == l:
+            t_ret = t + (tm.comm[u, o] if u != o else 0.0)
+            ret = Visit(o, 0, t_ret, t_ret, t_ret)
+            bwd_visits, e2e = backward(nodes, t_ret)
+            heapq.heappush(heap, (e2e, agent.id, o, t_ret, nodes, 1, (visits + (ret,), bwd_visits, swaps)))
+            continue
+        for x in range(1, s):
+            ns = cc2_extend(seq, swaps, x, config.max_swaps)
+            if ns is None:
+                continue
+            for v in stage_nodes[x]:
+                if v in banned:
+                    continue
+                arr = t + tm.comm[u, v]
+                st = start_at(v, arr, tm.fwd[v])
+                end = st + tm.fwd[v]
+                vis = Visit(v, x, arr, st, end)
+                heapq.heappush(heap, (end, agent.id, v, end, nodes + (v,), 0, (seq + (x,), ns, visits + (vis,))))
+    raise InfeasibleError(f"agent {agent.id}: no path satisfies its {sum(1 for c in constraints if c.agent == agent.id)} constraints")
+
+
+def time_fixed_path(agent_id: int, nodes: list[int], topology: Topology, assignment: StageAssignment,
+                    msg_bytes: float) -> PathPlan:
+    """Contention-free PathPlan of a given node sequence (used by the baselines)."""
+    tm = _Timing(topology, msg_bytes)
+    node_stage = assignment.node_stage()
+    o = nodes[0]
+    visits, t, prev = [], 0.0, None
+    for v in nodes:
+        arr = 0.0 if prev is None else t + tm.comm[prev, v]
+        visits.append(Visit(v, node_stage[v], arr, arr, arr + tm.fwd[v]))
+        t = arr + tm.fwd[v]
+        prev = v
+    t_ret = t + (tm.comm[prev, o] if prev != o else 0.0)
+    visits.append(Visit(o, 0, t_ret, t_ret, t_ret))
+    bwd, t, prev = [], t_ret, o
+    for v in reversed(nodes[1:]):
+        arr = t + tm.comm[prev, v]
+        bwd.append(Visit(v, node_stage[v], arr, arr, arr + tm.bwd[v]))
+        t, prev = arr + tm.bwd[v], v
+    arr = t + (tm.comm[prev, o] if prev != o else 0.0)
+    bwd.append(Visit(o, 0, arr, arr, arr + tm.bwd[o]))
+    stages = [node_stage[v] for v in nodes]
+    swaps = sum(1 for i in range(1, len(stages)) if stages[i] < stages[i - 1])
+    return PathPlan(agent_id, tuple(visits), tuple(bwd), swaps, arr + tm.bwd[o])
+
+
+# ---------------------------------------------------------------------------------------
+# conflicts
+# ---------------------------------------------------------------------------------------
+def stage_visit_counts(paths: dict, assignment: StageAssignment) -> list[int]:
+    counts = [0] * assignment.s
+    for p in paths.values():
+        for st in set(p.stages):
+            counts[st] += 1
+    return counts
+
+
+def node_path_counts(paths: dict, n: int) -> list[int]:
+    counts = [0] * n
+    for p in paths.values():
+        for v in set(p.nodes):
+            counts[v] += 1
+    return counts
+
+
+def critical_agent(paths: dict) -> int:
+    return min(paths, key=lambda a: (-paths[a].e2e, a))
+
+
+def detect_conflicts(node: SearchNode, topology: Topology, assignment: StageAssignment, m: int, cap: int | None = None,
+                     k=None) -> list:
+    """Typed conflicts ordered StageOveruse (by stage), NodeOveruse (by node), Collision
+    (critical-path first, then overlap start) — SPEC.md:268-276."""
+    paths = node.paths
+    out: list = []
+    if cap is None and k is not None:
+        cap = cc3_cap(len(paths), assignment.s, path_length(assignment.s, k))
+    if cap is not None:
+        for st, c in enumerate(stage_visit_counts(paths, assignment)):
+            if st >= 1 and c > cap:
+                out.append(StageOveruse(st, c, cap))
+    for v, c in enumerate(node_path_counts(paths, topology.n)):
+        if c > m:
+            out.append(NodeOveruse(v, c, m))
+    crit = critical_agent(paths) if paths else -1
+    by_node: dict[int, list] = {}
+    for a in sorted(paths):
+        for v, s0, e0 in paths[a].fwd_intervals():
+            by_node.setdefault(v, []).append((a, s0, e0))
+    cols = []
+    for v in sorted(by_node):
+        iv = by_node[v]
+        for (a, s1, e1), (b, s2, e2) in itertools.combinations(iv, 2):
+            if a == b:
+                continue
+            lo, hi = max(s1, s2), min(e1, e2)
+            if lo < hi:
+                i, j = (a, b) if a < b else (b, a)
+                ii, jj = ((s1, e1), (s2, e2)) if a < b else ((s2, e2), (s1, e1))
+                cols.append(Collision(i, j, v, (lo, hi), ii, jj))
+    cols.sort(key=lambda c: (0 if crit in (c.path_i, c.path_j) else 1, c.overlap[0], c.node, c.path_i, c.path_j))
+    return out + cols
+
+
+# ---------------------------------------------------------------------------------------
+# CBS
+# ---------------------------------------------------------------------------------------
+class _Planner:
+    def __init__(self, topology, assignment, config):
+        self.topology, self.assignment, self.config = topology, assignment, config
+        self.timing = _Timing(topology, config.msg_bytes)
+        self.agents = {a.id: a for a in make_agents(assignment, topology.mem_capacity)}
+        self.uid = itertools.count()
+
+    def plan(self, aid: int, constraints) -> PathPlan:
+        return astar_path(self.agents[aid], self.topology, self.assignment, constraints, self.config, self.timing)
+
+    def root(self) -> SearchNode:
+        paths = {a: self.plan(a, ()) for a in sorted(self.agents)}
+        return self.make(frozenset(), paths)
+
+    def make(self, constraints, paths) -> SearchNode:
+        return SearchNode(constraints, paths, max(p.e2e for p in paths.values()), next(self.uid))
+
+    def child(self, parent: SearchNode, new: list[IntervalConstraint]):
+        cons = parent.constraints | frozenset(new)
+        if cons == parent.constraints:
+            return None
+        paths = dict(parent.paths)
+        try:
+            for aid in sorted({c.agent for c in new}):
+                paths[aid] = self.plan(aid, cons)
+        except InfeasibleError:
+            return None
+        return self.make(cons, paths)
+
+
+def _exempt(paths: dict, fraction: float) -> set[int]:
+    n_ex = math.ceil(len(paths) * fraction)
+    slow = sorted(paths, key=lambda a: (-paths[a].e2e, a))
+    return set(slow[:n_ex])
+
+
+def _fastest(paths: dict, agents) -> list[int]:
+    return sorted(agents, key=lambda a: (paths[a].e2e, a))
+
+
+def find_candidates(topology: Topology, assignment: StageAssignment, agents, config: SchedulerConfig,
+                    _planner: _Planner | None = None) -> list[SearchNode]:
+    """Phase 1: best-first CBS until ``pool_size`` CC3-feasible nodes are collected (H1, H2)."""
+    pl = _planner or _Planner(topology, assignment, config)
+    if agents is not None:
+        pl.agents = {a.id: a for a in agents}
+    l = path_length(assignment.s, config.k)
+    cap = cc3_cap(len(pl.agents), assignment.s, l)
+    root = pl.root()
+    open_: list = [(root.key(), root)]
+    pool, seen_sig, seen_cons = [], set(), {root.constraints}
+    expansions = 0
+    while open_ and len(pool) < config.pool_size and expansions < config.max_expansions:
+        _, node = heapq.heappop(open_)
+        expansions += 1
+        counts = stage_visit_counts(node.paths, assignment)
+        over = [st for st in range(1, assignment.s) if counts[st] > cap]
+        if not over:
+            sig = node.signature()
+            if sig not in seen_sig:
+                seen_sig.add(sig)
+                pool.append(node)
+            continue
+        st = over[0]
+        offending = [a for a in node.paths if st in node.paths[a].stages]
+        need = len(offending) - cap
+        exempt = _exempt(node.paths, config.slow_exempt_fraction)
+        cand = _fastest(node.paths, [a for a in offending if a not in exempt])
+        need = min(need, len(cand))
+        if need <= 0:
+            continue
+        children = []
+        for combo in itertools.islice(itertools.combinations(cand, need), max(1, config.cc3_branching)):
+            new = [IntervalConstraint(a, v, -INF, INF) for a in combo for v in assignment.stage_nodes(st)]
+            ch = pl.child(node, new)
+            if ch is not None and ch.constraints not in seen_cons:
+                seen_cons.add(ch.constraints)
+                children.append(ch)
+        for ch in children:
+            heapq.heappush(open_, (ch.key(), ch))
+    if not pool:
+        raise InfeasibleError("phase 1 exhausted without a CC3-feasible candidate")
+    return pool
+
+
+def resolve_throughput(candidates: list[SearchNode], topology: Topology, assignment: StageAssignment,
+                       config: SchedulerConfig, _planner: _Planner | None = None) -> tuple[SearchNode, bool]:
+    """Phase 2: resolve TC1 then TC2 (critical path first, H3).  Returns (node, resolved)."""
+    if not candidates:
+        raise ValidationError("resolve_throughput needs a non-empty candidate list")
+    pl = _planner or _Planner(topology, assignment, config)
+    m = topology.mem_capacity
+    open_ = [(c.key(), c) for c in candidates]
+    heapq.heapify(open_)
+    seen_cons = {c.constraints for c in candidates}
+    best, best_key = None, None
+    expansions = 0
+    while open_ and expansions < config.max_expansions:
+        _, node = heapq.heappop(open_)
+        expansions += 1
+        conf = [c for c in detect_conflicts(node, topology, assignment, m)
+                if isinstance(c, NodeOveruse) or (config.resolve_tc2 and isinstance(c, Collision))]
+        k = (len(conf), node.key())
+        if best is None or k < best_key:
+            best, best_key = node, k
+        if not conf:
+            return node, True
+        c = conf[0]
+        children = []
+        if isinstance(c, NodeOveruse):
+            # the slowest path through the node is exempt; the paper's child bans the K−m fastest,
+            # further children (cc3_branching) ban the next subsets in speed-rank order
+            through = _fastest(node.paths, [a for a in node.paths if c.node in node.paths[a].nodes])
+            for combo in itertools.islice(itertools.combinations(through[:-1], c.count - c.m),
+                                          max(1, config.cc3_branching)):
+                children.append(pl.child(node, [IntervalConstraint(a, c.node, -INF, INF) for a in combo]))
+        else:
+            ei, ej = node.paths[c.path_i].e2e, node.paths[c.path_j].e2e
+            tie = abs(ei - ej) < config.delta_tie
+            if ei > ej or tie:   # p_j (faster) avoids p_i's window
+                children.append(pl.child(node, [IntervalConstraint(c.path_j, c.node, *c.interval_i)]))
+            if ei < ej or tie:
+                children.append(pl.child(node, [IntervalConstraint(c.path_i, c.node, *c.interval_j)]))
+        for ch in children:
+            if ch is not None and ch.constraints not in seen_cons:
+                seen_cons.add(ch.constraints)
+                heapq.heappush(open_, (ch.key(), ch))
+    return best, False
+
+
+# ---------------------------------------------------------------------------------------
+# end to end
+# ---------------------------------------------------------------------------------------
+@dataclass
+class Schedule:
+    config: SchedulerConfig
+    agents: list[Agent]
+    paths: dict          # agent id -> PathPlan
+    constraints: list
+    cost_ms: float
+    resolved: bool
+    kind: str = "SkipPipe"
+
+    def path_nodes(self) -> dict[int, tuple[int, ...]]:
+        return {a: p.nodes for a, p in self.paths.items()}
+
+    def to_dict(self) -> dict:
+        return {
+            "kind": self.kind,
+            "config": self.config.to_dict(),
+            "agents": [{"id": a.id, "origin": a.origin} for a in self.agents],
+            "paths": [self.paths[a.id].to_dict() for a in self.agents],
+            "constraints": [c.to_dict() for c in sorted(self.constraints)],
+            "cost_ms": self.cost_ms,
+            "resolved": self.resolved,
+        }
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "Schedule":
+        agents = [Agent(int(a["id"]), int(a["origin"])) for a in d["agents"]]
+        paths = {}
+        for p in d["paths"]:
+            pp = PathPlan.from_dict(p)
+            paths[pp.agent] = pp
+        return cls(SchedulerConfig.from_dict(d["config"]), agents, paths,
+                   [IntervalConstraint.from_dict(c) for c in d["constraints"]], float(d["cost_ms"]), bool(d["resolved"]),
+                   d.get("kind", "SkipPipe"))
+
+    def dumps(self) -> str:
+        return json.dumps(self.to_dict(), indent=2, sort_keys=True) + "\n"
+
+    def save(self, path) -> None:
+        with open(path, "w") as fh:
+            fh.write(self.dumps())
+
+    @classmethod
+    def load(cls, path) -> "Schedule":
+        with open(path) as fh:
+            return cls.from_dict(json.load(fh))
+
+
+def schedule(topology: Topology, assignment: StageAssignment, config: SchedulerConfig) -> Schedule:
+    """Algorithm 1: find_candidates then resolve_throughput; deterministic for fixed inputs."""
+    if assignment.n != topology.n:
+        raise ValidationError(f"assignment covers {assignment.n} nodes, topology has {topology.n}")
+    pl = _Planner(topology, assignment, config)
+    agents = [pl.agents[a] for a in sorted(pl.agents)]
+    pool = find_candidates(topology, assignment, None, config, pl)
+    node, resolved = resolve_throughput(pool, topology, assignment, config, pl)
+    return Schedule(config, agents, dict(node.paths), sorted(node.constraints), node.cost, resolved)

@@ -1,0 +1,86 @@
+"""tcgen05 GEMM (spx_gemm_bf16) against a plain torch fp32 reference of the same op."""
+
+import pytest
+import torch
+
+from paper_2502_19913_b200 import native
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    (128, 256, 64),
+    (256, 512, 128),
+    (300, 288, 288),       # llama-50m: ragged M, N=d=288, K=288 (not a multiple of 64)
+    (512, 864, 288),       # llama-50m QKV
+    (4096, 3072, 1024),    # llama-500m QKV
+    (4096, 1024, 2816),    # llama-500m down-proj (BN=128 path)
+]
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).norm() / (b.float().norm() + 1e-12)).item()
+
+
+def _mk(*shape, gen):
+    return (torch.randn(*shape, generator=gen, device="cpu") * 0.5).to(torch.bfloat16).cuda()
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True), (True, False)])
+def test_gemm_layouts(M, N, K, a_mn, b_mn):
+    if (a_mn and M % 8) or (b_mn and N % 8):
+        pytest.skip("TMA needs 16-byte row strides: MN-major operands need M/N % 8 == 0")
+    g = torch.Generator().manual_seed(M * 7 + N + K)
+    A = _mk(K, M, gen=g) if a_mn else _mk(M, K, gen=g)
+    B = _mk(K, N, gen=g) if b_mn else _mk(N, K, gen=g)
+    Am = A.float().t() if a_mn else A.float()
+    Bm = B.float().t() if b_mn else B.float()
+    ref = Am @ Bm.t()
+    C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    native.gemm(A, B, C, M=M, N=N, K=K, lda=A.shape[1], ldb=B.shape[1], ldc=N, a_mn=a_mn, b_mn=b_mn)
+    torch.cuda.synchronize()
+    assert _rel(C, ref) < 1e-2
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 288, 288), (4096, 1024, 1024)])
+def test_gemm_residual(M, N, K):
+    g = torch.Generator().manual_seed(1)
+    A, B, R = _mk(M, K, gen=g), _mk(N, K, gen=g), _mk(M, N, gen=g)
+    ref = A.float() @ B.float().t() + R.float()
+    native.gemm(A, B, R, M=M, N=N, K=K, lda=K, ldb=K, ldc=N, epilogue=native.EPI_BF16_RESID, R=R)
+    torch.cuda.synchronize()
+    assert _rel(R, ref) < 1e-2
+
+
+@pytest.mark.parametrize("M,N,K", [(288, 768, 512), (1024, 3072, 4096)])
+def test_gemm_f32_accumulate(M, N, K):
+    # wgrad form: dW[M=out,N=in] = dY^T X with both operands MN-major, accumulated twice.
+    g = torch.Generator().manual_seed(2)
+    dY, X = _mk(K, M, gen=g), _mk(K, N, gen=g)
+    ref = 2.0 * (dY.float().t() @ X.float())
+    C = torch.zeros(M, N, dtype=torch.float32, device="cuda")
+    for beta in (0.0, 1.0):
+        native.gemm(dY, X, C, M=M, N=N, K=K, lda=M, ldb=N, ldc=N, a_mn=True, b_mn=True,
+                    epilogue=native.EPI_F32, beta=beta)
+    torch.cuda.synchronize()
+    assert _rel(C, ref) < 5e-3
+
+
+@pytest.mark.parametrize("M,F,K", [(512, 768, 288), (4096, 2816, 1024)])
+def test_gemm_swiglu(M, F, K):
+    g = torch.Generator().manual_seed(3)
+    X = _mk(M, K, gen=g)
+    Wg, Wu = _mk(F, K, gen=g), _mk(F, K, gen=g)
+    # 128-row interleave: [g0..g127, u0..u127, g128.., u128..]
+    W = torch.stack([Wg.view(F // 128, 128, K), Wu.view(F // 128, 128, K)], dim=1).reshape(2 * F, K).contiguous()
+    H = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+    GU = torch.empty(M, 2 * F, dtype=torch.bfloat16, device="cuda")
+    native.gemm(X, W, H, M=M, N=2 * F, K=K, lda=K, ldb=K, ldc=F, epilogue=native.EPI_SWIGLU, C2=GU, ldc2=2 * F)
+    torch.cuda.synchronize()
+    gate = X.float() @ Wg.float().t()
+    up = X.float() @ Wu.float().t()
+    ref = torch.nn.functional.silu(gate) * up
+    assert _rel(H, ref) < 2e-2
+    gu = GU.view(M, F // 128, 2, 128)
+    assert _rel(gu[:, :, 0].reshape(M, F), gate) < 1e-2
+    assert _rel(gu[:, :, 1].reshape(M, F), up) < 1e-2
