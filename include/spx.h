@@ -64,6 +64,58 @@ int spx_gemm_bf16(const void* A, const void* B, void* C, const void* R, void* C2
                   int64_t lda, int64_t ldb, int64_t ldc, int64_t ldc2, int32_t a_mn_major, int32_t b_mn_major,
                   int32_t epilogue, float beta, void* stream);
 
+/* ---- attention (causal, GQA; q/k/v read from the fused QKV buffer) ----
+ * qkv [B*T][ld_qkv] bf16 with q heads at column h*hd, k heads at (H+j)*hd, v heads at (H+Hkv+j)*hd.
+ * o [B*T][ld_o] bf16, lse [B][H][T] f32 (natural log).  T % 64 == 0, hd in {48, 64, 128}. */
+int spx_attn_fwd(const void* qkv, void* o, float* lse, int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd,
+                 int64_t ld_qkv, int64_t ld_o, float scale, void* stream);
+/* dqkv gets dq/dk/dv in the same layout as qkv.  delta_ws: B*H*T floats of workspace. */
+int spx_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, float* delta_ws, void* dqkv,
+                 int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv, int64_t ld_o, float scale,
+                 void* stream);
+
+/* ---- RMSNorm ----
+ * fwd: y = x * rsqrt(mean(x^2) + eps) * g ; rstd[rows] saved.
+ * bwd: dx = dres + rstd*(g*dy - xhat*mean(xhat*g*dy)) (dres may be NULL); dg (f32) += sum_rows dy*xhat
+ *      via ws (spx_rmsnorm_ws_floats(d) floats), deterministic. */
+int spx_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int64_t rows, int64_t d, float eps, void* stream);
+int spx_rmsnorm_bwd(const void* x, const void* g, const float* rstd, const void* dy, const void* dres, void* dx,
+                    float* dg, float* ws, int64_t rows, int64_t d, void* stream);
+int64_t spx_rmsnorm_ws_floats(int64_t d);
+
+/* ---- RoPE (rotate-half), in place on the first n_heads heads of each row; position = row % T.
+ * cos_sin [T][hd/2][2] f32.  inverse = 1 rotates by -theta (backward). */
+int spx_rope(void* qkv, const float* cos_sin, int64_t rows, int64_t T, int64_t n_heads, int64_t hd, int64_t ld,
+             int32_t inverse, void* stream);
+
+/* ---- SwiGLU backward: gu [rows][2F] (gate/up interleaved per 128 columns), dh [rows][F] -> dgu [rows][2F] */
+int spx_swiglu_bwd(const void* gu, const void* dh, void* dgu, int64_t rows, int64_t F, void* stream);
+
+/* ---- embedding ----
+ * fwd: out[r] = table[ids[r]].
+ * bwd: deterministic scatter-add into the f32 table gradient; tokens grouped by id:
+ *      perm = positions sorted by (id, position), seg_start[n_segments+1], seg_id[n_segments]. */
+int spx_embed_fwd(const int32_t* ids, const void* table, void* out, int64_t n, int64_t d, void* stream);
+int spx_embed_bwd(const int32_t* perm, const int32_t* seg_start, const int32_t* seg_id, int64_t n_segments,
+                  const void* dout, float* dtable, int64_t d, void* stream);
+
+/* ---- softmax cross-entropy: row_loss[r] = lse(z_r) - z_r[t_r]; logits overwritten by
+ *      (softmax - onehot) * scale (bf16).  One pass pair per row, logits never re-materialised. */
+int spx_xent_fwd_bwd(void* logits, const int32_t* targets, float* row_loss, int64_t n, int64_t V, int64_t ld,
+                     float scale, void* stream);
+
+/* ---- reductions / optimizer ---- */
+int spx_sum_f32(const float* x, int64_t n, float* out, float scale, int32_t accumulate, void* stream);
+int64_t spx_sumsq_ws_floats(void);
+int spx_sumsq(const float* x, int64_t n, float* ws, float* out, void* stream);
+/* scale[0] = min(1, max_norm / (sqrt(sum(sumsq[0:count])) + 1e-6))  (torch clip_grad_norm_) */
+int spx_clip_scale(const float* sumsq, int32_t count, float max_norm, float* scale, float* norm_out, void* stream);
+/* torch.optim.AdamW update over a flat f32 parameter set; decay applies to [0, n_decay);
+ * gradients are multiplied by *grad_scale (may be NULL); p_bf16 receives the bf16 working copy. */
+int spx_adamw(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n, int64_t n_decay, float lr,
+              float beta1, float beta2, float eps, float weight_decay, int64_t step, const float* grad_scale,
+              void* stream);
+
 #ifdef __cplusplus
 }
 #endif

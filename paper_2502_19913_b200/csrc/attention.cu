@@ -1,0 +1,619 @@
+// Causal flash attention (forward + deterministic backward) for LLaMA decoder stages.
+//
+// Q/K/V are read in place from the fused QKV projection output [B*T, ld] (q heads at
+// column h*hd, k heads at (H + kv)*hd, v heads at (H + Hkv + kv)*hd, GQA when Hkv < H) and the
+// gradients are written into a buffer of the same layout, so the QKV dgrad / wgrad GEMMs
+// consume them without any transpose.  Softmax statistics are kept in the exp2 domain; the
+// saved log-sum-exp is natural-log.
+//
+// Round-1 implementation: warp-level mma.sync m16n8k16 (bf16 in, fp32 accumulate) with
+// ldmatrix-fed operands and cp.async double-buffered K/V tiles.  The backward splits into a
+// dK/dV kernel (one CTA per 64-key block, loops over query blocks and over the GQA group) and
+// a dQ kernel (one CTA per 64-query block), so no atomics are needed and results are
+// bit-reproducible run to run.
+#include <cmath>
+
+#include "spx_common.cuh"
+#include "spx_internal.h"
+
+namespace spx {
+namespace attn {
+
+constexpr int WARPS = 4;
+constexpr int THREADS = WARPS * 32;
+constexpr int BQ = 64;   // query rows per CTA (16 per warp)
+constexpr int BK = 64;   // keys per CTA tile
+constexpr float LOG2E = 1.4426950408889634f;
+
+SPX_DEVICE void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+SPX_DEVICE void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+SPX_DEVICE void ldsm_x4_t(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+SPX_DEVICE void ldsm_x2(uint32_t& r0, uint32_t& r1, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+
+SPX_DEVICE void ldsm_x2_t(uint32_t& r0, uint32_t& r1, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+
+SPX_DEVICE void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+SPX_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+SPX_DEVICE void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// smem tile of ROWS x HD bf16 with a 16-byte row pad (ldmatrix bank-conflict free)
+template <int HD>
+struct Tile {
+  static constexpr int LD = HD + 8;
+};
+
+// Load ROWS rows of HD bf16 (global row stride ld elements) into a padded smem tile.
+template <int ROWS, int HD>
+SPX_DEVICE void load_tile_async(__nv_bfloat16* s, const __nv_bfloat16* g, long long ld) {
+  constexpr int CH = HD / 8;  // 16-byte chunks per row
+  for (int i = threadIdx.x; i < ROWS * CH; i += THREADS) {
+    const int r = i / CH, c = i % CH;
+    cp_async16(s + r * Tile<HD>::LD + c * 8, g + (long long)r * ld + c * 8);
+  }
+}
+
+// A fragments (16 rows x HD) of a row-major smem tile starting at row r0.
+template <int HD>
+SPX_DEVICE void load_a_frags(uint32_t (&a)[HD / 16][4], const __nv_bfloat16* s, int r0) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int kc = 0; kc < HD / 16; ++kc) {
+    const __nv_bfloat16* p = s + (r0 + (lane & 15)) * Tile<HD>::LD + kc * 16 + (lane >> 4) * 8;
+    ldsm_x4(a[kc], smem_u32(p));
+  }
+}
+
+// B fragments for an n-tile pair (16 n-rows) x 16 k taken from an smem tile stored [n][k]
+// (non-transposed load): gives b0,b1 of n-tile n0 and of n-tile n0+8.
+template <int HD>
+SPX_DEVICE void load_b_nk(uint32_t (&b)[4], const __nv_bfloat16* s, int n0, int k0) {
+  const int lane = threadIdx.x & 31;
+  const __nv_bfloat16* p = s + (n0 + (lane & 7) + ((lane >> 4) << 3)) * Tile<HD>::LD + k0 + ((lane >> 3) & 1) * 8;
+  ldsm_x4(b, smem_u32(p));
+}
+
+// B fragments for 16 k x (two n-tiles) from an smem tile stored [k][n] (transposed load).
+template <int HD>
+SPX_DEVICE void load_b_kn(uint32_t (&b)[4], const __nv_bfloat16* s, int k0, int n0) {
+  const int lane = threadIdx.x & 31;
+  const __nv_bfloat16* p = s + (k0 + (lane & 7) + (((lane >> 3) & 1) << 3)) * Tile<HD>::LD + n0 + (lane >> 4) * 8;
+  ldsm_x4_t(b, smem_u32(p));
+}
+
+struct Params {
+  const __nv_bfloat16* qkv;
+  __nv_bfloat16* out;   // fwd: O [B*T, H*hd]; bwd: dQKV [B*T, ld]
+  const __nv_bfloat16* o;
+  const __nv_bfloat16* dout;
+  float* lse;           // [B, H, T]
+  float* delta;         // [B, H, T]
+  long long ld;         // qkv / dqkv row stride
+  long long ldo;        // O / dO row stride
+  int B, T, H, Hkv;
+  float scale;
+};
+
+// ----------------------------------------------------------------------------------------
+// forward
+// ----------------------------------------------------------------------------------------
+template <int HD>
+__global__ void __launch_bounds__(THREADS) attn_fwd_kernel(const Params p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  constexpr int LD = Tile<HD>::LD;
+  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  __nv_bfloat16* sK = sQ + BQ * LD;       // [2][BK][LD]
+  __nv_bfloat16* sV = sK + 2 * BK * LD;   // [2][BK][LD]
+
+  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int kvh = h / (p.H / p.Hkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const long long row0 = (long long)b * p.T;
+  const __nv_bfloat16* Qg = p.qkv + (row0 + qb * BQ) * p.ld + h * HD;
+  const __nv_bfloat16* Kg = p.qkv + row0 * p.ld + (p.H + kvh) * HD;
+  const __nv_bfloat16* Vg = p.qkv + row0 * p.ld + (p.H + p.Hkv + kvh) * HD;
+
+  load_tile_async<BQ, HD>(sQ, Qg, p.ld);
+  load_tile_async<BK, HD>(sK, Kg, p.ld);
+  load_tile_async<BK, HD>(sV, Vg, p.ld);
+  cp_async_commit();
+
+  float acc[HD / 8][4];
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const float sl2 = p.scale * LOG2E;
+  uint32_t qf[HD / 16][4];
+  const int nkb = qb + 1;  // causal: key blocks 0..qb (BQ == BK)
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int buf = kb & 1;
+    if (kb + 1 < nkb) {
+      load_tile_async<BK, HD>(sK + (buf ^ 1) * BK * LD, Kg + (long long)(kb + 1) * BK * p.ld, p.ld);
+      load_tile_async<BK, HD>(sV + (buf ^ 1) * BK * LD, Vg + (long long)(kb + 1) * BK * p.ld, p.ld);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (kb == 0) load_a_frags<HD>(qf, sQ, warp * 16);
+    const __nv_bfloat16* k_s = sK + buf * BK * LD;
+    const __nv_bfloat16* v_s = sV + buf * BK * LD;
+    float s[BK / 8][4];
+#pragma unroll
+    for (int j = 0; j < BK / 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+#pragma unroll
+    for (int kc = 0; kc < HD / 16; ++kc) {
+#pragma unroll
+      for (int j = 0; j < BK / 16; ++j) {
+        uint32_t bb[4];
+        load_b_nk<HD>(bb, k_s, j * 16, kc * 16);
+        mma16816(s[2 * j], qf[kc], bb[0], bb[1]);
+        mma16816(s[2 * j + 1], qf[kc], bb[2], bb[3]);
+      }
+    }
+    // scale (log2 domain) + causal mask on the diagonal block
+    const int qrow0 = qb * BQ + warp * 16 + g;
+    float mx0 = m0, mx1 = m1;
+#pragma unroll
+    for (int j = 0; j < BK / 8; ++j) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int key = kb * BK + j * 8 + 2 * t4 + (e & 1);
+        const int q = qrow0 + ((e >> 1) << 3);
+        float v = s[j][e] * sl2;
+        if (kb == qb && key > q) v = -INFINITY;
+        s[j][e] = v;
+      }
+      mx0 = fmaxf(mx0, fmaxf(s[j][0], s[j][1]));
+      mx1 = fmaxf(mx1, fmaxf(s[j][2], s[j][3]));
+    }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float c0 = exp2f(m0 - mx0), c1 = exp2f(m1 - mx1);
+    m0 = mx0;
+    m1 = mx1;
+    float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < BK / 8; ++j) {
+      s[j][0] = exp2f(s[j][0] - m0);
+      s[j][1] = exp2f(s[j][1] - m0);
+      s[j][2] = exp2f(s[j][2] - m1);
+      s[j][3] = exp2f(s[j][3] - m1);
+      rs0 += s[j][0] + s[j][1];
+      rs1 += s[j][2] + s[j][3];
+    }
+    l0 = l0 * c0 + rs0;
+    l1 = l1 * c1 + rs1;
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) {
+      acc[i][0] *= c0; acc[i][1] *= c0; acc[i][2] *= c1; acc[i][3] *= c1;
+    }
+    // O += P V
+#pragma unroll
+    for (int kc = 0; kc < BK / 16; ++kc) {
+      uint32_t a[4];
+      a[0] = pack_bf16(s[2 * kc][0], s[2 * kc][1]);
+      a[1] = pack_bf16(s[2 * kc][2], s[2 * kc][3]);
+      a[2] = pack_bf16(s[2 * kc + 1][0], s[2 * kc + 1][1]);
+      a[3] = pack_bf16(s[2 * kc + 1][2], s[2 * kc + 1][3]);
+#pragma unroll
+      for (int nt = 0; nt < HD / 16; ++nt) {
+        uint32_t bb[4];
+        load_b_kn<HD>(bb, v_s, kc * 16, nt * 16);
+        mma16816(acc[2 * nt], a, bb[0], bb[1]);
+        mma16816(acc[2 * nt + 1], a, bb[2], bb[3]);
+      }
+    }
+    __syncthreads();
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float inv0 = 1.f / l0, inv1 = 1.f / l1;
+  const int qr = qb * BQ + warp * 16 + g;
+  __nv_bfloat16* O0 = p.out + (row0 + qr) * p.ldo + h * HD;
+  __nv_bfloat16* O1 = O0 + 8 * p.ldo;
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) {
+    *reinterpret_cast<uint32_t*>(O0 + i * 8 + 2 * t4) = pack_bf16(acc[i][0] * inv0, acc[i][1] * inv0);
+    *reinterpret_cast<uint32_t*>(O1 + i * 8 + 2 * t4) = pack_bf16(acc[i][2] * inv1, acc[i][3] * inv1);
+  }
+  if (t4 == 0) {
+    float* L = p.lse + ((long long)b * p.H + h) * p.T;
+    L[qr] = (m0 + log2f(l0)) / LOG2E;
+    L[qr + 8] = (m1 + log2f(l1)) / LOG2E;
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// backward: delta = rowsum(dO * O)
+// ----------------------------------------------------------------------------------------
+template <int HD>
+__global__ void attn_bwd_delta_kernel(const Params p) {
+  // one warp per (row, head)
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long rows = (long long)p.B * p.T;
+  if (gw >= rows * p.H) return;
+  const long long r = gw / p.H;
+  const int h = (int)(gw % p.H);
+  const __nv_bfloat16* o = p.o + r * p.ldo + h * HD;
+  const __nv_bfloat16* d = p.dout + r * p.ldo + h * HD;
+  float s = 0.f;
+  for (int i = lane * 2; i < HD; i += 64) {
+    float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + i));
+    float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(d + i));
+    s += a.x * c.x + a.y * c.y;
+  }
+  s = warp_sum(s);
+  if (lane == 0) {
+    const int b = (int)(r / p.T), t = (int)(r % p.T);
+    p.delta[((long long)b * p.H + h) * p.T + t] = s;
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// backward: dK, dV (one CTA per 64-key block of one kv head; warps own 16 keys each)
+// ----------------------------------------------------------------------------------------
+template <int HD>
+__global__ void __launch_bounds__(THREADS) attn_bwd_dkdv_kernel(const Params p) {
+  constexpr int LD = Tile<HD>::LD;
+  constexpr int BQI = (HD > 64) ? 32 : 64;  // query rows per inner step
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [BK][LD]
+  __nv_bfloat16* sV = sK + BK * LD;                                // [BK][LD]
+  __nv_bfloat16* sQ = sV + BK * LD;                                // [BQI][LD]
+  __nv_bfloat16* sdO = sQ + BQI * LD;                              // [BQI][LD]
+  float* sL = reinterpret_cast<float*>(sdO + BQI * LD);            // [BQI]
+  float* sD = sL + BQI;                                            // [BQI]
+
+  const int kb = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+  const int group = p.H / p.Hkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const long long row0 = (long long)b * p.T;
+  load_tile_async<BK, HD>(sK, p.qkv + (row0 + kb * BK) * p.ld + (p.H + kvh) * HD, p.ld);
+  load_tile_async<BK, HD>(sV, p.qkv + (row0 + kb * BK) * p.ld + (p.H + p.Hkv + kvh) * HD, p.ld);
+  cp_async_commit();
+
+  float dk[HD / 8][4], dv[HD / 8][4];
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dk[i][e] = dv[i][e] = 0.f;
+  const float sl2 = p.scale * LOG2E;
+  const int key_w = kb * BK + warp * 16;  // first key of this warp
+
+  for (int hq = 0; hq < group; ++hq) {
+    const int h = kvh * group + hq;
+    const float* Lh = p.lse + ((long long)b * p.H + h) * p.T;
+    const float* Dh = p.delta + ((long long)b * p.H + h) * p.T;
+    for (int q0 = kb * BK; q0 < p.T; q0 += BQI) {
+      __syncthreads();  // previous step's smem reads done
+      load_tile_async<BQI, HD>(sQ, p.qkv + (row0 + q0) * p.ld + h * HD, p.ld);
+      load_tile_async<BQI, HD>(sdO, p.dout + (row0 + q0) * p.ldo + h * HD, p.ldo);
+      cp_async_commit();
+      for (int i = threadIdx.x; i < BQI; i += THREADS) {
+        sL[i] = Lh[q0 + i] * LOG2E;
+        sD[i] = Dh[q0 + i];
+      }
+      cp_async_wait<0>();
+      __syncthreads();
+      if (q0 + BQI <= key_w) continue;  // whole step masked for this warp (warp-uniform)
+      uint32_t kf[HD / 16][4], vf[HD / 16][4];
+      load_a_frags<HD>(kf, sK, warp * 16);
+      load_a_frags<HD>(vf, sV, warp * 16);
+      // S^T (16 keys x BQI queries) and dP^T
+      float s[BQI / 8][4], dp[BQI / 8][4];
+#pragma unroll
+      for (int j = 0; j < BQI / 8; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s[j][e] = dp[j][e] = 0.f;
+#pragma unroll
+      for (int kc = 0; kc < HD / 16; ++kc) {
+#pragma unroll
+        for (int j = 0; j < BQI / 16; ++j) {
+          uint32_t bb[4];
+          load_b_nk<HD>(bb, sQ, j * 16, kc * 16);
+          mma16816(s[2 * j], kf[kc], bb[0], bb[1]);
+          mma16816(s[2 * j + 1], kf[kc], bb[2], bb[3]);
+          load_b_nk<HD>(bb, sdO, j * 16, kc * 16);
+          mma16816(dp[2 * j], vf[kc], bb[0], bb[1]);
+          mma16816(dp[2 * j + 1], vf[kc], bb[2], bb[3]);
+        }
+      }
+      // P^T = exp2(S*scale*log2e - lse*log2e), dS^T = P^T (dP^T - D)
+#pragma unroll
+      for (int j = 0; j < BQI / 8; ++j) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int qi = j * 8 + 2 * t4 + (e & 1);
+          const int key = key_w + g + ((e >> 1) << 3);
+          float pv = exp2f(s[j][e] * sl2 - sL[qi]);
+          if (q0 + qi < key) pv = 0.f;
+          s[j][e] = pv;
+          dp[j][e] = pv * (dp[j][e] - sD[qi]);
+        }
+      }
+      // dV += P^T dO ; dK += dS^T Q
+#pragma unroll
+      for (int kc = 0; kc < BQI / 16; ++kc) {
+        uint32_t ap[4], ad[4];
+        ap[0] = pack_bf16(s[2 * kc][0], s[2 * kc][1]);
+        ap[1] = pack_bf16(s[2 * kc][2], s[2 * kc][3]);
+        ap[2] = pack_bf16(s[2 * kc + 1][0], s[2 * kc + 1][1]);
+        ap[3] = pack_bf16(s[2 * kc + 1][2], s[2 * kc + 1][3]);
+        ad[0] = pack_bf16(dp[2 * kc][0], dp[2 * kc][1]);
+        ad[1] = pack_bf16(dp[2 * kc][2], dp[2 * kc][3]);
+        ad[2] = pack_bf16(dp[2 * kc + 1][0], dp[2 * kc + 1][1]);
+        ad[3] = pack_bf16(dp[2 * kc + 1][2], dp[2 * kc + 1][3]);
+#pragma unroll
+        for (int nt = 0; nt < HD / 16; ++nt) {
+          uint32_t bb[4];
+          load_b_kn<HD>(bb, sdO, kc * 16, nt * 16);
+          mma16816(dv[2 * nt], ap, bb[0], bb[1]);
+          mma16816(dv[2 * nt + 1], ap, bb[2], bb[3]);
+          load_b_kn<HD>(bb, sQ, kc * 16, nt * 16);
+          mma16816(dk[2 * nt], ad, bb[0], bb[1]);
+          mma16816(dk[2 * nt + 1], ad, bb[2], bb[3]);
+        }
+      }
+    }
+  }
+  const int kr = kb * BK + warp * 16 + g;
+  __nv_bfloat16* dK0 = p.out + (row0 + kr) * p.ld + (p.H + kvh) * HD;
+  __nv_bfloat16* dV0 = p.out + (row0 + kr) * p.ld + (p.H + p.Hkv + kvh) * HD;
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) {
+    const int c = i * 8 + 2 * t4;
+    *reinterpret_cast<uint32_t*>(dK0 + c) = pack_bf16(dk[i][0] * p.scale, dk[i][1] * p.scale);
+    *reinterpret_cast<uint32_t*>(dK0 + 8 * p.ld + c) = pack_bf16(dk[i][2] * p.scale, dk[i][3] * p.scale);
+    *reinterpret_cast<uint32_t*>(dV0 + c) = pack_bf16(dv[i][0], dv[i][1]);
+    *reinterpret_cast<uint32_t*>(dV0 + 8 * p.ld + c) = pack_bf16(dv[i][2], dv[i][3]);
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// backward: dQ (one CTA per 64-query block; warps own 16 queries)
+// ----------------------------------------------------------------------------------------
+template <int HD>
+__global__ void __launch_bounds__(THREADS) attn_bwd_dq_kernel(const Params p) {
+  constexpr int LD = Tile<HD>::LD;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [BQ][LD]
+  __nv_bfloat16* sdO = sQ + BQ * LD;                               // [BQ][LD]
+  __nv_bfloat16* sK = sdO + BQ * LD;                               // [2][BK][LD]
+  __nv_bfloat16* sV = sK + 2 * BK * LD;                            // [2][BK][LD]
+
+  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int kvh = h / (p.H / p.Hkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const long long row0 = (long long)b * p.T;
+  const __nv_bfloat16* Kg = p.qkv + row0 * p.ld + (p.H + kvh) * HD;
+  const __nv_bfloat16* Vg = p.qkv + row0 * p.ld + (p.H + p.Hkv + kvh) * HD;
+  load_tile_async<BQ, HD>(sQ, p.qkv + (row0 + qb * BQ) * p.ld + h * HD, p.ld);
+  load_tile_async<BQ, HD>(sdO, p.dout + (row0 + qb * BQ) * p.ldo + h * HD, p.ldo);
+  load_tile_async<BK, HD>(sK, Kg, p.ld);
+  load_tile_async<BK, HD>(sV, Vg, p.ld);
+  cp_async_commit();
+
+  const int qr = qb * BQ + warp * 16 + g;
+  const float* Lh = p.lse + ((long long)b * p.H + h) * p.T;
+  const float* Dh = p.delta + ((long long)b * p.H + h) * p.T;
+  const float sl2 = p.scale * LOG2E;
+  const float lse0 = Lh[qr] * LOG2E, lse1 = Lh[qr + 8] * LOG2E;
+  const float d0 = Dh[qr], d1 = Dh[qr + 8];
+
+  float dq[HD / 8][4];
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.f;
+  uint32_t qf[HD / 16][4], of[HD / 16][4];
+  const int nkb = qb + 1;
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int buf = kb & 1;
+    if (kb + 1 < nkb) {
+      load_tile_async<BK, HD>(sK + (buf ^ 1) * BK * LD, Kg + (long long)(kb + 1) * BK * p.ld, p.ld);
+      load_tile_async<BK, HD>(sV + (buf ^ 1) * BK * LD, Vg + (long long)(kb + 1) * BK * p.ld, p.ld);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (kb == 0) {
+      load_a_frags<HD>(qf, sQ, warp * 16);
+      load_a_frags<HD>(of, sdO, warp * 16);
+    }
+    const __nv_bfloat16* k_s = sK + buf * BK * LD;
+    const __nv_bfloat16* v_s = sV + buf * BK * LD;
+    float s[BK / 8][4], dp[BK / 8][4];
+#pragma unroll
+    for (int j = 0; j < BK / 8; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s[j][e] = dp[j][e] = 0.f;
+#pragma unroll
+    for (int kc = 0; kc < HD / 16; ++kc) {
+#pragma unroll
+      for (int j = 0; j < BK / 16; ++j) {
+        uint32_t bb[4];
+        load_b_nk<HD>(bb, k_s, j * 16, kc * 16);
+        mma16816(s[2 * j], qf[kc], bb[0], bb[1]);
+        mma16816(s[2 * j + 1], qf[kc], bb[2], bb[3]);
+        load_b_nk<HD>(bb, v_s, j * 16, kc * 16);
+        mma16816(dp[2 * j], of[kc], bb[0], bb[1]);
+        mma16816(dp[2 * j + 1], of[kc], bb[2], bb[3]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < BK / 8; ++j) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int key = kb * BK + j * 8 + 2 * t4 + (e & 1);
+        const bool hi = e >> 1;
+        float pv = exp2f(s[j][e] * sl2 - (hi ? lse1 : lse0));
+        if (kb == qb && key > qr + (hi ? 8 : 0)) pv = 0.f;
+        dp[j][e] = pv * (dp[j][e] - (hi ? d1 : d0));
+      }
+    }
+#pragma unroll
+    for (int kc = 0; kc < BK / 16; ++kc) {
+      uint32_t a[4];
+      a[0] = pack_bf16(dp[2 * kc][0], dp[2 * kc][1]);
+      a[1] = pack_bf16(dp[2 * kc][2], dp[2 * kc][3]);
+      a[2] = pack_bf16(dp[2 * kc + 1][0], dp[2 * kc + 1][1]);
+      a[3] = pack_bf16(dp[2 * kc + 1][2], dp[2 * kc + 1][3]);
+#pragma unroll
+      for (int nt = 0; nt < HD / 16; ++nt) {
+        uint32_t bb[4];
+        load_b_kn<HD>(bb, k_s, kc * 16, nt * 16);
+        mma16816(dq[2 * nt], a, bb[0], bb[1]);
+        mma16816(dq[2 * nt + 1], a, bb[2], bb[3]);
+      }
+    }
+    __syncthreads();
+  }
+  __nv_bfloat16* dQ0 = p.out + (row0 + qr) * p.ld + h * HD;
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) {
+    const int c = i * 8 + 2 * t4;
+    *reinterpret_cast<uint32_t*>(dQ0 + c) = pack_bf16(dq[i][0] * p.scale, dq[i][1] * p.scale);
+    *reinterpret_cast<uint32_t*>(dQ0 + 8 * p.ld + c) = pack_bf16(dq[i][2] * p.scale, dq[i][3] * p.scale);
+  }
+}
+
+template <int HD>
+static int run_fwd(const Params& p, cudaStream_t s) {
+  constexpr int LD = Tile<HD>::LD;
+  const int smem = (BQ + 4 * BK) * LD * 2;
+  auto k = attn_fwd_kernel<HD>;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_fwd attr");
+    set = true;
+  }
+  k<<<dim3(p.T / BQ, p.H, p.B), THREADS, smem, s>>>(p);
+  return check_launch("attn_fwd_kernel");
+}
+
+template <int HD>
+static int run_bwd(const Params& p, cudaStream_t s) {
+  constexpr int LD = Tile<HD>::LD;
+  constexpr int BQI = (HD > 64) ? 32 : 64;
+  {
+    const long long warps = (long long)p.B * p.T * p.H;
+    const int threads = 256;
+    attn_bwd_delta_kernel<HD><<<(unsigned)((warps * 32 + threads - 1) / threads), threads, 0, s>>>(p);
+    int rc = check_launch("attn_bwd_delta_kernel");
+    if (rc) return rc;
+  }
+  {
+    const int smem = (2 * BK + 2 * BQI) * LD * 2 + 2 * BQI * 4;
+    auto k = attn_bwd_dkdv_kernel<HD>;
+    static bool set = false;
+    if (!set) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_dkdv attr");
+      set = true;
+    }
+    k<<<dim3(p.T / BK, p.Hkv, p.B), THREADS, smem, s>>>(p);
+    int rc = check_launch("attn_bwd_dkdv_kernel");
+    if (rc) return rc;
+  }
+  {
+    const int smem = (2 * BQ + 4 * BK) * LD * 2;
+    auto k = attn_bwd_dq_kernel<HD>;
+    static bool set = false;
+    if (!set) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_dq attr");
+      set = true;
+    }
+    k<<<dim3(p.T / BQ, p.H, p.B), THREADS, smem, s>>>(p);
+    return check_launch("attn_bwd_dq_kernel");
+  }
+}
+
+static int check_args(int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd) {
+  if (B <= 0 || T <= 0 || H <= 0 || Hkv <= 0) return set_error(SPX_ERR_ARG, "attn: non-positive shape");
+  if (T % 64) return set_error(SPX_ERR_ARG, "attn: T must be a multiple of 64");
+  if (H % Hkv) return set_error(SPX_ERR_ARG, "attn: H must be a multiple of Hkv");
+  if (hd != 48 && hd != 64 && hd != 128) return set_error(SPX_ERR_ARG, "attn: head_dim must be 48, 64 or 128");
+  return SPX_OK;
+}
+
+}  // namespace attn
+}  // namespace spx
+
+using namespace spx;
+
+extern "C" int spx_attn_fwd(const void* qkv, void* o, float* lse, int64_t B, int64_t T, int64_t H, int64_t Hkv,
+                            int64_t hd, int64_t ld_qkv, int64_t ld_o, float scale, void* stream) {
+  int rc = attn::check_args(B, T, H, Hkv, hd);
+  if (rc) return rc;
+  attn::Params p{};
+  p.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv);
+  p.out = reinterpret_cast<__nv_bfloat16*>(o);
+  p.lse = lse;
+  p.ld = ld_qkv;
+  p.ldo = ld_o;
+  p.B = (int)B; p.T = (int)T; p.H = (int)H; p.Hkv = (int)Hkv;
+  p.scale = scale;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (hd == 48) return attn::run_fwd<48>(p, s);
+  if (hd == 64) return attn::run_fwd<64>(p, s);
+  return attn::run_fwd<128>(p, s);
+}
+
+extern "C" int spx_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, float* delta_ws,
+                            void* dqkv, int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv,
+                            int64_t ld_o, float scale, void* stream) {
+  int rc = attn::check_args(B, T, H, Hkv, hd);
+  if (rc) return rc;
+  attn::Params p{};
+  p.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv);
+  p.out = reinterpret_cast<__nv_bfloat16*>(dqkv);
+  p.o = reinterpret_cast<const __nv_bfloat16*>(o);
+  p.dout = reinterpret_cast<const __nv_bfloat16*>(dout);
+  p.lse = const_cast<float*>(lse);
+  p.delta = delta_ws;
+  p.ld = ld_qkv;
+  p.ldo = ld_o;
+  p.B = (int)B; p.T = (int)T; p.H = (int)H; p.Hkv = (int)Hkv;
+  p.scale = scale;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (hd == 48) return attn::run_bwd<48>(p, s);
+  if (hd == 64) return attn::run_bwd<64>(p, s);
+  return attn::run_bwd<128>(p, s);
+}

@@ -1,0 +1,466 @@
+// HBM-bound kernels of a LLaMA stage and of the optimizer step: RMSNorm fwd/bwd, RoPE,
+// SwiGLU backward, embedding gather / deterministic scatter, fused softmax cross-entropy
+// (loss + dlogits in one pass pair), deterministic sums, grad-norm clip and fused AdamW.
+//
+// All row kernels use one warp per row with 16-byte vector accesses; reductions that feed
+// parameter gradients are two-pass (fixed-order partials, then a fixed-order final sum) so a
+// training step is bit-reproducible.
+#include <cmath>
+
+#include "spx_common.cuh"
+#include "spx_internal.h"
+
+namespace spx {
+namespace ew {
+
+constexpr int ROW_WARPS = 8;  // rows per 256-thread CTA
+
+union Vec8 {
+  uint4 u;
+  __nv_bfloat162 h[4];
+};
+
+SPX_DEVICE void load8(float (&f)[8], const __nv_bfloat16* p) {
+  Vec8 v;
+  v.u = *reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(v.h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+SPX_DEVICE void store8(__nv_bfloat16* p, const float (&f)[8]) {
+  Vec8 v;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v.h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = v.u;
+}
+
+// ---------------------------------------------------------------- RMSNorm
+__global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
+                                   __nv_bfloat16* __restrict__ y, float* __restrict__ rstd, int rows, int d,
+                                   float eps) {
+  const int row = blockIdx.x * ROW_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const __nv_bfloat16* xr = x + (size_t)row * d;
+  float ss = 0.f;
+  for (int c = lane * 8; c < d; c += 256) {
+    float f[8];
+    load8(f, xr + c);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss += f[i] * f[i];
+  }
+  ss = warp_sum(ss);
+  const float r = rsqrtf(ss / d + eps);
+  __nv_bfloat16* yr = y + (size_t)row * d;
+  for (int c = lane * 8; c < d; c += 256) {
+    float f[8], w[8];
+    load8(f, xr + c);
+    load8(w, g + c);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = f[i] * r * w[i];
+    store8(yr + c, f);
+  }
+  if (lane == 0) rstd[row] = r;
+}
+
+// dx = dres + rstd * (g*dy - xhat * mean(xhat*g*dy))
+__global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
+                                   const float* __restrict__ rstd, const __nv_bfloat16* __restrict__ dy,
+                                   const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx, int rows,
+                                   int d) {
+  const int row = blockIdx.x * ROW_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const size_t off = (size_t)row * d;
+  const float r = rstd[row];
+  float dot = 0.f;
+  for (int c = lane * 8; c < d; c += 256) {
+    float xf[8], w[8], gy[8];
+    load8(xf, x + off + c);
+    load8(w, g + c);
+    load8(gy, dy + off + c);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dot += xf[i] * r * w[i] * gy[i];
+  }
+  dot = warp_sum(dot) / d;
+  for (int c = lane * 8; c < d; c += 256) {
+    float xf[8], w[8], gy[8], o[8];
+    load8(xf, x + off + c);
+    load8(w, g + c);
+    load8(gy, dy + off + c);
+    if (dres) load8(o, dres + off + c);
+    else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] += r * (w[i] * gy[i] - xf[i] * r * dot);
+    store8(dx + off + c, o);
+  }
+}
+
+// dg partials: part[split][c] = sum_{rows in split} dy[r,c] * x[r,c] * rstd[r]
+constexpr int DG_SPLITS = 64;
+__global__ void rmsnorm_dg_partial_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ rstd,
+                                          const __nv_bfloat16* __restrict__ dy, float* __restrict__ part, int rows,
+                                          int d) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (c >= d) return;
+  const int split = blockIdx.y;
+  const int per = (rows + DG_SPLITS - 1) / DG_SPLITS;
+  const int r0 = split * per, r1 = min(rows, r0 + per);
+  float a0 = 0.f, a1 = 0.f;
+  for (int r = r0; r < r1; ++r) {
+    const float s = rstd[r];
+    float2 xv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + (size_t)r * d + c));
+    float2 gv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dy + (size_t)r * d + c));
+    a0 += gv.x * xv.x * s;
+    a1 += gv.y * xv.y * s;
+  }
+  part[(size_t)split * d + c] = a0;
+  part[(size_t)split * d + c + 1] = a1;
+}
+
+__global__ void colsum_add_kernel(const float* __restrict__ part, float* __restrict__ out, int nsplit, int d) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d) return;
+  float s = 0.f;
+  for (int i = 0; i < nsplit; ++i) s += part[(size_t)i * d + c];
+  out[c] += s;
+}
+
+// ---------------------------------------------------------------- RoPE (rotate-half convention)
+// in place on the q heads [0, H) and k heads [H, H+Hkv) of a fused QKV row; position = row % T
+__global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, const float* __restrict__ cs, int rows, int T, int nheads,
+                            int hd, long long ld, float sign) {
+  const int half = hd / 2;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per_row = (long long)nheads * half;
+  if (idx >= (long long)rows * per_row) return;
+  const int row = (int)(idx / per_row);
+  const int rem = (int)(idx % per_row);
+  const int h = rem / half, j = rem % half;
+  const int t = row % T;
+  const float c = cs[((size_t)t * half + j) * 2];
+  const float s = sign * cs[((size_t)t * half + j) * 2 + 1];
+  __nv_bfloat16* p = qkv + (size_t)row * ld + (size_t)h * hd;
+  const float a = __bfloat162float(p[j]), b = __bfloat162float(p[j + half]);
+  p[j] = __float2bfloat16(a * c - b * s);
+  p[j + half] = __float2bfloat16(b * c + a * s);
+}
+
+// ---------------------------------------------------------------- SwiGLU backward
+// gu [rows, 2F] with gate/up interleaved in 128-column blocks; dh [rows, F]; dgu [rows, 2F]
+__global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __nv_bfloat16* __restrict__ dh,
+                                  __nv_bfloat16* __restrict__ dgu, int rows, int F) {
+  const long long idx = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (idx >= (long long)rows * F) return;
+  const int row = (int)(idx / F);
+  const int c = (int)(idx % F);
+  const int blk = c >> 7, j = c & 127;
+  const size_t gofs = (size_t)row * 2 * F + (size_t)blk * 256 + j;
+  float g[8], u[8], d[8], og[8], ou[8];
+  load8(g, gu + gofs);
+  load8(u, gu + gofs + 128);
+  load8(d, dh + (size_t)row * F + c);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float sg = 1.f / (1.f + __expf(-g[i]));
+    const float silu = g[i] * sg;
+    og[i] = d[i] * u[i] * sg * (1.f + g[i] * (1.f - sg));
+    ou[i] = d[i] * silu;
+  }
+  store8(dgu + gofs, og);
+  store8(dgu + gofs + 128, ou);
+}
+
+// ---------------------------------------------------------------- embedding
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ table,
+                                 __nv_bfloat16* __restrict__ out, int n, int d) {
+  const int row = blockIdx.x * ROW_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const __nv_bfloat16* src = table + (size_t)ids[row] * d;
+  __nv_bfloat16* dst = out + (size_t)row * d;
+  for (int c = lane * 8; c < d; c += 256)
+    *reinterpret_cast<uint4*>(dst + c) = *reinterpret_cast<const uint4*>(src + c);
+}
+
+// Deterministic scatter-add: tokens pre-grouped by id (perm sorted by (id, position)); one CTA
+// per distinct id sums its rows in position order and adds once into the fp32 table gradient.
+__global__ void embed_bwd_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ seg_start,
+                                 const int32_t* __restrict__ seg_id, const __nv_bfloat16* __restrict__ dout,
+                                 float* __restrict__ dtable, int d) {
+  const int seg = blockIdx.x;
+  const int a = seg_start[seg], b = seg_start[seg + 1];
+  float* dst = dtable + (size_t)seg_id[seg] * d;
+  for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int k = a; k < b; ++k) {
+      float f[8];
+      load8(f, dout + (size_t)perm[k] * d + c);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += f[i];
+    }
+    float4* o = reinterpret_cast<float4*>(dst + c);
+    float4 o0 = o[0], o1 = o[1];
+    o0.x += acc[0]; o0.y += acc[1]; o0.z += acc[2]; o0.w += acc[3];
+    o1.x += acc[4]; o1.y += acc[5]; o1.z += acc[6]; o1.w += acc[7];
+    o[0] = o0;
+    o[1] = o1;
+  }
+}
+
+// ---------------------------------------------------------------- softmax cross-entropy
+// One CTA per row: loss_r = logsumexp(z) - z[target]; dlogits = (softmax(z) - onehot) * scale
+// written in place over the bf16 logits.
+constexpr int XE_THREADS = 512;
+__global__ void __launch_bounds__(XE_THREADS) xent_kernel(__nv_bfloat16* __restrict__ logits,
+                                                          const int32_t* __restrict__ targets,
+                                                          float* __restrict__ row_loss, int V, long long ld,
+                                                          float scale) {
+  __shared__ float red_m[XE_THREADS / 32], red_s[XE_THREADS / 32];
+  const int row = blockIdx.x;
+  __nv_bfloat16* z = logits + (size_t)row * ld;
+  float m = -INFINITY, s = 0.f;
+  for (int c = threadIdx.x * 8; c < V; c += XE_THREADS * 8) {
+    float f[8];
+    load8(f, z + c);
+    float mx = f[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) mx = fmaxf(mx, f[i]);
+    const float nm = fmaxf(m, mx);
+    s *= __expf(m - nm);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += __expf(f[i] - nm);
+    m = nm;
+  }
+  // warp then block reduction of (m, s)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
+    const float nm = fmaxf(m, om);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+    m = nm;
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    red_m[w] = m;
+    red_s[w] = s;
+  }
+  __syncthreads();
+  if (w == 0) {
+    m = lane < XE_THREADS / 32 ? red_m[lane] : -INFINITY;
+    s = lane < XE_THREADS / 32 ? red_s[lane] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
+      const float nm = fmaxf(m, om);
+      s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+      m = nm;
+    }
+    if (lane == 0) {
+      red_m[0] = m;
+      red_s[0] = s;
+    }
+  }
+  __syncthreads();
+  m = red_m[0];
+  s = red_s[0];
+  const int tgt = targets[row];
+  const float zt = __bfloat162float(z[tgt]);
+  __syncthreads();
+  const float inv = 1.f / s;
+  for (int c = threadIdx.x * 8; c < V; c += XE_THREADS * 8) {
+    float f[8];
+    load8(f, z + c);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = (__expf(f[i] - m) * inv - (c + i == tgt ? 1.f : 0.f)) * scale;
+    store8(z + c, f);
+  }
+  if (threadIdx.x == 0) row_loss[row] = logf(s) + m - zt;
+}
+
+// ---------------------------------------------------------------- reductions
+// out[0] (+)= scale * sum(x[0:n])   (single CTA, fixed order)
+__global__ void sum_kernel(const float* __restrict__ x, long long n, float* __restrict__ out, float scale,
+                           int accumulate) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    const float v = (float)(t * scale);
+    out[0] = accumulate ? out[0] + v : v;
+  }
+}
+
+constexpr int SUMSQ_BLOCKS = 592;  // 4 per SM
+__global__ void sumsq_partial_kernel(const float* __restrict__ x, long long n, float* __restrict__ part) {
+  __shared__ float red[32];
+  float s = 0.f;
+  const long long n4 = n / 4;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = x4[i];
+    s += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  if (blockIdx.x == 0)
+    for (long long i = n4 * 4 + threadIdx.x; i < n; i += blockDim.x) s += x[i] * x[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    part[blockIdx.x] = t;
+  }
+}
+
+// scale = min(1, max_norm / (||g|| + 1e-6)) from per-set squared norms (torch clip_grad_norm_)
+__global__ void clip_scale_kernel(const float* __restrict__ sumsq, int count, float max_norm, float* __restrict__ scale,
+                                  float* __restrict__ norm_out) {
+  if (threadIdx.x != 0) return;
+  double t = 0.0;
+  for (int i = 0; i < count; ++i) t += sumsq[i];
+  const float nrm = (float)sqrt(t);
+  if (norm_out) norm_out[0] = nrm;
+  const float c = max_norm / (nrm + 1e-6f);
+  scale[0] = c < 1.f ? c : 1.f;
+}
+
+// ---------------------------------------------------------------- AdamW (torch.optim.AdamW math)
+__global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                             float* __restrict__ v, __nv_bfloat16* __restrict__ pb, long long n, long long n_decay,
+                             float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
+                             const float* __restrict__ gscale) {
+  const float sc = gscale ? gscale[0] : 1.f;
+  const float step = lr / bc1;
+  const float rbc2 = rsqrtf(bc2);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float gi = g[i] * sc;
+    float pi = p[i];
+    if (i < n_decay) pi *= (1.f - lr * wd);
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    pi -= step * mi / (sqrtf(vi) * rbc2 + eps);
+    p[i] = pi;
+    pb[i] = __float2bfloat16(pi);
+  }
+}
+
+}  // namespace ew
+}  // namespace spx
+
+using namespace spx;
+using namespace spx::ew;
+
+#define SPX_S reinterpret_cast<cudaStream_t>(stream)
+#define BF(p) reinterpret_cast<__nv_bfloat16*>(p)
+#define CBF(p) reinterpret_cast<const __nv_bfloat16*>(p)
+
+extern "C" int spx_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int64_t rows, int64_t d, float eps,
+                               void* stream) {
+  if (d % 8) return set_error(SPX_ERR_ARG, "rmsnorm: d must be a multiple of 8");
+  rmsnorm_fwd_kernel<<<(unsigned)((rows + ROW_WARPS - 1) / ROW_WARPS), ROW_WARPS * 32, 0, SPX_S>>>(
+      CBF(x), CBF(g), BF(y), rstd, (int)rows, (int)d, eps);
+  return check_launch("rmsnorm_fwd_kernel");
+}
+
+extern "C" int spx_rmsnorm_bwd(const void* x, const void* g, const float* rstd, const void* dy, const void* dres,
+                               void* dx, float* dg, float* ws, int64_t rows, int64_t d, void* stream) {
+  if (d % 8) return set_error(SPX_ERR_ARG, "rmsnorm: d must be a multiple of 8");
+  rmsnorm_bwd_kernel<<<(unsigned)((rows + ROW_WARPS - 1) / ROW_WARPS), ROW_WARPS * 32, 0, SPX_S>>>(
+      CBF(x), CBF(g), rstd, CBF(dy), CBF(dres), BF(dx), (int)rows, (int)d);
+  int rc = check_launch("rmsnorm_bwd_kernel");
+  if (rc || dg == nullptr) return rc;
+  dim3 grid((unsigned)((d / 2 + 127) / 128), DG_SPLITS);
+  rmsnorm_dg_partial_kernel<<<grid, 128, 0, SPX_S>>>(CBF(x), rstd, CBF(dy), ws, (int)rows, (int)d);
+  rc = check_launch("rmsnorm_dg_partial_kernel");
+  if (rc) return rc;
+  colsum_add_kernel<<<(unsigned)((d + 255) / 256), 256, 0, SPX_S>>>(ws, dg, DG_SPLITS, (int)d);
+  return check_launch("colsum_add_kernel");
+}
+
+extern "C" int64_t spx_rmsnorm_ws_floats(int64_t d) { return (int64_t)DG_SPLITS * d; }
+
+extern "C" int spx_rope(void* qkv, const float* cos_sin, int64_t rows, int64_t T, int64_t n_heads, int64_t hd,
+                        int64_t ld, int32_t inverse, void* stream) {
+  if (hd % 2) return set_error(SPX_ERR_ARG, "rope: odd head dim");
+  const long long total = rows * n_heads * (hd / 2);
+  rope_kernel<<<(unsigned)((total + 255) / 256), 256, 0, SPX_S>>>(BF(qkv), cos_sin, (int)rows, (int)T, (int)n_heads,
+                                                                 (int)hd, ld, inverse ? -1.f : 1.f);
+  return check_launch("rope_kernel");
+}
+
+extern "C" int spx_swiglu_bwd(const void* gu, const void* dh, void* dgu, int64_t rows, int64_t F, void* stream) {
+  if (F % 128) return set_error(SPX_ERR_ARG, "swiglu_bwd: F must be a multiple of 128");
+  const long long total = rows * F / 8;
+  swiglu_bwd_kernel<<<(unsigned)((total + 255) / 256), 256, 0, SPX_S>>>(CBF(gu), CBF(dh), BF(dgu), (int)rows, (int)F);
+  return check_launch("swiglu_bwd_kernel");
+}
+
+extern "C" int spx_embed_fwd(const int32_t* ids, const void* table, void* out, int64_t n, int64_t d, void* stream) {
+  if (d % 8) return set_error(SPX_ERR_ARG, "embed: d must be a multiple of 8");
+  embed_fwd_kernel<<<(unsigned)((n + ROW_WARPS - 1) / ROW_WARPS), ROW_WARPS * 32, 0, SPX_S>>>(ids, CBF(table), BF(out),
+                                                                                            (int)n, (int)d);
+  return check_launch("embed_fwd_kernel");
+}
+
+extern "C" int spx_embed_bwd(const int32_t* perm, const int32_t* seg_start, const int32_t* seg_id, int64_t n_segments,
+                             const void* dout, float* dtable, int64_t d, void* stream) {
+  if (d % 8) return set_error(SPX_ERR_ARG, "embed: d must be a multiple of 8");
+  if (n_segments == 0) return SPX_OK;
+  embed_bwd_kernel<<<(unsigned)n_segments, 128, 0, SPX_S>>>(perm, seg_start, seg_id, CBF(dout), dtable, (int)d);
+  return check_launch("embed_bwd_kernel");
+}
+
+extern "C" int spx_xent_fwd_bwd(void* logits, const int32_t* targets, float* row_loss, int64_t n, int64_t V, int64_t ld,
+                                float scale, void* stream) {
+  if (V % 8 || ld % 8) return set_error(SPX_ERR_ARG, "xent: V and ld must be multiples of 8");
+  xent_kernel<<<(unsigned)n, XE_THREADS, 0, SPX_S>>>(BF(logits), targets, row_loss, (int)V, ld, scale);
+  return check_launch("xent_kernel");
+}
+
+extern "C" int spx_sum_f32(const float* x, int64_t n, float* out, float scale, int32_t accumulate, void* stream) {
+  sum_kernel<<<1, 1024, 0, SPX_S>>>(x, n, out, scale, accumulate);
+  return check_launch("sum_kernel");
+}
+
+extern "C" int64_t spx_sumsq_ws_floats(void) { return SUMSQ_BLOCKS; }
+
+extern "C" int spx_sumsq(const float* x, int64_t n, float* ws, float* out, void* stream) {
+  sumsq_partial_kernel<<<SUMSQ_BLOCKS, 256, 0, SPX_S>>>(x, n, ws);
+  int rc = check_launch("sumsq_partial_kernel");
+  if (rc) return rc;
+  sum_kernel<<<1, 1024, 0, SPX_S>>>(ws, SUMSQ_BLOCKS, out, 1.f, 0);
+  return check_launch("sum_kernel");
+}
+
+extern "C" int spx_clip_scale(const float* sumsq, int32_t count, float max_norm, float* scale, float* norm_out,
+                              void* stream) {
+  clip_scale_kernel<<<1, 32, 0, SPX_S>>>(sumsq, count, max_norm, scale, norm_out);
+  return check_launch("clip_scale_kernel");
+}
+
+extern "C" int spx_adamw(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n, int64_t n_decay,
+                         float lr, float beta1, float beta2, float eps, float weight_decay, int64_t step,
+                         const float* grad_scale, void* stream) {
+  if (step < 1) return set_error(SPX_ERR_ARG, "adamw: step must be >= 1");
+  const float bc1 = 1.f - powf(beta1, (float)step);
+  const float bc2 = 1.f - powf(beta2, (float)step);
+  const int blocks = num_sms() * 8;
+  adamw_kernel<<<blocks, 256, 0, SPX_S>>>(p, g, m, v, BF(p_bf16), n, n_decay, lr, beta1, beta2, eps, weight_decay, bc1,
+                                          bc2, grad_scale);
+  return check_launch("adamw_kernel");
+}

@@ -27,7 +27,24 @@ SIGNATURES: dict[str, list] = {
     "spx_enable_peer_access": [_I32, _I32],
     "spx_hop": [_I32, _P, _I32, _P, _I64, _P],
     "spx_gemm_bf16": [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _F, _P],
+    "spx_attn_fwd": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P],
+    "spx_attn_bwd": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P],
+    "spx_rmsnorm_fwd": [_P, _P, _P, _P, _I64, _I64, _F, _P],
+    "spx_rmsnorm_bwd": [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _P],
+    "spx_rmsnorm_ws_floats": [_I64],
+    "spx_rope": [_P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _P],
+    "spx_swiglu_bwd": [_P, _P, _P, _I64, _I64, _P],
+    "spx_embed_fwd": [_P, _P, _P, _I64, _I64, _P],
+    "spx_embed_bwd": [_P, _P, _P, _I64, _P, _P, _I64, _P],
+    "spx_xent_fwd_bwd": [_P, _P, _P, _I64, _I64, _I64, _F, _P],
+    "spx_sum_f32": [_P, _I64, _P, _F, _I32, _P],
+    "spx_sumsq_ws_floats": [],
+    "spx_sumsq": [_P, _I64, _P, _P, _P],
+    "spx_clip_scale": [_P, _I32, _F, _P, _P, _P],
+    "spx_adamw": [_P, _P, _P, _P, _P, _I64, _I64, _F, _F, _F, _F, _F, _I64, _P, _P],
 }
+_RESTYPE = {"spx_last_error": ctypes.c_char_p, "spx_rmsnorm_ws_floats": ctypes.c_int64,
+            "spx_sumsq_ws_floats": ctypes.c_int64}
 
 EPI_BF16, EPI_BF16_RESID, EPI_F32, EPI_SWIGLU = 0, 1, 2, 3
 
@@ -57,7 +74,7 @@ def load() -> ctypes.CDLL:
     for name, argtypes in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
-        fn.restype = ctypes.c_char_p if name == "spx_last_error" else ctypes.c_int
+        fn.restype = _RESTYPE.get(name, ctypes.c_int)
     _lib = lib
     return lib
 
@@ -94,3 +111,74 @@ def hop(dst, dst_dev: int, src, src_dev: int, nbytes: int, stream=None) -> None:
 
 def enable_peer_access(dev: int, peer: int) -> None:
     _check(load().spx_enable_peer_access(dev, peer), "spx_enable_peer_access")
+
+
+def attn_fwd(qkv, o, lse, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, stream=None) -> None:
+    _check(load().spx_attn_fwd(_ptr(qkv), _ptr(o), _ptr(lse), B, T, H, Hkv, hd, ld_qkv, ld_o, float(scale),
+                               _stream(stream)), "spx_attn_fwd")
+
+
+def attn_bwd(qkv, o, dout, lse, delta_ws, dqkv, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, stream=None) -> None:
+    _check(load().spx_attn_bwd(_ptr(qkv), _ptr(o), _ptr(dout), _ptr(lse), _ptr(delta_ws), _ptr(dqkv), B, T, H, Hkv,
+                               hd, ld_qkv, ld_o, float(scale), _stream(stream)), "spx_attn_bwd")
+
+
+def rmsnorm_fwd(x, g, y, rstd, *, rows, d, eps, stream=None) -> None:
+    _check(load().spx_rmsnorm_fwd(_ptr(x), _ptr(g), _ptr(y), _ptr(rstd), rows, d, float(eps), _stream(stream)),
+           "spx_rmsnorm_fwd")
+
+
+def rmsnorm_bwd(x, g, rstd, dy, dres, dx, dg, ws, *, rows, d, stream=None) -> None:
+    _check(load().spx_rmsnorm_bwd(_ptr(x), _ptr(g), _ptr(rstd), _ptr(dy), _ptr(dres), _ptr(dx), _ptr(dg), _ptr(ws),
+                                  rows, d, _stream(stream)), "spx_rmsnorm_bwd")
+
+
+def rmsnorm_ws_floats(d: int) -> int:
+    return int(load().spx_rmsnorm_ws_floats(d))
+
+
+def rope(qkv, cos_sin, *, rows, T, n_heads, hd, ld, inverse=False, stream=None) -> None:
+    _check(load().spx_rope(_ptr(qkv), _ptr(cos_sin), rows, T, n_heads, hd, ld, int(inverse), _stream(stream)),
+           "spx_rope")
+
+
+def swiglu_bwd(gu, dh, dgu, *, rows, F, stream=None) -> None:
+    _check(load().spx_swiglu_bwd(_ptr(gu), _ptr(dh), _ptr(dgu), rows, F, _stream(stream)), "spx_swiglu_bwd")
+
+
+def embed_fwd(ids, table, out, *, n, d, stream=None) -> None:
+    _check(load().spx_embed_fwd(_ptr(ids), _ptr(table), _ptr(out), n, d, _stream(stream)), "spx_embed_fwd")
+
+
+def embed_bwd(perm, seg_start, seg_id, n_segments, dout, dtable, *, d, stream=None) -> None:
+    _check(load().spx_embed_bwd(_ptr(perm), _ptr(seg_start), _ptr(seg_id), n_segments, _ptr(dout), _ptr(dtable), d,
+                                _stream(stream)), "spx_embed_bwd")
+
+
+def xent_fwd_bwd(logits, targets, row_loss, *, n, V, ld, scale, stream=None) -> None:
+    _check(load().spx_xent_fwd_bwd(_ptr(logits), _ptr(targets), _ptr(row_loss), n, V, ld, float(scale),
+                                   _stream(stream)), "spx_xent_fwd_bwd")
+
+
+def sum_f32(x, n, out, *, scale=1.0, accumulate=False, stream=None) -> None:
+    _check(load().spx_sum_f32(_ptr(x), n, _ptr(out), float(scale), int(accumulate), _stream(stream)), "spx_sum_f32")
+
+
+def sumsq_ws_floats() -> int:
+    return int(load().spx_sumsq_ws_floats())
+
+
+def sumsq(x, n, ws, out, *, stream=None) -> None:
+    _check(load().spx_sumsq(_ptr(x), n, _ptr(ws), _ptr(out), _stream(stream)), "spx_sumsq")
+
+
+def clip_scale(sumsq_vec, count, max_norm, scale_out, norm_out=None, *, stream=None) -> None:
+    _check(load().spx_clip_scale(_ptr(sumsq_vec), count, float(max_norm), _ptr(scale_out), _ptr(norm_out),
+                                 _stream(stream)), "spx_clip_scale")
+
+
+def adamw(p, g, m, v, p_bf16, *, n, n_decay, lr, beta1, beta2, eps, weight_decay, step, grad_scale=None,
+          stream=None) -> None:
+    _check(load().spx_adamw(_ptr(p), _ptr(g), _ptr(m), _ptr(v), _ptr(p_bf16), n, n_decay, float(lr), float(beta1),
+                            float(beta2), float(eps), float(weight_decay), int(step), _ptr(grad_scale),
+                            _stream(stream)), "spx_adamw")

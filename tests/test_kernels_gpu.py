@@ -1,0 +1,230 @@
+"""Stage kernels of libspx (attention, RMSNorm, RoPE, SwiGLU, embedding, cross-entropy, AdamW,
+grad-norm) against plain torch fp32 references of the same ops."""
+
+import math
+
+import pytest
+import torch
+
+from paper_2502_19913_b200 import native
+
+pytestmark = pytest.mark.gpu
+dev = "cuda"
+
+
+def rel(a, b):
+    return ((a.float() - b.float()).norm() / (b.float().norm() + 1e-12)).item()
+
+
+def bf(x):
+    return x.to(torch.bfloat16)
+
+
+def rope_table(T, hd, theta=10000.0):
+    inv = 1.0 / (theta ** (torch.arange(0, hd, 2, dtype=torch.float64) / hd))
+    ang = torch.arange(T, dtype=torch.float64)[:, None] * inv[None, :]
+    return torch.stack([ang.cos(), ang.sin()], dim=-1).float()  # [T, hd/2, 2]
+
+
+def rope_ref(x, cs):  # x [B, T, H, hd] fp32
+    hd = x.shape[-1]
+    c = cs[..., 0][None, :, None, :]
+    s = cs[..., 1][None, :, None, :]
+    x1, x2 = x[..., : hd // 2], x[..., hd // 2:]
+    return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1)
+
+
+def attn_ref(q, k, v, scale):  # [B, H, T, hd] fp32, causal, GQA by repeat
+    rep = q.shape[1] // k.shape[1]
+    k = k.repeat_interleave(rep, dim=1)
+    v = v.repeat_interleave(rep, dim=1)
+    s = (q @ k.transpose(-1, -2)) * scale
+    T = q.shape[2]
+    mask = torch.ones(T, T, dtype=torch.bool, device=q.device).triu(1)
+    s = s.masked_fill(mask, float("-inf"))
+    lse = torch.logsumexp(s, dim=-1)
+    return torch.softmax(s, dim=-1) @ v, lse
+
+
+@pytest.mark.parametrize("B,T,H,Hkv,hd", [(2, 256, 6, 6, 48), (2, 1024, 16, 16, 64), (1, 512, 8, 2, 128),
+                                          (1, 256, 4, 4, 128)])
+def test_attention_fwd_bwd(B, T, H, Hkv, hd):
+    g = torch.Generator().manual_seed(B * T + H + hd)
+    W = (H + 2 * Hkv) * hd
+    qkv = bf(torch.randn(B * T, W, generator=g)).to(dev)
+    do = bf(torch.randn(B * T, H * hd, generator=g)).to(dev)
+    scale = 1.0 / math.sqrt(hd)
+    o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device=dev)
+    lse = torch.empty(B, H, T, dtype=torch.float32, device=dev)
+    native.attn_fwd(qkv, o, lse, B=B, T=T, H=H, Hkv=Hkv, hd=hd, ld_qkv=W, ld_o=H * hd, scale=scale)
+    dqkv = torch.zeros_like(qkv)
+    delta = torch.empty(B, H, T, dtype=torch.float32, device=dev)
+    native.attn_bwd(qkv, o, do, lse, delta, dqkv, B=B, T=T, H=H, Hkv=Hkv, hd=hd, ld_qkv=W, ld_o=H * hd, scale=scale)
+    torch.cuda.synchronize()
+
+    x = qkv.float().view(B, T, H + 2 * Hkv, hd)
+    q = x[:, :, :H].permute(0, 2, 1, 3).clone().requires_grad_()
+    k = x[:, :, H:H + Hkv].permute(0, 2, 1, 3).clone().requires_grad_()
+    v = x[:, :, H + Hkv:].permute(0, 2, 1, 3).clone().requires_grad_()
+    ref, ref_lse = attn_ref(q, k, v, scale)
+    ref.backward(do.float().view(B, T, H, hd).permute(0, 2, 1, 3))
+    ref_o = ref.permute(0, 2, 1, 3).reshape(B * T, H * hd)
+    assert rel(o, ref_o) < 1e-2
+    assert (lse - ref_lse).abs().max().item() < 1e-2
+    dx = dqkv.float().view(B, T, H + 2 * Hkv, hd)
+    assert rel(dx[:, :, :H].permute(0, 2, 1, 3), q.grad) < 2e-2
+    assert rel(dx[:, :, H:H + Hkv].permute(0, 2, 1, 3), k.grad) < 2e-2
+    assert rel(dx[:, :, H + Hkv:].permute(0, 2, 1, 3), v.grad) < 2e-2
+
+
+def test_attention_deterministic():
+    B, T, H, hd = 1, 512, 4, 64
+    g = torch.Generator().manual_seed(7)
+    W = 3 * H * hd
+    qkv = bf(torch.randn(B * T, W, generator=g)).to(dev)
+    do = bf(torch.randn(B * T, H * hd, generator=g)).to(dev)
+    outs = []
+    for _ in range(2):
+        o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device=dev)
+        lse = torch.empty(B, H, T, device=dev)
+        native.attn_fwd(qkv, o, lse, B=B, T=T, H=H, Hkv=H, hd=hd, ld_qkv=W, ld_o=H * hd, scale=0.125)
+        d = torch.zeros_like(qkv)
+        native.attn_bwd(qkv, o, do, lse, torch.empty_like(lse), d, B=B, T=T, H=H, Hkv=H, hd=hd, ld_qkv=W,
+                        ld_o=H * hd, scale=0.125)
+        outs.append((o, d))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("rows,d", [(512, 288), (4096, 1024)])
+def test_rmsnorm(rows, d):
+    g = torch.Generator().manual_seed(d)
+    x = bf(torch.randn(rows, d, generator=g)).to(dev)
+    w = bf(1 + 0.1 * torch.randn(d, generator=g)).to(dev)
+    dy = bf(torch.randn(rows, d, generator=g)).to(dev)
+    dres = bf(torch.randn(rows, d, generator=g)).to(dev)
+    y = torch.empty_like(x)
+    rstd = torch.empty(rows, device=dev)
+    native.rmsnorm_fwd(x, w, y, rstd, rows=rows, d=d, eps=1e-5)
+    dx = torch.empty_like(x)
+    dg = torch.full((d,), 0.5, device=dev)
+    ws = torch.empty(native.rmsnorm_ws_floats(d), device=dev)
+    native.rmsnorm_bwd(x, w, rstd, dy, dres, dx, dg, ws, rows=rows, d=d)
+    torch.cuda.synchronize()
+    xr = x.float().requires_grad_()
+    wr = w.float().requires_grad_()
+    yr = xr * torch.rsqrt(xr.pow(2).mean(-1, keepdim=True) + 1e-5) * wr
+    yr.backward(dy.float())
+    assert rel(y, yr) < 1e-2
+    assert rel(dx, xr.grad + dres.float()) < 1e-2
+    assert rel(dg - 0.5, wr.grad) < 1e-3
+
+
+def test_rope_roundtrip():
+    B, T, H, Hkv, hd = 2, 256, 4, 2, 64
+    W = (H + 2 * Hkv) * hd
+    g = torch.Generator().manual_seed(0)
+    qkv = bf(torch.randn(B * T, W, generator=g)).to(dev)
+    cs = rope_table(T, hd).to(dev)
+    out = qkv.clone()
+    native.rope(out, cs, rows=B * T, T=T, n_heads=H + Hkv, hd=hd, ld=W)
+    torch.cuda.synchronize()
+    x = qkv.float().view(B, T, H + 2 * Hkv, hd)
+    ref = rope_ref(x[:, :, : H + Hkv], cs)
+    assert rel(out.float().view(B, T, -1, hd)[:, :, : H + Hkv], ref) < 1e-2
+    assert torch.equal(out.view(B, T, -1, hd)[:, :, H + Hkv:], qkv.view(B, T, -1, hd)[:, :, H + Hkv:])
+    native.rope(out, cs, rows=B * T, T=T, n_heads=H + Hkv, hd=hd, ld=W, inverse=True)
+    torch.cuda.synchronize()
+    assert rel(out, qkv) < 2e-2
+
+
+@pytest.mark.parametrize("rows,F", [(512, 768), (4096, 2816)])
+def test_swiglu_bwd(rows, F):
+    g = torch.Generator().manual_seed(F)
+    gate = torch.randn(rows, F, generator=g)
+    up = torch.randn(rows, F, generator=g)
+    dh = bf(torch.randn(rows, F, generator=g)).to(dev)
+    gu = torch.stack([gate.view(rows, F // 128, 128), up.view(rows, F // 128, 128)], dim=2).reshape(rows, 2 * F)
+    gu = bf(gu).to(dev)
+    dgu = torch.empty_like(gu)
+    native.swiglu_bwd(gu, dh, dgu, rows=rows, F=F)
+    torch.cuda.synchronize()
+    gr = gu.float().view(rows, F // 128, 2, 128)
+    gt = gr[:, :, 0].reshape(rows, F).requires_grad_()
+    ut = gr[:, :, 1].reshape(rows, F).requires_grad_()
+    (torch.nn.functional.silu(gt) * ut).backward(dh.float())
+    d = dgu.float().view(rows, F // 128, 2, 128)
+    assert rel(d[:, :, 0].reshape(rows, F), gt.grad) < 1e-2
+    assert rel(d[:, :, 1].reshape(rows, F), ut.grad) < 1e-2
+
+
+def test_embedding():
+    V, d, n = 1000, 288, 512
+    g = torch.Generator().manual_seed(0)
+    table = bf(torch.randn(V, d, generator=g)).to(dev)
+    ids_cpu = torch.randint(0, 50, (n,), generator=g, dtype=torch.int32)  # many repeats
+    ids = ids_cpu.to(dev)
+    out = torch.empty(n, d, dtype=torch.bfloat16, device=dev)
+    native.embed_fwd(ids, table, out, n=n, d=d)
+    dout = bf(torch.randn(n, d, generator=g)).to(dev)
+    perm = torch.argsort(ids_cpu.long() * n + torch.arange(n)).to(torch.int32)
+    sid = ids_cpu[perm.long()]
+    uniq, counts = torch.unique_consecutive(sid, return_counts=True)
+    seg = torch.cat([torch.zeros(1, dtype=torch.int64), counts.cumsum(0)]).to(torch.int32)
+    dtab = torch.zeros(V, d, device=dev)
+    native.embed_bwd(perm.to(dev), seg.to(dev), uniq.to(torch.int32).to(dev), len(uniq), dout, dtab, d=d)
+    torch.cuda.synchronize()
+    assert torch.equal(out, table[ids.long()])
+    ref = torch.zeros(V, d, device=dev).index_add_(0, ids.long(), dout.float())
+    assert rel(dtab, ref) < 1e-5
+
+
+@pytest.mark.parametrize("n,V", [(512, 32000), (300, 1024)])
+def test_xent(n, V):
+    g = torch.Generator().manual_seed(V)
+    z = bf(3 * torch.randn(n, V, generator=g)).to(dev)
+    t = torch.randint(0, V, (n,), generator=g, dtype=torch.int32).to(dev)
+    zz = z.clone()
+    rl = torch.empty(n, device=dev)
+    scale = 1.0 / n
+    native.xent_fwd_bwd(zz, t, rl, n=n, V=V, ld=V, scale=scale)
+    tot = torch.zeros(1, device=dev)
+    native.sum_f32(rl, n, tot, scale=scale)
+    torch.cuda.synchronize()
+    zr = z.float().requires_grad_()
+    loss = torch.nn.functional.cross_entropy(zr, t.long())
+    loss.backward()
+    assert abs(tot.item() - loss.item()) < 1e-3 * max(1, loss.item())
+    assert rel(zz, zr.grad) < 1e-2
+
+
+def test_adamw_and_clip():
+    n, nd = 10_000, 7_000
+    g = torch.Generator().manual_seed(0)
+    p0 = torch.randn(n, generator=g)
+    grads = [torch.randn(n, generator=g) * 3 for _ in range(3)]
+    p = p0.clone().to(dev)
+    m = torch.zeros(n, device=dev)
+    v = torch.zeros(n, device=dev)
+    pb = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    ws = torch.empty(native.sumsq_ws_floats(), device=dev)
+    ss = torch.empty(1, device=dev)
+    sc = torch.empty(1, device=dev)
+    # torch reference: two param groups (decay / no decay), clip_grad_norm_ 1.0
+    pr1 = p0[:nd].clone().requires_grad_()
+    pr2 = p0[nd:].clone().requires_grad_()
+    opt = torch.optim.AdamW([{"params": [pr1], "weight_decay": 0.1}, {"params": [pr2], "weight_decay": 0.0}],
+                            lr=3e-4, betas=(0.9, 0.95), eps=1e-8)
+    for step, gr in enumerate(grads, start=1):
+        gd = gr.to(dev)
+        native.sumsq(gd, n, ws, ss)
+        native.clip_scale(ss, 1, 1.0, sc)
+        native.adamw(p, gd, m, v, pb, n=n, n_decay=nd, lr=3e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1,
+                     step=step, grad_scale=sc)
+        pr1.grad, pr2.grad = gr[:nd].clone(), gr[nd:].clone()
+        torch.nn.utils.clip_grad_norm_([pr1, pr2], 1.0)
+        opt.step()
+    torch.cuda.synchronize()
+    ref = torch.cat([pr1.detach(), pr2.detach()])
+    assert (p.cpu() - ref).abs().max().item() < 1e-6
+    assert torch.equal(pb, p.to(torch.bfloat16))
