@@ -1,0 +1,259 @@
+"""Benchmark: SkipPipe partial-pipeline training iteration on B200 (BASELINE.json metric:
+"iteration time (ms) & tokens/s, LLaMa-500M 25% skip, 1/2/4/8 B200 vs full PP").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One "step" = one synchronous training iteration of config C2 (LLaMa-500M, 4 stages x 2
+replicas, 25% skip, M=32 microbatches of 4x1024 tokens = 131,072 tokens) — F, loss and B of
+every microbatch along its scheduled path, replica gradient sync, clip and AdamW.  Inputs are
+synthetic uniform token ids; weights random N(0, 0.02).  At N=1 all 8 logical nodes are
+resident on one GPU; at N>1 (torchrun, one process per GPU) the nodes are placed over the
+GPUs and hops go over NVLink (see dist_trainer.py).
+
+`value` is tokens/s with the step's inputs already in HBM; `e2e` is the same metric through the
+public ``Trainer.step(tokens)`` call with host token buffers (H2D staging and the loss readback
+inside the timed region).  `--impl reference` times the CPU fp32 oracle (the reference ships no
+executor) on a bounded sample of the same workload on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "iteration time (ms) & tokens/s, LLaMa-500M 25% skip, 1/2/4/8 B200 vs full PP"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int = 0):
+        self.proc = None
+        self.gpu = gpu_index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.gpu), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+                for nm, val in zip(names, f[5:9]):
+                    if val.lower() == "active":
+                        reasons.add(nm)
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(rc, budget_s: float = 20.0) -> dict:
+    """CPU fp32 oracle on a bounded sample: one microbatch path (F through its stages, loss, B)
+    of the same model, b=1, timed on all host threads; reported as tokens/s."""
+    import torch
+
+    from oracle import train_ref
+    from paper_2502_19913_b200.model import init_params, synthetic_tokens
+
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    params = init_params(rc.model, rc.layers, seed=0)
+    sch = rc.schedule()
+    agents = sorted(a.id for a in sch.agents)
+    stages = sch.paths[agents[0]].stages
+    tokens = synthetic_tokens(rc.model, 1, 1, rc.T, seed=1234)
+    times = []
+    t_end = time.time() + budget_s
+    while time.time() < t_end or not times:
+        t0 = time.perf_counter()
+        train_ref.iteration(rc.model, rc.layers, params, [stages], tokens, update=False)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 3:
+            break
+    sec = statistics.median(times)
+    return {"value": rc.T / sec, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"1 microbatch (1x{rc.T} tokens) along path stages {list(stages)}: F+loss+B, fp32 torch CPU, "
+                      f"median of {len(times)}"}
+
+
+def run_reference(args, rc):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    t0 = time.time()
+    cb = cpu_baseline(rc, budget_s=min(30.0, 10.0 * max(1, args.steps)))
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": rc.M * rc.tokens_per_mb / cb["value"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": rc.name, "model": rc.model.name, "global_batch": rc.M * rc.b, "seq_len": rc.T,
+                       "parallelism": "cpu"},
+            "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                                         "d2h_bytes_per_step": 0},
+            "wall_s": time.time() - t0}
+    print(json.dumps(line), flush=True)
+
+
+def gemm_roofline(tr, peak_tflops: float, reps: int = 5) -> dict:
+    """Per-launch timing of every tcgen05 GEMM of one iteration (same shapes, layouts and
+    epilogues as inside the captured graphs), on the executor's stream with CUDA events."""
+    import torch
+
+    from paper_2502_19913_b200 import native
+
+    calls = native.recorded_gemms()
+    s = tr.streams[tr.devices[0]]
+    total_flops, total_ms = 0.0, 0.0
+    per = {}
+    for key, (count, fn) in calls.items():
+        with torch.cuda.stream(s):
+            fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(reps):
+                fn()
+            e1.record(s)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        M, N, K = key[0], key[1], key[2]
+        fl = 2.0 * M * N * K
+        total_flops += fl * count
+        total_ms += ms * count
+        per[str(key)] = {"launches_per_step": count, "us": round(ms * 1e3, 2), "tflops": round(fl / ms / 1e9, 1)}
+    ach = total_flops / total_ms / 1e9 if total_ms else 0.0
+    return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak_tflops, "unit": "TFLOP/s",
+            "frac": round(ach / peak_tflops, 4), "traffic": None, "kernel": "spx gemm_bf16_kernel (tcgen05, all shapes)",
+            "gemm_ms_per_step": round(total_ms, 3), "per_shape": per}
+
+
+def run_ours(args, rc):
+    import torch
+
+    from paper_2502_19913_b200 import native
+    from paper_2502_19913_b200.executor import Trainer
+    from paper_2502_19913_b200.model import synthetic_tokens
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_2502_19913_b200.dist_trainer import run_bench_dist
+
+        return run_bench_dist(args, rc)
+    torch.cuda.set_device(0)
+    burst, sustained, hbm, peak_kind = _peaks()
+    tokens = synthetic_tokens(rc.model, rc.M, rc.b, rc.T, seed=1234)
+    native.record_gemms(True)
+    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T,
+                 placement=[0] * rc.topology().n)
+    native.record_gemms(False)
+    launches = tr.launches_per_step()
+    host = tr._stage_inputs(tokens)
+    dev_inputs = {k: v.cuda() for k, v in host.items()}
+    # L2 (126 MB) is far smaller than one step's working set (~tens of GB of activations and
+    # weights), so no explicit flush is needed between steps.
+    for _ in range(args.warmup):
+        tr.step(dev_inputs)
+    torch.cuda.synchronize()
+    s = tr.streams[0]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(args.steps):
+            res = tr.step(dev_inputs)
+        e1.record(s)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    tok = rc.M * rc.tokens_per_mb
+    value = tok / (ms / 1e3)
+    # e2e through the public API: host token tensor in, host loss out, every step
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = tr.step(tokens)
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    flops = rc.train_flops()
+    roof = gemm_roofline(tr, burst)
+    cb = cpu_baseline(rc, budget_s=15.0) if not args.no_cpu_baseline else None
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": rc.name, "model": rc.model.name, "global_batch": rc.M * rc.b, "seq_len": rc.T,
+                   "microbatches": rc.M, "tokens_per_step": tok, "stages": rc.s, "replicas": rc.sizes,
+                   "skip_pct": rc.k, "m": rc.m, "parallelism": "pp-skip(4x2 logical nodes on 1 GPU)",
+                   "l2_flush": "inputs+activations per step >> 126 MB L2", "kind": rc.kind},
+        "loss": round(res["loss"], 5),
+        "e2e": {"value": round(tok / (e2e_ms / 1e3), 1), "unit": "tokens/s",
+                "h2d_bytes_per_step": tr.h2d_bytes(tokens), "d2h_bytes_per_step": 4 * rc.M},
+        "gpu_launches": launches,
+        "step_tflops": round(flops / (ms / 1e3) / 1e12, 1),
+        "step_tensor_frac": round(flops / (ms / 1e3) / 1e12 / sustained, 4),
+        "roofline": {**roof, "peak_kind": f"{peak_kind} burst bf16 (GEMMs timed alone)"},
+        "cpu_baseline": cb,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from paper_2502_19913_b200.configs import get_config
+
+    rc = get_config(args.config)
+    if args.impl == "reference":
+        run_reference(args, rc)
+    else:
+        run_ours(args, rc)
+
+
+if __name__ == "__main__":
+    main()

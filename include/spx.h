@@ -94,10 +94,11 @@ int spx_swiglu_bwd(const void* gu, const void* dh, void* dgu, int64_t rows, int6
 /* ---- embedding ----
  * fwd: out[r] = table[ids[r]].
  * bwd: deterministic scatter-add into the f32 table gradient; tokens grouped by id:
- *      perm = positions sorted by (id, position), seg_start[n_segments+1], seg_id[n_segments]. */
+ *      perm = positions sorted by (id, position), seg_start[n+1], seg_id[n]; the segment count is read
+ *      from device memory (*n_segments <= max_segments) so the call can sit inside a CUDA graph. */
 int spx_embed_fwd(const int32_t* ids, const void* table, void* out, int64_t n, int64_t d, void* stream);
-int spx_embed_bwd(const int32_t* perm, const int32_t* seg_start, const int32_t* seg_id, int64_t n_segments,
-                  const void* dout, float* dtable, int64_t d, void* stream);
+int spx_embed_bwd(const int32_t* perm, const int32_t* seg_start, const int32_t* seg_id, const int32_t* n_segments,
+                  int64_t max_segments, const void* dout, float* dtable, int64_t d, void* stream);
 
 /* ---- softmax cross-entropy: row_loss[r] = lse(z_r) - z_r[t_r]; logits overwritten by
  *      (softmax - onehot) * scale (bf16).  One pass pair per row, logits never re-materialised. */

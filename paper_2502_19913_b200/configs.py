@@ -1,0 +1,135 @@
+"""The five configurations of BASELINE.json as runnable objects.
+
+Each config bundles the model, stage assignment (explicit sizes — Eq. 1 has no integral
+solution on 8 GPUs), the B200 topology the scheduler plans on, the scheduler /
+simulator configs and the microbatch shape.  Node compute times for the planner come from the
+FLOP model at a nominal sustained rate (``PLAN_TFLOPS``) — they only steer path choice and op
+order, and they are frozen here so that the op order (which the executor replays) is a pure
+function of the config.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .allocation import StageAssignment
+from .model import ModelConfig, layer_split, model_config
+from .scheduler import Schedule, SchedulerConfig, path_length, schedule
+from .simulator import SimConfig
+from .topology import Topology, activation_bytes, b200_box
+
+PLAN_TFLOPS = 1000.0   # nominal sustained bf16 rate used only to derive planning times
+
+
+@dataclass
+class RunConfig:
+    name: str
+    model: ModelConfig
+    sizes: list[int]
+    k: float
+    m: int
+    b: int
+    T: int
+    M: int
+    split: list[int] | None = None
+    description: str = ""
+    kind: str = "skippipe"          # or "full" (dtfm_full sequential pipelines)
+    _cache: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def s(self) -> int:
+        return len(self.sizes)
+
+    @property
+    def assignment(self) -> StageAssignment:
+        return StageAssignment.contiguous(self.sizes)
+
+    @property
+    def layers(self) -> list[int]:
+        return layer_split(self.model, self.s, self.split)
+
+    @property
+    def tokens_per_mb(self) -> int:
+        return self.b * self.T
+
+    @property
+    def msg_bytes(self) -> int:
+        return self.model.d * self.T * self.b * 2
+
+    def planning_times(self) -> tuple[list[float], float]:
+        """(compute_fwd_ms per node, loss_ms) from the FLOP model at PLAN_TFLOPS."""
+        c, n_tok = self.model, self.tokens_per_mb
+        stage_of = self.assignment.node_stage()
+        fwd = []
+        for v in range(sum(self.sizes)):
+            fl = self.layers[stage_of[v]] * c.layer_flops_per_token(self.T) * n_tok
+            fwd.append(fl / (PLAN_TFLOPS * 1e12) * 1e3)
+        loss_ms = 3 * c.head_flops_per_token() * n_tok / (PLAN_TFLOPS * 1e12) * 1e3
+        return fwd, loss_ms
+
+    def topology(self) -> Topology:
+        fwd, _ = self.planning_times()
+        return b200_box(fwd, mem_capacity=self.m)
+
+    def scheduler_config(self) -> SchedulerConfig:
+        return SchedulerConfig(k=self.k, msg_bytes=float(self.msg_bytes))
+
+    def sim_config(self, record_trace: bool = False) -> SimConfig:
+        _, loss_ms = self.planning_times()
+        return SimConfig(total_microbatches=self.M, msg_bytes=float(self.msg_bytes), record_trace=record_trace,
+                         loss_ms=loss_ms)
+
+    def schedule(self) -> Schedule:
+        if "schedule" not in self._cache:
+            if self.kind == "full":
+                from .baselines import dtfm_full
+
+                self._cache["schedule"] = dtfm_full(self.topology(), self.s, msg_bytes=float(self.msg_bytes),
+                                                    assignment=self.assignment)
+            else:
+                self._cache["schedule"] = schedule(self.topology(), self.assignment, self.scheduler_config())
+        return self._cache["schedule"]
+
+    def path_len(self) -> int:
+        return path_length(self.s, self.k)
+
+    def train_flops(self) -> float:
+        """Algorithmic FLOPs of one iteration: 3x forward (fwd + 2x bwd) over every microbatch's
+        executed stages + the head, causal attention at half."""
+        c = self.model
+        sch = self.schedule()
+        agents = sorted(a.id for a in sch.agents)
+        total = 0.0
+        for mb in range(self.M):
+            stages = sch.paths[agents[mb % len(agents)]].stages
+            per_tok = sum(self.layers[st] for st in stages) * c.layer_flops_per_token(self.T) + c.head_flops_per_token()
+            total += 3 * per_tok * self.tokens_per_mb
+        return total
+
+
+def get_config(name: str, **over) -> RunConfig:
+    """C1..C5 (+ "-full" variants with k=0 disjoint sequential pipelines)."""
+    base = name.replace("-full", "")
+    full = name.endswith("-full")
+    if base == "C1":
+        rc = RunConfig("C1", model_config("llama-50m"), [2, 2, 2, 2], 25, 2, 2, 256, 8,
+                       description="tiny LLaMA SkipPipe iteration (4 stages x 2 replicas, 25% skip)")
+    elif base == "C2":
+        rc = RunConfig("C2", model_config("llama-500m"), [2, 2, 2, 2], 25, 2, 4, 1024, 32,
+                       description="LLaMa-500M, 4 stages x 2 replicas, 25% stage skip")
+    elif base == "C3":
+        rc = RunConfig("C3", model_config("llama-1.5b"), [1] * 8, 25, 8, 1, 4096, 32,
+                       description="LLaMa-1.5B, 8 stages x 1, skip + swap")
+    elif base == "C4":
+        rc = RunConfig("C4", model_config("llama-8b"), [1] * 8, 37.5, 8, 1, 4096, 64,
+                       description="LLaMa-8B, 8 stages, 33% skip (l=5 -> effective 37.5%), long queue")
+    elif base == "C5":
+        rc = RunConfig("C5", model_config("llama-500m"), [2, 2, 2, 2], 50, 2, 4, 1024, 32,
+                       description="LLaMa-500M skip sweep point (50%)")
+    else:
+        raise KeyError(name)
+    if full:
+        rc.kind, rc.k, rc.name = "full", 0, rc.name + "-full"
+    for k_, v in over.items():
+        setattr(rc, k_, v)
+    return rc

@@ -193,9 +193,10 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ ids, const __nv_bfl
 // Deterministic scatter-add: tokens pre-grouped by id (perm sorted by (id, position)); one CTA
 // per distinct id sums its rows in position order and adds once into the fp32 table gradient.
 __global__ void embed_bwd_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ seg_start,
-                                 const int32_t* __restrict__ seg_id, const __nv_bfloat16* __restrict__ dout,
-                                 float* __restrict__ dtable, int d) {
+                                 const int32_t* __restrict__ seg_id, const int32_t* __restrict__ n_seg,
+                                 const __nv_bfloat16* __restrict__ dout, float* __restrict__ dtable, int d) {
   const int seg = blockIdx.x;
+  if (seg >= n_seg[0]) return;
   const int a = seg_start[seg], b = seg_start[seg + 1];
   float* dst = dtable + (size_t)seg_id[seg] * d;
   for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
@@ -417,11 +418,13 @@ extern "C" int spx_embed_fwd(const int32_t* ids, const void* table, void* out, i
   return check_launch("embed_fwd_kernel");
 }
 
-extern "C" int spx_embed_bwd(const int32_t* perm, const int32_t* seg_start, const int32_t* seg_id, int64_t n_segments,
-                             const void* dout, float* dtable, int64_t d, void* stream) {
+extern "C" int spx_embed_bwd(const int32_t* perm, const int32_t* seg_start, const int32_t* seg_id,
+                             const int32_t* n_segments, int64_t max_segments, const void* dout, float* dtable, int64_t d,
+                             void* stream) {
   if (d % 8) return set_error(SPX_ERR_ARG, "embed: d must be a multiple of 8");
-  if (n_segments == 0) return SPX_OK;
-  embed_bwd_kernel<<<(unsigned)n_segments, 128, 0, SPX_S>>>(perm, seg_start, seg_id, CBF(dout), dtable, (int)d);
+  if (max_segments <= 0) return SPX_OK;
+  embed_bwd_kernel<<<(unsigned)max_segments, 128, 0, SPX_S>>>(perm, seg_start, seg_id, n_segments, CBF(dout), dtable,
+                                                              (int)d);
   return check_launch("embed_bwd_kernel");
 }
 

@@ -35,7 +35,7 @@ SIGNATURES: dict[str, list] = {
     "spx_rope": [_P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _P],
     "spx_swiglu_bwd": [_P, _P, _P, _I64, _I64, _P],
     "spx_embed_fwd": [_P, _P, _P, _I64, _I64, _P],
-    "spx_embed_bwd": [_P, _P, _P, _I64, _P, _P, _I64, _P],
+    "spx_embed_bwd": [_P, _P, _P, _P, _I64, _P, _P, _I64, _P],
     "spx_xent_fwd_bwd": [_P, _P, _P, _I64, _I64, _I64, _F, _P],
     "spx_sum_f32": [_P, _I64, _P, _F, _I32, _P],
     "spx_sumsq_ws_floats": [],
@@ -47,6 +47,27 @@ _RESTYPE = {"spx_last_error": ctypes.c_char_p, "spx_rmsnorm_ws_floats": ctypes.c
             "spx_sumsq_ws_floats": ctypes.c_int64}
 
 EPI_BF16, EPI_BF16_RESID, EPI_F32, EPI_SWIGLU = 0, 1, 2, 3
+
+
+# kernel-launch accounting (bench.py "gpu_launches") and GEMM call recording (roofline timing)
+_STATS = {"launches": 0, "record": False, "gemms": {}}
+
+
+def launches() -> int:
+    return _STATS["launches"]
+
+
+def _count(n: int) -> None:
+    _STATS["launches"] += n
+
+
+def record_gemms(on: bool) -> None:
+    _STATS["record"] = bool(on)
+
+
+def recorded_gemms() -> dict:
+    """(M, N, K, a_mn, b_mn, epilogue) -> (calls recorded, closure re-issuing one such call)."""
+    return _STATS["gemms"]
 
 
 class NativeError(RuntimeError):
@@ -103,6 +124,23 @@ def gemm(A, B, C, *, M, N, K, lda, ldb, ldc, a_mn=False, b_mn=False, epilogue=EP
     rc = load().spx_gemm_bf16(_ptr(A), _ptr(B), _ptr(C), _ptr(R), _ptr(C2), M, N, K, lda, ldb, ldc, ldc2,
                               int(a_mn), int(b_mn), epilogue, float(beta), _stream(stream))
     _check(rc, "spx_gemm_bf16")
+    _count(1)
+    if _STATS["record"]:
+        key = (M, N, K, bool(a_mn), bool(b_mn), int(epilogue))
+        cnt = _STATS["gemms"].get(key, (0, None))[0]
+        args = (A, B, C)
+        kw = dict(M=M, N=N, K=K, lda=lda, ldb=ldb, ldc=ldc, a_mn=a_mn, b_mn=b_mn, epilogue=epilogue, R=R, C2=C2,
+                  ldc2=ldc2, beta=beta)
+
+        def again(args=args, kw=kw):
+            rec = _STATS["record"]
+            _STATS["record"] = False
+            try:
+                gemm(*args, **kw)
+            finally:
+                _STATS["record"] = rec
+
+        _STATS["gemms"][key] = (cnt + 1, again)
 
 
 def hop(dst, dst_dev: int, src, src_dev: int, nbytes: int, stream=None) -> None:
@@ -116,21 +154,25 @@ def enable_peer_access(dev: int, peer: int) -> None:
 def attn_fwd(qkv, o, lse, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, stream=None) -> None:
     _check(load().spx_attn_fwd(_ptr(qkv), _ptr(o), _ptr(lse), B, T, H, Hkv, hd, ld_qkv, ld_o, float(scale),
                                _stream(stream)), "spx_attn_fwd")
+    _count(1)
 
 
 def attn_bwd(qkv, o, dout, lse, delta_ws, dqkv, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, stream=None) -> None:
     _check(load().spx_attn_bwd(_ptr(qkv), _ptr(o), _ptr(dout), _ptr(lse), _ptr(delta_ws), _ptr(dqkv), B, T, H, Hkv,
                                hd, ld_qkv, ld_o, float(scale), _stream(stream)), "spx_attn_bwd")
+    _count(3)
 
 
 def rmsnorm_fwd(x, g, y, rstd, *, rows, d, eps, stream=None) -> None:
     _check(load().spx_rmsnorm_fwd(_ptr(x), _ptr(g), _ptr(y), _ptr(rstd), rows, d, float(eps), _stream(stream)),
            "spx_rmsnorm_fwd")
+    _count(1)
 
 
 def rmsnorm_bwd(x, g, rstd, dy, dres, dx, dg, ws, *, rows, d, stream=None) -> None:
     _check(load().spx_rmsnorm_bwd(_ptr(x), _ptr(g), _ptr(rstd), _ptr(dy), _ptr(dres), _ptr(dx), _ptr(dg), _ptr(ws),
                                   rows, d, _stream(stream)), "spx_rmsnorm_bwd")
+    _count(3 if dg is not None else 1)
 
 
 def rmsnorm_ws_floats(d: int) -> int:
@@ -140,28 +182,52 @@ def rmsnorm_ws_floats(d: int) -> int:
 def rope(qkv, cos_sin, *, rows, T, n_heads, hd, ld, inverse=False, stream=None) -> None:
     _check(load().spx_rope(_ptr(qkv), _ptr(cos_sin), rows, T, n_heads, hd, ld, int(inverse), _stream(stream)),
            "spx_rope")
+    _count(1)
 
 
 def swiglu_bwd(gu, dh, dgu, *, rows, F, stream=None) -> None:
     _check(load().spx_swiglu_bwd(_ptr(gu), _ptr(dh), _ptr(dgu), rows, F, _stream(stream)), "spx_swiglu_bwd")
+    _count(1)
 
 
 def embed_fwd(ids, table, out, *, n, d, stream=None) -> None:
     _check(load().spx_embed_fwd(_ptr(ids), _ptr(table), _ptr(out), n, d, _stream(stream)), "spx_embed_fwd")
+    _count(1)
 
 
-def embed_bwd(perm, seg_start, seg_id, n_segments, dout, dtable, *, d, stream=None) -> None:
-    _check(load().spx_embed_bwd(_ptr(perm), _ptr(seg_start), _ptr(seg_id), n_segments, _ptr(dout), _ptr(dtable), d,
-                                _stream(stream)), "spx_embed_bwd")
+def embed_bwd(perm, seg_start, seg_id, n_segments, max_segments, dout, dtable, *, d, stream=None) -> None:
+    """n_segments: int32 device tensor holding the segment count (graph-capturable)."""
+    _check(load().spx_embed_bwd(_ptr(perm), _ptr(seg_start), _ptr(seg_id), _ptr(n_segments), int(max_segments),
+                                _ptr(dout), _ptr(dtable), d, _stream(stream)), "spx_embed_bwd")
+    _count(1)
+
+
+def embed_segments(ids) -> tuple:
+    """Host-side grouping of token positions by id for the deterministic embedding backward:
+    (perm, seg_start, seg_id, n_segments) as int32 CPU tensors padded to len(ids)."""
+    import torch
+
+    ids = ids.reshape(-1).to(torch.int64).cpu()
+    n = ids.numel()
+    perm = torch.argsort(ids * n + torch.arange(n))
+    sid = ids[perm]
+    uniq, counts = torch.unique_consecutive(sid, return_counts=True)
+    seg_start = torch.zeros(n + 1, dtype=torch.int32)
+    seg_start[1:len(uniq) + 1] = counts.cumsum(0).to(torch.int32)
+    seg_id = torch.zeros(n, dtype=torch.int32)
+    seg_id[:len(uniq)] = uniq.to(torch.int32)
+    return perm.to(torch.int32), seg_start, seg_id, torch.tensor([len(uniq)], dtype=torch.int32)
 
 
 def xent_fwd_bwd(logits, targets, row_loss, *, n, V, ld, scale, stream=None) -> None:
     _check(load().spx_xent_fwd_bwd(_ptr(logits), _ptr(targets), _ptr(row_loss), n, V, ld, float(scale),
                                    _stream(stream)), "spx_xent_fwd_bwd")
+    _count(1)
 
 
 def sum_f32(x, n, out, *, scale=1.0, accumulate=False, stream=None) -> None:
     _check(load().spx_sum_f32(_ptr(x), n, _ptr(out), float(scale), int(accumulate), _stream(stream)), "spx_sum_f32")
+    _count(1)
 
 
 def sumsq_ws_floats() -> int:
@@ -170,11 +236,13 @@ def sumsq_ws_floats() -> int:
 
 def sumsq(x, n, ws, out, *, stream=None) -> None:
     _check(load().spx_sumsq(_ptr(x), n, _ptr(ws), _ptr(out), _stream(stream)), "spx_sumsq")
+    _count(2)
 
 
 def clip_scale(sumsq_vec, count, max_norm, scale_out, norm_out=None, *, stream=None) -> None:
     _check(load().spx_clip_scale(_ptr(sumsq_vec), count, float(max_norm), _ptr(scale_out), _ptr(norm_out),
                                  _stream(stream)), "spx_clip_scale")
+    _count(1)
 
 
 def adamw(p, g, m, v, p_bf16, *, n, n_decay, lr, beta1, beta2, eps, weight_decay, step, grad_scale=None,
@@ -182,3 +250,4 @@ def adamw(p, g, m, v, p_bf16, *, n, n_decay, lr, beta1, beta2, eps, weight_decay
     _check(load().spx_adamw(_ptr(p), _ptr(g), _ptr(m), _ptr(v), _ptr(p_bf16), n, n_decay, float(lr), float(beta1),
                             float(beta2), float(eps), float(weight_decay), int(step), _ptr(grad_scale),
                             _stream(stream)), "spx_adamw")
+    _count(1)

@@ -466,12 +466,19 @@ class _Planner:
 
 def _exempt(paths: dict, fraction: float) -> set[int]:
     n_ex = math.ceil(len(paths) * fraction)
-    slow = sorted(paths, key=lambda a: (-paths[a].e2e, a))
+    slow = sorted(paths, key=lambda a: (-round(paths[a].e2e, 9), a))
     return set(slow[:n_ex])
 
 
-def _fastest(paths: dict, agents) -> list[int]:
-    return sorted(agents, key=lambda a: (paths[a].e2e, a))
+def _fastest(paths: dict, agents, constraints=()) -> list[int]:
+    """Agents by e2e ascending.  Ties (common on uniform topologies, where every path of the same
+    length costs the same) go to the agent with fewer permanent bans, then the lower id — so the
+    skip budget is spread over agents instead of exhausting one agent's."""
+    bans: dict[int, int] = {}
+    for c in constraints:
+        if c.permanent:
+            bans[c.agent] = bans.get(c.agent, 0) + 1
+    return sorted(agents, key=lambda a: (round(paths[a].e2e, 9), bans.get(a, 0), a))
 
 
 def find_candidates(topology: Topology, assignment: StageAssignment, agents, config: SchedulerConfig,
@@ -501,7 +508,7 @@ def find_candidates(topology: Topology, assignment: StageAssignment, agents, con
         offending = [a for a in node.paths if st in node.paths[a].stages]
         need = len(offending) - cap
         exempt = _exempt(node.paths, config.slow_exempt_fraction)
-        cand = _fastest(node.paths, [a for a in offending if a not in exempt])
+        cand = _fastest(node.paths, [a for a in offending if a not in exempt], node.constraints)
         need = min(need, len(cand))
         if need <= 0:
             continue
@@ -546,7 +553,7 @@ def resolve_throughput(candidates: list[SearchNode], topology: Topology, assignm
         if isinstance(c, NodeOveruse):
             # the slowest path through the node is exempt; the paper's child bans the K−m fastest,
             # further children (cc3_branching) ban the next subsets in speed-rank order
-            through = _fastest(node.paths, [a for a in node.paths if c.node in node.paths[a].nodes])
+            through = _fastest(node.paths, [a for a in node.paths if c.node in node.paths[a].nodes], node.constraints)
             for combo in itertools.islice(itertools.combinations(through[:-1], c.count - c.m),
                                           max(1, config.cc3_branching)):
                 children.append(pl.child(node, [IntervalConstraint(a, c.node, -INF, INF) for a in combo]))

@@ -167,12 +167,9 @@ def test_embedding():
     out = torch.empty(n, d, dtype=torch.bfloat16, device=dev)
     native.embed_fwd(ids, table, out, n=n, d=d)
     dout = bf(torch.randn(n, d, generator=g)).to(dev)
-    perm = torch.argsort(ids_cpu.long() * n + torch.arange(n)).to(torch.int32)
-    sid = ids_cpu[perm.long()]
-    uniq, counts = torch.unique_consecutive(sid, return_counts=True)
-    seg = torch.cat([torch.zeros(1, dtype=torch.int64), counts.cumsum(0)]).to(torch.int32)
+    perm, seg, sid, nseg = native.embed_segments(ids_cpu)
     dtab = torch.zeros(V, d, device=dev)
-    native.embed_bwd(perm.to(dev), seg.to(dev), uniq.to(torch.int32).to(dev), len(uniq), dout, dtab, d=d)
+    native.embed_bwd(perm.to(dev), seg.to(dev), sid.to(dev), nseg.to(dev), n, dout, dtab, d=d)
     torch.cuda.synchronize()
     assert torch.equal(out, table[ids.long()])
     ref = torch.zeros(V, d, device=dev).index_add_(0, ids.long(), dout.float())
