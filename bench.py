@@ -143,10 +143,12 @@ def gemm_roofline(tr, peak_tflops: float, reps: int = 5) -> dict:
     from paper_2502_19913_b200 import native
 
     calls = native.recorded_gemms()
+    counts = tr.gemm_counts_per_step()
     s = tr.streams[tr.devices[0]]
     total_flops, total_ms = 0.0, 0.0
     per = {}
-    for key, (count, fn) in calls.items():
+    for key, (_, fn) in calls.items():
+        count = counts.get(key, 0)
         with torch.cuda.stream(s):
             fn()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

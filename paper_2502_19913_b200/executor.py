@@ -315,6 +315,7 @@ class Trainer:
         self._slot_of = {(op.mb, op.node): op.slot for op in self.ops if op.kind == F}
         self._graphs: dict = {}
         self._graph_launches: dict = {}
+        self._graph_gemms: dict = {}
         self._opt_launches = 0
         self._bwd_out: dict = {}
         self._sumsq = {d: torch.zeros(len(self.psets), dtype=F32, device=torch.device("cuda", d)) for d in self.devices}
@@ -352,9 +353,11 @@ class Trainer:
                 g = torch.cuda.CUDAGraph()
                 s.wait_stream(torch.cuda.current_stream())
                 n0 = native.launches()
+                native.take_gemm_log()
                 with torch.cuda.graph(g, stream=s):
                     out = self._run_op(kind, v, slot, torch.cuda.current_stream())
                 self._graph_launches[(kind, v, slot)] = native.launches() - n0
+                self._graph_gemms[(kind, v, slot)] = native.take_gemm_log()
                 self._graphs[(kind, v, slot)] = g
                 self._bwd_out[(kind, v, slot)] = out
         torch.cuda.synchronize()
@@ -474,6 +477,14 @@ class Trainer:
             self._opt_launch_probe()
             self._opt_launches = native.launches() - n0
         return sum(self._graph_launches[(op.kind, op.node, op.slot)] for op in self.ops) + self._opt_launches
+
+    def gemm_counts_per_step(self) -> dict:
+        """GEMM key -> launches per iteration (recorded at capture when native.record_gemms(True))."""
+        out: dict = {}
+        for op in self.ops:
+            for key in self._graph_gemms.get((op.kind, op.node, op.slot), []):
+                out[key] = out.get(key, 0) + 1
+        return out
 
     def _opt_launch_probe(self):
         # 2 (sumsq) per distinct stage + 1 (clip) + 1 (adamw) per parameter set

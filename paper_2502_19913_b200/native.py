@@ -50,7 +50,7 @@ EPI_BF16, EPI_BF16_RESID, EPI_F32, EPI_SWIGLU = 0, 1, 2, 3
 
 
 # kernel-launch accounting (bench.py "gpu_launches") and GEMM call recording (roofline timing)
-_STATS = {"launches": 0, "record": False, "gemms": {}}
+_STATS = {"launches": 0, "record": False, "gemms": {}, "gemm_log": []}
 
 
 def launches() -> int:
@@ -63,6 +63,13 @@ def _count(n: int) -> None:
 
 def record_gemms(on: bool) -> None:
     _STATS["record"] = bool(on)
+
+
+def take_gemm_log() -> list:
+    """GEMM keys recorded since the last call (the executor tags them per captured graph)."""
+    log = _STATS["gemm_log"]
+    _STATS["gemm_log"] = []
+    return log
 
 
 def recorded_gemms() -> dict:
@@ -141,6 +148,7 @@ def gemm(A, B, C, *, M, N, K, lda, ldb, ldc, a_mn=False, b_mn=False, epilogue=EP
                 _STATS["record"] = rec
 
         _STATS["gemms"][key] = (cnt + 1, again)
+        _STATS["gemm_log"].append(key)
 
 
 def hop(dst, dst_dev: int, src, src_dev: int, nbytes: int, stream=None) -> None:

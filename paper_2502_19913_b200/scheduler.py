@@ -481,6 +481,24 @@ def _fastest(paths: dict, agents, constraints=()) -> list[int]:
     return sorted(agents, key=lambda a: (round(paths[a].e2e, 9), bans.get(a, 0), a))
 
 
+def _cc3_children(pl, node: SearchNode, st: int, cap: int, config: SchedulerConfig,
+                  assignment: StageAssignment) -> list[SearchNode]:
+    """Branch on a CC3 conflict at stage ``st``: ban every node of the stage for K−cap of the
+    offending paths — the fastest non-exempt ones first (Algorithm 2, H2), then further subsets."""
+    offending = [a for a in node.paths if st in node.paths[a].stages]
+    exempt = _exempt(node.paths, config.slow_exempt_fraction)
+    cand = _fastest(node.paths, [a for a in offending if a not in exempt], node.constraints)
+    need = min(len(offending) - cap, len(cand))
+    out = []
+    if need <= 0:
+        return out
+    for combo in itertools.islice(itertools.combinations(cand, need), max(1, config.cc3_branching)):
+        ch = pl.child(node, [IntervalConstraint(a, v, -INF, INF) for a in combo for v in assignment.stage_nodes(st)])
+        if ch is not None:
+            out.append(ch)
+    return out
+
+
 def find_candidates(topology: Topology, assignment: StageAssignment, agents, config: SchedulerConfig,
                     _planner: _Planner | None = None) -> list[SearchNode]:
     """Phase 1: best-first CBS until ``pool_size`` CC3-feasible nodes are collected (H1, H2)."""
@@ -504,19 +522,9 @@ def find_candidates(topology: Topology, assignment: StageAssignment, agents, con
                 seen_sig.add(sig)
                 pool.append(node)
             continue
-        st = over[0]
-        offending = [a for a in node.paths if st in node.paths[a].stages]
-        need = len(offending) - cap
-        exempt = _exempt(node.paths, config.slow_exempt_fraction)
-        cand = _fastest(node.paths, [a for a in offending if a not in exempt], node.constraints)
-        need = min(need, len(cand))
-        if need <= 0:
-            continue
         children = []
-        for combo in itertools.islice(itertools.combinations(cand, need), max(1, config.cc3_branching)):
-            new = [IntervalConstraint(a, v, -INF, INF) for a in combo for v in assignment.stage_nodes(st)]
-            ch = pl.child(node, new)
-            if ch is not None and ch.constraints not in seen_cons:
+        for ch in _cc3_children(pl, node, over[0], cap, config, assignment):
+            if ch.constraints not in seen_cons:
                 seen_cons.add(ch.constraints)
                 children.append(ch)
         for ch in children:
@@ -533,6 +541,7 @@ def resolve_throughput(candidates: list[SearchNode], topology: Topology, assignm
         raise ValidationError("resolve_throughput needs a non-empty candidate list")
     pl = _planner or _Planner(topology, assignment, config)
     m = topology.mem_capacity
+    cap = cc3_cap(len(candidates[0].paths), assignment.s, path_length(assignment.s, config.k))
     open_ = [(c.key(), c) for c in candidates]
     heapq.heapify(open_)
     seen_cons = {c.constraints for c in candidates}
@@ -541,16 +550,19 @@ def resolve_throughput(candidates: list[SearchNode], topology: Topology, assignm
     while open_ and expansions < config.max_expansions:
         _, node = heapq.heappop(open_)
         expansions += 1
-        conf = [c for c in detect_conflicts(node, topology, assignment, m)
-                if isinstance(c, NodeOveruse) or (config.resolve_tc2 and isinstance(c, Collision))]
-        k = (len(conf), node.key())
+        conf = [c for c in detect_conflicts(node, topology, assignment, m, cap=cap)
+                if not isinstance(c, Collision) or config.resolve_tc2]
+        k = (any(isinstance(c, StageOveruse) for c in conf), len(conf), node.key())
         if best is None or k < best_key:
             best, best_key = node, k
         if not conf:
             return node, True
         c = conf[0]
         children = []
-        if isinstance(c, NodeOveruse):
+        if isinstance(c, StageOveruse):
+            # a TC1/TC2 re-route broke CC3: restore it first (SPEC.md:290 holds for every output)
+            children.extend(_cc3_children(pl, node, c.stage, cap, config, assignment))
+        elif isinstance(c, NodeOveruse):
             # the slowest path through the node is exempt; the paper's child bans the K−m fastest,
             # further children (cc3_branching) ban the next subsets in speed-rank order
             through = _fastest(node.paths, [a for a in node.paths if c.node in node.paths[a].nodes], node.constraints)

@@ -1,0 +1,126 @@
+"""Allocation (Eq. 1 stage sizes, GA clustering, exact closed TSP) — SPEC.md:142-196 KATs."""
+
+import itertools
+
+import numpy as np
+import pytest
+
+from paper_2502_19913_b200.allocation import (GAConfig, StageAssignment, cluster_nodes, order_stages,
+                                              partition_fitness, solve_closed_tsp, stage_sizes, tour_cost)
+from paper_2502_19913_b200.baselines import compensate, dtfm_full
+from paper_2502_19913_b200.configs import get_config
+from paper_2502_19913_b200.errors import ValidationError
+from paper_2502_19913_b200.simulator import simulate
+from paper_2502_19913_b200.topology import Topology, b200_box
+
+
+def test_stage_sizes_kats():
+    # SPEC.md:148-150, acceptance 1
+    assert stage_sizes(18, 4, 25) == [6, 4, 4, 4]
+    assert stage_sizes(20, 6, 100 / 3) == [5, 3, 3, 3, 3, 3]
+    assert stage_sizes(16, 4, 0) == [4, 4, 4, 4]
+
+
+def test_stage_sizes_errors():
+    with pytest.raises(ValidationError, match="nearest feasible node counts: \\[9\\]"):
+        stage_sizes(8, 4, 25)                       # no integral solution at n=8
+    with pytest.raises(ValidationError):
+        stage_sizes(18, 4, 75)                      # k too large
+    with pytest.raises(ValidationError):
+        stage_sizes(18, 1, 0)
+
+
+def brute_force_tsp(w):
+    s = w.shape[0]
+    best = None
+    for rest in itertools.permutations(range(1, s)):
+        t = [0, *rest]
+        c = tour_cost(w, t)
+        if best is None or c < best[1] - 1e-12:
+            best = (t, c)
+    return best
+
+
+def test_tsp_kat_and_bruteforce():
+    w = np.array([[0, 1, 10], [1, 0, 1], [10, 1, 0.0]])
+    assert solve_closed_tsp(w) == ([0, 1, 2], 12.0)
+    rng = np.random.default_rng(0)
+    for _ in range(30):
+        s = int(rng.integers(3, 8))
+        pts = rng.uniform(0, 10, size=s)
+        w = np.abs(pts[:, None] - pts[None, :])
+        tour, cost = solve_closed_tsp(w)
+        bt, bc = brute_force_tsp(w)
+        assert cost == pytest.approx(bc)
+        assert tour_cost(w, tour) == pytest.approx(bc)
+    # uniform costs -> lexicographically smallest tour
+    assert solve_closed_tsp(np.ones((5, 5)) - np.eye(5))[0] == [0, 1, 2, 3, 4]
+
+
+def test_tsp_bound():
+    with pytest.raises(ValidationError):
+        solve_closed_tsp(np.ones((13, 13)))
+
+
+def _two_regions(n_per=4, intra=1.0, inter=100.0):
+    n = 2 * n_per
+    lat = np.full((n, n), inter)
+    for r in range(2):
+        lat[r * n_per:(r + 1) * n_per, r * n_per:(r + 1) * n_per] = intra
+    np.fill_diagonal(lat, 0.0)
+    bw = np.full((n, n), 1e12)
+    return Topology(n=n, latency_ms=lat, bandwidth_bytes_per_ms=bw, compute_fwd_ms=np.ones(n))
+
+
+def test_cluster_nodes_regions_and_determinism():
+    # SPEC.md:158 (reduced 8-node version): clusters never mix regions when sizes allow
+    T = _two_regions()
+    cfg = GAConfig(population=32, generations=60, seed=1)
+    mem = cluster_nodes(T, [4, 2, 2], cfg)
+    assert sorted(v for m in mem for v in m) == list(range(8))
+    assert [len(m) for m in mem] == [4, 2, 2]
+    assert partition_fitness(T, mem) == pytest.approx(1.0 + 1e8 / 1e12)
+    assert cluster_nodes(T, [4, 2, 2], cfg) == mem
+
+
+def test_order_stages_designates_largest_s0():
+    T = _two_regions()
+    mem = [[4, 5], [0, 1, 2, 3], [6, 7]]
+    a = order_stages(T, mem, 1e6)
+    assert a.order[0] == 1 and a.stage_nodes(0) == [0, 1, 2, 3]
+    assert sorted(a.order) == [0, 1, 2]
+
+
+def test_assignment_json_roundtrip(tmp_path):
+    a = StageAssignment.contiguous([2, 2, 2, 2])
+    p = tmp_path / "a.json"
+    a.save(p)
+    assert StageAssignment.load(p) == a
+    with pytest.raises(ValidationError):
+        StageAssignment(s=2, sizes=[1, 1], members=[[0], [0]], order=[0, 1])
+
+
+def test_dtfm_full_disjoint_pipelines():
+    # SPEC.md:413-414
+    T = b200_box([1.0] * 16, mem_capacity=1)
+    sch = dtfm_full(T, 4, msg_bytes=1e6, assignment=StageAssignment.contiguous([4, 4, 4, 4]))
+    chains = [p.nodes for p in sch.paths.values()]
+    assert all(len(c) == 4 for c in chains)
+    assert sorted(v for c in chains for v in c) == list(range(16))
+    assert len({round(p.e2e, 9) for p in sch.paths.values()}) == 1
+
+
+def test_skippipe_beats_full_pipeline_in_simulation():
+    # the metric's comparison on the B200 box (C2 vs the same config at k=0)
+    a, b = get_config("C2"), get_config("C2-full")
+    ra = simulate(a.schedule(), a.topology(), a.sim_config())
+    rb = simulate(b.schedule(), b.topology(), b.sim_config())
+    assert ra.iteration_makespan < rb.iteration_makespan
+
+
+def test_compensate_kats():
+    assert compensate(18.0, 18, 20) == pytest.approx(16.2)
+    assert compensate(10.0, 16, 18) == pytest.approx(8.888888888)
+    assert compensate(7.0, 5, 5) == 7.0
+    with pytest.raises(ValidationError):
+        compensate(1.0, 0, 5)

@@ -1,0 +1,224 @@
+"""Scheduler (A* + two-phase CBS) against the SPEC known-answer tests and the exhaustive route
+enumerator oracle (acceptance criteria 2, 3, 6, 7)."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle.path_enum import _valid_cc2, best_route
+from paper_2502_19913_b200 import scheduler as S
+from paper_2502_19913_b200.allocation import StageAssignment
+from paper_2502_19913_b200.errors import InfeasibleError, ValidationError
+from paper_2502_19913_b200.topology import Topology, b200_box, comm_matrix
+
+
+def line_instance(n=4, compute=10.0, hop=5.0, m=1):
+    return Topology(n=n, latency_ms=np.full((n, n), hop), bandwidth_bytes_per_ms=np.full((n, n), 1e18),
+                    compute_fwd_ms=np.full(n, compute), mem_capacity=m)
+
+
+def test_astar_line_instance_160():
+    # forward (4x10 + 4x5) + backward (4x20 + 4x5) = 160 ms
+    T = line_instance()
+    A = StageAssignment.contiguous([1, 1, 1, 1])
+    p = S.astar_path(S.Agent(0, 0), T, A, (), S.SchedulerConfig(k=0, msg_bytes=1.0))
+    assert p.e2e == 160.0
+    assert p.nodes == (0, 1, 2, 3) and p.visits[0].node == p.visits[-1].node == 0
+
+
+def test_astar_visits_exactly_l_stages():
+    # s=6, k=100/3 -> 4 stages incl. S0
+    T = b200_box([1.0] * 6)
+    A = StageAssignment.contiguous([1] * 6)
+    p = S.astar_path(S.Agent(0, 0), T, A, (), S.SchedulerConfig(k=100 / 3, msg_bytes=1e6))
+    assert len(p.stages) == 4 and p.stages[0] == 0 and len(set(p.stages)) == 4
+
+
+def _random_instance(rng, n_max=8, s_max=4):
+    s = int(rng.integers(2, s_max + 1))
+    sizes = [1] + [int(x) for x in rng.integers(1, 3, size=s - 1)]
+    while sum(sizes) > n_max:
+        sizes[int(np.argmax(sizes))] -= 1
+    n = sum(sizes)
+    lat = rng.uniform(1, 20, size=(n, n))
+    bw = rng.uniform(1e5, 1e6, size=(n, n))
+    comp = rng.uniform(5, 50, size=n)
+    T = Topology(n=n, latency_ms=lat, bandwidth_bytes_per_ms=bw, compute_fwd_ms=comp, bwd_ratio=float(rng.uniform(1, 3)))
+    A = StageAssignment.contiguous(sizes)
+    l = int(rng.integers(2, s + 1))
+    k = 100 * (s - l) / s
+    return T, A, k, l
+
+
+def test_astar_equals_exhaustive_on_200_instances():
+    # A* e2e equals exhaustive enumeration exactly on <= 8 nodes / <= 4 stages
+    rng = np.random.default_rng(2024)
+    for _ in range(200):
+        T, A, k, l = _random_instance(rng)
+        cfg = S.SchedulerConfig(k=k, msg_bytes=1e6)
+        p = S.astar_path(S.Agent(0, 0), T, A, (), cfg)
+        cm = comm_matrix(T, 1e6)
+        fwd = T.compute_fwd_ms
+        bwd = fwd * T.bwd_ratio
+        want, nodes = best_route(0, [A.stage_nodes(i) for i in range(A.s)], l, fwd, bwd, cm)
+        assert p.e2e == pytest.approx(want, rel=1e-12, abs=1e-9)
+        assert _valid_cc2(p.stages)
+
+
+def test_astar_constraint_avoids_node_and_stays_optimal():
+    # permanent ban on the fastest route's node
+    rng = np.random.default_rng(7)
+    for _ in range(40):
+        T, A, k, l = _random_instance(rng)
+        cfg = S.SchedulerConfig(k=k, msg_bytes=1e6)
+        p = S.astar_path(S.Agent(0, 0), T, A, (), cfg)
+        if len(p.nodes) < 2:
+            continue
+        x = p.nodes[1]
+        alt = [v for v in A.stage_nodes(p.stages[1]) if v != x]
+        cons = [S.IntervalConstraint(0, x, -math.inf, math.inf)]
+        cm = comm_matrix(T, 1e6)
+        want, _ = best_route(0, [A.stage_nodes(i) for i in range(A.s)], l, T.compute_fwd_ms,
+                             T.compute_fwd_ms * T.bwd_ratio, cm, banned={x})
+        if want == math.inf:
+            with pytest.raises(InfeasibleError):
+                S.astar_path(S.Agent(0, 0), T, A, cons, cfg)
+            continue
+        q = S.astar_path(S.Agent(0, 0), T, A, cons, cfg)
+        assert x not in q.nodes
+        assert q.e2e == pytest.approx(want)
+        assert q.e2e >= p.e2e  # monotonicity
+        assert alt is not None
+
+
+def test_interval_constraint_defers_entry():
+    T = line_instance()
+    A = StageAssignment.contiguous([1, 1, 1, 1])
+    cfg = S.SchedulerConfig(k=0, msg_bytes=1.0)
+    win = {1: [(12.0, 30.0)]}
+    p = S.astar_path(S.Agent(0, 0), T, A, [S.IntervalConstraint(0, 1, 12.0, 30.0)], cfg)
+    v1 = next(v for v in p.visits[:-1] if v.node == 1)
+    assert not (v1.start < 30.0 and 12.0 < v1.end)          # entry deferred out of the window
+    want, _ = best_route(0, [[0], [1], [2], [3]], 4, T.compute_fwd_ms, T.compute_fwd_ms * 2,
+                         comm_matrix(T, 1.0), windows=win)
+    assert p.e2e == pytest.approx(want)
+    # with the swap forbidden by a second window the agent must wait at node 1 until 30
+    q = S.astar_path(S.Agent(0, 0), T, A, [S.IntervalConstraint(0, 1, 12.0, 30.0),
+                                            S.IntervalConstraint(0, 2, 0.0, 1000.0)], cfg)
+    assert q.e2e > p.e2e
+
+
+def test_cc2_rule():
+    assert S.cc2_extend((0, 2), 0, 1) == 1        # one adjacent transposition
+    assert S.cc2_extend((0, 2, 1), 1, 3) == 1     # continue increasing after the swap
+    assert S.cc2_extend((0, 2, 1), 1, 0) is None  # revisit
+    assert S.cc2_extend((0, 3, 1), 1, 2) is None  # second descent
+    assert S.cc2_extend((0, 1), 0, 3) == 0
+    assert S.cc2_extend((0,), 0, 2) == 0
+
+
+def test_detect_conflicts_kats():
+    # SPEC.md:274-276
+    T = b200_box([1.0] * 5, mem_capacity=2)
+    A = StageAssignment.contiguous([2, 1, 1, 1])
+
+    def plan(agent, nodes, starts, dur=10.0):
+        vis = tuple(S.Visit(v, A.node_stage()[v], st, st, st + dur) for v, st in zip(nodes, starts))
+        ret = S.Visit(nodes[0], 0, 100.0, 100.0, 100.0)
+        return S.PathPlan(agent, vis + (ret,), (), 0, 200.0 + agent)
+
+    paths = {0: plan(0, [0, 2], [0, 10]), 1: plan(1, [1, 3], [0, 15])}
+    node = S.SearchNode(frozenset(), paths, 201.0)
+    assert S.detect_conflicts(node, T, A, 2) == []
+    paths = {0: plan(0, [0, 2], [0, 10]), 1: plan(1, [1, 2], [0, 15]), 2: plan(2, [0, 2], [30, 40])}
+    confs = S.detect_conflicts(S.SearchNode(frozenset(), paths, 202.0), T, A, 2)
+    over = [c for c in confs if isinstance(c, S.NodeOveruse)]
+    assert over == [S.NodeOveruse(2, 3, 2)]
+    cols = [c for c in confs if isinstance(c, S.Collision) and c.node == 2]
+    assert any(c.overlap == (15.0, 20.0) for c in cols)
+
+
+def _check_schedule(sch, T, A, k, check_tc=True):
+    l = S.path_length(A.s, k)
+    paths = sch.paths
+    for p in paths.values():
+        assert p.visits[0].node == p.visits[-1].node                # starts and ends at origin
+        assert p.stages[0] == 0 and len(p.stages) == l               # CC1, exact l
+        assert len(set(p.stages)) == l and _valid_cc2(p.stages)      # CC2
+    counts = S.stage_visit_counts(paths, A)[1:]
+    assert max(counts) <= S.cc3_cap(len(paths), A.s, l)              # CC3 cap
+    if sch.resolved and check_tc:
+        assert max(S.node_path_counts(paths, T.n)) <= T.mem_capacity  # TC1
+        node = S.SearchNode(frozenset(sch.constraints), paths, sch.cost_ms)
+        assert not [c for c in S.detect_conflicts(node, T, A, T.mem_capacity) if isinstance(c, S.Collision)]
+
+
+def test_b200_c2_schedule_constraints():
+    T = b200_box([0.8, 0.8] + [0.5] * 6)
+    A = StageAssignment.contiguous([2, 2, 2, 2])
+    sch = S.schedule(T, A, S.SchedulerConfig(k=25))
+    assert sch.resolved
+    _check_schedule(sch, T, A, 25)
+
+
+def test_schedule_homogeneous_full_pipeline():
+    # homogeneous 16 nodes, s=4, k=0, m=1 -> |S0| parallel sequential pipelines
+    T = b200_box([1.0] * 16, mem_capacity=1)
+    A = StageAssignment.contiguous([4, 4, 4, 4])
+    sch = S.schedule(T, A, S.SchedulerConfig(k=0, msg_bytes=9e8))
+    assert sch.resolved
+    hop = T.latency_ms[0, 1] + 9e8 / T.bandwidth_bytes_per_ms[0, 1]
+    analytic = 4 * 1.0 + 4 * hop + 4 * 2.0 + 4 * hop
+    assert sch.cost_ms == pytest.approx(analytic)
+    used = [p.nodes for p in sch.paths.values()]
+    assert sorted(v for ns in used for v in ns) == list(range(16))   # disjoint pipelines
+
+
+def test_pool_bounded_and_deterministic():
+    T = b200_box([1.0, 1.0] + [0.6] * 6)
+    A = StageAssignment.contiguous([2, 2, 2, 2])
+    cfg = S.SchedulerConfig(k=25, pool_size=32)
+    pool = S.find_candidates(T, A, None, cfg)
+    assert 1 <= len(pool) <= 32
+    a = S.schedule(T, A, cfg).dumps()
+    b = S.schedule(T, A, cfg).dumps()
+    assert a == b
+
+
+def test_schedule_json_roundtrip(tmp_path):
+    T = b200_box([1.0, 1.0] + [0.6] * 6)
+    A = StageAssignment.contiguous([2, 2, 2, 2])
+    sch = S.schedule(T, A, S.SchedulerConfig(k=25))
+    p = tmp_path / "s.json"
+    sch.save(p)
+    back = S.Schedule.load(p)
+    assert back.dumps() == sch.dumps()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_constraint_suite_sampled(seed):
+    # SPEC.md:533 (reduced count for the CPU suite): every emitted schedule satisfies CC1-CC3,
+    # resolved ones also TC1 and zero planned collisions
+    from paper_2502_19913_b200.topology import TopologyProfile, sample_topology
+
+    rng = np.random.default_rng(seed)
+    s = int(rng.choice([4, 6]))
+    k = 25 if s == 4 else 100 / 3
+    sizes = [3, 2, 2, 2] if s == 4 else [2, 1, 1, 1, 1, 1]
+    prof = TopologyProfile(regions=2, nodes_per_region=sum(sizes) // 2 + 1, seed=seed)
+    T = sample_topology(prof).restrict(list(range(sum(sizes))))
+    A = StageAssignment.contiguous(sizes)
+    cfg = S.SchedulerConfig(k=k, msg_bytes=1e6, max_expansions=300)
+    try:
+        sch = S.schedule(T, A, cfg)
+    except InfeasibleError:
+        pytest.skip("no CC3-feasible candidate under the expansion budget")
+    _check_schedule(sch, T, A, k)
+
+
+def test_path_length_validation():
+    assert S.path_length(4, 25) == 3
+    assert S.path_length(6, 100 / 3) == 4
+    with pytest.raises(ValidationError):
+        S.path_length(8, 100 / 3)
