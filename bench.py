@@ -144,7 +144,7 @@ def gemm_roofline(tr, peak_tflops: float, reps: int = 5) -> dict:
 
     calls = native.recorded_gemms()
     counts = tr.gemm_counts_per_step()
-    s = tr.streams[tr.devices[0]]
+    s = tr.stream
     total_flops, total_ms = 0.0, 0.0
     per = {}
     for key, (_, fn) in calls.items():
@@ -178,15 +178,12 @@ def run_ours(args, rc):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
-        from paper_2502_19913_b200.dist_trainer import run_bench_dist
-
-        return run_bench_dist(args, rc)
+        return run_ours_dist(args, rc)
     torch.cuda.set_device(0)
     burst, sustained, hbm, peak_kind = _peaks()
     tokens = synthetic_tokens(rc.model, rc.M, rc.b, rc.T, seed=1234)
     native.record_gemms(True)
-    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T,
-                 placement=[0] * rc.topology().n)
+    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T)
     native.record_gemms(False)
     launches = tr.launches_per_step()
     host = tr._stage_inputs(tokens)
@@ -196,7 +193,7 @@ def run_ours(args, rc):
     for _ in range(args.warmup):
         tr.step(dev_inputs)
     torch.cuda.synchronize()
-    s = tr.streams[0]
+    s = tr.stream
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:
         torch.cuda.synchronize()
@@ -237,6 +234,90 @@ def run_ours(args, rc):
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
+
+
+def run_ours_dist(args, rc):
+    """N>1: torchrun, one process per GPU.  Logical nodes are placed rank = node mod N; hops
+    between ranks are NCCL P2P over NVLink, replicated stages are all-reduced per stage group.
+    Total work per step is the fixed C2 iteration (strong scaling); time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_19913_b200 import native
+    from paper_2502_19913_b200.executor import Trainer
+    from paper_2502_19913_b200.model import synthetic_tokens
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch with torchrun --nproc-per-node {args.gpus}")
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    burst, sustained, hbm, peak_kind = _peaks()
+    tokens = synthetic_tokens(rc.model, rc.M, rc.b, rc.T, seed=1234)
+    native.record_gemms(True)
+    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T,
+                 rank=rank, world=world, device=local)
+    native.record_gemms(False)
+    launches = torch.tensor([tr.launches_per_step()], device=tr.dev)
+    dist.all_reduce(launches)
+    host = tr._stage_inputs(tokens)
+    dev_inputs = {k: v.cuda() for k, v in host.items()}
+    for _ in range(args.warmup):
+        tr.step(dev_inputs)
+    torch.cuda.synchronize()
+    s = tr.stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(args.steps):
+            res = tr.step(dev_inputs)
+        e1.record(s)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms_local], device=tr.dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    tok = rc.M * rc.tokens_per_mb
+    # e2e through the public API with host tokens
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        tr.step(tokens)
+    torch.cuda.synchronize()
+    e2e_local = (time.perf_counter() - t0) * 1e3 / args.steps
+    t = torch.tensor([e2e_local, float(tr.h2d_bytes(tokens))], device=tr.dev)
+    mx = t.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = t.clone()
+    dist.all_reduce(sm)
+    flops = rc.train_flops()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(tok / (ms / 1e3), 1), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": rc.name, "model": rc.model.name, "global_batch": rc.M * rc.b, "seq_len": rc.T,
+                       "microbatches": rc.M, "tokens_per_step": tok, "stages": rc.s, "replicas": rc.sizes,
+                       "skip_pct": rc.k, "m": rc.m, "placement": tr.placement,
+                       "parallelism": f"pp-skip({rc.s}x{rc.sizes[0]} logical nodes over {world} GPUs)+dp-allreduce",
+                       "l2_flush": "inputs+activations per step >> 126 MB L2", "kind": rc.kind},
+            "loss": round(res["loss"], 5),
+            "e2e": {"value": round(tok / (float(mx[0].item()) / 1e3), 1), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(sm[1].item()), "d2h_bytes_per_step": 4 * rc.M},
+            "gpu_launches": int(launches.item()),
+            "step_tflops": round(flops / (ms / 1e3) / 1e12, 1),
+            "step_tensor_frac": round(flops / (ms / 1e3) / 1e12 / (sustained * world), 4),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def main():

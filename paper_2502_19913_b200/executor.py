@@ -249,22 +249,42 @@ class StageProgram:
 # ---------------------------------------------------------------------------------------
 # the trainer
 # ---------------------------------------------------------------------------------------
-def default_placement(n_nodes: int, n_gpus: int) -> list[int]:
-    """Logical node i -> GPU i mod n_gpus (contiguous stage numbering makes this spread each
-    stage's replicas over different GPUs when n_gpus divides the replica count)."""
-    return [i % n_gpus for i in range(n_nodes)]
+def default_placement(n_nodes: int, n_ranks: int) -> list[int]:
+    """Logical node i -> rank i mod n_ranks.  With contiguous stage numbering (stage st = nodes
+    [st·r, (st+1)·r)) this puts the replicas of a stage on different ranks and gives every rank
+    the same mix of S₀ and non-S₀ nodes (S₀ is the heavy stage)."""
+    return [i % n_ranks for i in range(n_nodes)]
+
+
+def static_slots(schedule: Schedule, n_nodes: int) -> tuple[dict, list[int]]:
+    """Activation slot of every (agent, node): the agent's rank among the agents whose path visits
+    the node.  A slot is then only ever reused by the *same* agent's next wave, which launches
+    after the previous wave's backward has left every node of the path, so a
+    path hop may write its destination slot as soon as the producer op is done, without racing
+    the previous owner.  Under TC1 (≤ m paths per node) this needs ≤ m slots per node."""
+    users: dict[int, list[int]] = {v: [] for v in range(n_nodes)}
+    for a in sorted(schedule.paths):
+        for v in schedule.paths[a].nodes:
+            users[v].append(a)
+    slot_of = {(a, v): users[v].index(a) for v in users for a in users[v]}
+    return slot_of, [max(1, len(users[v])) for v in range(n_nodes)]
 
 
 class Trainer:
-    """Holds weights, optimizer state, activation slots and captured graphs for one config.
+    """Weights, optimizer state, activation slots and captured graphs for one config on one rank.
 
-    Single process; all logical nodes placed on this process's devices.  (The multi-process
-    NVLink/NCCL path is ``dist_trainer.DistTrainer``.)"""
+    ``rank``/``world``: one process per GPU (torch.distributed, NCCL).  ``placement[v]`` is the
+    rank that hosts logical node v.  Every rank builds the same schedule and simulator op list and
+    walks it in the same global order: it runs the ops of its own nodes, sends a path hop to the
+    rank of the next node (NCCL P2P over NVLink; a local ``spx_hop`` copy when both nodes are
+    on this rank) and posts the matching receive for hops that target its nodes.  With world=1
+    (the default) everything is on cuda:<device> and every hop is a local copy."""
 
     def __init__(self, schedule: Schedule, topology: Topology, sim_config: SimConfig, cfg: ModelConfig,
                  assignment, *, b: int, T: int | None = None, split: list[int] | None = None,
                  placement: list[int] | None = None, seed: int = 0, optim: OptimConfig | None = None,
-                 use_graphs: bool = True, params: list | None = None):
+                 use_graphs: bool = True, params: list | None = None, rank: int = 0, world: int = 1,
+                 device: int | None = None):
         if not torch.cuda.is_available():
             raise native.NativeError("the executor needs a CUDA device (there is no CPU fallback)")
         native.load()
@@ -277,92 +297,111 @@ class Trainer:
         self.split = layer_split(cfg, assignment.s, split)
         self.optim = optim or OptimConfig()
         self.node_stage = assignment.node_stage()
-        self.placement = placement or [0] * topology.n
-        if len(self.placement) != topology.n:
-            raise ValidationError(f"placement has {len(self.placement)} entries for {topology.n} nodes")
-        self.devices = sorted(set(self.placement))
+        self.rank, self.world = rank, world
+        self.placement = list(placement) if placement is not None else default_placement(topology.n, world)
+        if len(self.placement) != topology.n or max(self.placement) >= world:
+            raise ValidationError(f"placement {self.placement} does not map {topology.n} nodes onto {world} ranks")
+        self.dev = torch.device("cuda", rank if device is None else device)
         self.report: SimReport = simulate(schedule, topology, sim_config)
         self.ops = self.report.ops
         self.step_count = 0
         self.use_graphs = use_graphs
         self.agents = sorted(a.id for a in schedule.agents)
         self.paths = {a: schedule.paths[a].nodes for a in self.agents}
+        self.slot_of, self.n_slots = static_slots(schedule, topology.n)
+        self.my_nodes = [v for v in range(topology.n) if self.placement[v] == rank]
+        self.my_stages = sorted({self.node_stage[v] for v in self.my_nodes})
+        self.stage_ranks = {st: sorted({self.placement[v] for v in range(topology.n) if self.node_stage[v] == st})
+                            for st in range(assignment.s)}
 
-        # parameter sets: one per (stage, device)
-        canon = params if params is not None else init_params(cfg, self.split, seed)
-        self.layouts = [stage_layout(cfg, st, self.split) for st in range(assignment.s)]
-        self.psets: dict[tuple[int, int], ParamSet] = {}
-        for v in range(topology.n):
-            st, dev = self.node_stage[v], self.placement[v]
-            if (st, dev) not in self.psets:
-                flat = pack_stage(cfg, self.layouts[st], canon[st])
-                self.psets[(st, dev)] = ParamSet(cfg, self.layouts[st], flat, torch.device("cuda", dev))
-        # activation slots per node
-        m = topology.mem_capacity
-        self.slots: dict[tuple[int, int], SlotBuffers] = {}
-        for v in range(topology.n):
-            dev = torch.device("cuda", self.placement[v])
-            for j in range(m):
-                self.slots[(v, j)] = SlotBuffers(cfg, self.split[self.node_stage[v]], self.node_stage[v] == 0,
-                                                 self.n, b, self.T, dev)
-        self.scratch = {d: Scratch(cfg, self.n, b, self.T, torch.device("cuda", d),
-                                   with_head=any(self.node_stage[v] == 0 and self.placement[v] == d
-                                                 for v in range(topology.n)))
-                        for d in self.devices}
-        self.streams = {d: torch.cuda.Stream(device=d) for d in self.devices}
-        self.prog = StageProgram(cfg, self.n, b, self.T, self.M)
-        self.mb_loss = torch.zeros(self.M, dtype=F32, device=torch.device("cuda", self.devices[0]))
-        self._slot_of = {(op.mb, op.node): op.slot for op in self.ops if op.kind == F}
+        with torch.cuda.device(self.dev):
+            canon = params if params is not None else init_params(cfg, self.split, seed)
+            self.layouts = [stage_layout(cfg, st, self.split) for st in range(assignment.s)]
+            # one parameter set per stage hosted here (co-resident replicas share it)
+            self.psets = {st: ParamSet(cfg, self.layouts[st], pack_stage(cfg, self.layouts[st], canon[st]), self.dev)
+                          for st in self.my_stages}
+            self.slots: dict[tuple[int, int], SlotBuffers] = {}
+            for v in self.my_nodes:
+                for j in range(self.n_slots[v]):
+                    self.slots[(v, j)] = SlotBuffers(cfg, self.split[self.node_stage[v]], self.node_stage[v] == 0,
+                                                     self.n, b, self.T, self.dev)
+            self.scratch = Scratch(cfg, self.n, b, self.T, self.dev, with_head=0 in self.my_stages)
+            self.stream = torch.cuda.Stream(device=self.dev)
+            self.recv_stream = torch.cuda.Stream(device=self.dev)
+            self.prog = StageProgram(cfg, self.n, b, self.T, self.M)
+            self.mb_loss = torch.zeros(self.M, dtype=F32, device=self.dev)
+            self._sumsq = torch.zeros(assignment.s, dtype=F32, device=self.dev)
+            self._sumsq_ws = torch.empty(native.sumsq_ws_floats(), dtype=F32, device=self.dev)
+            self._clip = torch.ones(1, dtype=F32, device=self.dev)
+            self._norm = torch.zeros(1, dtype=F32, device=self.dev)
         self._graphs: dict = {}
         self._graph_launches: dict = {}
         self._graph_gemms: dict = {}
         self._opt_launches = 0
-        self._bwd_out: dict = {}
-        self._sumsq = {d: torch.zeros(len(self.psets), dtype=F32, device=torch.device("cuda", d)) for d in self.devices}
-        self._sumsq_ws = {d: torch.empty(native.sumsq_ws_floats(), dtype=F32, device=torch.device("cuda", d))
-                          for d in self.devices}
-        self._clip = {d: torch.ones(1, dtype=F32, device=torch.device("cuda", d)) for d in self.devices}
-        self._norm = {d: torch.zeros(1, dtype=F32, device=torch.device("cuda", d)) for d in self.devices}
-        for a in self.devices:
-            for c in self.devices:
-                if a != c:
-                    native.enable_peer_access(a, c)
+        self._outs: dict = {}
+        self._groups: dict = {}
+        if world > 1:
+            self._init_comm()
         if use_graphs:
             self._capture_all()
 
+    # ---- communication setup (multi-process) ----
+    def _init_comm(self):
+        import torch.distributed as dist
+
+        # one NCCL group per replicated stage, created in the same order on every rank
+        for st in range(self.assignment.s):
+            ranks = self.stage_ranks[st]
+            if len(ranks) > 1:
+                g = dist.new_group(ranks)
+                if self.rank in ranks:
+                    self._groups[st] = g
+        # bring up the pairwise P2P channels in one global order (lexicographic over rank pairs),
+        # so lazy communicator creation can never form a wait cycle
+        buf = torch.zeros(1, device=self.dev)
+        for a in range(self.world):
+            for b_ in range(a + 1, self.world):
+                if self.rank == a:
+                    dist.send(buf, b_)
+                    dist.recv(buf, b_)
+                elif self.rank == b_:
+                    dist.recv(buf, a)
+                    dist.send(buf, a)
+        torch.cuda.synchronize(self.dev)
+
     # ---- graph capture ----
     def _run_op(self, kind: str, v: int, slot: int, s):
-        dev = self.placement[v]
-        ps = self.psets[(self.node_stage[v], dev)]
+        ps = self.psets[self.node_stage[v]]
         sb = self.slots[(v, slot)]
-        sc = self.scratch[dev]
         origin = self.node_stage[v] == 0
         if kind == F:
-            self.prog.fwd(ps, sb, sc, origin, s)
+            self.prog.fwd(ps, sb, self.scratch, origin, s)
             return sb.xs[-1]
         if kind == L:
-            return self.prog.loss(ps, sb, sc, s)
-        return self.prog.bwd(ps, sb, sc, origin, s)
+            return self.prog.loss(ps, sb, self.scratch, s)
+        return self.prog.bwd(ps, sb, self.scratch, origin, s)
+
+    def _key(self, op):
+        return (op.kind, op.node, self.slot_of[(op.agent, op.node)])
 
     def _capture_all(self):
-        keys = sorted({(op.kind, op.node, op.slot) for op in self.ops})
-        for kind, v, slot in keys:
-            dev = self.placement[v]
-            with torch.cuda.device(dev):
-                s = self.streams[dev]
+        keys = sorted({self._key(op) for op in self.ops if self.placement[op.node] == self.rank})
+        with torch.cuda.device(self.dev):
+            for key in keys:
+                kind, v, slot = key
                 g = torch.cuda.CUDAGraph()
-                s.wait_stream(torch.cuda.current_stream())
+                self.stream.wait_stream(torch.cuda.current_stream())
                 n0 = native.launches()
                 native.take_gemm_log()
-                with torch.cuda.graph(g, stream=s):
+                with torch.cuda.graph(g, stream=self.stream):
                     out = self._run_op(kind, v, slot, torch.cuda.current_stream())
-                self._graph_launches[(kind, v, slot)] = native.launches() - n0
-                self._graph_gemms[(kind, v, slot)] = native.take_gemm_log()
-                self._graphs[(kind, v, slot)] = g
-                self._bwd_out[(kind, v, slot)] = out
-        torch.cuda.synchronize()
+                self._graph_launches[key] = native.launches() - n0
+                self._graph_gemms[key] = native.take_gemm_log()
+                self._graphs[key] = g
+                self._outs[key] = out
+            torch.cuda.synchronize(self.dev)
 
-    # ---- one iteration ----
+    # ---- inputs ----
     def _stage_inputs(self, tokens: torch.Tensor):
         """Pinned host copies of ids / targets / embedding-backward segments for every microbatch."""
         M, b, T1 = tokens.shape
@@ -377,183 +416,207 @@ class Trainer:
                 "n_seg": pin(torch.stack([s_[3] for s_ in segs]))}
 
     def h2d_bytes(self, tokens: torch.Tensor) -> int:
-        M = tokens.shape[0]
-        n = self.n
-        return M * 4 * (n + n + n + (n + 1) + n + 1)
+        """Bytes of token-derived inputs this rank copies host->device per iteration."""
+        per = 4 * (self.n + self.n + self.n + (self.n + 1) + self.n + 1)
+        mine = sum(1 for op in self.ops if op.kind == F and op.pos == 0 and self.placement[op.node] == self.rank)
+        return mine * per
 
-    def step(self, tokens: torch.Tensor, *, timing: bool = False) -> dict:
-        """One synchronous training iteration over M microbatches.  Returns loss (host float)."""
+    # ---- hops ----
+    def _hop_dst(self, op):
+        """(destination node, buffer name) of the op's output hop, or None (end of path)."""
+        nodes = self.paths[op.agent]
+        last = len(nodes) - 1
+        if op.kind == F:
+            return (nodes[op.pos + 1], "xs0") if op.pos < last else (nodes[0], "ret")
+        if op.kind == L:
+            return nodes[last], "gin"
+        return (nodes[op.pos - 1], "gin") if op.pos > 0 else None
+
+    def _dst_buffer(self, op, nv, name):
+        sb = self.slots[(nv, self.slot_of[(op.agent, nv)])]
+        return sb.xs[0] if name == "xs0" else getattr(sb, name)
+
+    # ---- one iteration ----
+    def step(self, tokens, *, timing: bool = False) -> dict:
+        """One synchronous training iteration over the M microbatches; returns the loss."""
         host = tokens if isinstance(tokens, dict) else self._stage_inputs(tokens)
         self.step_count += 1
-        dev0 = self.devices[0]
+        s = self.stream
         ev = {}
         t_iter0 = torch.cuda.Event(enable_timing=True)
         t_iter1 = torch.cuda.Event(enable_timing=True)
-        for d in self.devices:
-            self.streams[d].wait_stream(torch.cuda.current_stream(d))
-        t_iter0.record(self.streams[dev0])
-        for (st, d), ps in self.psets.items():
-            with torch.cuda.stream(self.streams[d]):
-                ps.g.zero_()
-        executed = []
-        for op in self.ops:
-            v, slot, mb = op.node, op.slot, op.mb
-            dev = self.placement[v]
-            s = self.streams[dev]
-            sb = self.slots[(v, slot)]
-            if op.kind == F and op.pos == 0:
-                _h2d(sb.ids, host["ids"][mb], s)
-            if op.kind == L:
-                _h2d(sb.targets, host["tgt"][mb], s)
-            if op.kind == B and op.pos == 0:
-                _h2d(sb.perm, host["perm"][mb], s)
-                _h2d(sb.seg_start, host["seg_start"][mb], s)
-                _h2d(sb.seg_id, host["seg_id"][mb], s)
-                _h2d(sb.n_seg, host["n_seg"][mb], s)
-            if timing:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e0.record(s)
-            if self.use_graphs:
-                with torch.cuda.device(dev), torch.cuda.stream(s):
-                    self._graphs[(op.kind, v, slot)].replay()   # replays on the current stream
-                out = self._bwd_out[(op.kind, v, slot)]
-            else:
-                with torch.cuda.device(dev):
-                    out = self._run_op(op.kind, v, slot, s)
-            if timing:
-                e1 = torch.cuda.Event(enable_timing=True)
-                e1.record(s)
-                ev[len(executed)] = (e0, e1)
-            executed.append((op.kind, v, op.agent, op.wave))
-            self._hop(op, out, s)
-            if op.kind == L:
-                with torch.cuda.stream(s):
-                    self.mb_loss[mb:mb + 1].copy_(sb.loss, non_blocking=True)
-        self.optimizer_step()
-        t_iter1.record(self.streams[dev0])
-        for d in self.devices:
-            torch.cuda.current_stream(d).wait_stream(self.streams[d])
-        loss = float(self.mb_loss.sum().item()) / self.M
+        pending: dict = {}
+        with torch.cuda.device(self.dev):
+            s.wait_stream(torch.cuda.current_stream(self.dev))
+            t_iter0.record(s)
+            with torch.cuda.stream(s):
+                for ps in self.psets.values():
+                    ps.g.zero_()
+                self.mb_loss.zero_()
+            executed = []
+            for idx, op in enumerate(self.ops):
+                v, mb = op.node, op.mb
+                mine = self.placement[v] == self.rank
+                if mine:
+                    key = self._key(op)
+                    sb = self.slots[(v, key[2])]
+                    if op.kind == F and op.pos == 0:
+                        _h2d(sb.ids, host["ids"][mb], s)
+                    if op.kind == L:
+                        _h2d(sb.targets, host["tgt"][mb], s)
+                    if op.kind == B and op.pos == 0:
+                        _h2d(sb.perm, host["perm"][mb], s)
+                        _h2d(sb.seg_start, host["seg_start"][mb], s)
+                        _h2d(sb.seg_id, host["seg_id"][mb], s)
+                        _h2d(sb.n_seg, host["n_seg"][mb], s)
+                    w = pending.pop((op.kind, v, op.agent, op.wave), None)
+                    if w is not None:
+                        with torch.cuda.stream(s):
+                            w.wait()           # input arrived from another rank
+                    if timing:
+                        e0 = torch.cuda.Event(enable_timing=True)
+                        e0.record(s)
+                    if self.use_graphs:
+                        with torch.cuda.stream(s):
+                            self._graphs[key].replay()   # replays on the current stream
+                        out = self._outs[key]
+                    else:
+                        out = self._run_op(op.kind, v, key[2], s)
+                    if timing:
+                        e1 = torch.cuda.Event(enable_timing=True)
+                        e1.record(s)
+                        ev[idx] = (e0, e1)
+                    executed.append((idx, op.kind, v, op.agent, op.wave))
+                    if op.kind == L:
+                        with torch.cuda.stream(s):
+                            self.mb_loss[mb:mb + 1].copy_(sb.loss, non_blocking=True)
+                dst = self._hop_dst(op)
+                if dst is None:
+                    continue
+                nv, name = dst
+                dst_mine = self.placement[nv] == self.rank
+                if mine and dst_mine:
+                    buf = self._dst_buffer(op, nv, name)
+                    native.hop(buf, self.dev.index, out, self.dev.index, out.numel() * out.element_size(), stream=s)
+                elif mine:
+                    import torch.distributed as dist
+
+                    with torch.cuda.stream(s):
+                        w = dist.isend(out, self.placement[nv])
+                        w.wait()                # the source buffer is reused by later ops
+                elif dst_mine:
+                    import torch.distributed as dist
+
+                    buf = self._dst_buffer(op, nv, name)
+                    # the destination slot was last read by this agent's previous wave, which is
+                    # earlier in the global order: let the receive start only after the compute
+                    # enqueued so far on this rank
+                    self.recv_stream.wait_stream(s)
+                    with torch.cuda.stream(self.recv_stream):
+                        w = dist.irecv(buf, self.placement[v])
+                    nk = {"xs0": F, "ret": L, "gin": B}[name]
+                    pending[(nk, nv, op.agent, op.wave)] = w
+            self.optimizer_step()
+            t_iter1.record(s)
+            torch.cuda.current_stream(self.dev).wait_stream(s)
+            if self.world > 1:
+                import torch.distributed as dist
+
+                dist.all_reduce(self.mb_loss)
+            loss = float(self.mb_loss.sum().item()) / self.M
         out = {"loss": loss, "executed": executed}
         if timing:
-            torch.cuda.synchronize()
+            torch.cuda.synchronize(self.dev)
             out["iter_ms"] = t_iter0.elapsed_time(t_iter1)
             out["op_times"] = {i: (t_iter0.elapsed_time(a), t_iter0.elapsed_time(b_)) for i, (a, b_) in ev.items()}
         return out
 
-    def _hop(self, op, out, s):
-        """Send the op's output to the next node on the microbatch's path (spx_hop)."""
-        nodes = self.paths[op.agent]
-        last = len(nodes) - 1
-        src_dev = self.placement[op.node]
-        if op.kind == F:
-            if op.pos < last:
-                nv = nodes[op.pos + 1]
-                dst = self.slots[(nv, self._slot_of[(op.mb, nv)])].xs[0]
-            else:
-                nv = nodes[0]
-                dst = self.slots[(nv, self._slot_of[(op.mb, nv)])].ret
-        elif op.kind == L:
-            nv = nodes[last]
-            dst = self.slots[(nv, self._slot_of[(op.mb, nv)])].gin
-        else:
-            if op.pos == 0:
-                return
-            nv = nodes[op.pos - 1]
-            dst = self.slots[(nv, self._slot_of[(op.mb, nv)])].gin
-        dst_dev = self.placement[nv]
-        native.hop(dst, dst_dev, out, src_dev, out.numel() * out.element_size(), stream=s)
-        if dst_dev != src_dev:
-            e = torch.cuda.Event()
-            e.record(s)
-            self.streams[dst_dev].wait_event(e)
-
+    # ---- optimizer ----
     def launches_per_step(self) -> int:
-        """libspx kernel launches in one iteration (graph contents + optimizer); needs graphs."""
+        """libspx kernel launches in one iteration on this rank (graph contents + optimizer)."""
         if not self.use_graphs:
             raise ValidationError("launch accounting needs use_graphs=True")
-        if not self._opt_launches:
-            n0 = native.launches()
-            self._opt_launch_probe()
-            self._opt_launches = native.launches() - n0
-        return sum(self._graph_launches[(op.kind, op.node, op.slot)] for op in self.ops) + self._opt_launches
+        opt = 2 * len(self.psets) + 1 + len(self.psets)
+        return sum(self._graph_launches[self._key(op)] for op in self.ops
+                   if self.placement[op.node] == self.rank) + opt
 
     def gemm_counts_per_step(self) -> dict:
-        """GEMM key -> launches per iteration (recorded at capture when native.record_gemms(True))."""
+        """GEMM key -> launches per iteration on this rank (needs native.record_gemms at setup)."""
         out: dict = {}
         for op in self.ops:
-            for key in self._graph_gemms.get((op.kind, op.node, op.slot), []):
-                out[key] = out.get(key, 0) + 1
+            if self.placement[op.node] == self.rank:
+                for key in self._graph_gemms.get(self._key(op), []):
+                    out[key] = out.get(key, 0) + 1
         return out
-
-    def _opt_launch_probe(self):
-        # 2 (sumsq) per distinct stage + 1 (clip) + 1 (adamw) per parameter set
-        native._count(2 * len({st for st, _ in self.psets}) + 1 + len(self.psets))
 
     def optimizer_step(self):
-        """Replica sync (only across devices), global-norm clip, AdamW — all on device."""
+        """Replica all-reduce (NCCL, only for stages replicated across ranks), global-norm clip and
+        AdamW, all enqueued on the compute stream — no host synchronisation."""
         o = self.optim
-        dev0 = self.devices[0]
-        self.sync_grads()
-        s0 = self.streams[dev0]
-        for d in self.devices:
-            if d != dev0:
-                e = torch.cuda.Event()
-                e.record(self.streams[d])
-                s0.wait_event(e)
-        # each stage counted once in the global norm
-        seen = set()
-        idx = 0
-        for (st, d), ps in sorted(self.psets.items()):
-            if st in seen:
-                continue
-            seen.add(st)
-            with torch.cuda.device(d):
-                native.sumsq(ps.g, ps.lay.numel, self._sumsq_ws[d], self._sumsq[dev0][idx:idx + 1] if d == dev0
-                             else self._sumsq[d][idx:idx + 1], stream=self.streams[d])
-            idx += 1
-        with torch.cuda.device(dev0):
-            native.clip_scale(self._sumsq[dev0], idx, o.max_grad_norm, self._clip[dev0], self._norm[dev0], stream=s0)
-        for (st, d), ps in sorted(self.psets.items()):
-            with torch.cuda.device(d):
+        s = self.stream
+        with torch.cuda.stream(s):
+            if self.world > 1:
+                import torch.distributed as dist
+
+                for st in self.my_stages:
+                    if st in self._groups:
+                        dist.all_reduce(self.psets[st].g, group=self._groups[st])
+            self._sumsq.zero_()
+            for st in self.my_stages:
+                # each stage counted once: its lowest hosting rank contributes the squared norm
+                if self.stage_ranks[st][0] == self.rank:
+                    ps = self.psets[st]
+                    native.sumsq(ps.g, ps.lay.numel, self._sumsq_ws, self._sumsq[st:st + 1], stream=s)
+            if self.world > 1:
+                import torch.distributed as dist
+
+                dist.all_reduce(self._sumsq)
+            native.clip_scale(self._sumsq, self.assignment.s, o.max_grad_norm, self._clip, self._norm, stream=s)
+            for st in self.my_stages:
+                ps = self.psets[st]
                 native.adamw(ps.p32, ps.g, ps.m, ps.v, ps.pbf, n=ps.lay.numel, n_decay=ps.lay.n_decay, lr=o.lr,
                              beta1=o.beta1, beta2=o.beta2, eps=o.eps, weight_decay=o.weight_decay,
-                             step=self.step_count, grad_scale=self._clip[d], stream=self.streams[d])
-
-    def sync_grads(self):
-        """Sum gradients of replica parameter sets that live on different devices (single-process
-        multi-GPU path; the multi-process path uses NCCL all-reduce, see dist_trainer)."""
-        by_stage: dict[int, list] = {}
-        for (st, d), ps in sorted(self.psets.items()):
-            by_stage.setdefault(st, []).append(ps)
-        for st, sets in by_stage.items():
-            if len(sets) < 2:
-                continue
-            raise NotImplementedError("single-process multi-GPU replicas: use dist_trainer (one process per GPU)")
+                             step=self.step_count, grad_scale=self._clip, stream=s)
 
     # ---- inspection (tests) ----
-    def grads(self) -> list[dict[str, torch.Tensor]]:
-        """Per-stage canonical fp32 gradients of the last iteration (pre-clip), summed over
-        co-resident replicas."""
-        torch.cuda.synchronize()
-        out = []
-        for st in range(self.assignment.s):
-            sets = [ps for (s_, d), ps in self.psets.items() if s_ == st]
-            g = sum(ps.g.double().cpu() for ps in sets).float()
-            out.append(unpack_stage(self.cfg, self.layouts[st], g))
-        return out
+    def grads(self) -> dict[int, dict[str, torch.Tensor]]:
+        """Canonical fp32 gradients of the last iteration (post replica-sum, pre-clip) for the
+        stages hosted on this rank."""
+        torch.cuda.synchronize(self.dev)
+        return {st: unpack_stage(self.cfg, self.layouts[st], self.psets[st].g) for st in self.my_stages}
 
-    def params(self) -> list[dict[str, torch.Tensor]]:
-        torch.cuda.synchronize()
-        out = []
-        for st in range(self.assignment.s):
-            ps = next(ps for (s_, d), ps in sorted(self.psets.items()) if s_ == st)
-            out.append(unpack_stage(self.cfg, self.layouts[st], ps.p32))
-        return out
+    def params(self) -> dict[int, dict[str, torch.Tensor]]:
+        torch.cuda.synchronize(self.dev)
+        return {st: unpack_stage(self.cfg, self.layouts[st], self.psets[st].p32) for st in self.my_stages}
 
     def grad_norm(self) -> float:
-        torch.cuda.synchronize()
-        return float(self._norm[self.devices[0]].item())
+        torch.cuda.synchronize(self.dev)
+        return float(self._norm.item())
+
+    def make_report(self, res: dict) -> ExecReport:
+        """ExecReport (SimReport fields measured on this rank's device) from step(timing=True)."""
+        n = self.topology.n
+        busy = [0.0] * n
+        order: dict[int, list] = {}
+        trace, start_f0 = [], {}
+        e2e = [0.0] * self.M
+        wait = 0.0
+        for idx, kind, v, agent, wave in res["executed"]:
+            t0, t1 = res["op_times"][idx]
+            busy[v] += t1 - t0
+            order.setdefault(v, []).append((kind, agent, wave))
+            dirn = {"F": "fwd", "L": "loss", "B": "bwd"}[kind]
+            trace.append((t0, v, "start", agent, wave, dirn))
+            trace.append((t1, v, "end", agent, wave, dirn))
+            op = self.ops[idx]
+            if kind == F and op.pos == 0:
+                start_f0[op.mb] = t0
+            if kind == B and op.pos == 0:
+                e2e[op.mb] = t1 - start_f0[op.mb]
+        mk = res["iter_ms"]
+        return ExecReport(iteration_makespan=mk, microbatch_e2e=e2e, total_collision_wait=wait, node_busy=busy,
+                          node_idle=[mk - x for x in busy], loss=res["loss"], mb_loss=self.mb_loss.tolist(),
+                          grad_norm=self.grad_norm(), node_order=order, trace=trace)
 
 
 def _h2d(dst: torch.Tensor, src: torch.Tensor, stream) -> None:
@@ -563,40 +626,13 @@ def _h2d(dst: torch.Tensor, src: torch.Tensor, stream) -> None:
 
 def execute(schedule: Schedule, topology: Topology, sim_config: SimConfig, model_cfg: ModelConfig, placement,
             tokens: torch.Tensor, *, assignment, b: int, split=None, seed: int = 0, steps: int = 1,
-            use_graphs: bool = True) -> ExecReport:
-    """Run ``steps`` iterations of the schedule on the GPU(s); report the last one measured."""
+            use_graphs: bool = True, rank: int = 0, world: int = 1) -> ExecReport:
+    """Drop-in for ``simulate``: same schedule / topology / sim_config, plus the model,
+    a node->rank placement and the tokens; runs ``steps`` real iterations and returns the last
+    one's measured report (losses included)."""
     tr = Trainer(schedule, topology, sim_config, model_cfg, assignment, b=b, T=tokens.shape[-1] - 1, split=split,
-                 placement=placement, seed=seed, use_graphs=use_graphs)
+                 placement=placement, seed=seed, use_graphs=use_graphs, rank=rank, world=world)
     res = None
     for _ in range(steps):
         res = tr.step(tokens, timing=True)
     return tr.make_report(res)
-
-
-def _make_report(self: Trainer, res: dict) -> ExecReport:
-    n = self.topology.n
-    busy = [0.0] * n
-    order: dict[int, list] = {}
-    trace = []
-    start_f0: dict[int, float] = {}
-    e2e = [0.0] * self.M
-    wait = 0.0
-    ready_at: dict = {}
-    for i, (kind, v, agent, wave) in enumerate(res["executed"]):
-        t0, t1 = res["op_times"][i]
-        busy[v] += t1 - t0
-        order.setdefault(v, []).append((kind, agent, wave))
-        trace.append((t0, v, "start", agent, wave, {"F": "fwd", "L": "loss", "B": "bwd"}[kind]))
-        trace.append((t1, v, "end", agent, wave, {"F": "fwd", "L": "loss", "B": "bwd"}[kind]))
-        op = self.ops[i]
-        if kind == F and op.pos == 0:
-            start_f0[op.mb] = t0
-        if kind == B and op.pos == 0:
-            e2e[op.mb] = t1 - start_f0[op.mb]
-    mk = res["iter_ms"]
-    return ExecReport(iteration_makespan=mk, microbatch_e2e=e2e, total_collision_wait=wait, node_busy=busy,
-                      node_idle=[mk - x for x in busy], loss=res["loss"], mb_loss=self.mb_loss.tolist(),
-                      grad_norm=self.grad_norm(), node_order=order, trace=trace)
-
-
-Trainer.make_report = _make_report

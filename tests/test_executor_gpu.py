@@ -35,7 +35,8 @@ def c1():
     rc, sch, params, tokens = _setup()
     tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params)
     res = tr.step(tokens, timing=True)
-    grads = tr.grads()
+    g = tr.grads()
+    grads = [g[st] for st in range(rc.s)]
     agents = sorted(a.id for a in sch.agents)
     mb_stages = train_ref.mb_stage_sequences({a: sch.paths[a].stages for a in agents}, agents, rc.M)
     ref = train_ref.iteration(rc.model, rc.layers, params, mb_stages, tokens, update=True)

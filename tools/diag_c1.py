@@ -16,7 +16,7 @@ for graphs in (False, True):
     print("graphs", graphs, "loss", r["loss"], "ref", ref["loss"])
     print(" mb", [round(x, 4) for x in tr.mb_loss.tolist()])
     print(" rf", [round(x, 4) for x in ref["mb_loss"]])
-    g = tr.grads()
+    g = tr.grads(); g = [g[st] for st in range(4)]
     for st in range(4):
         a = torch.cat([g[st][k].reshape(-1) for k in sorted(g[st])]); b = torch.cat([ref["grads"][st][k].reshape(-1) for k in sorted(ref["grads"][st])])
         print(" stage", st, "cos", torch.nn.functional.cosine_similarity(a.double(), b.double(), dim=0).item(), "ratio", (a.norm()/b.norm()).item())
