@@ -64,24 +64,38 @@ int spx_gemm_bf16(const void* A, const void* B, void* C, const void* R, void* C2
                   int64_t lda, int64_t ldb, int64_t ldc, int64_t ldc2, int32_t a_mn_major, int32_t b_mn_major,
                   int32_t epilogue, float beta, void* stream);
 
+/* Register a zero-initialised int32 buffer (>= max tiles of any GEMM, e.g. 65536) for the current
+ * device.  When set, fp32-accumulating GEMMs (epilogue 2) with too few tiles for the SMs split K
+ * and add their partial sums into C in split order (deterministic).  NULL disables split-K.  One
+ * GEMM at a time may use the buffer on a device (the executor runs one compute stream per GPU). */
+int spx_gemm_set_workspace(int32_t* sem, int64_t n_ints);
+
+/* QKV projection with RoPE fused into the epilogue: C = A.B^T, then rotate-half RoPE (position =
+ * row % T, cos_sin [T][hd/2][2]) on columns [0, rope_cols) (the q and k heads).  head_dim 64 or 128. */
+int spx_gemm_bf16_rope(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K, int64_t lda,
+                       int64_t ldb, int64_t ldc, const float* cos_sin, int64_t rope_cols, int64_t T, int64_t head_dim,
+                       void* stream);
+
 /* ---- attention (causal, GQA; q/k/v read from the fused QKV buffer) ----
  * qkv [B*T][ld_qkv] bf16 with q heads at column h*hd, k heads at (H+j)*hd, v heads at (H+Hkv+j)*hd.
  * o [B*T][ld_o] bf16, lse [B][H][T] f32 (natural log).  T % 64 == 0, hd in {48, 64, 128}. */
 int spx_attn_fwd(const void* qkv, void* o, float* lse, int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd,
                  int64_t ld_qkv, int64_t ld_o, float scale, void* stream);
-/* dqkv gets dq/dk/dv in the same layout as qkv.  delta_ws: B*H*T floats of workspace. */
+/* dqkv gets dq/dk/dv in the same layout as qkv.  delta_ws: B*H*T floats of workspace.
+ * rope_cos_sin (may be NULL): when given, dq and dk are written back through the inverse RoPE
+ * rotation (the gradient w.r.t. the pre-RoPE projections). */
 int spx_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, float* delta_ws, void* dqkv,
                  int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv, int64_t ld_o, float scale,
-                 void* stream);
+                 const float* rope_cos_sin, void* stream);
 
 /* ---- RMSNorm ----
  * fwd: y = x * rsqrt(mean(x^2) + eps) * g ; rstd[rows] saved.
  * bwd: dx = dres + rstd*(g*dy - xhat*mean(xhat*g*dy)) (dres may be NULL); dg (f32) += sum_rows dy*xhat
- *      via ws (spx_rmsnorm_ws_floats(d) floats), deterministic. */
+ *      via ws (spx_rmsnorm_ws_floats(rows, d) floats), deterministic (fixed-order partials). */
 int spx_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int64_t rows, int64_t d, float eps, void* stream);
 int spx_rmsnorm_bwd(const void* x, const void* g, const float* rstd, const void* dy, const void* dres, void* dx,
                     float* dg, float* ws, int64_t rows, int64_t d, void* stream);
-int64_t spx_rmsnorm_ws_floats(int64_t d);
+int64_t spx_rmsnorm_ws_floats(int64_t rows, int64_t d);
 
 /* ---- RoPE (rotate-half), in place on the first n_heads heads of each row; position = row % T.
  * cos_sin [T][hd/2][2] f32.  inverse = 1 rotates by -theta (backward). */

@@ -106,6 +106,25 @@ SPX_DEVICE void load_b_kn(uint32_t (&b)[4], const __nv_bfloat16* s, int k0, int 
   ldsm_x4_t(b, smem_u32(p));
 }
 
+// Inverse rotate-half RoPE on a thread's accumulator fragments: the thread holds columns
+// 8i + 2t4 + {0,1} of rows r and r+8; column j and j + HD/2 sit in n-tiles i and i + HD/16.
+template <int HD>
+SPX_DEVICE void unrope_frags(float (&acc)[HD / 8][4], const float* cs, int pos0, int pos1, int t4) {
+  const float2* c0 = reinterpret_cast<const float2*>(cs) + (size_t)pos0 * (HD / 2);
+  const float2* c1 = reinterpret_cast<const float2*>(cs) + (size_t)pos1 * (HD / 2);
+#pragma unroll
+  for (int i = 0; i < HD / 16; ++i) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = 8 * i + 2 * t4 + (e & 1);
+      const float2 w = (e >> 1) ? c1[j] : c0[j];
+      const float a = acc[i][e], b = acc[i + HD / 16][e];
+      acc[i][e] = a * w.x + b * w.y;
+      acc[i + HD / 16][e] = b * w.x - a * w.y;
+    }
+  }
+}
+
 struct Params {
   const __nv_bfloat16* qkv;
   __nv_bfloat16* out;   // fwd: O [B*T, H*hd]; bwd: dQKV [B*T, ld]
@@ -113,6 +132,7 @@ struct Params {
   const __nv_bfloat16* dout;
   float* lse;           // [B, H, T]
   float* delta;         // [B, H, T]
+  const float* rope_cs; // bwd: [T][hd/2][2] cos/sin -> dq, dk written un-rotated (inverse RoPE)
   long long ld;         // qkv / dqkv row stride
   long long ldo;        // O / dO row stride
   int B, T, H, Hkv;
@@ -391,6 +411,7 @@ __global__ void __launch_bounds__(THREADS) attn_bwd_dkdv_kernel(const Params p) 
     }
   }
   const int kr = kb * BK + warp * 16 + g;
+  if (p.rope_cs) unrope_frags<HD>(dk, p.rope_cs, kr, kr + 8, t4);
   __nv_bfloat16* dK0 = p.out + (row0 + kr) * p.ld + (p.H + kvh) * HD;
   __nv_bfloat16* dV0 = p.out + (row0 + kr) * p.ld + (p.H + p.Hkv + kvh) * HD;
 #pragma unroll
@@ -503,6 +524,7 @@ __global__ void __launch_bounds__(THREADS) attn_bwd_dq_kernel(const Params p) {
     }
     __syncthreads();
   }
+  if (p.rope_cs) unrope_frags<HD>(dq, p.rope_cs, qr, qr + 8, t4);
   __nv_bfloat16* dQ0 = p.out + (row0 + qr) * p.ld + h * HD;
 #pragma unroll
   for (int i = 0; i < HD / 8; ++i) {
@@ -598,7 +620,7 @@ extern "C" int spx_attn_fwd(const void* qkv, void* o, float* lse, int64_t B, int
 
 extern "C" int spx_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, float* delta_ws,
                             void* dqkv, int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv,
-                            int64_t ld_o, float scale, void* stream) {
+                            int64_t ld_o, float scale, const float* rope_cos_sin, void* stream) {
   int rc = attn::check_args(B, T, H, Hkv, hd);
   if (rc) return rc;
   attn::Params p{};
@@ -608,6 +630,7 @@ extern "C" int spx_attn_bwd(const void* qkv, const void* o, const void* dout, co
   p.dout = reinterpret_cast<const __nv_bfloat16*>(dout);
   p.lse = const_cast<float*>(lse);
   p.delta = delta_ws;
+  p.rope_cs = rope_cos_sin;
   p.ld = ld_qkv;
   p.ldo = ld_o;
   p.B = (int)B; p.T = (int)T; p.H = (int)H; p.Hkv = (int)Hkv;

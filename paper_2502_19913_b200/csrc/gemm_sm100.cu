@@ -32,6 +32,13 @@ enum GemmEpilogue : int {
   EPI_BF16_RESID = 1,  // C(bf16) = acc + R(bf16)            (R may alias C)
   EPI_F32 = 2,         // C(f32)  = acc (+ C if beta != 0)   (wgrad accumulation)
   EPI_SWIGLU = 3,      // H(bf16)[m, N/2] = silu(g)*u ; GU(bf16)[m, N] = (g,u) raw, 128-col interleave
+  EPI_ROPE64 = 4,      // C(bf16) = acc with rotate-half RoPE on columns < rope_cols (head dim 64)
+  EPI_ROPE128 = 5,     // same, head dim 128
+};
+
+template <int EPI>
+struct RopeHd {
+  static constexpr int value = EPI == EPI_ROPE64 ? 64 : (EPI == EPI_ROPE128 ? 128 : 0);
 };
 
 template <int BN>
@@ -51,6 +58,10 @@ struct GemmArgs {
   void* C2;
   long long ldc, ldr, ldc2;
   float beta;
+  const float* rope_cs;  // [T][hd/2][2] (cos, sin)
+  int rope_cols, rope_T;
+  int splits;            // split-K factor (EPI_F32 only); units = tiles * splits
+  int* sem;              // per-tile split-order semaphores (zero between launches)
 };
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
@@ -73,6 +84,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int num_n = (args.N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
   const int num_kb = (args.K + GEMM_BK - 1) / GEMM_BK;
+  // work unit u = split * num_tiles + tile: every CTA walks its units in increasing order, so a
+  // split only ever waits for a lower unit (no deadlock with all CTAs resident)
+  const int num_units = num_tiles * args.splits;
+  const int kbs = (num_kb + args.splits - 1) / args.splits;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
@@ -98,10 +113,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ---------------- TMA producer ----------------
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      const int tile = u % num_tiles, kb0 = (u / num_tiles) * kbs, kb1 = min(num_kb, kb0 + kbs);
       const int m0 = (tile % num_m) * GEMM_BM;
       const int n0 = (tile / num_m) * BN;
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
         uint8_t* sb = sa + Cfg::A_BYTES;
@@ -128,13 +144,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+      const int kb0 = (u / num_tiles) * kbs, kb1 = min(num_kb, kb0 + kbs);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
@@ -145,7 +162,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                    : umma_desc_sw128(sa + kk * 32, 16, 1024);
           const uint64_t bd = B_MN ? umma_desc_sw128(sb + kk * 2048, GEMM_BK * 128, 1024)
                                    : umma_desc_sw128(sb + kk * 32, 16, 1024);
-          mma_bf16_ss(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
+          mma_bf16_ss(d_tmem, ad, bd, IDESC, (kb != kb0) || (kk != 0));
         }
         mma_commit(&empty_bar[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -157,7 +174,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int wq = warp & 3;
     const int row_in_tile = wq * 32 + lane;
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+      const int tile = u % num_tiles, split = u / num_tiles;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int m0 = (tile % num_m) * GEMM_BM;
@@ -167,7 +185,53 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t t_row = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
       const int row = m0 + row_in_tile;
       const bool row_ok = row < args.M;
-      if (EPI == EPI_SWIGLU) {
+      if constexpr (RopeHd<EPI>::value != 0) {
+        // RoPE fused into the QKV projection: each thread owns one row, a head's hd columns sit
+        // in one 256-wide tile, and the rotate-half pairs (j, j + hd/2) are both in registers.
+        constexpr int HD = RopeHd<EPI>::value;
+        const int t = row % args.rope_T;
+        const bool rope_tile = n0 < args.rope_cols;  // rope_cols and n0 are multiples of 256 / HD
+        // one row per thread, one position per row: the row's cos/sin are reused by every head of
+        // the tile (kept in registers for HD=64, re-read from L1 for HD=128)
+        float2 cs_reg[HD == 64 ? 32 : 1];
+        const float2* cs_row = reinterpret_cast<const float2*>(args.rope_cs) + (size_t)t * (HD / 2);
+        if constexpr (HD == 64) {
+          if (rope_tile && row_ok) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) cs_reg[j] = cs_row[j];
+          }
+        }
+#pragma unroll 1
+        for (int hb = 0; hb < BN; hb += HD) {
+          float f[HD];
+#pragma unroll
+          for (int c = 0; c < HD; c += 32) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_row + hb + c, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[c + j] = __uint_as_float(v[j]);
+          }
+          if (row_ok && n0 + hb < args.N) {
+            if (n0 + hb < args.rope_cols) {
+#pragma unroll
+              for (int j = 0; j < HD / 2; ++j) {
+                float2 w;
+                if constexpr (HD == 64) w = cs_reg[j];
+                else w = cs_row[j];
+                const float a = f[j], b = f[j + HD / 2];
+                f[j] = a * w.x - b * w.y;
+                f[j + HD / 2] = b * w.x + a * w.y;
+              }
+            }
+            uint4* C4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.C) + (size_t)row * args.ldc + n0 + hb);
+#pragma unroll
+            for (int q = 0; q < HD / 8; ++q)
+              C4[q] = make_uint4(pack_bf16(f[8 * q], f[8 * q + 1]), pack_bf16(f[8 * q + 2], f[8 * q + 3]),
+                                 pack_bf16(f[8 * q + 4], f[8 * q + 5]), pack_bf16(f[8 * q + 6], f[8 * q + 7]));
+          }
+        }
+      } else if (EPI == EPI_SWIGLU) {
 #pragma unroll 1
         for (int c = 0; c < BN / 2; c += 32) {
           uint32_t g[32], u[32];
@@ -201,6 +265,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
       } else {
+        const bool ordered = EPI == EPI_F32 && args.splits > 1;
+        if (ordered) {
+          // deterministic split-K: split s adds into C only after split s-1 of this tile did
+          int v;
+          do {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(args.sem + tile) : "memory");
+          } while (v != split);
+        }
+        const bool add = (split > 0) || (args.beta != 0.f);
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t v[32];
@@ -210,7 +283,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if (EPI == EPI_F32) {
               float* C = reinterpret_cast<float*>(args.C) + (size_t)row * args.ldc + n0 + c;
               float4* C4 = reinterpret_cast<float4*>(C);
-              if (args.beta != 0.f) {
+              if (add) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                   float4 o = C4[q];
@@ -248,6 +321,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                    pack_bf16(f[8 * q + 4], f[8 * q + 5]), pack_bf16(f[8 * q + 6], f[8 * q + 7]));
             }
           }
+        }
+        if (ordered) {
+          __threadfence();
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+          if (threadIdx.x == 128) atomicExch(args.sem + tile, split + 1 == args.splits ? 0 : split + 1);
         }
       }
       tc_fence_before();
@@ -306,7 +384,7 @@ static int launch_gemm(const void* A, const void* B, long long lda, long long ld
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm)");
     attr_set = true;
   }
-  const int tiles = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + BN - 1) / BN);
+  const int tiles = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + BN - 1) / BN) * args.splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   kern<<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, stream>>>(ta, tb, args);
   return check_launch("gemm_bf16_kernel");
@@ -319,6 +397,36 @@ static int dispatch_major(const void* A, const void* B, long long lda, long long
   if (!a_mn && b_mn) return launch_gemm<BN, false, true, EPI>(A, B, lda, ldb, args, s);
   if (a_mn && b_mn) return launch_gemm<BN, true, true, EPI>(A, B, lda, ldb, args, s);
   return launch_gemm<BN, true, false, EPI>(A, B, lda, ldb, args, s);
+}
+
+// Per-device split-K semaphores, registered once by the caller (no allocation in the GEMM path).
+static int* g_sem[64] = {nullptr};
+static int64_t g_sem_n[64] = {0};
+
+// Split-K factor for the fp32 (wgrad) epilogue: maximise wave efficiency of tiles x splits on the
+// SMs, keeping >= 8 k-blocks per split; splits add into C in split order (deterministic).
+static void pick_splits(GemmArgs& a, int bn) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int tiles = ((a.M + GEMM_BM - 1) / GEMM_BM) * ((a.N + bn - 1) / bn);
+  const int num_kb = (a.K + GEMM_BK - 1) / GEMM_BK;
+  if (dev < 0 || dev >= 64 || g_sem[dev] == nullptr || tiles > g_sem_n[dev]) return;
+  const int sms = num_sms();
+  double best = 0.0;
+  int best_s = 1;
+  for (int s = 1; s <= 8; ++s) {
+    const int kbs = (num_kb + s - 1) / s;
+    if (kbs < 8 && s > 1) break;
+    const int s_eff = (num_kb + kbs - 1) / kbs;
+    const long units = (long)tiles * s_eff;
+    const double eff = (double)units / (double)(((units + sms - 1) / sms) * sms);
+    if (eff > best + 0.05) {
+      best = eff;
+      best_s = s_eff;
+    }
+  }
+  a.splits = best_s;
+  a.sem = best_s > 1 ? g_sem[dev] : nullptr;
 }
 
 static int pick_bn(int M, int N) {
@@ -334,6 +442,37 @@ static int pick_bn(int M, int N) {
 
 using namespace spx;
 
+extern "C" int spx_gemm_set_workspace(int32_t* sem, int64_t n_ints) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return set_error(SPX_ERR_ARG, "gemm workspace: bad device");
+  if (sem == nullptr || n_ints <= 0) {
+    g_sem[dev] = nullptr;
+    g_sem_n[dev] = 0;
+    return SPX_OK;
+  }
+  cudaError_t e = cudaMemset(sem, 0, (size_t)n_ints * sizeof(int32_t));
+  if (e != cudaSuccess) return set_cuda_error(e, "gemm workspace memset");
+  g_sem[dev] = sem;
+  g_sem_n[dev] = n_ints;
+  return SPX_OK;
+}
+
+extern "C" int spx_gemm_bf16_rope(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K, int64_t lda,
+                                  int64_t ldb, int64_t ldc, const float* cos_sin, int64_t rope_cols, int64_t T,
+                                  int64_t head_dim, void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0) return set_error(SPX_ERR_ARG, "gemm_rope: non-positive shape");
+  if (N % 32 != 0 || K % 8 != 0 || lda % 8 != 0 || ldb % 8 != 0)
+    return set_error(SPX_ERR_ARG, "gemm_rope: N % 32, K/lda/ldb % 8 required");
+  if (head_dim != 64 && head_dim != 128) return set_error(SPX_ERR_ARG, "gemm_rope: head_dim must be 64 or 128");
+  if (rope_cols % head_dim || T <= 0) return set_error(SPX_ERR_ARG, "gemm_rope: rope_cols must be whole heads");
+  GemmArgs args{(int)M, (int)N, (int)K, C, nullptr, nullptr, (long long)ldc, (long long)ldc, 0, 0.f,
+                cos_sin, (int)rope_cols, (int)T, 1, nullptr};
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (head_dim == 64) return launch_gemm<256, false, false, EPI_ROPE64>(A, B, lda, ldb, args, s);
+  return launch_gemm<256, false, false, EPI_ROPE128>(A, B, lda, ldb, args, s);
+}
+
 extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* R, void* C2, int64_t M, int64_t N,
                              int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int64_t ldc2, int32_t a_mn_major,
                              int32_t b_mn_major, int32_t epilogue, float beta, void* stream) {
@@ -345,9 +484,11 @@ extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* 
   if (epilogue == EPI_SWIGLU && (N % 256 != 0 || C2 == nullptr))
     return set_error(SPX_ERR_ARG, "gemm: swiglu epilogue needs N % 256 == 0 and a GU output");
   if (epilogue == EPI_BF16_RESID && R == nullptr) return set_error(SPX_ERR_ARG, "gemm: residual epilogue needs R");
-  GemmArgs args{(int)M, (int)N, (int)K, C, R, C2, (long long)ldc, (long long)ldc, (long long)ldc2, beta};
+  GemmArgs args{(int)M, (int)N, (int)K, C, R, C2, (long long)ldc, (long long)ldc, (long long)ldc2, beta, nullptr, 0, 1,
+                1, nullptr};
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int bn = (epilogue == EPI_SWIGLU) ? 256 : pick_bn((int)M, (int)N);
+  const int bn = (epilogue == EPI_SWIGLU || epilogue == EPI_F32) ? 256 : pick_bn((int)M, (int)N);
+  if (epilogue == EPI_F32) pick_splits(args, bn);
   switch (epilogue) {
     case EPI_BF16:
       return bn == 256 ? dispatch_major<256, EPI_BF16>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s)

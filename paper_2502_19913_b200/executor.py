@@ -142,7 +142,7 @@ class Scratch:
         self.do = torch.empty(n, cfg.n_heads * cfg.head_dim, **e)
         self.dqkv = torch.empty(n, cfg.qkv_dim, **e)
         self.delta = torch.empty(b, cfg.n_heads, T, dtype=F32, device=device)
-        self.rms_ws = torch.empty(native.rmsnorm_ws_floats(d), dtype=F32, device=device)
+        self.rms_ws = torch.empty(native.rmsnorm_ws_floats(n, d), dtype=F32, device=device)
         self.rope = rope_cos_sin(T, cfg.head_dim, cfg.rope_theta).to(device)
         if with_head:
             self.xf = torch.empty(n, d, **e)
@@ -167,8 +167,12 @@ class StageProgram:
         d, f, qd, hd = c.d, c.ffn, c.qkv_dim, c.head_dim
         od = c.n_heads * hd
         native.rmsnorm_fwd(x, ps.w(f"l{i}.attn_norm"), a.xn1, a.rstd1, rows=n, d=d, eps=c.eps, stream=s)
-        native.gemm(a.xn1, ps.w(f"l{i}.wqkv"), a.qkv, M=n, N=qd, K=d, lda=d, ldb=d, ldc=qd, stream=s)
-        native.rope(a.qkv, sc.rope, rows=n, T=self.T, n_heads=c.n_heads + c.n_kv_heads, hd=hd, ld=qd, stream=s)
+        if hd in (64, 128):
+            native.gemm_rope(a.xn1, ps.w(f"l{i}.wqkv"), a.qkv, M=n, N=qd, K=d, lda=d, ldb=d, ldc=qd, cos_sin=sc.rope,
+                             rope_cols=(c.n_heads + c.n_kv_heads) * hd, T=self.T, head_dim=hd, stream=s)
+        else:
+            native.gemm(a.xn1, ps.w(f"l{i}.wqkv"), a.qkv, M=n, N=qd, K=d, lda=d, ldb=d, ldc=qd, stream=s)
+            native.rope(a.qkv, sc.rope, rows=n, T=self.T, n_heads=c.n_heads + c.n_kv_heads, hd=hd, ld=qd, stream=s)
         native.attn_fwd(a.qkv, a.o, a.lse, B=self.b, T=self.T, H=c.n_heads, Hkv=c.n_kv_heads, hd=hd, ld_qkv=qd,
                         ld_o=od, scale=self.scale, stream=s)
         native.gemm(a.o, ps.w(f"l{i}.wo"), a.xmid, M=n, N=d, K=od, lda=od, ldb=od, ldc=d,
@@ -200,10 +204,9 @@ class StageProgram:
         native.gemm(sc.dxm, ps.w(f"l{i}.wo"), sc.do, M=n, N=od, K=d, lda=d, ldb=od, ldc=od, b_mn=True, stream=s)
         native.gemm(sc.dxm, a.o, ps.gv(f"l{i}.wo"), M=d, N=od, K=n, lda=d, ldb=od, ldc=od, a_mn=True, b_mn=True,
                     epilogue=F32E, beta=1.0, stream=s)
+        # dq, dk leave the attention backward already un-rotated (inverse RoPE fused)
         native.attn_bwd(a.qkv, a.o, sc.do, a.lse, sc.delta, sc.dqkv, B=self.b, T=self.T, H=c.n_heads,
-                        Hkv=c.n_kv_heads, hd=hd, ld_qkv=qd, ld_o=od, scale=self.scale, stream=s)
-        native.rope(sc.dqkv, sc.rope, rows=n, T=self.T, n_heads=c.n_heads + c.n_kv_heads, hd=hd, ld=qd, inverse=True,
-                    stream=s)
+                        Hkv=c.n_kv_heads, hd=hd, ld_qkv=qd, ld_o=od, scale=self.scale, rope_cs=sc.rope, stream=s)
         native.gemm(sc.dqkv, ps.w(f"l{i}.wqkv"), sc.dxn, M=n, N=d, K=qd, lda=qd, ldb=d, ldc=d, b_mn=True, stream=s)
         native.gemm(sc.dqkv, a.xn1, ps.gv(f"l{i}.wqkv"), M=qd, N=d, K=n, lda=qd, ldb=d, ldc=d, a_mn=True, b_mn=True,
                     epilogue=F32E, beta=1.0, stream=s)
@@ -270,6 +273,28 @@ def static_slots(schedule: Schedule, n_nodes: int) -> tuple[dict, list[int]]:
     return slot_of, [max(1, len(users[v])) for v in range(n_nodes)]
 
 
+def hop_plan(ops, paths: dict, placement: list[int]) -> list:
+    """Per op (global order): the path hop that follows it, or None at the end of a path.
+
+    Entry = (dst_node, buffer, src_rank, dst_rank, consumer_kind): F feeds the next node's F (its
+    layer-0 input ``xs0``) or, after the last stage, the origin's loss op (``ret``); L feeds the
+    last node's B (``gin``); B feeds the previous node's B.  Every rank derives the same plan from
+    the same simulator ops, so sends and receives between any two ranks are posted in the same
+    (global) order on both sides."""
+    out = []
+    for op in ops:
+        nodes = paths[op.agent]
+        last = len(nodes) - 1
+        if op.kind == F:
+            dst = (nodes[op.pos + 1], "xs0", F) if op.pos < last else (nodes[0], "ret", L)
+        elif op.kind == L:
+            dst = (nodes[last], "gin", B)
+        else:
+            dst = (nodes[op.pos - 1], "gin", B) if op.pos > 0 else None
+        out.append(None if dst is None else (dst[0], dst[1], placement[op.node], placement[dst[0]], dst[2]))
+    return out
+
+
 class Trainer:
     """Weights, optimizer state, activation slots and captured graphs for one config on one rank.
 
@@ -309,6 +334,7 @@ class Trainer:
         self.agents = sorted(a.id for a in schedule.agents)
         self.paths = {a: schedule.paths[a].nodes for a in self.agents}
         self.slot_of, self.n_slots = static_slots(schedule, topology.n)
+        self.hops = hop_plan(self.ops, self.paths, self.placement)
         self.my_nodes = [v for v in range(topology.n) if self.placement[v] == rank]
         self.my_stages = sorted({self.node_stage[v] for v in self.my_nodes})
         self.stage_ranks = {st: sorted({self.placement[v] for v in range(topology.n) if self.node_stage[v] == st})
@@ -326,6 +352,8 @@ class Trainer:
                     self.slots[(v, j)] = SlotBuffers(cfg, self.split[self.node_stage[v]], self.node_stage[v] == 0,
                                                      self.n, b, self.T, self.dev)
             self.scratch = Scratch(cfg, self.n, b, self.T, self.dev, with_head=0 in self.my_stages)
+            self._gemm_sem = torch.zeros(1 << 16, dtype=torch.int32, device=self.dev)
+            native.gemm_set_workspace(self._gemm_sem)
             self.stream = torch.cuda.Stream(device=self.dev)
             self.recv_stream = torch.cuda.Stream(device=self.dev)
             self.prog = StageProgram(cfg, self.n, b, self.T, self.M)
@@ -356,17 +384,24 @@ class Trainer:
                 g = dist.new_group(ranks)
                 if self.rank in ranks:
                     self._groups[st] = g
-        # bring up the pairwise P2P channels in one global order (lexicographic over rank pairs),
-        # so lazy communicator creation can never form a wait cycle
+        # one process group (own NCCL communicator and stream) per rank pair for the path hops, so
+        # hops between different pairs, and the replica all-reduces, never serialise behind each
+        # other; created and warmed up in one global (lexicographic) order on every rank
+        self._pair = {}
+        for a in range(self.world):
+            for b_ in range(a + 1, self.world):
+                g = dist.new_group([a, b_])
+                if self.rank in (a, b_):
+                    self._pair[b_ if self.rank == a else a] = g
         buf = torch.zeros(1, device=self.dev)
         for a in range(self.world):
             for b_ in range(a + 1, self.world):
                 if self.rank == a:
-                    dist.send(buf, b_)
-                    dist.recv(buf, b_)
+                    dist.send(buf, b_, group=self._pair[b_])
+                    dist.recv(buf, b_, group=self._pair[b_])
                 elif self.rank == b_:
-                    dist.recv(buf, a)
-                    dist.send(buf, a)
+                    dist.recv(buf, a, group=self._pair[a])
+                    dist.send(buf, a, group=self._pair[a])
         torch.cuda.synchronize(self.dev)
 
     # ---- graph capture ----
@@ -421,17 +456,7 @@ class Trainer:
         mine = sum(1 for op in self.ops if op.kind == F and op.pos == 0 and self.placement[op.node] == self.rank)
         return mine * per
 
-    # ---- hops ----
-    def _hop_dst(self, op):
-        """(destination node, buffer name) of the op's output hop, or None (end of path)."""
-        nodes = self.paths[op.agent]
-        last = len(nodes) - 1
-        if op.kind == F:
-            return (nodes[op.pos + 1], "xs0") if op.pos < last else (nodes[0], "ret")
-        if op.kind == L:
-            return nodes[last], "gin"
-        return (nodes[op.pos - 1], "gin") if op.pos > 0 else None
-
+    # ---- hop destinations ----
     def _dst_buffer(self, op, nv, name):
         sb = self.slots[(nv, self.slot_of[(op.agent, nv)])]
         return sb.xs[0] if name == "xs0" else getattr(sb, name)
@@ -490,11 +515,11 @@ class Trainer:
                     if op.kind == L:
                         with torch.cuda.stream(s):
                             self.mb_loss[mb:mb + 1].copy_(sb.loss, non_blocking=True)
-                dst = self._hop_dst(op)
-                if dst is None:
+                hop = self.hops[idx]
+                if hop is None:
                     continue
-                nv, name = dst
-                dst_mine = self.placement[nv] == self.rank
+                nv, name, _, dst_rank, consumer = hop
+                dst_mine = dst_rank == self.rank
                 if mine and dst_mine:
                     buf = self._dst_buffer(op, nv, name)
                     native.hop(buf, self.dev.index, out, self.dev.index, out.numel() * out.element_size(), stream=s)
@@ -502,7 +527,7 @@ class Trainer:
                     import torch.distributed as dist
 
                     with torch.cuda.stream(s):
-                        w = dist.isend(out, self.placement[nv])
+                        w = dist.isend(out, dst_rank, group=self._pair[dst_rank])
                         w.wait()                # the source buffer is reused by later ops
                 elif dst_mine:
                     import torch.distributed as dist
@@ -513,9 +538,8 @@ class Trainer:
                     # enqueued so far on this rank
                     self.recv_stream.wait_stream(s)
                     with torch.cuda.stream(self.recv_stream):
-                        w = dist.irecv(buf, self.placement[v])
-                    nk = {"xs0": F, "ret": L, "gin": B}[name]
-                    pending[(nk, nv, op.agent, op.wave)] = w
+                        w = dist.irecv(buf, self.placement[v], group=self._pair[self.placement[v]])
+                    pending[(consumer, nv, op.agent, op.wave)] = w
             self.optimizer_step()
             t_iter1.record(s)
             torch.cuda.current_stream(self.dev).wait_stream(s)

@@ -28,10 +28,12 @@ SIGNATURES: dict[str, list] = {
     "spx_hop": [_I32, _P, _I32, _P, _I64, _P],
     "spx_gemm_bf16": [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _F, _P],
     "spx_attn_fwd": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P],
-    "spx_attn_bwd": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P],
+    "spx_attn_bwd": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P, _P],
+    "spx_gemm_set_workspace": [_P, _I64],
+    "spx_gemm_bf16_rope": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _I64, _I64, _P],
     "spx_rmsnorm_fwd": [_P, _P, _P, _P, _I64, _I64, _F, _P],
     "spx_rmsnorm_bwd": [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _P],
-    "spx_rmsnorm_ws_floats": [_I64],
+    "spx_rmsnorm_ws_floats": [_I64, _I64],
     "spx_rope": [_P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _P],
     "spx_swiglu_bwd": [_P, _P, _P, _I64, _I64, _P],
     "spx_embed_fwd": [_P, _P, _P, _I64, _I64, _P],
@@ -151,6 +153,33 @@ def gemm(A, B, C, *, M, N, K, lda, ldb, ldc, a_mn=False, b_mn=False, epilogue=EP
         _STATS["gemm_log"].append(key)
 
 
+def gemm_rope(A, B, C, *, M, N, K, lda, ldb, ldc, cos_sin, rope_cols, T, head_dim, stream=None) -> None:
+    """QKV projection with RoPE fused into the epilogue (spx_gemm_bf16_rope)."""
+    _check(load().spx_gemm_bf16_rope(_ptr(A), _ptr(B), _ptr(C), M, N, K, lda, ldb, ldc, _ptr(cos_sin), rope_cols, T,
+                                     head_dim, _stream(stream)), "spx_gemm_bf16_rope")
+    _count(1)
+    if _STATS["record"]:
+        key = (M, N, K, False, False, 4)
+        cnt = _STATS["gemms"].get(key, (0, None))[0]
+
+        def again(a=(A, B, C), kw=dict(M=M, N=N, K=K, lda=lda, ldb=ldb, ldc=ldc, cos_sin=cos_sin,
+                                        rope_cols=rope_cols, T=T, head_dim=head_dim)):
+            rec = _STATS["record"]
+            _STATS["record"] = False
+            try:
+                gemm_rope(*a, **kw)
+            finally:
+                _STATS["record"] = rec
+
+        _STATS["gemms"][key] = (cnt + 1, again)
+        _STATS["gemm_log"].append(key)
+
+
+def gemm_set_workspace(sem) -> None:
+    """Register the split-K semaphore buffer (int32 device tensor, zeroed) for the current device."""
+    _check(load().spx_gemm_set_workspace(_ptr(sem), 0 if sem is None else sem.numel()), "spx_gemm_set_workspace")
+
+
 def hop(dst, dst_dev: int, src, src_dev: int, nbytes: int, stream=None) -> None:
     _check(load().spx_hop(dst_dev, _ptr(dst), src_dev, _ptr(src), nbytes, _stream(stream)), "spx_hop")
 
@@ -165,9 +194,10 @@ def attn_fwd(qkv, o, lse, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, stream=None)
     _count(1)
 
 
-def attn_bwd(qkv, o, dout, lse, delta_ws, dqkv, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, stream=None) -> None:
+def attn_bwd(qkv, o, dout, lse, delta_ws, dqkv, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, rope_cs=None,
+             stream=None) -> None:
     _check(load().spx_attn_bwd(_ptr(qkv), _ptr(o), _ptr(dout), _ptr(lse), _ptr(delta_ws), _ptr(dqkv), B, T, H, Hkv,
-                               hd, ld_qkv, ld_o, float(scale), _stream(stream)), "spx_attn_bwd")
+                               hd, ld_qkv, ld_o, float(scale), _ptr(rope_cs), _stream(stream)), "spx_attn_bwd")
     _count(3)
 
 
@@ -180,11 +210,11 @@ def rmsnorm_fwd(x, g, y, rstd, *, rows, d, eps, stream=None) -> None:
 def rmsnorm_bwd(x, g, rstd, dy, dres, dx, dg, ws, *, rows, d, stream=None) -> None:
     _check(load().spx_rmsnorm_bwd(_ptr(x), _ptr(g), _ptr(rstd), _ptr(dy), _ptr(dres), _ptr(dx), _ptr(dg), _ptr(ws),
                                   rows, d, _stream(stream)), "spx_rmsnorm_bwd")
-    _count(3 if dg is not None else 1)
+    _count(2 if dg is not None else 1)
 
 
-def rmsnorm_ws_floats(d: int) -> int:
-    return int(load().spx_rmsnorm_ws_floats(d))
+def rmsnorm_ws_floats(rows: int, d: int) -> int:
+    return int(load().spx_rmsnorm_ws_floats(rows, d))
 
 
 def rope(qkv, cos_sin, *, rows, T, n_heads, hd, ld, inverse=False, stream=None) -> None:

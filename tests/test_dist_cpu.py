@@ -1,0 +1,84 @@
+"""Multi-process host logic on CPU (gloo, world_size 2 and 4): every rank derives the same hop
+plan from the same schedule and posts sends/receives in global op order, so each message lands on
+the intended receive — the property the NCCL P2P hops of the multi-GPU executor rely on."""
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2502_19913_b200.configs import get_config
+from paper_2502_19913_b200.executor import default_placement, hop_plan, static_slots
+from paper_2502_19913_b200.simulator import simulate
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cfg_name, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rc = get_config(cfg_name)
+        sch = rc.schedule()
+        ops = simulate(sch, rc.topology(), rc.sim_config()).ops
+        paths = {a: sch.paths[a].nodes for a in sch.paths}
+        placement = default_placement(rc.topology().n, world)
+        plan = hop_plan(ops, paths, placement)
+        got, sent, pending = [], 0, []
+        for idx, (op, hop) in enumerate(zip(ops, plan)):
+            if hop is None:
+                continue
+            nv, name, src_rank, dst_rank, consumer = hop
+            assert src_rank == placement[op.node]
+            if src_rank == dst_rank:
+                continue
+            if rank == src_rank:
+                pending.append(dist.isend(torch.tensor([idx, op.mb, nv]), dst_rank))
+                sent += 1
+            elif rank == dst_rank:
+                buf = torch.zeros(3, dtype=torch.int64)
+                dist.recv(buf, src_rank)
+                got.append((idx, tuple(buf.tolist()), (idx, op.mb, nv)))
+        for w in pending:
+            w.wait()
+        dist.barrier()
+        q.put((rank, sent, got))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,cfg", [(2, "C2"), (4, "C2"), (2, "C1")])
+def test_cross_rank_hops_match(world, cfg):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    total_sent = sum(r[1] for r in results)
+    received = [g for r in results for g in r[2]]
+    assert total_sent == len(received) > 0
+    for idx, got, want in received:
+        assert got == want, (idx, got, want)
+
+
+def test_static_slots_respect_tc1():
+    rc = get_config("C2")
+    sch = rc.schedule()
+    slot_of, n_slots = static_slots(sch, rc.topology().n)
+    assert max(n_slots) <= rc.m                       # TC1 => at most m slots per node
+    for (a, v), j in slot_of.items():
+        assert 0 <= j < n_slots[v] and v in sch.paths[a].nodes

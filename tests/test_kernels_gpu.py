@@ -108,7 +108,7 @@ def test_rmsnorm(rows, d):
     native.rmsnorm_fwd(x, w, y, rstd, rows=rows, d=d, eps=1e-5)
     dx = torch.empty_like(x)
     dg = torch.full((d,), 0.5, device=dev)
-    ws = torch.empty(native.rmsnorm_ws_floats(d), device=dev)
+    ws = torch.empty(native.rmsnorm_ws_floats(rows, d), device=dev)
     native.rmsnorm_bwd(x, w, rstd, dy, dres, dx, dg, ws, rows=rows, d=d)
     torch.cuda.synchronize()
     xr = x.float().requires_grad_()
@@ -225,3 +225,41 @@ def test_adamw_and_clip():
     ref = torch.cat([pr1.detach(), pr2.detach()])
     assert (p.cpu() - ref).abs().max().item() < 1e-6
     assert torch.equal(pb, p.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("hd,H,Hkv", [(64, 16, 16), (128, 8, 2)])
+def test_gemm_rope_epilogue(hd, H, Hkv):
+    B, T, d = 2, 256, 512
+    g = torch.Generator().manual_seed(hd)
+    W = (H + 2 * Hkv) * hd
+    x = bf(torch.randn(B * T, d, generator=g) * 0.5).to(dev)
+    w = bf(torch.randn(W, d, generator=g) * 0.05).to(dev)
+    cs = rope_table(T, hd).to(dev)
+    out = torch.empty(B * T, W, dtype=torch.bfloat16, device=dev)
+    native.gemm_rope(x, w, out, M=B * T, N=W, K=d, lda=d, ldb=d, ldc=W, cos_sin=cs, rope_cols=(H + Hkv) * hd, T=T,
+                     head_dim=hd)
+    torch.cuda.synchronize()
+    raw = (x.float() @ w.float().t()).view(B, T, H + 2 * Hkv, hd)
+    ref = torch.cat([rope_ref(raw[:, :, : H + Hkv], cs), raw[:, :, H + Hkv:]], dim=2)
+    assert rel(out.view(B, T, -1, hd), ref) < 1e-2
+
+
+def test_attention_bwd_inverse_rope():
+    B, T, H, hd = 1, 256, 4, 64
+    g = torch.Generator().manual_seed(11)
+    W = 3 * H * hd
+    qkv = bf(torch.randn(B * T, W, generator=g)).to(dev)
+    do = bf(torch.randn(B * T, H * hd, generator=g)).to(dev)
+    cs = rope_table(T, hd).to(dev)
+    o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device=dev)
+    lse = torch.empty(B, H, T, device=dev)
+    native.attn_fwd(qkv, o, lse, B=B, T=T, H=H, Hkv=H, hd=hd, ld_qkv=W, ld_o=H * hd, scale=0.125)
+    plain = torch.zeros_like(qkv)
+    fused = torch.zeros_like(qkv)
+    delta = torch.empty_like(lse)
+    kw = dict(B=B, T=T, H=H, Hkv=H, hd=hd, ld_qkv=W, ld_o=H * hd, scale=0.125)
+    native.attn_bwd(qkv, o, do, lse, delta, plain, **kw)
+    native.attn_bwd(qkv, o, do, lse, delta, fused, rope_cs=cs, **kw)
+    native.rope(plain, cs, rows=B * T, T=T, n_heads=2 * H, hd=hd, ld=W, inverse=True)
+    torch.cuda.synchronize()
+    assert rel(fused, plain) < 1e-2

@@ -1,0 +1,63 @@
+"""Multi-GPU parity driver (launched by tests/test_dist_gpu.py under torchrun):
+config C1 on WORLD_SIZE GPUs vs the CPU oracle and vs the per-node op order of the simulator.
+Rank 0 prints one JSON line with the comparison results."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import train_ref  # noqa: E402
+from paper_2502_19913_b200.configs import get_config  # noqa: E402
+from paper_2502_19913_b200.executor import Trainer  # noqa: E402
+from paper_2502_19913_b200.model import init_params, synthetic_tokens  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rc = get_config(os.environ.get("SPX_CONFIG", "C1"))
+    sch = rc.schedule()
+    params = init_params(rc.model, rc.layers, seed=0)
+    tokens = synthetic_tokens(rc.model, rc.M, rc.b, rc.T, seed=1234)
+    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params,
+                 rank=rank, world=world, device=local)
+    res = tr.step(tokens, timing=True)
+    rep = tr.make_report(res)
+    grads = tr.grads()
+    gnorm = tr.grad_norm()
+    res2 = tr.step(tokens)
+    # per-node order of the ops this rank executed vs the simulator's
+    sim = {}
+    for op in tr.ops:
+        if tr.placement[op.node] == rank:
+            sim.setdefault(op.node, []).append((op.kind, op.agent, op.wave))
+    order_ok = rep.node_order == sim
+    out = [None] * world
+    dist.all_gather_object(out, {"rank": rank, "grads": {k: {n: t for n, t in v.items()} for k, v in grads.items()},
+                                 "order_ok": order_ok})
+    if rank == 0:
+        agents = sorted(a.id for a in sch.agents)
+        mbs = train_ref.mb_stage_sequences({a: sch.paths[a].stages for a in agents}, agents, rc.M)
+        ref = train_ref.iteration(rc.model, rc.layers, params, mbs, tokens, update=False)
+        stage_cos = {}
+        for o in out:
+            for st, g in o["grads"].items():
+                a = torch.cat([g[k].reshape(-1) for k in sorted(g)]).double()
+                b = torch.cat([ref["grads"][st][k].reshape(-1) for k in sorted(g)]).double()
+                stage_cos[f"{o['rank']}:{st}"] = [torch.nn.functional.cosine_similarity(a, b, dim=0).item(),
+                                                   ((a - b).norm() / b.norm()).item()]
+        print(json.dumps({"world": world, "loss": res["loss"], "loss2": res2["loss"], "ref_loss": ref["loss"],
+                          "order_ok": all(o["order_ok"] for o in out), "stage_cos_rel": stage_cos,
+                          "grad_norm": gnorm, "ref_grad_norm": ref["grad_norm"]}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -15,6 +15,7 @@ from paper_2502_19913_b200 import native  # noqa: E402
 SHAPES = [
     # name, M, N, K, a_mn, b_mn, epi
     ("qkv fwd", 4096, 3072, 1024, False, False, native.EPI_BF16),
+    ("qkv fwd+rope", 4096, 3072, 1024, False, False, "rope"),
     ("o fwd+res", 4096, 1024, 1024, False, False, native.EPI_BF16_RESID),
     ("gate/up fwd swiglu", 4096, 5632, 1024, False, False, native.EPI_SWIGLU),
     ("down fwd+res", 4096, 1024, 2816, False, False, native.EPI_BF16_RESID),
@@ -24,18 +25,25 @@ SHAPES = [
     ("qkv wgrad", 3072, 1024, 4096, True, True, native.EPI_F32),
     ("gate/up wgrad", 5632, 1024, 4096, True, True, native.EPI_F32),
     ("down wgrad", 1024, 2816, 4096, True, True, native.EPI_F32),
+    ("o wgrad", 1024, 1024, 4096, True, True, native.EPI_F32),
+    ("o dgrad", 4096, 1024, 1024, False, True, native.EPI_BF16),
+    ("down dgrad", 4096, 2816, 1024, False, True, native.EPI_BF16),
     ("head wgrad", 32000, 1024, 4096, True, True, native.EPI_F32),
 ]
 
 
 def main():
     dev = torch.device("cuda")
+    sem = torch.zeros(1 << 16, dtype=torch.int32, device=dev)
+    native.gemm_set_workspace(sem)
     res = []
     for name, M, N, K, a_mn, b_mn, epi in SHAPES:
         A = torch.randn((K, M) if a_mn else (M, K), device=dev).to(torch.bfloat16)
         B = torch.randn((K, N) if b_mn else (N, K), device=dev).to(torch.bfloat16)
         if epi == native.EPI_F32:
             C = torch.zeros(M, N, device=dev)
+        elif epi == "rope":
+            C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
         elif epi == native.EPI_SWIGLU:
             C = torch.empty(M, N // 2, device=dev, dtype=torch.bfloat16)
         else:
@@ -44,7 +52,12 @@ def main():
         R = torch.randn(M, N, device=dev).to(torch.bfloat16) if epi == native.EPI_BF16_RESID else None
         ldc = N // 2 if epi == native.EPI_SWIGLU else N
 
+        cs = torch.randn(1024, 32, 2, device=dev)
+
         def run():
+            if epi == "rope":
+                return native.gemm_rope(A, B, C, M=M, N=N, K=K, lda=K, ldb=K, ldc=N, cos_sin=cs, rope_cols=2048, T=1024,
+                                        head_dim=64)
             native.gemm(A, B, C, M=M, N=N, K=K, lda=A.shape[1], ldb=B.shape[1], ldc=ldc, a_mn=a_mn, b_mn=b_mn,
                         epilogue=epi, R=R, C2=C2, ldc2=N, beta=1.0 if epi == native.EPI_F32 else 0.0)
 
