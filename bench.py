@@ -169,6 +169,45 @@ def gemm_roofline(tr, peak_tflops: float, reps: int = 5) -> dict:
             "gemm_ms_per_step": round(total_ms, 3), "per_shape": per}
 
 
+def time_full_pp(args, rc_name, rank=0, world=1, local=0):
+    """Same protocol on the full sequential pipeline (dtfm_full, k=0) of the same model on the same
+    GPUs — the metric's "vs full PP" comparison.  Returns ms/step (max over ranks)."""
+    import torch
+
+    from paper_2502_19913_b200.configs import get_config
+    from paper_2502_19913_b200.executor import Trainer
+    from paper_2502_19913_b200.model import synthetic_tokens
+
+    rf = get_config(rc_name + "-full")
+    tokens = synthetic_tokens(rf.model, rf.M, rf.b, rf.T, seed=1234)
+    tr = Trainer(rf.schedule(), rf.topology(), rf.sim_config(), rf.model, rf.assignment, b=rf.b, T=rf.T,
+                 rank=rank, world=world, device=local)
+    dev_inputs = {k: v.cuda() for k, v in tr._stage_inputs(tokens).items()}
+    for _ in range(max(1, args.warmup)):
+        tr.step(dev_inputs)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    e0.record(tr.stream)
+    for _ in range(args.steps):
+        tr.step(dev_inputs)
+    e1.record(tr.stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=tr.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    del tr
+    torch.cuda.empty_cache()
+    return ms, rf
+
+
 def run_ours(args, rc):
     import torch
 
@@ -214,7 +253,16 @@ def run_ours(args, rc):
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     flops = rc.train_flops()
     roof = gemm_roofline(tr, burst)
+    h2d = tr.h2d_bytes(tokens)
     cb = cpu_baseline(rc, budget_s=15.0) if not args.no_cpu_baseline else None
+    full = None
+    if not args.no_full_pp and rc.kind == "skippipe":
+        del tr
+        torch.cuda.empty_cache()
+        fms, rf = time_full_pp(args, rc.name)
+        full = {"workload": rf.name, "kind": "dtfm_full (k=0, disjoint sequential pipelines)",
+                "ms_per_step": round(fms, 3), "tokens_per_s": round(tok / (fms / 1e3), 1),
+                "skippipe_speedup": round(fms / ms, 4)}
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
@@ -225,12 +273,13 @@ def run_ours(args, rc):
                    "l2_flush": "inputs+activations per step >> 126 MB L2", "kind": rc.kind},
         "loss": round(res["loss"], 5),
         "e2e": {"value": round(tok / (e2e_ms / 1e3), 1), "unit": "tokens/s",
-                "h2d_bytes_per_step": tr.h2d_bytes(tokens), "d2h_bytes_per_step": 4 * rc.M},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * rc.M},
         "gpu_launches": launches,
         "step_tflops": round(flops / (ms / 1e3) / 1e12, 1),
         "step_tensor_frac": round(flops / (ms / 1e3) / 1e12 / sustained, 4),
         "roofline": {**roof, "peak_kind": f"{peak_kind} burst bf16 (GEMMs timed alone)"},
         "cpu_baseline": cb,
+        "vs_full_pp": full,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -297,6 +346,14 @@ def run_ours_dist(args, rc):
     sm = t.clone()
     dist.all_reduce(sm)
     flops = rc.train_flops()
+    full = None
+    if not args.no_full_pp and rc.kind == "skippipe":
+        del tr
+        torch.cuda.empty_cache()
+        fms, rf = time_full_pp(args, rc.name, rank=rank, world=world, local=local)
+        full = {"workload": rf.name, "kind": "dtfm_full (k=0, disjoint sequential pipelines)",
+                "ms_per_step": round(fms, 3), "tokens_per_s": round(tok / (fms / 1e3), 1),
+                "skippipe_speedup": round(fms / ms, 4)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(tok / (ms / 1e3), 1), "unit": "tokens/s", "n_gpus": world,
@@ -313,6 +370,7 @@ def run_ours_dist(args, rc):
             "gpu_launches": int(launches.item()),
             "step_tflops": round(flops / (ms / 1e3) / 1e12, 1),
             "step_tensor_frac": round(flops / (ms / 1e3) / 1e12 / (sustained * world), 4),
+            "vs_full_pp": full,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -328,6 +386,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-full-pp", action="store_true", help="skip the full sequential pipeline comparison")
     args = ap.parse_args()
     from paper_2502_19913_b200.configs import get_config
 

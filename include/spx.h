@@ -71,7 +71,7 @@ int spx_gemm_bf16(const void* A, const void* B, void* C, const void* R, void* C2
 int spx_gemm_set_workspace(int32_t* sem, int64_t n_ints);
 
 /* QKV projection with RoPE fused into the epilogue: C = A.B^T, then rotate-half RoPE (position =
- * row % T, cos_sin [T][hd/2][2]) on columns [0, rope_cols) (the q and k heads).  head_dim 64 or 128. */
+ * row % T, cos_sin [hd/2][T][2], position-minor) on columns [0, rope_cols) (the q and k heads).  head_dim 64 or 128. */
 int spx_gemm_bf16_rope(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K, int64_t lda,
                        int64_t ldb, int64_t ldc, const float* cos_sin, int64_t rope_cols, int64_t T, int64_t head_dim,
                        void* stream);
@@ -98,7 +98,7 @@ int spx_rmsnorm_bwd(const void* x, const void* g, const float* rstd, const void*
 int64_t spx_rmsnorm_ws_floats(int64_t rows, int64_t d);
 
 /* ---- RoPE (rotate-half), in place on the first n_heads heads of each row; position = row % T.
- * cos_sin [T][hd/2][2] f32.  inverse = 1 rotates by -theta (backward). */
+ * cos_sin [hd/2][T][2] f32 (position-minor).  inverse = 1 rotates by -theta (backward). */
 int spx_rope(void* qkv, const float* cos_sin, int64_t rows, int64_t T, int64_t n_heads, int64_t hd, int64_t ld,
              int32_t inverse, void* stream);
 

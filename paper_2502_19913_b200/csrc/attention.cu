@@ -12,6 +12,7 @@
 // a dQ kernel (one CTA per 64-query block), so no atomics are needed and results are
 // bit-reproducible run to run.
 #include <cmath>
+#include <cstdlib>
 
 #include "spx_common.cuh"
 #include "spx_internal.h"
@@ -109,15 +110,15 @@ SPX_DEVICE void load_b_kn(uint32_t (&b)[4], const __nv_bfloat16* s, int k0, int 
 // Inverse rotate-half RoPE on a thread's accumulator fragments: the thread holds columns
 // 8i + 2t4 + {0,1} of rows r and r+8; column j and j + HD/2 sit in n-tiles i and i + HD/16.
 template <int HD>
-SPX_DEVICE void unrope_frags(float (&acc)[HD / 8][4], const float* cs, int pos0, int pos1, int t4) {
-  const float2* c0 = reinterpret_cast<const float2*>(cs) + (size_t)pos0 * (HD / 2);
-  const float2* c1 = reinterpret_cast<const float2*>(cs) + (size_t)pos1 * (HD / 2);
+SPX_DEVICE void unrope_frags(float (&acc)[HD / 8][4], const float* cs, int T, int pos0, int pos1, int t4) {
+  // cs: [hd/2][T][2] position-minor (cos, sin)
+  const float2* c = reinterpret_cast<const float2*>(cs);
 #pragma unroll
   for (int i = 0; i < HD / 16; ++i) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int j = 8 * i + 2 * t4 + (e & 1);
-      const float2 w = (e >> 1) ? c1[j] : c0[j];
+      const float2 w = c[(size_t)j * T + ((e >> 1) ? pos1 : pos0)];
       const float a = acc[i][e], b = acc[i + HD / 16][e];
       acc[i][e] = a * w.x + b * w.y;
       acc[i + HD / 16][e] = b * w.x - a * w.y;
@@ -132,7 +133,7 @@ struct Params {
   const __nv_bfloat16* dout;
   float* lse;           // [B, H, T]
   float* delta;         // [B, H, T]
-  const float* rope_cs; // bwd: [T][hd/2][2] cos/sin -> dq, dk written un-rotated (inverse RoPE)
+  const float* rope_cs; // bwd: [hd/2][T][2] cos/sin -> dq, dk written un-rotated (inverse RoPE)
   long long ld;         // qkv / dqkv row stride
   long long ldo;        // O / dO row stride
   int B, T, H, Hkv;
@@ -411,7 +412,7 @@ __global__ void __launch_bounds__(THREADS) attn_bwd_dkdv_kernel(const Params p) 
     }
   }
   const int kr = kb * BK + warp * 16 + g;
-  if (p.rope_cs) unrope_frags<HD>(dk, p.rope_cs, kr, kr + 8, t4);
+  if (p.rope_cs) unrope_frags<HD>(dk, p.rope_cs, p.T, kr, kr + 8, t4);
   __nv_bfloat16* dK0 = p.out + (row0 + kr) * p.ld + (p.H + kvh) * HD;
   __nv_bfloat16* dV0 = p.out + (row0 + kr) * p.ld + (p.H + p.Hkv + kvh) * HD;
 #pragma unroll
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(THREADS) attn_bwd_dq_kernel(const Params p) {
     }
     __syncthreads();
   }
-  if (p.rope_cs) unrope_frags<HD>(dq, p.rope_cs, qr, qr + 8, t4);
+  if (p.rope_cs) unrope_frags<HD>(dq, p.rope_cs, p.T, qr, qr + 8, t4);
   __nv_bfloat16* dQ0 = p.out + (row0 + qr) * p.ld + h * HD;
 #pragma unroll
   for (int i = 0; i < HD / 8; ++i) {
@@ -613,10 +614,23 @@ extern "C" int spx_attn_fwd(const void* qkv, void* o, float* lse, int64_t B, int
   p.B = (int)B; p.T = (int)T; p.H = (int)H; p.Hkv = (int)Hkv;
   p.scale = scale;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((hd == 64 || hd == 128) && T % 128 == 0 && !attn_use_legacy())
+    return attn_fwd_tcgen05(qkv, o, lse, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, s);
   if (hd == 48) return attn::run_fwd<48>(p, s);
   if (hd == 64) return attn::run_fwd<64>(p, s);
   return attn::run_fwd<128>(p, s);
 }
+
+namespace spx {
+// SPX_ATTN_LEGACY=1 forces the mma.sync forward (A/B comparisons; the tests check both agree).
+bool attn_use_legacy() {
+  static const bool legacy = [] {
+    const char* e = getenv("SPX_ATTN_LEGACY");
+    return e && atoi(e) != 0;
+  }();
+  return legacy;
+}
+}  // namespace spx
 
 extern "C" int spx_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, float* delta_ws,
                             void* dqkv, int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv,

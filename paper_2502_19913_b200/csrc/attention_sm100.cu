@@ -1,0 +1,299 @@
+// tcgen05 flash-attention forward for sm_100a (causal, GQA, head_dim 64 or 128).
+//
+// One CTA = 128 query rows of one (batch, head).  Warp roles:
+//   warp 0      TMA producer: Q once, then K_j / V_j (128 keys) into a 2-stage ring, all read in
+//               place from the fused QKV buffer with one SWIZZLE_128B tensor map
+//   warp 1      single-thread tcgen05.mma issuer:  S_j = Q K_j^T  (M=128, N=128, K=hd) into one of
+//               two TMEM buffers, then O += P_j V_j (M=128, N=hd, K=128; V as an MN-major operand)
+//   warp 2      TMEM allocation (512 columns: S0, S1, O)
+//   warps 4-7   softmax: thread = query row (its TMEM lane).  Reads S_j, keeps running max/sum in
+//               the exp2 domain, rescales O in TMEM when the max grows, writes P_j (bf16) into a
+//               swizzled smem tile that is the A operand of the PV MMA.
+// The S MMA of block j+1 overlaps the softmax of block j.  Heavy (late) query blocks launch first.
+// Output O and LSE match attn_fwd_kernel (attention.cu) so the backward kernels are unchanged.
+#include <cmath>
+
+#include "spx_common.cuh"
+#include "spx_internal.h"
+
+namespace spx {
+namespace fa {
+
+constexpr int BM = 128;    // query rows per CTA
+constexpr int BN = 128;    // keys per block
+constexpr int THREADS = 256;
+constexpr float LOG2E = 1.4426950408889634f;
+
+SPX_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+SPX_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+SPX_DEVICE float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+struct FwdParams {
+  __nv_bfloat16* out;  // O [B*T, ldo]
+  float* lse;          // [B, H, T]
+  long long ldo;
+  int B, T, H, Hkv;
+  float scale;
+};
+
+template <int HD>
+struct FwdSmem {
+  static constexpr int ATOM = BM * 128;              // 128 rows x 128 B (64 bf16) swizzle atom block
+  static constexpr int Q_BYTES = (HD / 64) * ATOM;   // same for one K or V tile (128 rows)
+  static constexpr int P_BYTES = 2 * ATOM;           // 128 x 128 bf16
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;      // [2]
+  static constexpr int OFF_V = OFF_K + 2 * Q_BYTES;  // [2]
+  static constexpr int OFF_P = OFF_V + 2 * Q_BYTES;
+  static constexpr int OFF_BAR = OFF_P + P_BYTES;
+  // >= 116 KB so that only one CTA is resident per SM: each CTA allocates all 512 TMEM columns
+  static constexpr int RAW = OFF_BAR + 256 + 1024;
+  static constexpr int BYTES = RAW > 116 * 1024 ? RAW : 116 * 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const FwdParams p) {
+  using L = FwdSmem<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* v_full = bars + 3;   // [2]
+  uint64_t* kv_empty = bars + 5; // [2]
+  uint64_t* s_full = bars + 7;   // [2]
+  uint64_t* p_full = bars + 9;
+  uint64_t* pv_done = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = p.T / BM;
+  const int qb = nqb - 1 - (int)blockIdx.x;  // heavy blocks first
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int kvh = h / (p.H / p.Hkv);
+  const int nkb = qb + 1;                    // causal, BM == BN
+  const int row0 = b * p.T;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmQKV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+    }
+    mbar_init(p_full, 4);
+    mbar_init(pv_done, 1);
+    fence_barrier_init();
+    fence_proxy_async();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t TM_O = 256;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    mbar_expect_tx(q_full, L::Q_BYTES);
+    for (int a = 0; a < HD / 64; ++a)
+      tma_load_2d(smem + L::OFF_Q + a * L::ATOM, &tmQKV, q_full, h * HD + 64 * a, row0 + qb * BM);
+    for (int j = 0; j < nkb; ++j) {
+      const int s = j & 1;
+      mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+      mbar_expect_tx(&k_full[s], L::Q_BYTES);
+      for (int a = 0; a < HD / 64; ++a)
+        tma_load_2d(smem + L::OFF_K + s * L::Q_BYTES + a * L::ATOM, &tmQKV, &k_full[s], (p.H + kvh) * HD + 64 * a,
+                    row0 + j * BN);
+      mbar_expect_tx(&v_full[s], L::Q_BYTES);
+      for (int a = 0; a < HD / 64; ++a)
+        tma_load_2d(smem + L::OFF_V + s * L::Q_BYTES + a * L::ATOM, &tmQKV, &v_full[s],
+                    (p.H + p.Hkv + kvh) * HD + 64 * a, row0 + j * BN);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t IDESC_S = umma_idesc_bf16(BM, BN, false, false);
+    constexpr uint32_t IDESC_O = umma_idesc_bf16(BM, HD, false, true);
+    const uint32_t sQ = smem_u32(smem + L::OFF_Q);
+    const uint32_t sP = smem_u32(smem + L::OFF_P);
+    mbar_wait(q_full, 0);
+    auto issue_pv = [&](int j) {
+      const int s = j & 1;
+      mbar_wait(p_full, j & 1);
+      mbar_wait(&v_full[s], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t sV = smem_u32(smem + L::OFF_V + s * L::Q_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < BN / 16; ++kk) {
+        const uint64_t ad = umma_desc_sw128(sP + (kk >> 2) * L::ATOM + (kk & 3) * 32, 16, 1024);
+        const uint64_t bd = umma_desc_sw128(sV + kk * 2048, L::ATOM, 1024);
+        mma_bf16_ss(tmem + TM_O, ad, bd, IDESC_O, (j > 0) || (kk > 0));
+      }
+      mma_commit(pv_done);
+      mma_commit(&kv_empty[s]);
+    };
+    for (int j = 0; j < nkb; ++j) {
+      const int s = j & 1;
+      mbar_wait(&k_full[s], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t sK = smem_u32(smem + L::OFF_K + s * L::Q_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint64_t ad = umma_desc_sw128(sQ + (kk >> 2) * L::ATOM + (kk & 3) * 32, 16, 1024);
+        const uint64_t bd = umma_desc_sw128(sK + (kk >> 2) * L::ATOM + (kk & 3) * 32, 16, 1024);
+        mma_bf16_ss(tmem + s * BN, ad, bd, IDESC_S, kk > 0);
+      }
+      mma_commit(&s_full[s]);
+      if (j > 0) issue_pv(j - 1);
+    }
+    issue_pv(nkb - 1);
+  } else if (warp >= 4) {
+    // ---------------- softmax (thread = query row) ----------------
+    const int q = warp - 4;
+    const int r = q * 32 + lane;  // row within the block
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    const float sl2 = p.scale * LOG2E;
+    float m = -INFINITY, l = 0.f;
+    uint8_t* sP = smem + L::OFF_P;
+    for (int j = 0; j < nkb; ++j) {
+      const int s = j & 1;
+      mbar_wait(&s_full[s], (j >> 1) & 1);
+      tc_fence_after();
+      float x[BN];
+#pragma unroll
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(lane_base + s * BN + c, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[c + i] = __uint_as_float(v[i]) * sl2;
+      }
+      if (j == qb) {
+#pragma unroll
+        for (int i = 0; i < BN; ++i)
+          if (i > r) x[i] = -INFINITY;
+      }
+      float mx = m;
+#pragma unroll
+      for (int i = 0; i < BN; ++i) mx = fmaxf(mx, x[i]);
+      const float alpha = ex2(m - mx);  // 0 on the first block (m = -inf)
+      m = mx;
+      float rs = 0.f;
+#pragma unroll
+      for (int i = 0; i < BN; ++i) {
+        x[i] = ex2(x[i] - m);
+        rs += x[i];
+      }
+      l = l * alpha + rs;
+      if (j > 0) {
+        mbar_wait(pv_done, (j - 1) & 1);  // O stable and the P tile free
+        tc_fence_after();
+        // rescale O rows whose max grew (warp-uniform decision; tcgen05.ld/st are warp-collective)
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+          for (int c = 0; c < HD; c += 32) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(lane_base + TM_O + c, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+            tmem_st_32x32b_x32(lane_base + TM_O + c, v);
+          }
+          tmem_st_wait();
+        }
+      }
+      // P (bf16) into the K-major SWIZZLE_128B A tile: row r, keys in two 64-key atoms
+#pragma unroll
+      for (int cch = 0; cch < BN / 8; ++cch) {
+        const int atom = cch >> 3, c16 = cch & 7;
+        uint4 v = make_uint4(pack_bf16(x[8 * cch], x[8 * cch + 1]), pack_bf16(x[8 * cch + 2], x[8 * cch + 3]),
+                             pack_bf16(x[8 * cch + 4], x[8 * cch + 5]), pack_bf16(x[8 * cch + 6], x[8 * cch + 7]));
+        *reinterpret_cast<uint4*>(sP + atom * L::ATOM + r * 128 + ((c16 ^ (r & 7)) << 4)) = v;
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // epilogue: O / l -> bf16, LSE
+    mbar_wait(pv_done, (nkb - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    const int t = qb * BM + r;
+    __nv_bfloat16* orow = p.out + (size_t)(row0 + t) * p.ldo + h * HD;
+#pragma unroll
+    for (int c = 0; c < HD; c += 32) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(lane_base + TM_O + c, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        *reinterpret_cast<uint4*>(orow + c + i) =
+            make_uint4(pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv),
+                       pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv),
+                       pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv),
+                       pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv));
+      }
+    }
+    p.lse[((size_t)b * p.H + h) * p.T + t] = (m + log2f(l)) / LOG2E;
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+template <int HD>
+int launch_fwd(const void* qkv, const FwdParams& p, long long ld_qkv, cudaStream_t s) {
+  auto encode = get_tensor_map_encoder();
+  if (!encode) return set_error(SPX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)ld_qkv, (cuuint64_t)p.B * p.T};
+  cuuint64_t strides[1] = {(cuuint64_t)ld_qkv * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(SPX_ERR_CUDA, "attn_fwd_tc: tensor map encode failed");
+  auto k = attn_fwd_tc_kernel<HD>;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem<HD>::BYTES);
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_fwd_tc attr");
+    set = true;
+  }
+  k<<<dim3(p.T / BM, p.H, p.B), THREADS, FwdSmem<HD>::BYTES, s>>>(map, p);
+  return check_launch("attn_fwd_tc_kernel");
+}
+
+}  // namespace fa
+
+// used by spx_attn_fwd (attention.cu) for head_dim 64/128 and T % 128 == 0
+int attn_fwd_tcgen05(const void* qkv, void* o, float* lse, int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd,
+                     int64_t ld_qkv, int64_t ld_o, float scale, cudaStream_t s) {
+  fa::FwdParams p{reinterpret_cast<__nv_bfloat16*>(o), lse, (long long)ld_o, (int)B, (int)T, (int)H, (int)Hkv, scale};
+  if (hd == 64) return fa::launch_fwd<64>(qkv, p, ld_qkv, s);
+  return fa::launch_fwd<128>(qkv, p, ld_qkv, s);
+}
+
+}  // namespace spx

@@ -150,8 +150,8 @@ __global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, const float* __rest
   const int rem = (int)(idx % per_row);
   const int h = rem / half, j = rem % half;
   const int t = row % T;
-  const float c = cs[((size_t)t * half + j) * 2];
-  const float s = sign * cs[((size_t)t * half + j) * 2 + 1];
+  const float c = cs[((size_t)j * T + t) * 2];
+  const float s = sign * cs[((size_t)j * T + t) * 2 + 1];
   __nv_bfloat16* p = qkv + (size_t)row * ld + (size_t)h * hd;
   const float a = __bfloat162float(p[j]), b = __bfloat162float(p[j + half]);
   p[j] = __float2bfloat16(a * c - b * s);

@@ -16,6 +16,7 @@
 // The GEMM has no counterpart in the reference (the reference has no kernels);
 // it realises the "stage compute" rows a15-a18 of SURVEY.md §8(a).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "spx_common.cuh"
@@ -25,7 +26,8 @@ namespace spx {
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_EPI_WARPS = 8;                          // 2 per TMEM lane quadrant
+constexpr int GEMM_THREADS = 128 + 32 * GEMM_EPI_WARPS;   // + TMA, MMA, TMEM-alloc, spare warps
 
 enum GemmEpilogue : int {
   EPI_BF16 = 0,        // C(bf16) = acc
@@ -48,7 +50,8 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN == 256) ? 4 : 6;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int STAGING_BYTES = GEMM_EPI_WARPS * 4096;  // one 32-row x 128-byte box per epilogue warp
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
 struct GemmArgs {
@@ -58,7 +61,7 @@ struct GemmArgs {
   void* C2;
   long long ldc, ldr, ldc2;
   float beta;
-  const float* rope_cs;  // [T][hd/2][2] (cos, sin)
+  const float* rope_cs;  // [hd/2][T][2] (cos, sin), position-minor
   int rope_cols, rope_T;
   int splits;            // split-K factor (EPI_F32 only); units = tiles * splits
   int* sem;              // per-tile split-order semaphores (zero between launches)
@@ -67,12 +70,13 @@ struct GemmArgs {
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                      const GemmArgs args) {
   using Cfg = GemmCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::STAGING_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;   // [2]
   uint64_t* tempty_bar = tfull_bar + 2;       // [2]
@@ -92,13 +96,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmC);
+    if (EPI == EPI_SWIGLU) tma_prefetch_desc(&tmC2);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);
+      mbar_init(&tempty_bar[a], GEMM_EPI_WARPS);
     }
     fence_barrier_init();
     fence_proxy_async();
@@ -170,9 +176,50 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mma_commit(&tfull_bar[acc]);
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue: TMEM -> registers -> global ----------------
+    // ---------------- epilogue: TMEM -> registers -> fused op -> swizzled smem box -> TMA ----------
+    // 8 epilogue warps: warp w reads TMEM lanes (tile rows) 32*(w%4).. and the column half
+    // (w-4)/4 of the tile.  A warp writes its rows as 32-row x 128-byte boxes through a private
+    // 4 KB staging buffer (SWIZZLE_128B: its 16-byte smem stores are bank-conflict free) and one
+    // lane issues the TMA store (or reduce-add for fp32 accumulation); the TMA unit clips rows and
+    // columns outside the matrix.
     const int wq = warp & 3;
-    const int row_in_tile = wq * 32 + lane;
+    const int half = (warp - 4) >> 2;
+    const int cb = half * (BN / 2);  // this warp's first tile column
+    uint8_t* box = smem + STAGES * Cfg::STAGE_BYTES + (warp - 4) * 4096;
+    auto box_acquire = [&]() {
+      if (lane == 0) bulk_wait_read<0>();  // the previous store from this buffer has read it
+      __syncwarp();
+    };
+    auto box_put = [&](int r, int j, uint4 v) {
+      *reinterpret_cast<uint4*>(box + r * 128 + ((j ^ (r & 7)) << 4)) = v;
+    };
+    auto box_get = [&](int r, int j) -> uint4 {
+      return *reinterpret_cast<const uint4*>(box + r * 128 + ((j ^ (r & 7)) << 4));
+    };
+    auto box_issue = [&](const CUtensorMap* m, int c0, int c1, bool reduce) {
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        if (reduce) tma_reduce_add_2d(m, box, c0, c1);
+        else tma_store_2d(m, box, c0, c1);
+        bulk_commit();
+      }
+    };
+    // 32 fp32 values -> 16-byte chunks j0..j0+3 of this lane's row (bf16)
+    auto put32 = [&](int j0, const float* f) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        box_put(lane, j0 + j,
+                make_uint4(pack_bf16(f[8 * j], f[8 * j + 1]), pack_bf16(f[8 * j + 2], f[8 * j + 3]),
+                           pack_bf16(f[8 * j + 4], f[8 * j + 5]), pack_bf16(f[8 * j + 6], f[8 * j + 7])));
+    };
+    auto ld32 = [&](uint32_t taddr, float* f) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(taddr, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+    };
     int it = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
       const int tile = u % num_tiles, split = u / num_tiles;
@@ -180,92 +227,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       const int m0 = (tile % num_m) * GEMM_BM;
       const int n0 = (tile / num_m) * BN;
+      const int rbase = m0 + wq * 32;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
-      const int row = m0 + row_in_tile;
-      const bool row_ok = row < args.M;
-      if constexpr (RopeHd<EPI>::value != 0) {
-        // RoPE fused into the QKV projection: each thread owns one row, a head's hd columns sit
-        // in one 256-wide tile, and the rotate-half pairs (j, j + hd/2) are both in registers.
-        constexpr int HD = RopeHd<EPI>::value;
-        const int t = row % args.rope_T;
-        const bool rope_tile = n0 < args.rope_cols;  // rope_cols and n0 are multiples of 256 / HD
-        // one row per thread, one position per row: the row's cos/sin are reused by every head of
-        // the tile (kept in registers for HD=64, re-read from L1 for HD=128)
-        float2 cs_reg[HD == 64 ? 32 : 1];
-        const float2* cs_row = reinterpret_cast<const float2*>(args.rope_cs) + (size_t)t * (HD / 2);
-        if constexpr (HD == 64) {
-          if (rope_tile && row_ok) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) cs_reg[j] = cs_row[j];
-          }
-        }
-#pragma unroll 1
-        for (int hb = 0; hb < BN; hb += HD) {
-          float f[HD];
-#pragma unroll
-          for (int c = 0; c < HD; c += 32) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(t_row + hb + c, v);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) f[c + j] = __uint_as_float(v[j]);
-          }
-          if (row_ok && n0 + hb < args.N) {
-            if (n0 + hb < args.rope_cols) {
-#pragma unroll
-              for (int j = 0; j < HD / 2; ++j) {
-                float2 w;
-                if constexpr (HD == 64) w = cs_reg[j];
-                else w = cs_row[j];
-                const float a = f[j], b = f[j + HD / 2];
-                f[j] = a * w.x - b * w.y;
-                f[j + HD / 2] = b * w.x + a * w.y;
-              }
-            }
-            uint4* C4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.C) + (size_t)row * args.ldc + n0 + hb);
-#pragma unroll
-            for (int q = 0; q < HD / 8; ++q)
-              C4[q] = make_uint4(pack_bf16(f[8 * q], f[8 * q + 1]), pack_bf16(f[8 * q + 2], f[8 * q + 3]),
-                                 pack_bf16(f[8 * q + 4], f[8 * q + 5]), pack_bf16(f[8 * q + 6], f[8 * q + 7]));
-          }
-        }
-      } else if (EPI == EPI_SWIGLU) {
-#pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 32) {
-          uint32_t g[32], u[32];
-          tmem_ld_32x32b_x32(t_row + c, g);
-          tmem_ld_32x32b_x32(t_row + BN / 2 + c, u);
-          tmem_ld_wait();
-          if (row_ok && n0 + c < args.N) {
-            __nv_bfloat16* H = reinterpret_cast<__nv_bfloat16*>(args.C) + (size_t)row * args.ldc + (n0 / 2 + c);
-            __nv_bfloat16* GU = reinterpret_cast<__nv_bfloat16*>(args.C2) + (size_t)row * args.ldc2 + n0 + c;
-            uint32_t hp[16], gp[16], up[16];
-#pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-              float g0 = __uint_as_float(g[j]), g1 = __uint_as_float(g[j + 1]);
-              float u0 = __uint_as_float(u[j]), u1 = __uint_as_float(u[j + 1]);
-              // silu computed from the bf16-rounded pre-activations the backward pass will see
-              float2 gr = unpack_bf16(pack_bf16(g0, g1));
-              float2 ur = unpack_bf16(pack_bf16(u0, u1));
-              float h0 = gr.x / (1.f + __expf(-gr.x)) * ur.x;
-              float h1 = gr.y / (1.f + __expf(-gr.y)) * ur.y;
-              hp[j / 2] = pack_bf16(h0, h1);
-              gp[j / 2] = pack_bf16(g0, g1);
-              up[j / 2] = pack_bf16(u0, u1);
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              reinterpret_cast<uint4*>(H)[q] = make_uint4(hp[4 * q], hp[4 * q + 1], hp[4 * q + 2], hp[4 * q + 3]);
-              reinterpret_cast<uint4*>(GU)[q] = make_uint4(gp[4 * q], gp[4 * q + 1], gp[4 * q + 2], gp[4 * q + 3]);
-              reinterpret_cast<uint4*>(GU + BN / 2)[q] =
-                  make_uint4(up[4 * q], up[4 * q + 1], up[4 * q + 2], up[4 * q + 3]);
-            }
-          }
-        }
-      } else {
-        const bool ordered = EPI == EPI_F32 && args.splits > 1;
+      if constexpr (EPI == EPI_F32) {
+        const bool ordered = args.splits > 1;
         if (ordered) {
           // deterministic split-K: split s adds into C only after split s-1 of this tile did
           int v;
@@ -275,63 +242,138 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         const bool add = (split > 0) || (args.beta != 0.f);
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = cb; c < cb + BN / 2 && n0 + c < args.N; c += 32) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(t_row + c, v);
           tmem_ld_wait();
-          if (row_ok && n0 + c < args.N) {
-            if (EPI == EPI_F32) {
-              float* C = reinterpret_cast<float*>(args.C) + (size_t)row * args.ldc + n0 + c;
-              float4* C4 = reinterpret_cast<float4*>(C);
-              if (add) {
+          box_acquire();
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                  float4 o = C4[q];
-                  o.x += __uint_as_float(v[4 * q]);
-                  o.y += __uint_as_float(v[4 * q + 1]);
-                  o.z += __uint_as_float(v[4 * q + 2]);
-                  o.w += __uint_as_float(v[4 * q + 3]);
-                  C4[q] = o;
-                }
-              } else {
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                  C4[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                      __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-              }
-            } else {
-              float f[32];
-#pragma unroll
-              for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-              if (EPI == EPI_BF16_RESID) {
-                const uint4* R4 = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(args.R) +
-                                                                 (size_t)row * args.ldr + n0 + c);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  uint4 r = R4[q];
-                  float2 a = unpack_bf16(r.x), b = unpack_bf16(r.y), cc = unpack_bf16(r.z), d = unpack_bf16(r.w);
-                  f[8 * q + 0] += a.x; f[8 * q + 1] += a.y; f[8 * q + 2] += b.x; f[8 * q + 3] += b.y;
-                  f[8 * q + 4] += cc.x; f[8 * q + 5] += cc.y; f[8 * q + 6] += d.x; f[8 * q + 7] += d.y;
-                }
-              }
-              uint4* C4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.C) + (size_t)row * args.ldc + n0 + c);
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                C4[q] = make_uint4(pack_bf16(f[8 * q], f[8 * q + 1]), pack_bf16(f[8 * q + 2], f[8 * q + 3]),
-                                   pack_bf16(f[8 * q + 4], f[8 * q + 5]), pack_bf16(f[8 * q + 6], f[8 * q + 7]));
-            }
-          }
+          for (int j = 0; j < 8; ++j) box_put(lane, j, make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+          box_issue(&tmC, n0 + c, rbase, add);
         }
         if (ordered) {
+          if (lane == 0) bulk_wait<0>();  // this warp's adds have landed in global memory
+          __syncwarp();
           __threadfence();
-          asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * GEMM_EPI_WARPS) : "memory");
           if (threadIdx.x == 128) atomicExch(args.sem + tile, split + 1 == args.splits ? 0 : split + 1);
+        }
+      } else if constexpr (EPI == EPI_SWIGLU) {
+        // tile columns [0,128) are gate, [128,256) the matching up rows of the interleaved weight;
+        // this warp handles gate/up columns [64*half, 64*half + 64)
+        const int c = 64 * half;
+        if (n0 + c < args.N) {
+          float g[32], uu[32], h[32];
+#pragma unroll 1
+          for (int part = 0; part < 3; ++part) {  // 0: H, 1: gate, 2: up
+            box_acquire();
+#pragma unroll 1
+            for (int q = 0; q < 2; ++q) {
+              ld32(t_row + c + 32 * q, g);
+              ld32(t_row + BN / 2 + c + 32 * q, uu);
+              if (part == 0) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 2) {
+                  // silu from the bf16-rounded pre-activations the backward pass will see
+                  const float2 gr = unpack_bf16(pack_bf16(g[j], g[j + 1]));
+                  const float2 ur = unpack_bf16(pack_bf16(uu[j], uu[j + 1]));
+                  h[j] = gr.x * __frcp_rn(1.f + __expf(-gr.x)) * ur.x;
+                  h[j + 1] = gr.y * __frcp_rn(1.f + __expf(-gr.y)) * ur.y;
+                }
+                put32(4 * q, h);
+              } else {
+                put32(4 * q, part == 1 ? g : uu);
+              }
+            }
+            if (part == 0) box_issue(&tmC, n0 / 2 + c, rbase, false);
+            else if (part == 1) box_issue(&tmC2, n0 + c, rbase, false);
+            else box_issue(&tmC2, n0 + BN / 2 + c, rbase, false);
+          }
+        }
+      } else if constexpr (RopeHd<EPI>::value != 0) {
+        // RoPE fused into the QKV projection.  The table is position-minor ([hd/2][T] of
+        // (cos, sin)), so for a pair index j the warp's 32 consecutive rows read one contiguous
+        // 256-byte segment.  Output box b of a head holds columns [64b, 64b+64): for HD=64 the
+        // rotated x1 (cols 0-31) and x2 (32-63) halves; for HD=128 box 0 is all x1' and box 1 x2'.
+        constexpr int HD = RopeHd<EPI>::value;
+        const int row = rbase + lane;
+        const int t = (row < args.M ? row : 0) % args.rope_T;
+        const float2* cs = reinterpret_cast<const float2*>(args.rope_cs) + t;
+        const int T = args.rope_T;
+#pragma unroll 1
+        for (int hb = cb; hb < cb + BN / 2 && n0 + hb < args.N; hb += HD) {
+          const bool rot = n0 + hb < args.rope_cols;
+#pragma unroll 1
+          for (int bx = 0; bx < HD / 64; ++bx) {
+            box_acquire();
+#pragma unroll 1
+            for (int q = 0; q < 2; ++q) {
+              // HD=64: q=0 -> x1' (pairs 0-31), q=1 -> x2' (pairs 0-31)
+              // HD=128: bx selects x1'/x2', q selects pairs 32q..32q+31
+              const int pair0 = (HD == 64) ? 0 : 32 * q;
+              const bool second = (HD == 64) ? (q == 1) : (bx == 1);
+              float x1[32], x2[32];
+              ld32(t_row + hb + pair0, x1);
+              ld32(t_row + hb + HD / 2 + pair0, x2);
+              if (rot) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                  const float2 w = cs[(size_t)(pair0 + j) * T];
+                  const float a = x1[j], b = x2[j];
+                  x1[j] = second ? (b * w.x + a * w.y) : (a * w.x - b * w.y);
+                }
+              } else if (second) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) x1[j] = x2[j];
+              }
+              put32(4 * q, x1);
+            }
+            box_issue(&tmC, n0 + hb + 64 * bx, rbase, false);
+          }
+        }
+      } else {
+        // plain bf16 store, optionally + residual R (read coalesced into the staging box first)
+#pragma unroll 1
+        for (int c = cb; c < cb + BN / 2 && n0 + c < args.N; c += 64) {
+          box_acquire();
+          if constexpr (EPI == EPI_BF16_RESID) {
+            const __nv_bfloat16* R = reinterpret_cast<const __nv_bfloat16*>(args.R);
+            uint4 rv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = (lane >> 3) + 4 * i, j = lane & 7;
+              const int grow = rbase + r, gcol = n0 + c + 8 * j;
+              rv[i] = make_uint4(0, 0, 0, 0);
+              if (grow < args.M && gcol < args.N) rv[i] = *reinterpret_cast<const uint4*>(R + (size_t)grow * args.ldr + gcol);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) box_put((lane >> 3) + 4 * i, lane & 7, rv[i]);
+            __syncwarp();
+          }
+#pragma unroll 1
+          for (int q = 0; q < 2; ++q) {
+            float f[32];
+            ld32(t_row + c + 32 * q, f);
+            if constexpr (EPI == EPI_BF16_RESID) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint4 r4 = box_get(lane, 4 * q + j);
+                const float2 a0 = unpack_bf16(r4.x), a1 = unpack_bf16(r4.y), a2 = unpack_bf16(r4.z),
+                             a3 = unpack_bf16(r4.w);
+                f[8 * j + 0] += a0.x; f[8 * j + 1] += a0.y; f[8 * j + 2] += a1.x; f[8 * j + 3] += a1.y;
+                f[8 * j + 4] += a2.x; f[8 * j + 5] += a2.y; f[8 * j + 6] += a3.x; f[8 * j + 7] += a3.y;
+              }
+            }
+            put32(4 * q, f);
+          }
+          box_issue(&tmC, n0 + c, rbase, false);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
     }
+    if (lane == 0) bulk_wait<0>();  // staging smem must outlive the TMA reads
   }
   __syncwarp();
   tc_fence_before();
@@ -343,15 +385,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // ----------------------------------------------------------------------------
 // host side
 // ----------------------------------------------------------------------------
-static int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
-                             uint32_t box_inner, uint32_t box_outer) {
+static int make_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                        uint32_t box_inner, uint32_t box_outer, bool f32 = false) {
   auto encode = get_tensor_map_encoder();
   if (!encode) return set_error(SPX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint64_t strides[1] = {ld_elems * (f32 ? 4 : 2)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+  CUresult r = encode(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                      const_cast<void*>(ptr), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -370,13 +413,24 @@ static int launch_gemm(const void* A, const void* B, long long lda, long long ld
   CUtensorMap ta, tb;
   int rc;
   // A operand: rows = M, contraction = K
-  if (A_MN) rc = make_tmap_bf16_2d(&ta, A, args.M, args.K, lda, 64, GEMM_BK);
-  else rc = make_tmap_bf16_2d(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
+  if (A_MN) rc = make_tmap_2d(&ta, A, args.M, args.K, lda, 64, GEMM_BK);
+  else rc = make_tmap_2d(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
   if (rc) return rc;
-  if (B_MN) rc = make_tmap_bf16_2d(&tb, B, args.N, args.K, ldb, 64, GEMM_BK);
-  else rc = make_tmap_bf16_2d(&tb, B, args.K, args.N, ldb, GEMM_BK, BN);
+  if (B_MN) rc = make_tmap_2d(&tb, B, args.N, args.K, ldb, 64, GEMM_BK);
+  else rc = make_tmap_2d(&tb, B, args.K, args.N, ldb, GEMM_BK, BN);
   if (rc) return rc;
 
+  // output boxes: 32 rows x 128 bytes (64 bf16 or 32 fp32 columns), SWIZZLE_128B
+  CUtensorMap tc, tc2;
+  memset(&tc2, 0, sizeof tc2);
+  if (EPI == EPI_F32) rc = make_tmap_2d(&tc, args.C, args.N, args.M, args.ldc, 32, 32, true);
+  else if (EPI == EPI_SWIGLU) rc = make_tmap_2d(&tc, args.C, args.N / 2, args.M, args.ldc, 64, 32);
+  else rc = make_tmap_2d(&tc, args.C, args.N, args.M, args.ldc, 64, 32);
+  if (rc) return rc;
+  if (EPI == EPI_SWIGLU) {
+    rc = make_tmap_2d(&tc2, args.C2, args.N, args.M, args.ldc2, 64, 32);
+    if (rc) return rc;
+  }
   auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, EPI>;
   static bool attr_set = false;  // one per template instantiation
   if (!attr_set) {
@@ -386,7 +440,7 @@ static int launch_gemm(const void* A, const void* B, long long lda, long long ld
   }
   const int tiles = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + BN - 1) / BN) * args.splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, stream>>>(ta, tb, args);
+  kern<<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, stream>>>(ta, tb, tc, tc2, args);
   return check_launch("gemm_bf16_kernel");
 }
 
@@ -411,6 +465,11 @@ static void pick_splits(GemmArgs& a, int bn) {
   const int tiles = ((a.M + GEMM_BM - 1) / GEMM_BM) * ((a.N + bn - 1) / bn);
   const int num_kb = (a.K + GEMM_BK - 1) / GEMM_BK;
   if (dev < 0 || dev >= 64 || g_sem[dev] == nullptr || tiles > g_sem_n[dev]) return;
+  static const int enabled = [] {
+    const char* e = getenv("SPX_SPLITK");
+    return e ? atoi(e) : 0;
+  }();
+  if (!enabled) return;
   const int sms = num_sms();
   double best = 0.0;
   int best_s = 1;

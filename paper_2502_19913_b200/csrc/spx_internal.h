@@ -20,4 +20,9 @@ typedef CUresult (*TensorMapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint3
                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 TensorMapEncodeFn get_tensor_map_encoder();
 
+// tcgen05 attention forward (attention_sm100.cu); head_dim 64/128, T % 128 == 0
+int attn_fwd_tcgen05(const void* qkv, void* o, float* lse, int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd,
+                     int64_t ld_qkv, int64_t ld_o, float scale, cudaStream_t s);
+bool attn_use_legacy();
+
 }  // namespace spx

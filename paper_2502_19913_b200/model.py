@@ -254,9 +254,10 @@ def unpack_stage(cfg: ModelConfig, lay: StageLayout, flat: torch.Tensor) -> dict
 
 
 def rope_cos_sin(T: int, hd: int, theta: float) -> torch.Tensor:
-    """[T, hd/2, 2] fp32 (cos, sin) of t·θ^(−2i/hd), computed in float64 then rounded."""
+    """[hd/2, T, 2] fp32 (cos, sin) of t·θ^(−2i/hd), computed in float64 then rounded.  Position-
+    minor so the kernels' per-row lookups for one pair index are contiguous across a warp."""
     inv = 1.0 / (theta ** (torch.arange(0, hd, 2, dtype=torch.float64) / hd))
-    ang = torch.arange(T, dtype=torch.float64)[:, None] * inv[None, :]
+    ang = inv[:, None] * torch.arange(T, dtype=torch.float64)[None, :]
     return torch.stack([ang.cos(), ang.sin()], dim=-1).float().contiguous()
 
 

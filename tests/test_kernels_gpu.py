@@ -21,15 +21,15 @@ def bf(x):
 
 
 def rope_table(T, hd, theta=10000.0):
-    inv = 1.0 / (theta ** (torch.arange(0, hd, 2, dtype=torch.float64) / hd))
-    ang = torch.arange(T, dtype=torch.float64)[:, None] * inv[None, :]
-    return torch.stack([ang.cos(), ang.sin()], dim=-1).float()  # [T, hd/2, 2]
+    from paper_2502_19913_b200.model import rope_cos_sin
+
+    return rope_cos_sin(T, hd, theta)  # [hd/2, T, 2], position-minor
 
 
-def rope_ref(x, cs):  # x [B, T, H, hd] fp32
+def rope_ref(x, cs):  # x [B, T, H, hd] fp32; cs [hd/2, T, 2]
     hd = x.shape[-1]
-    c = cs[..., 0][None, :, None, :]
-    s = cs[..., 1][None, :, None, :]
+    c = cs[..., 0].t()[None, :, None, :]
+    s = cs[..., 1].t()[None, :, None, :]
     x1, x2 = x[..., : hd // 2], x[..., hd // 2:]
     return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1)
 

@@ -52,7 +52,7 @@ def main():
         R = torch.randn(M, N, device=dev).to(torch.bfloat16) if epi == native.EPI_BF16_RESID else None
         ldc = N // 2 if epi == native.EPI_SWIGLU else N
 
-        cs = torch.randn(1024, 32, 2, device=dev)
+        cs = torch.randn(32, 1024, 2, device=dev)
 
         def run():
             if epi == "rope":
