@@ -561,6 +561,9 @@ static int run_bwd(const Params& p, cudaStream_t s) {
     int rc = check_launch("attn_bwd_delta_kernel");
     if (rc) return rc;
   }
+  if ((HD == 64 || HD == 128) && p.T % 128 == 0 && !attn_use_legacy())
+    return attn_bwd_tcgen05(p.qkv, p.dout, p.lse, p.delta, p.out, p.B, p.T, p.H, p.Hkv, HD, p.ld, p.ldo, p.scale,
+                            p.rope_cs, s);
   {
     const int smem = (2 * BK + 2 * BQI) * LD * 2 + 2 * BQI * 4;
     auto k = attn_bwd_dkdv_kernel<HD>;

@@ -1,0 +1,492 @@
+// tcgen05 flash-attention backward for sm_100a (causal, GQA, head_dim 64/128), deterministic.
+//
+// Two kernels, no atomics (every output element is written by exactly one CTA):
+//   dkdv: CTA = 128 keys of one (batch, kv-head); loops over the GQA group and the query blocks
+//         at or after it.  Per step: S^T = K Q^T and dP^T = V dO^T (M=128 keys, N=128 queries) in
+//         TMEM; 8 elementwise warps (thread = key row, half the query columns each) form
+//         P^T = exp2(S^T*scale*log2e - lse*log2e) and dS^T = P^T (dP^T - D) as bf16 swizzled
+//         smem tiles; then dV += P^T dO and dK += dS^T Q accumulate in TMEM (dO and Q tiles are
+//         re-used as MN-major B operands).
+//   dq:   CTA = 128 queries of one head; loops over key blocks 0..its own.  S = Q K^T and
+//         dP = dO V^T in TMEM, dS (bf16 smem) -> dQ += dS K (K re-used as MN-major B).
+// Both write bf16 gradients into the dQKV buffer (same layout as QKV) with the inverse RoPE
+// applied to dq/dk when a table is given, scale folded in.  D = rowsum(dO*O) comes from
+// attn_bwd_delta_kernel (attention.cu).
+#include <cmath>
+
+#include "spx_common.cuh"
+#include "spx_internal.h"
+
+namespace spx {
+namespace fab {
+
+constexpr int BLK = 128;                 // rows per block (queries and keys)
+constexpr int EW_WARPS = 8;              // elementwise warps: 2 per TMEM lane quadrant
+constexpr int THREADS = 128 + 32 * EW_WARPS;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr int ATOM = BLK * 128;          // 128 rows x 128 B swizzle atom block
+
+SPX_DEVICE float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+SPX_DEVICE void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+struct BwdParams {
+  __nv_bfloat16* dqkv;   // [B*T, ld]
+  const float* lse;      // [B, H, T]
+  const float* delta;    // [B, H, T]
+  const float* rope_cs;  // [hd/2][T][2] or null
+  long long ld;
+  int B, T, H, Hkv;
+  float scale;
+};
+
+// store one 128-column bf16 tile row of P^T / dS^T / dS (K-major SWIZZLE_128B, two 64-col atoms)
+SPX_DEVICE void put_row8(uint8_t* tile, int r, int c8, const float* v) {
+  const int atom = c8 >> 3, chunk = c8 & 7;
+  *reinterpret_cast<uint4*>(tile + atom * ATOM + r * 128 + ((chunk ^ (r & 7)) << 4)) =
+      make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+}
+
+// write a 128 x HD accumulator row (TMEM lane) as bf16, optionally through the inverse RoPE
+template <int HD>
+SPX_DEVICE void store_grad_row(uint32_t taddr, __nv_bfloat16* dst, float scale, const float* cs, int T, int pos) {
+  if (cs) {
+    const float2* c2 = reinterpret_cast<const float2*>(cs);
+#pragma unroll 1
+    for (int j0 = 0; j0 < HD / 2; j0 += 32) {
+      uint32_t a[32], b[32];
+      tmem_ld_32x32b_x32(taddr + j0, a);
+      tmem_ld_32x32b_x32(taddr + HD / 2 + j0, b);
+      tmem_ld_wait();
+      float o1[32], o2[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float2 w = c2[(size_t)(j0 + j) * T + pos];
+        const float x1 = __uint_as_float(a[j]) * scale, x2 = __uint_as_float(b[j]) * scale;
+        o1[j] = x1 * w.x + x2 * w.y;
+        o2[j] = x2 * w.x - x1 * w.y;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        *reinterpret_cast<uint4*>(dst + j0 + j) =
+            make_uint4(pack_bf16(o1[j], o1[j + 1]), pack_bf16(o1[j + 2], o1[j + 3]), pack_bf16(o1[j + 4], o1[j + 5]),
+                       pack_bf16(o1[j + 6], o1[j + 7]));
+        *reinterpret_cast<uint4*>(dst + HD / 2 + j0 + j) =
+            make_uint4(pack_bf16(o2[j], o2[j + 1]), pack_bf16(o2[j + 2], o2[j + 3]), pack_bf16(o2[j + 4], o2[j + 5]),
+                       pack_bf16(o2[j + 6], o2[j + 7]));
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < HD; c += 32) {
+      uint32_t a[32];
+      tmem_ld_32x32b_x32(taddr + c, a);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; j += 8)
+        *reinterpret_cast<uint4*>(dst + c + j) = make_uint4(
+            pack_bf16(__uint_as_float(a[j]) * scale, __uint_as_float(a[j + 1]) * scale),
+            pack_bf16(__uint_as_float(a[j + 2]) * scale, __uint_as_float(a[j + 3]) * scale),
+            pack_bf16(__uint_as_float(a[j + 4]) * scale, __uint_as_float(a[j + 5]) * scale),
+            pack_bf16(__uint_as_float(a[j + 6]) * scale, __uint_as_float(a[j + 7]) * scale));
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// dK / dV
+// ------------------------------------------------------------------------------------------
+template <int HD>
+struct DkdvSmem {
+  static constexpr int NST = HD == 64 ? 2 : 1;      // Q/dO ring depth
+  static constexpr int TILE = (HD / 64) * ATOM;     // 128 x HD bf16
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + TILE;
+  static constexpr int OFF_Q = OFF_V + TILE;        // [NST]
+  static constexpr int OFF_DO = OFF_Q + NST * TILE; // [NST]
+  static constexpr int OFF_PT = OFF_DO + NST * TILE;
+  static constexpr int OFF_DST = OFF_PT + 2 * ATOM;
+  static constexpr int OFF_LSE = OFF_DST + 2 * ATOM;  // [NST][128] f32
+  static constexpr int OFF_D = OFF_LSE + NST * 512;   // [NST][128] f32
+  static constexpr int OFF_BAR = OFF_D + NST * 512;
+  static constexpr int BYTES = OFF_BAR + 256 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
+                            const BwdParams p) {
+  using L = DkdvSmem<HD>;
+  constexpr int NST = L::NST;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* full = bars + 1;      // [NST]
+  uint64_t* empty = bars + 3;     // [NST]
+  uint64_t* sdp_full = bars + 5;
+  uint64_t* p_ready = bars + 6;
+  uint64_t* mma2_done = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = p.T / BLK;
+  const int jb = nqb - 1 - (int)blockIdx.x;  // key block; heavy (early) blocks first
+  const int kvh = blockIdx.y, b = blockIdx.z;
+  const int group = p.H / p.Hkv;
+  const int nq = nqb - jb;                   // query blocks jb..nqb-1
+  const int n_it = group * nq;
+  const int row0 = b * p.T;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmQKV);
+    tma_prefetch_desc(&tmDO);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(sdp_full, 1);
+    mbar_init(p_ready, EW_WARPS);
+    mbar_init(mma2_done, 1);
+    fence_barrier_init();
+    fence_proxy_async();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DV = 256, TM_DK = 256 + HD;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- producer ----------------
+    mbar_expect_tx(kv_full, 2 * L::TILE);
+    for (int a = 0; a < HD / 64; ++a) {
+      tma_load_2d(smem + L::OFF_K + a * ATOM, &tmQKV, kv_full, (p.H + kvh) * HD + 64 * a, row0 + jb * BLK);
+      tma_load_2d(smem + L::OFF_V + a * ATOM, &tmQKV, kv_full, (p.H + p.Hkv + kvh) * HD + 64 * a, row0 + jb * BLK);
+    }
+    for (int it = 0; it < n_it; ++it) {
+      const int s = it % NST;
+      const int h = kvh * group + it / nq, qb = jb + it % nq;
+      mbar_wait(&empty[s], ((it / NST) & 1) ^ 1);
+      mbar_expect_tx(&full[s], 2 * L::TILE + 1024);
+      for (int a = 0; a < HD / 64; ++a) {
+        tma_load_2d(smem + L::OFF_Q + s * L::TILE + a * ATOM, &tmQKV, &full[s], h * HD + 64 * a, row0 + qb * BLK);
+        tma_load_2d(smem + L::OFF_DO + s * L::TILE + a * ATOM, &tmDO, &full[s], h * HD + 64 * a, row0 + qb * BLK);
+      }
+      const size_t off = ((size_t)b * p.H + h) * p.T + qb * BLK;
+      bulk_load(smem + L::OFF_LSE + s * 512, p.lse + off, 512, &full[s]);
+      bulk_load(smem + L::OFF_D + s * 512, p.delta + off, 512, &full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t ID_S = umma_idesc_bf16(BLK, BLK, false, false);   // K.Q^T, V.dO^T
+    constexpr uint32_t ID_G = umma_idesc_bf16(BLK, HD, false, true);     // P^T.dO, dS^T.Q
+    const uint32_t sK = smem_u32(smem + L::OFF_K), sV = smem_u32(smem + L::OFF_V);
+    const uint32_t sPT = smem_u32(smem + L::OFF_PT), sDST = smem_u32(smem + L::OFF_DST);
+    mbar_wait(kv_full, 0);
+    for (int it = 0; it < n_it; ++it) {
+      const int s = it % NST;
+      mbar_wait(&full[s], (it / NST) & 1);
+      if (it > 0) mbar_wait(p_ready, (it - 1) & 1);  // S / dP of the previous step consumed
+      tc_fence_after();
+      const uint32_t sQ = smem_u32(smem + L::OFF_Q + s * L::TILE), sDO = smem_u32(smem + L::OFF_DO + s * L::TILE);
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint32_t ko = (kk >> 2) * ATOM + (kk & 3) * 32;
+        mma_bf16_ss(tmem + TM_S, umma_desc_sw128(sK + ko, 16, 1024), umma_desc_sw128(sQ + ko, 16, 1024), ID_S, kk > 0);
+        mma_bf16_ss(tmem + TM_DP, umma_desc_sw128(sV + ko, 16, 1024), umma_desc_sw128(sDO + ko, 16, 1024), ID_S,
+                    kk > 0);
+      }
+      mma_commit(sdp_full);
+      mbar_wait(p_ready, it & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < BLK / 16; ++kk) {
+        const uint32_t ao = (kk >> 2) * ATOM + (kk & 3) * 32;
+        const uint32_t bo = kk * 2048;
+        const uint32_t acc = (it > 0) || (kk > 0);
+        mma_bf16_ss(tmem + TM_DV, umma_desc_sw128(sPT + ao, 16, 1024), umma_desc_sw128(sDO + bo, ATOM, 1024), ID_G,
+                    acc);
+        mma_bf16_ss(tmem + TM_DK, umma_desc_sw128(sDST + ao, 16, 1024), umma_desc_sw128(sQ + bo, ATOM, 1024), ID_G,
+                    acc);
+      }
+      mma_commit(mma2_done);
+      mma_commit(&empty[s]);
+    }
+  } else if (warp >= 4) {
+    // ---------------- elementwise: thread = key row, 64 query columns ----------------
+    const int quad = warp & 3, half = (warp - 4) >> 2;
+    const int r = quad * 32 + lane;  // key row within the block
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+    const float sl2 = p.scale * LOG2E;
+    uint8_t* sPT = smem + L::OFF_PT;
+    uint8_t* sDST = smem + L::OFF_DST;
+    for (int it = 0; it < n_it; ++it) {
+      const int s = it % NST;
+      const int qb = jb + it % nq;
+      const bool diag = qb == jb;
+      mbar_wait(&full[s], (it / NST) & 1);  // lse / D of this step are in smem
+      mbar_wait(sdp_full, it & 1);
+      tc_fence_after();
+      if (it > 0) mbar_wait(mma2_done, (it - 1) & 1);  // P^T / dS^T tiles free
+      const float* lse = reinterpret_cast<const float*>(smem + L::OFF_LSE + s * 512);
+      const float* dd = reinterpret_cast<const float*>(smem + L::OFF_D + s * 512);
+#pragma unroll 1
+      for (int c0 = 64 * half; c0 < 64 * half + 64; c0 += 32) {
+        uint32_t sv[32], dv[32];
+        tmem_ld_32x32b_x32(lane_base + TM_S + c0, sv);
+        tmem_ld_32x32b_x32(lane_base + TM_DP + c0, dv);
+        tmem_ld_wait();
+        float pv[32], ds[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int c = c0 + j;
+          float pp = ex2(__uint_as_float(sv[j]) * sl2 - lse[c] * LOG2E);
+          if (diag && c < r) pp = 0.f;  // query before key
+          pv[j] = pp;
+          ds[j] = pp * (__uint_as_float(dv[j]) - dd[c]);
+        }
+#pragma unroll
+        for (int q8 = 0; q8 < 4; ++q8) {
+          put_row8(sPT, r, (c0 >> 3) + q8, pv + 8 * q8);
+          put_row8(sDST, r, (c0 >> 3) + q8, ds + 8 * q8);
+        }
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_ready);
+    }
+    // outputs: half 0 writes dV, half 1 writes dK (scaled, inverse RoPE)
+    mbar_wait(mma2_done, (n_it - 1) & 1);
+    tc_fence_after();
+    const int key = jb * BLK + r;
+    __nv_bfloat16* dst = p.dqkv + (size_t)(row0 + key) * p.ld;
+    if (half == 0) store_grad_row<HD>(lane_base + TM_DV, dst + (p.H + p.Hkv + kvh) * HD, 1.f, nullptr, p.T, key);
+    else store_grad_row<HD>(lane_base + TM_DK, dst + (p.H + kvh) * HD, p.scale, p.rope_cs, p.T, key);
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+// ------------------------------------------------------------------------------------------
+// dQ
+// ------------------------------------------------------------------------------------------
+template <int HD>
+struct DqSmem {
+  static constexpr int TILE = (HD / 64) * ATOM;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_DO = OFF_Q + TILE;
+  static constexpr int OFF_K = OFF_DO + TILE;     // [2]
+  static constexpr int OFF_V = OFF_K + 2 * TILE;  // [2]
+  static constexpr int OFF_DS = OFF_V + 2 * TILE;
+  static constexpr int OFF_BAR = OFF_DS + 2 * ATOM;
+  static constexpr int BYTES = OFF_BAR + 256 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
+                          const BwdParams p) {
+  using L = DqSmem<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* qdo_full = bars + 0;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* sdp_full = bars + 5;
+  uint64_t* p_ready = bars + 6;
+  uint64_t* mma2_done = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = p.T / BLK;
+  const int ib = nqb - 1 - (int)blockIdx.x;  // heavy blocks first
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int kvh = h / (p.H / p.Hkv);
+  const int nkb = ib + 1;
+  const int row0 = b * p.T;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmQKV);
+    tma_prefetch_desc(&tmDO);
+    mbar_init(qdo_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(sdp_full, 1);
+    mbar_init(p_ready, EW_WARPS);
+    mbar_init(mma2_done, 1);
+    fence_barrier_init();
+    fence_proxy_async();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 256;
+
+  if (warp == 0 && lane == 0) {
+    mbar_expect_tx(qdo_full, 2 * L::TILE);
+    for (int a = 0; a < HD / 64; ++a) {
+      tma_load_2d(smem + L::OFF_Q + a * ATOM, &tmQKV, qdo_full, h * HD + 64 * a, row0 + ib * BLK);
+      tma_load_2d(smem + L::OFF_DO + a * ATOM, &tmDO, qdo_full, h * HD + 64 * a, row0 + ib * BLK);
+    }
+    for (int j = 0; j < nkb; ++j) {
+      const int s = j & 1;
+      mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+      mbar_expect_tx(&kv_full[s], 2 * L::TILE);
+      for (int a = 0; a < HD / 64; ++a) {
+        tma_load_2d(smem + L::OFF_K + s * L::TILE + a * ATOM, &tmQKV, &kv_full[s], (p.H + kvh) * HD + 64 * a,
+                    row0 + j * BLK);
+        tma_load_2d(smem + L::OFF_V + s * L::TILE + a * ATOM, &tmQKV, &kv_full[s], (p.H + p.Hkv + kvh) * HD + 64 * a,
+                    row0 + j * BLK);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t ID_S = umma_idesc_bf16(BLK, BLK, false, false);  // Q.K^T, dO.V^T
+    constexpr uint32_t ID_G = umma_idesc_bf16(BLK, HD, false, true);    // dS.K
+    const uint32_t sQ = smem_u32(smem + L::OFF_Q), sDO = smem_u32(smem + L::OFF_DO);
+    const uint32_t sDS = smem_u32(smem + L::OFF_DS);
+    mbar_wait(qdo_full, 0);
+    for (int j = 0; j < nkb; ++j) {
+      const int s = j & 1;
+      mbar_wait(&kv_full[s], (j >> 1) & 1);
+      if (j > 0) mbar_wait(p_ready, (j - 1) & 1);
+      tc_fence_after();
+      const uint32_t sK = smem_u32(smem + L::OFF_K + s * L::TILE), sV = smem_u32(smem + L::OFF_V + s * L::TILE);
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint32_t ko = (kk >> 2) * ATOM + (kk & 3) * 32;
+        mma_bf16_ss(tmem + TM_S, umma_desc_sw128(sQ + ko, 16, 1024), umma_desc_sw128(sK + ko, 16, 1024), ID_S, kk > 0);
+        mma_bf16_ss(tmem + TM_DP, umma_desc_sw128(sDO + ko, 16, 1024), umma_desc_sw128(sV + ko, 16, 1024), ID_S,
+                    kk > 0);
+      }
+      mma_commit(sdp_full);
+      mbar_wait(p_ready, j & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < BLK / 16; ++kk) {
+        const uint32_t ao = (kk >> 2) * ATOM + (kk & 3) * 32;
+        mma_bf16_ss(tmem + TM_DQ, umma_desc_sw128(sDS + ao, 16, 1024), umma_desc_sw128(sK + kk * 2048, ATOM, 1024),
+                    ID_G, (j > 0) || (kk > 0));
+      }
+      mma_commit(mma2_done);
+      mma_commit(&kv_empty[s]);
+    }
+  } else if (warp >= 4) {
+    // ---------------- elementwise: thread = query row, 64 key columns ----------------
+    const int quad = warp & 3, half = (warp - 4) >> 2;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+    const float sl2 = p.scale * LOG2E;
+    const int t = ib * BLK + r;
+    const size_t stat = ((size_t)b * p.H + h) * p.T + t;
+    const float lse2 = p.lse[stat] * LOG2E, dr = p.delta[stat];
+    uint8_t* sDS = smem + L::OFF_DS;
+    for (int j = 0; j < nkb; ++j) {
+      const bool diag = j == ib;
+      mbar_wait(sdp_full, j & 1);
+      tc_fence_after();
+      if (j > 0) mbar_wait(mma2_done, (j - 1) & 1);  // dS tile free
+#pragma unroll 1
+      for (int c0 = 64 * half; c0 < 64 * half + 64; c0 += 32) {
+        uint32_t sv[32], dv[32];
+        tmem_ld_32x32b_x32(lane_base + TM_S + c0, sv);
+        tmem_ld_32x32b_x32(lane_base + TM_DP + c0, dv);
+        tmem_ld_wait();
+        float ds[32];
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+          float pp = ex2(__uint_as_float(sv[jj]) * sl2 - lse2);
+          if (diag && c0 + jj > r) pp = 0.f;  // key after query
+          ds[jj] = pp * (__uint_as_float(dv[jj]) - dr);
+        }
+#pragma unroll
+        for (int q8 = 0; q8 < 4; ++q8) put_row8(sDS, r, (c0 >> 3) + q8, ds + 8 * q8);
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_ready);
+    }
+    mbar_wait(mma2_done, (nkb - 1) & 1);
+    tc_fence_after();
+    if (half == 0)
+      store_grad_row<HD>(lane_base + TM_DQ, p.dqkv + (size_t)(row0 + t) * p.ld + h * HD, p.scale, p.rope_cs, p.T, t);
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+static int make_map(CUtensorMap* m, const void* ptr, long long ld, long long rows) {
+  auto encode = get_tensor_map_encoder();
+  if (!encode) return set_error(SPX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? SPX_OK : set_error(SPX_ERR_CUDA, "attn_bwd_tc: tensor map encode failed");
+}
+
+template <int HD>
+static int launch(const void* qkv, const void* dout, long long ld_o, const BwdParams& p, cudaStream_t s) {
+  CUtensorMap mq, md;
+  int rc = make_map(&mq, qkv, p.ld, (long long)p.B * p.T);
+  if (rc) return rc;
+  rc = make_map(&md, dout, ld_o, (long long)p.B * p.T);
+  if (rc) return rc;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         DkdvSmem<HD>::BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               DqSmem<HD>::BYTES);
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc attr");
+    set = true;
+  }
+  const int nqb = p.T / BLK;
+  attn_bwd_dkdv_tc_kernel<HD><<<dim3(nqb, p.Hkv, p.B), THREADS, DkdvSmem<HD>::BYTES, s>>>(mq, md, p);
+  rc = check_launch("attn_bwd_dkdv_tc_kernel");
+  if (rc) return rc;
+  attn_bwd_dq_tc_kernel<HD><<<dim3(nqb, p.H, p.B), THREADS, DqSmem<HD>::BYTES, s>>>(mq, md, p);
+  return check_launch("attn_bwd_dq_tc_kernel");
+}
+
+}  // namespace fab
+
+// used by spx_attn_bwd (attention.cu) for head_dim 64/128, T % 128 == 0; delta must be computed
+int attn_bwd_tcgen05(const void* qkv, const void* dout, const float* lse, const float* delta, void* dqkv, int64_t B,
+                     int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv, int64_t ld_o, float scale,
+                     const float* rope_cs, cudaStream_t s) {
+  fab::BwdParams p{reinterpret_cast<__nv_bfloat16*>(dqkv), lse, delta, rope_cs, (long long)ld_qkv,
+                   (int)B, (int)T, (int)H, (int)Hkv, scale};
+  if (hd == 64) return fab::launch<64>(qkv, dout, ld_o, p, s);
+  return fab::launch<128>(qkv, dout, ld_o, p, s);
+}
+
+}  // namespace spx

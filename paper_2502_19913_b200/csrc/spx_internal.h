@@ -23,6 +23,9 @@ TensorMapEncodeFn get_tensor_map_encoder();
 // tcgen05 attention forward (attention_sm100.cu); head_dim 64/128, T % 128 == 0
 int attn_fwd_tcgen05(const void* qkv, void* o, float* lse, int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd,
                      int64_t ld_qkv, int64_t ld_o, float scale, cudaStream_t s);
+int attn_bwd_tcgen05(const void* qkv, const void* dout, const float* lse, const float* delta, void* dqkv, int64_t B,
+                     int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv, int64_t ld_o, float scale,
+                     const float* rope_cs, cudaStream_t s);
 bool attn_use_legacy();
 
 }  // namespace spx

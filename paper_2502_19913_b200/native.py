@@ -198,7 +198,7 @@ def attn_bwd(qkv, o, dout, lse, delta_ws, dqkv, *, B, T, H, Hkv, hd, ld_qkv, ld_
              stream=None) -> None:
     _check(load().spx_attn_bwd(_ptr(qkv), _ptr(o), _ptr(dout), _ptr(lse), _ptr(delta_ws), _ptr(dqkv), B, T, H, Hkv,
                                hd, ld_qkv, ld_o, float(scale), _ptr(rope_cs), _stream(stream)), "spx_attn_bwd")
-    _count(3)
+    _count(3)  # delta + dK/dV + dQ
 
 
 def rmsnorm_fwd(x, g, y, rstd, *, rows, d, eps, stream=None) -> None:
