@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* sdp_full = bars + 5;
   uint64_t* p_ready = bars + 6;
   uint64_t* mma2_done = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  uint64_t* tmem_free = bars + 8;   // S / dP of the current step copied to registers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = p.T / BLK;
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(sdp_full, 1);
     mbar_init(p_ready, EW_WARPS);
     mbar_init(mma2_done, 1);
+    mbar_init(tmem_free, EW_WARPS);
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -195,10 +197,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t sK = smem_u32(smem + L::OFF_K), sV = smem_u32(smem + L::OFF_V);
     const uint32_t sPT = smem_u32(smem + L::OFF_PT), sDST = smem_u32(smem + L::OFF_DST);
     mbar_wait(kv_full, 0);
-    for (int it = 0; it < n_it; ++it) {
+    auto issue_sdp = [&](int it) {
       const int s = it % NST;
       mbar_wait(&full[s], (it / NST) & 1);
-      if (it > 0) mbar_wait(p_ready, (it - 1) & 1);  // S / dP of the previous step consumed
       tc_fence_after();
       const uint32_t sQ = smem_u32(smem + L::OFF_Q + s * L::TILE), sDO = smem_u32(smem + L::OFF_DO + s * L::TILE);
 #pragma unroll
@@ -209,8 +210,19 @@ __global__ void __launch_bounds__(THREADS, 1)
                     kk > 0);
       }
       mma_commit(sdp_full);
+    };
+    issue_sdp(0);
+    for (int it = 0; it < n_it; ++it) {
+      const int s = it % NST;
+      // S/dP of step it are in registers: compute step it+1's S/dP while the warps do the math
+      mbar_wait(tmem_free, it & 1);
+      tc_fence_after();
+      // with a 2-deep Q/dO ring the next S/dP can go first; with one stage the next Q/dO tile only
+      // lands after this step's dV/dK MMAs released the stage
+      if (NST > 1 && it + 1 < n_it) issue_sdp(it + 1);
       mbar_wait(p_ready, it & 1);
       tc_fence_after();
+      const uint32_t sQ = smem_u32(smem + L::OFF_Q + s * L::TILE), sDO = smem_u32(smem + L::OFF_DO + s * L::TILE);
 #pragma unroll
       for (int kk = 0; kk < BLK / 16; ++kk) {
         const uint32_t ao = (kk >> 2) * ATOM + (kk & 3) * 32;
@@ -223,6 +235,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       mma_commit(mma2_done);
       mma_commit(&empty[s]);
+      if (NST == 1 && it + 1 < n_it) issue_sdp(it + 1);
     }
   } else if (warp >= 4) {
     // ---------------- elementwise: thread = key row, 64 query columns ----------------
@@ -239,32 +252,34 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(&full[s], (it / NST) & 1);  // lse / D of this step are in smem
       mbar_wait(sdp_full, it & 1);
       tc_fence_after();
-      if (it > 0) mbar_wait(mma2_done, (it - 1) & 1);  // P^T / dS^T tiles free
       const float* lse = reinterpret_cast<const float*>(smem + L::OFF_LSE + s * 512);
       const float* dd = reinterpret_cast<const float*>(smem + L::OFF_D + s * 512);
-#pragma unroll 1
-      for (int c0 = 64 * half; c0 < 64 * half + 64; c0 += 32) {
-        uint32_t sv[32], dv[32];
-        tmem_ld_32x32b_x32(lane_base + TM_S + c0, sv);
-        tmem_ld_32x32b_x32(lane_base + TM_DP + c0, dv);
-        tmem_ld_wait();
-        float pv[32], ds[32];
+      const int cb = 64 * half;
+      uint32_t sv[64], dv[64];
+      tmem_ld_32x32b_x32(lane_base + TM_S + cb, *reinterpret_cast<uint32_t(*)[32]>(sv));
+      tmem_ld_32x32b_x32(lane_base + TM_S + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+      tmem_ld_32x32b_x32(lane_base + TM_DP + cb, *reinterpret_cast<uint32_t(*)[32]>(dv));
+      tmem_ld_32x32b_x32(lane_base + TM_DP + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tmem_free);
+      if (it > 0) mbar_wait(mma2_done, (it - 1) & 1);  // P^T / dS^T tiles free
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int c = c0 + j;
-          float pp = ex2(__uint_as_float(sv[j]) * sl2 - lse[c] * LOG2E);
+      for (int c8 = 0; c8 < 8; ++c8) {
+        float pv[8], ds[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int c = cb + 8 * c8 + j;
+          float pp = ex2(fmaf(__uint_as_float(sv[8 * c8 + j]), sl2, -lse[c] * LOG2E));
           if (diag && c < r) pp = 0.f;  // query before key
           pv[j] = pp;
-          ds[j] = pp * (__uint_as_float(dv[j]) - dd[c]);
+          ds[j] = pp * (__uint_as_float(dv[8 * c8 + j]) - dd[c]);
         }
-#pragma unroll
-        for (int q8 = 0; q8 < 4; ++q8) {
-          put_row8(sPT, r, (c0 >> 3) + q8, pv + 8 * q8);
-          put_row8(sDST, r, (c0 >> 3) + q8, ds + 8 * q8);
-        }
+        put_row8(sPT, r, (cb >> 3) + c8, pv);
+        put_row8(sDST, r, (cb >> 3) + c8, ds);
       }
       fence_proxy_async();
-      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_ready);
     }
@@ -312,7 +327,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* sdp_full = bars + 5;
   uint64_t* p_ready = bars + 6;
   uint64_t* mma2_done = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  uint64_t* tmem_free = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = p.T / BLK;
@@ -333,6 +349,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(sdp_full, 1);
     mbar_init(p_ready, EW_WARPS);
     mbar_init(mma2_done, 1);
+    mbar_init(tmem_free, EW_WARPS);
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -366,10 +383,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t sQ = smem_u32(smem + L::OFF_Q), sDO = smem_u32(smem + L::OFF_DO);
     const uint32_t sDS = smem_u32(smem + L::OFF_DS);
     mbar_wait(qdo_full, 0);
-    for (int j = 0; j < nkb; ++j) {
+    auto issue_sdp = [&](int j) {
       const int s = j & 1;
       mbar_wait(&kv_full[s], (j >> 1) & 1);
-      if (j > 0) mbar_wait(p_ready, (j - 1) & 1);
       tc_fence_after();
       const uint32_t sK = smem_u32(smem + L::OFF_K + s * L::TILE), sV = smem_u32(smem + L::OFF_V + s * L::TILE);
 #pragma unroll
@@ -380,8 +396,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                     kk > 0);
       }
       mma_commit(sdp_full);
+    };
+    issue_sdp(0);
+    for (int j = 0; j < nkb; ++j) {
+      const int s = j & 1;
+      mbar_wait(tmem_free, j & 1);
+      tc_fence_after();
+      if (j + 1 < nkb) issue_sdp(j + 1);
       mbar_wait(p_ready, j & 1);
       tc_fence_after();
+      const uint32_t sK = smem_u32(smem + L::OFF_K + s * L::TILE);
 #pragma unroll
       for (int kk = 0; kk < BLK / 16; ++kk) {
         const uint32_t ao = (kk >> 2) * ATOM + (kk & 3) * 32;
@@ -405,25 +429,30 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool diag = j == ib;
       mbar_wait(sdp_full, j & 1);
       tc_fence_after();
+      const int cb = 64 * half;
+      uint32_t sv[64], dv[64];
+      tmem_ld_32x32b_x32(lane_base + TM_S + cb, *reinterpret_cast<uint32_t(*)[32]>(sv));
+      tmem_ld_32x32b_x32(lane_base + TM_S + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+      tmem_ld_32x32b_x32(lane_base + TM_DP + cb, *reinterpret_cast<uint32_t(*)[32]>(dv));
+      tmem_ld_32x32b_x32(lane_base + TM_DP + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tmem_free);
       if (j > 0) mbar_wait(mma2_done, (j - 1) & 1);  // dS tile free
-#pragma unroll 1
-      for (int c0 = 64 * half; c0 < 64 * half + 64; c0 += 32) {
-        uint32_t sv[32], dv[32];
-        tmem_ld_32x32b_x32(lane_base + TM_S + c0, sv);
-        tmem_ld_32x32b_x32(lane_base + TM_DP + c0, dv);
-        tmem_ld_wait();
-        float ds[32];
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
-          float pp = ex2(__uint_as_float(sv[jj]) * sl2 - lse2);
-          if (diag && c0 + jj > r) pp = 0.f;  // key after query
-          ds[jj] = pp * (__uint_as_float(dv[jj]) - dr);
+      for (int c8 = 0; c8 < 8; ++c8) {
+        float ds[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int c = cb + 8 * c8 + jj;
+          float pp = ex2(fmaf(__uint_as_float(sv[8 * c8 + jj]), sl2, -lse2));
+          if (diag && c > r) pp = 0.f;  // key after query
+          ds[jj] = pp * (__uint_as_float(dv[8 * c8 + jj]) - dr);
         }
-#pragma unroll
-        for (int q8 = 0; q8 < 4; ++q8) put_row8(sDS, r, (c0 >> 3) + q8, ds + 8 * q8);
+        put_row8(sDS, r, (cb >> 3) + c8, ds);
       }
       fence_proxy_async();
-      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_ready);
     }

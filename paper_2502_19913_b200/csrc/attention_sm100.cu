@@ -178,28 +178,29 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(&s_full[s], (j >> 1) & 1);
       tc_fence_after();
       float x[BN];
+      {
+        uint32_t* xv = reinterpret_cast<uint32_t*>(x);
 #pragma unroll
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(lane_base + s * BN + c, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) x[c + i] = __uint_as_float(v[i]) * sl2;
+        for (int c = 0; c < BN; c += 32)
+          tmem_ld_32x32b_x32(lane_base + s * BN + c, *reinterpret_cast<uint32_t(*)[32]>(xv + c));
+        tmem_ld_wait();  // one wait for the four loads
       }
       if (j == qb) {
 #pragma unroll
         for (int i = 0; i < BN; ++i)
           if (i > r) x[i] = -INFINITY;
       }
-      float mx = m;
+      // running max on the raw scores (the scale is positive), exp2 via one FFMA per element
+      float mraw = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < BN; ++i) mx = fmaxf(mx, x[i]);
+      for (int i = 0; i < BN; ++i) mraw = fmaxf(mraw, x[i]);
+      const float mx = fmaxf(m, mraw * sl2);
       const float alpha = ex2(m - mx);  // 0 on the first block (m = -inf)
       m = mx;
       float rs = 0.f;
 #pragma unroll
       for (int i = 0; i < BN; ++i) {
-        x[i] = ex2(x[i] - m);
+        x[i] = ex2(fmaf(x[i], sl2, -m));
         rs += x[i];
       }
       l = l * alpha + rs;

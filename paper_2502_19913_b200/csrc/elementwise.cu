@@ -67,67 +67,63 @@ __global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __
   if (lane == 0) rstd[row] = r;
 }
 
-// Fused RMSNorm backward: one CTA = 8 warps x RB_ROWS_PER_WARP rows.  Per row
-//   dx = dres + rstd * (g*dy - xhat * mean(xhat*g*dy)),  xhat = x * rstd
-// and the CTA's contribution to dg = sum_rows dy * xhat is accumulated in shared memory (each
-// warp owns one smem row, each lane its own columns: no atomics), reduced over the 8 warps in a
-// fixed order and written as one partial row; colsum_add_kernel then sums the partial rows in
-// order.  x and dy are read once for both outputs.
-constexpr int RB_WARPS = 8;
-constexpr int RB_ROWS_PER_WARP = 4;
-constexpr int RB_ROWS = RB_WARPS * RB_ROWS_PER_WARP;
-__global__ void __launch_bounds__(RB_WARPS * 32) rmsnorm_bwd_fused_kernel(
-    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd,
-    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx,
-    float* __restrict__ part, int rows, int d) {
-  extern __shared__ float sdg[];  // [RB_WARPS][d]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* mine = sdg + (size_t)warp * d;
-  for (int c = lane * 8; c < d; c += 256)
+// RMSNorm backward, dx:  dx = dres + rstd * (g*dy - xhat * mean(xhat*g*dy)), xhat = x*rstd.
+// One warp per row, 16-byte vectors (HBM-bound: reads x, dy, dres, writes dx).
+__global__ void rmsnorm_bwd_dx_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
+                                      const float* __restrict__ rstd, const __nv_bfloat16* __restrict__ dy,
+                                      const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx,
+                                      int rows, int d) {
+  const int row = blockIdx.x * ROW_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const size_t off = (size_t)row * d;
+  const float r = rstd[row];
+  float dot = 0.f;
+  for (int c = lane * 8; c < d; c += 256) {
+    float xf[8], w[8], gy[8];
+    load8(xf, x + off + c);
+    load8(w, g + c);
+    load8(gy, dy + off + c);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) mine[c + i] = 0.f;
-  for (int k = 0; k < RB_ROWS_PER_WARP; ++k) {
-    const int row = blockIdx.x * RB_ROWS + warp * RB_ROWS_PER_WARP + k;
-    if (row >= rows) break;
-    const size_t off = (size_t)row * d;
-    const float r = rstd[row];
-    float dot = 0.f;
-    for (int c = lane * 8; c < d; c += 256) {
-      float xf[8], w[8], gy[8];
-      load8(xf, x + off + c);
-      load8(w, g + c);
-      load8(gy, dy + off + c);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        dot += xf[i] * w[i] * gy[i];
-        mine[c + i] += gy[i] * xf[i] * r;
-      }
-    }
-    dot = warp_sum(dot) * r / d;
-    for (int c = lane * 8; c < d; c += 256) {
-      float xf[8], w[8], gy[8], o[8];
-      load8(xf, x + off + c);
-      load8(w, g + c);
-      load8(gy, dy + off + c);
-      if (dres) load8(o, dres + off + c);
-      else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = 0.f;
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] += r * (w[i] * gy[i] - xf[i] * r * dot);
-      store8(dx + off + c, o);
-    }
+    for (int i = 0; i < 8; ++i) dot += xf[i] * w[i] * gy[i];
   }
-  __syncthreads();
-  if (part) {
-    for (int c = threadIdx.x; c < d; c += blockDim.x) {
-      float acc = 0.f;
+  dot = warp_sum(dot) * r / d;
+  for (int c = lane * 8; c < d; c += 256) {
+    float xf[8], w[8], gy[8], o[8];
+    load8(xf, x + off + c);
+    load8(w, g + c);
+    load8(gy, dy + off + c);
+    if (dres) load8(o, dres + off + c);
+    else {
 #pragma unroll
-      for (int w = 0; w < RB_WARPS; ++w) acc += sdg[(size_t)w * d + c];
-      part[(size_t)blockIdx.x * d + c] = acc;
+      for (int i = 0; i < 8; ++i) o[i] = 0.f;
     }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] += r * (w[i] * gy[i] - xf[i] * r * dot);
+    store8(dx + off + c, o);
   }
+}
+
+// RMSNorm backward, dg partials: CTA (column block of 256, row chunk of DG_ROWS rows) sums
+// dy * x * rstd over its rows in order; thread = 2 adjacent columns, 128 threads per block.
+constexpr int DG_ROWS = 64;
+__global__ void __launch_bounds__(128) rmsnorm_dg_partial_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                 const float* __restrict__ rstd,
+                                                                 const __nv_bfloat16* __restrict__ dy,
+                                                                 float* __restrict__ part, int rows, int d) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (c >= d) return;
+  const int r0 = blockIdx.y * DG_ROWS, r1 = min(rows, r0 + DG_ROWS);
+  float a0 = 0.f, a1 = 0.f;
+#pragma unroll 8
+  for (int r = r0; r < r1; ++r) {
+    const float s = rstd[r];
+    const float2 xv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + (size_t)r * d + c));
+    const float2 gv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dy + (size_t)r * d + c));
+    a0 += gv.x * xv.x * s;
+    a1 += gv.y * xv.y * s;
+  }
+  *reinterpret_cast<float2*>(part + (size_t)blockIdx.y * d + c) = make_float2(a0, a1);
 }
 
 __global__ void colsum_add_kernel(const float* __restrict__ part, float* __restrict__ out, int nsplit, int d) {
@@ -386,25 +382,20 @@ extern "C" int spx_rmsnorm_fwd(const void* x, const void* g, void* y, float* rst
 extern "C" int spx_rmsnorm_bwd(const void* x, const void* g, const float* rstd, const void* dy, const void* dres,
                                void* dx, float* dg, float* ws, int64_t rows, int64_t d, void* stream) {
   if (d % 8) return set_error(SPX_ERR_ARG, "rmsnorm: d must be a multiple of 8");
-  const int blocks = (int)((rows + RB_ROWS - 1) / RB_ROWS);
-  const size_t smem = (size_t)RB_WARPS * d * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(rmsnorm_bwd_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         RB_WARPS * 4096 * (int)sizeof(float));
-    if (e != cudaSuccess) return set_cuda_error(e, "rmsnorm_bwd attr");
-    attr = true;
-  }
-  if (d > 4096) return set_error(SPX_ERR_ARG, "rmsnorm_bwd: d > 4096 unsupported");
-  rmsnorm_bwd_fused_kernel<<<blocks, RB_WARPS * 32, smem, SPX_S>>>(CBF(x), CBF(g), rstd, CBF(dy), CBF(dres), BF(dx),
-                                                                   dg ? ws : nullptr, (int)rows, (int)d);
-  int rc = check_launch("rmsnorm_bwd_fused_kernel");
+  rmsnorm_bwd_dx_kernel<<<(unsigned)((rows + ROW_WARPS - 1) / ROW_WARPS), ROW_WARPS * 32, 0, SPX_S>>>(
+      CBF(x), CBF(g), rstd, CBF(dy), CBF(dres), BF(dx), (int)rows, (int)d);
+  int rc = check_launch("rmsnorm_bwd_dx_kernel");
   if (rc || dg == nullptr) return rc;
-  colsum_add_kernel<<<(unsigned)((d + 255) / 256), 256, 0, SPX_S>>>(ws, dg, blocks, (int)d);
+  const int chunks = (int)((rows + DG_ROWS - 1) / DG_ROWS);
+  rmsnorm_dg_partial_kernel<<<dim3((unsigned)((d / 2 + 127) / 128), (unsigned)chunks), 128, 0, SPX_S>>>(
+      CBF(x), rstd, CBF(dy), ws, (int)rows, (int)d);
+  rc = check_launch("rmsnorm_dg_partial_kernel");
+  if (rc) return rc;
+  colsum_add_kernel<<<(unsigned)((d + 255) / 256), 256, 0, SPX_S>>>(ws, dg, chunks, (int)d);
   return check_launch("colsum_add_kernel");
 }
 
-extern "C" int64_t spx_rmsnorm_ws_floats(int64_t rows, int64_t d) { return ((rows + RB_ROWS - 1) / RB_ROWS) * d; }
+extern "C" int64_t spx_rmsnorm_ws_floats(int64_t rows, int64_t d) { return ((rows + DG_ROWS - 1) / DG_ROWS) * d; }
 
 extern "C" int spx_rope(void* qkv, const float* cos_sin, int64_t rows, int64_t T, int64_t n_heads, int64_t hd,
                         int64_t ld, int32_t inverse, void* stream) {

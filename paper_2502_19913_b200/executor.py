@@ -259,6 +259,21 @@ def default_placement(n_nodes: int, n_ranks: int) -> list[int]:
     return [i % n_ranks for i in range(n_nodes)]
 
 
+def balanced_placement(report: SimReport, n_nodes: int, n_ranks: int) -> list[int]:
+    """Longest-processing-time placement of logical nodes onto ranks by the simulator's per-node
+    busy time (F + L + B over the whole iteration).  The scheduler is placement-blind on a uniform
+    NVSwitch box, so its paths can load replica nodes unevenly; co-resident nodes of one stage then
+    share a parameter set.  Deterministic: ties go to the lower node / rank id."""
+    busy = list(report.node_busy) + [0.0] * (n_nodes - len(report.node_busy))
+    load = [0.0] * n_ranks
+    out = [0] * n_nodes
+    for v in sorted(range(n_nodes), key=lambda v: (-round(busy[v], 9), v)):
+        r = min(range(n_ranks), key=lambda r: (round(load[r], 9), r))
+        out[v] = r
+        load[r] += busy[v]
+    return out
+
+
 def static_slots(schedule: Schedule, n_nodes: int) -> tuple[dict, list[int]]:
     """Activation slot of every (agent, node): the agent's rank among the agents whose path visits
     the node.  A slot is then only ever reused by the *same* agent's next wave, which launches
@@ -323,11 +338,13 @@ class Trainer:
         self.optim = optim or OptimConfig()
         self.node_stage = assignment.node_stage()
         self.rank, self.world = rank, world
-        self.placement = list(placement) if placement is not None else default_placement(topology.n, world)
+        self.report: SimReport = simulate(schedule, topology, sim_config)
+        if placement is None:
+            placement = balanced_placement(self.report, topology.n, world)
+        self.placement = list(placement)
         if len(self.placement) != topology.n or max(self.placement) >= world:
             raise ValidationError(f"placement {self.placement} does not map {topology.n} nodes onto {world} ranks")
         self.dev = torch.device("cuda", rank if device is None else device)
-        self.report: SimReport = simulate(schedule, topology, sim_config)
         self.ops = self.report.ops
         self.step_count = 0
         self.use_graphs = use_graphs

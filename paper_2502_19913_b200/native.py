@@ -210,7 +210,7 @@ def rmsnorm_fwd(x, g, y, rstd, *, rows, d, eps, stream=None) -> None:
 def rmsnorm_bwd(x, g, rstd, dy, dres, dx, dg, ws, *, rows, d, stream=None) -> None:
     _check(load().spx_rmsnorm_bwd(_ptr(x), _ptr(g), _ptr(rstd), _ptr(dy), _ptr(dres), _ptr(dx), _ptr(dg), _ptr(ws),
                                   rows, d, _stream(stream)), "spx_rmsnorm_bwd")
-    _count(2 if dg is not None else 1)
+    _count(3 if dg is not None else 1)
 
 
 def rmsnorm_ws_floats(rows: int, d: int) -> int:
