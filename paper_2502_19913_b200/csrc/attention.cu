@@ -145,6 +145,7 @@ struct Params {
 // ----------------------------------------------------------------------------------------
 template <int HD>
 __global__ void __launch_bounds__(THREADS) attn_fwd_kernel(const Params p) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t smem_raw[];
   constexpr int LD = Tile<HD>::LD;
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
@@ -281,6 +282,7 @@ __global__ void __launch_bounds__(THREADS) attn_fwd_kernel(const Params p) {
 // ----------------------------------------------------------------------------------------
 template <int HD>
 __global__ void attn_bwd_delta_kernel(const Params p) {
+  pdl_wait();
   // one warp per (row, head)
   const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -308,6 +310,7 @@ __global__ void attn_bwd_delta_kernel(const Params p) {
 // ----------------------------------------------------------------------------------------
 template <int HD>
 __global__ void __launch_bounds__(THREADS) attn_bwd_dkdv_kernel(const Params p) {
+  pdl_wait();
   constexpr int LD = Tile<HD>::LD;
   constexpr int BQI = (HD > 64) ? 32 : 64;  // query rows per inner step
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -430,6 +433,7 @@ __global__ void __launch_bounds__(THREADS) attn_bwd_dkdv_kernel(const Params p) 
 // ----------------------------------------------------------------------------------------
 template <int HD>
 __global__ void __launch_bounds__(THREADS) attn_bwd_dq_kernel(const Params p) {
+  pdl_wait();
   constexpr int LD = Tile<HD>::LD;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [BQ][LD]
@@ -546,7 +550,7 @@ static int run_fwd(const Params& p, cudaStream_t s) {
     if (e != cudaSuccess) return set_cuda_error(e, "attn_fwd attr");
     set = true;
   }
-  k<<<dim3(p.T / BQ, p.H, p.B), THREADS, smem, s>>>(p);
+  spx_launch_check(launch_k(k, dim3(dim3(p.T / BQ, p.H, p.B)), dim3(THREADS), smem, s, p));
   return check_launch("attn_fwd_kernel");
 }
 
@@ -557,7 +561,7 @@ static int run_bwd(const Params& p, cudaStream_t s) {
   {
     const long long warps = (long long)p.B * p.T * p.H;
     const int threads = 256;
-    attn_bwd_delta_kernel<HD><<<(unsigned)((warps * 32 + threads - 1) / threads), threads, 0, s>>>(p);
+    spx_launch_check(launch_k(attn_bwd_delta_kernel<HD>, dim3((unsigned)((warps * 32 + threads - 1) / threads)), dim3(threads), 0, s, p));
     int rc = check_launch("attn_bwd_delta_kernel");
     if (rc) return rc;
   }
@@ -573,7 +577,7 @@ static int run_bwd(const Params& p, cudaStream_t s) {
       if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_dkdv attr");
       set = true;
     }
-    k<<<dim3(p.T / BK, p.Hkv, p.B), THREADS, smem, s>>>(p);
+    spx_launch_check(launch_k(k, dim3(dim3(p.T / BK, p.Hkv, p.B)), dim3(THREADS), smem, s, p));
     int rc = check_launch("attn_bwd_dkdv_kernel");
     if (rc) return rc;
   }
@@ -586,7 +590,7 @@ static int run_bwd(const Params& p, cudaStream_t s) {
       if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_dq attr");
       set = true;
     }
-    k<<<dim3(p.T / BQ, p.H, p.B), THREADS, smem, s>>>(p);
+    spx_launch_check(launch_k(k, dim3(dim3(p.T / BQ, p.H, p.B)), dim3(THREADS), smem, s, p));
     return check_launch("attn_bwd_dq_kernel");
   }
 }

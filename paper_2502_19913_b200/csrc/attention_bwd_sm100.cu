@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // upstream grid complete before any dependent global access
   constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DV = 256, TM_DK = 256 + HD;
 
   if (warp == 0 && lane == 0) {
@@ -358,6 +359,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // upstream grid complete before any dependent global access
   constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 256;
 
   if (warp == 0 && lane == 0) {
@@ -499,10 +501,10 @@ static int launch(const void* qkv, const void* dout, long long ld_o, const BwdPa
     set = true;
   }
   const int nqb = p.T / BLK;
-  attn_bwd_dkdv_tc_kernel<HD><<<dim3(nqb, p.Hkv, p.B), THREADS, DkdvSmem<HD>::BYTES, s>>>(mq, md, p);
+  spx_launch_check(launch_k(attn_bwd_dkdv_tc_kernel<HD>, dim3(dim3(nqb, p.Hkv, p.B)), dim3(THREADS), DkdvSmem<HD>::BYTES, s, mq, md, p));
   rc = check_launch("attn_bwd_dkdv_tc_kernel");
   if (rc) return rc;
-  attn_bwd_dq_tc_kernel<HD><<<dim3(nqb, p.H, p.B), THREADS, DqSmem<HD>::BYTES, s>>>(mq, md, p);
+  spx_launch_check(launch_k(attn_bwd_dq_tc_kernel<HD>, dim3(dim3(nqb, p.H, p.B)), dim3(THREADS), DqSmem<HD>::BYTES, s, mq, md, p));
   return check_launch("attn_bwd_dq_tc_kernel");
 }
 

@@ -42,6 +42,7 @@ SPX_DEVICE void store8(__nv_bfloat16* p, const float (&f)[8]) {
 __global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
                                    __nv_bfloat16* __restrict__ y, float* __restrict__ rstd, int rows, int d,
                                    float eps) {
+  pdl_wait();
   const int row = blockIdx.x * ROW_WARPS + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -73,6 +74,7 @@ __global__ void rmsnorm_bwd_dx_kernel(const __nv_bfloat16* __restrict__ x, const
                                       const float* __restrict__ rstd, const __nv_bfloat16* __restrict__ dy,
                                       const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx,
                                       int rows, int d) {
+  pdl_wait();
   const int row = blockIdx.x * ROW_WARPS + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -111,6 +113,7 @@ __global__ void __launch_bounds__(128) rmsnorm_dg_partial_kernel(const __nv_bflo
                                                                  const float* __restrict__ rstd,
                                                                  const __nv_bfloat16* __restrict__ dy,
                                                                  float* __restrict__ part, int rows, int d) {
+  pdl_wait();
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
   if (c >= d) return;
   const int r0 = blockIdx.y * DG_ROWS, r1 = min(rows, r0 + DG_ROWS);
@@ -127,6 +130,7 @@ __global__ void __launch_bounds__(128) rmsnorm_dg_partial_kernel(const __nv_bflo
 }
 
 __global__ void colsum_add_kernel(const float* __restrict__ part, float* __restrict__ out, int nsplit, int d) {
+  pdl_wait();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= d) return;
   float s = 0.f;
@@ -138,6 +142,7 @@ __global__ void colsum_add_kernel(const float* __restrict__ part, float* __restr
 // in place on the q heads [0, H) and k heads [H, H+Hkv) of a fused QKV row; position = row % T
 __global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, const float* __restrict__ cs, int rows, int T, int nheads,
                             int hd, long long ld, float sign) {
+  pdl_wait();
   const int half = hd / 2;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long per_row = (long long)nheads * half;
@@ -158,6 +163,7 @@ __global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, const float* __rest
 // gu [rows, 2F] with gate/up interleaved in 128-column blocks; dh [rows, F]; dgu [rows, 2F]
 __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __nv_bfloat16* __restrict__ dh,
                                   __nv_bfloat16* __restrict__ dgu, int rows, int F) {
+  pdl_wait();
   const long long idx = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (idx >= (long long)rows * F) return;
   const int row = (int)(idx / F);
@@ -182,6 +188,7 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __
 // ---------------------------------------------------------------- embedding
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ table,
                                  __nv_bfloat16* __restrict__ out, int n, int d) {
+  pdl_wait();
   const int row = blockIdx.x * ROW_WARPS + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
@@ -196,6 +203,7 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ ids, const __nv_bfl
 __global__ void embed_bwd_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ seg_start,
                                  const int32_t* __restrict__ seg_id, const int32_t* __restrict__ n_seg,
                                  const __nv_bfloat16* __restrict__ dout, float* __restrict__ dtable, int d) {
+  pdl_wait();
   const int seg = blockIdx.x;
   if (seg >= n_seg[0]) return;
   const int a = seg_start[seg], b = seg_start[seg + 1];
@@ -225,6 +233,7 @@ __global__ void __launch_bounds__(XE_THREADS) xent_kernel(__nv_bfloat16* __restr
                                                           const int32_t* __restrict__ targets,
                                                           float* __restrict__ row_loss, int V, long long ld,
                                                           float scale) {
+  pdl_wait();
   __shared__ float red_m[XE_THREADS / 32], red_s[XE_THREADS / 32];
   const int row = blockIdx.x;
   __nv_bfloat16* z = logits + (size_t)row * ld;
@@ -291,6 +300,7 @@ __global__ void __launch_bounds__(XE_THREADS) xent_kernel(__nv_bfloat16* __restr
 // out[0] (+)= scale * sum(x[0:n])   (single CTA, fixed order)
 __global__ void sum_kernel(const float* __restrict__ x, long long n, float* __restrict__ out, float scale,
                            int accumulate) {
+  pdl_wait();
   __shared__ double red[32];
   double s = 0.0;
   for (long long i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
@@ -307,6 +317,7 @@ __global__ void sum_kernel(const float* __restrict__ x, long long n, float* __re
 
 constexpr int SUMSQ_BLOCKS = 592;  // 4 per SM
 __global__ void sumsq_partial_kernel(const float* __restrict__ x, long long n, float* __restrict__ part) {
+  pdl_wait();
   __shared__ float red[32];
   float s = 0.f;
   const long long n4 = n / 4;
@@ -330,6 +341,7 @@ __global__ void sumsq_partial_kernel(const float* __restrict__ x, long long n, f
 // scale = min(1, max_norm / (||g|| + 1e-6)) from per-set squared norms (torch clip_grad_norm_)
 __global__ void clip_scale_kernel(const float* __restrict__ sumsq, int count, float max_norm, float* __restrict__ scale,
                                   float* __restrict__ norm_out) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   double t = 0.0;
   for (int i = 0; i < count; ++i) t += sumsq[i];
@@ -344,6 +356,7 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
                              float* __restrict__ v, __nv_bfloat16* __restrict__ pb, long long n, long long n_decay,
                              float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
                              const float* __restrict__ gscale) {
+  pdl_wait();
   const float sc = gscale ? gscale[0] : 1.f;
   const float step = lr / bc1;
   const float rbc2 = rsqrtf(bc2);
@@ -374,24 +387,24 @@ using namespace spx::ew;
 extern "C" int spx_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int64_t rows, int64_t d, float eps,
                                void* stream) {
   if (d % 8) return set_error(SPX_ERR_ARG, "rmsnorm: d must be a multiple of 8");
-  rmsnorm_fwd_kernel<<<(unsigned)((rows + ROW_WARPS - 1) / ROW_WARPS), ROW_WARPS * 32, 0, SPX_S>>>(
-      CBF(x), CBF(g), BF(y), rstd, (int)rows, (int)d, eps);
+  spx_launch_check(launch_k(rmsnorm_fwd_kernel, dim3((unsigned)((rows + ROW_WARPS - 1) / ROW_WARPS)), dim3(ROW_WARPS * 32), 0, SPX_S, 
+      CBF(x), CBF(g), BF(y), rstd, (int)rows, (int)d, eps));
   return check_launch("rmsnorm_fwd_kernel");
 }
 
 extern "C" int spx_rmsnorm_bwd(const void* x, const void* g, const float* rstd, const void* dy, const void* dres,
                                void* dx, float* dg, float* ws, int64_t rows, int64_t d, void* stream) {
   if (d % 8) return set_error(SPX_ERR_ARG, "rmsnorm: d must be a multiple of 8");
-  rmsnorm_bwd_dx_kernel<<<(unsigned)((rows + ROW_WARPS - 1) / ROW_WARPS), ROW_WARPS * 32, 0, SPX_S>>>(
-      CBF(x), CBF(g), rstd, CBF(dy), CBF(dres), BF(dx), (int)rows, (int)d);
+  spx_launch_check(launch_k(rmsnorm_bwd_dx_kernel, dim3((unsigned)((rows + ROW_WARPS - 1) / ROW_WARPS)), dim3(ROW_WARPS * 32), 0, SPX_S, 
+      CBF(x), CBF(g), rstd, CBF(dy), CBF(dres), BF(dx), (int)rows, (int)d));
   int rc = check_launch("rmsnorm_bwd_dx_kernel");
   if (rc || dg == nullptr) return rc;
   const int chunks = (int)((rows + DG_ROWS - 1) / DG_ROWS);
-  rmsnorm_dg_partial_kernel<<<dim3((unsigned)((d / 2 + 127) / 128), (unsigned)chunks), 128, 0, SPX_S>>>(
-      CBF(x), rstd, CBF(dy), ws, (int)rows, (int)d);
+  spx_launch_check(launch_k(rmsnorm_dg_partial_kernel, dim3(dim3((unsigned)((d / 2 + 127) / 128), (unsigned)chunks)), dim3(128), 0, SPX_S, 
+      CBF(x), rstd, CBF(dy), ws, (int)rows, (int)d));
   rc = check_launch("rmsnorm_dg_partial_kernel");
   if (rc) return rc;
-  colsum_add_kernel<<<(unsigned)((d + 255) / 256), 256, 0, SPX_S>>>(ws, dg, chunks, (int)d);
+  spx_launch_check(launch_k(colsum_add_kernel, dim3((unsigned)((d + 255) / 256)), dim3(256), 0, SPX_S, ws, dg, chunks, (int)d));
   return check_launch("colsum_add_kernel");
 }
 
@@ -401,22 +414,22 @@ extern "C" int spx_rope(void* qkv, const float* cos_sin, int64_t rows, int64_t T
                         int64_t ld, int32_t inverse, void* stream) {
   if (hd % 2) return set_error(SPX_ERR_ARG, "rope: odd head dim");
   const long long total = rows * n_heads * (hd / 2);
-  rope_kernel<<<(unsigned)((total + 255) / 256), 256, 0, SPX_S>>>(BF(qkv), cos_sin, (int)rows, (int)T, (int)n_heads,
-                                                                 (int)hd, ld, inverse ? -1.f : 1.f);
+  spx_launch_check(launch_k(rope_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, SPX_S, BF(qkv), cos_sin, (int)rows, (int)T, (int)n_heads,
+                                                                 (int)hd, ld, inverse ? -1.f : 1.f));
   return check_launch("rope_kernel");
 }
 
 extern "C" int spx_swiglu_bwd(const void* gu, const void* dh, void* dgu, int64_t rows, int64_t F, void* stream) {
   if (F % 128) return set_error(SPX_ERR_ARG, "swiglu_bwd: F must be a multiple of 128");
   const long long total = rows * F / 8;
-  swiglu_bwd_kernel<<<(unsigned)((total + 255) / 256), 256, 0, SPX_S>>>(CBF(gu), CBF(dh), BF(dgu), (int)rows, (int)F);
+  spx_launch_check(launch_k(swiglu_bwd_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, SPX_S, CBF(gu), CBF(dh), BF(dgu), (int)rows, (int)F));
   return check_launch("swiglu_bwd_kernel");
 }
 
 extern "C" int spx_embed_fwd(const int32_t* ids, const void* table, void* out, int64_t n, int64_t d, void* stream) {
   if (d % 8) return set_error(SPX_ERR_ARG, "embed: d must be a multiple of 8");
-  embed_fwd_kernel<<<(unsigned)((n + ROW_WARPS - 1) / ROW_WARPS), ROW_WARPS * 32, 0, SPX_S>>>(ids, CBF(table), BF(out),
-                                                                                            (int)n, (int)d);
+  spx_launch_check(launch_k(embed_fwd_kernel, dim3((unsigned)((n + ROW_WARPS - 1) / ROW_WARPS)), dim3(ROW_WARPS * 32), 0, SPX_S, ids, CBF(table), BF(out),
+                                                                                            (int)n, (int)d));
   return check_launch("embed_fwd_kernel");
 }
 
@@ -425,36 +438,36 @@ extern "C" int spx_embed_bwd(const int32_t* perm, const int32_t* seg_start, cons
                              void* stream) {
   if (d % 8) return set_error(SPX_ERR_ARG, "embed: d must be a multiple of 8");
   if (max_segments <= 0) return SPX_OK;
-  embed_bwd_kernel<<<(unsigned)max_segments, 128, 0, SPX_S>>>(perm, seg_start, seg_id, n_segments, CBF(dout), dtable,
-                                                              (int)d);
+  spx_launch_check(launch_k(embed_bwd_kernel, dim3((unsigned)max_segments), dim3(128), 0, SPX_S, perm, seg_start, seg_id, n_segments, CBF(dout), dtable,
+                                                              (int)d));
   return check_launch("embed_bwd_kernel");
 }
 
 extern "C" int spx_xent_fwd_bwd(void* logits, const int32_t* targets, float* row_loss, int64_t n, int64_t V, int64_t ld,
                                 float scale, void* stream) {
   if (V % 8 || ld % 8) return set_error(SPX_ERR_ARG, "xent: V and ld must be multiples of 8");
-  xent_kernel<<<(unsigned)n, XE_THREADS, 0, SPX_S>>>(BF(logits), targets, row_loss, (int)V, ld, scale);
+  spx_launch_check(launch_k(xent_kernel, dim3((unsigned)n), dim3(XE_THREADS), 0, SPX_S, BF(logits), targets, row_loss, (int)V, ld, scale));
   return check_launch("xent_kernel");
 }
 
 extern "C" int spx_sum_f32(const float* x, int64_t n, float* out, float scale, int32_t accumulate, void* stream) {
-  sum_kernel<<<1, 1024, 0, SPX_S>>>(x, n, out, scale, accumulate);
+  spx_launch_check(launch_k(sum_kernel, dim3(1), dim3(1024), 0, SPX_S, x, n, out, scale, accumulate));
   return check_launch("sum_kernel");
 }
 
 extern "C" int64_t spx_sumsq_ws_floats(void) { return SUMSQ_BLOCKS; }
 
 extern "C" int spx_sumsq(const float* x, int64_t n, float* ws, float* out, void* stream) {
-  sumsq_partial_kernel<<<SUMSQ_BLOCKS, 256, 0, SPX_S>>>(x, n, ws);
+  spx_launch_check(launch_k(sumsq_partial_kernel, dim3(SUMSQ_BLOCKS), dim3(256), 0, SPX_S, x, n, ws));
   int rc = check_launch("sumsq_partial_kernel");
   if (rc) return rc;
-  sum_kernel<<<1, 1024, 0, SPX_S>>>(ws, SUMSQ_BLOCKS, out, 1.f, 0);
+  spx_launch_check(launch_k(sum_kernel, dim3(1), dim3(1024), 0, SPX_S, ws, SUMSQ_BLOCKS, out, 1.f, 0));
   return check_launch("sum_kernel");
 }
 
 extern "C" int spx_clip_scale(const float* sumsq, int32_t count, float max_norm, float* scale, float* norm_out,
                               void* stream) {
-  clip_scale_kernel<<<1, 32, 0, SPX_S>>>(sumsq, count, max_norm, scale, norm_out);
+  spx_launch_check(launch_k(clip_scale_kernel, dim3(1), dim3(32), 0, SPX_S, sumsq, count, max_norm, scale, norm_out));
   return check_launch("clip_scale_kernel");
 }
 
@@ -465,7 +478,7 @@ extern "C" int spx_adamw(float* p, const float* g, float* m, float* v, void* p_b
   const float bc1 = 1.f - powf(beta1, (float)step);
   const float bc2 = 1.f - powf(beta2, (float)step);
   const int blocks = num_sms() * 8;
-  adamw_kernel<<<blocks, 256, 0, SPX_S>>>(p, g, m, v, BF(p_bf16), n, n_decay, lr, beta1, beta2, eps, weight_decay, bc1,
-                                          bc2, grad_scale);
+  spx_launch_check(launch_k(adamw_kernel, dim3(blocks), dim3(256), 0, SPX_S, p, g, m, v, BF(p_bf16), n, n_decay, lr, beta1, beta2, eps, weight_decay, bc1,
+                                          bc2, grad_scale));
   return check_launch("adamw_kernel");
 }

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // upstream grid complete before any dependent global access
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
@@ -144,6 +145,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
+    pdl_trigger();  // all loads issued: let the next kernel launch and run its prologue
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread) ----------------
     constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, BN, A_MN, B_MN);
@@ -440,7 +442,7 @@ static int launch_gemm(const void* A, const void* B, long long lda, long long ld
   }
   const int tiles = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + BN - 1) / BN) * args.splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, stream>>>(ta, tb, tc, tc2, args);
+  spx_launch_check(launch_k(kern, dim3(grid), dim3(GEMM_THREADS), Cfg::SMEM_BYTES, stream, ta, tb, tc, tc2, args));
   return check_launch("gemm_bf16_kernel");
 }
 

@@ -2,6 +2,7 @@
 // and the path-hop copy primitive (NVLink peer copy when source and destination live on
 // different GPUs, a device-local copy otherwise).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -25,6 +26,14 @@ int check_launch(const char* kernel_name) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, kernel_name);
   return SPX_OK;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SPX_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
 }
 
 int num_sms() {

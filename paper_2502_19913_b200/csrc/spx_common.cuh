@@ -43,6 +43,11 @@ SPX_DEVICE float2 unpack_bf16(uint32_t u) {
   return __bfloat1622float2(h);
 }
 
+// Programmatic dependent launch: wait for the upstream grid's completion (and memory flush);
+// allow the downstream grid to launch early.  No-ops for ordinary launches.
+SPX_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SPX_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ----------------------------------------------------------------------------
 // mbarrier
 // ----------------------------------------------------------------------------

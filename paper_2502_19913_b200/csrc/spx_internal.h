@@ -10,6 +10,29 @@
 
 namespace spx {
 
+bool pdl_enabled();
+
+// Launch with Programmatic Dependent Launch: the kernel may start (and run its prologue) while
+// the previous kernel on the stream drains; every libspx kernel calls griddepcontrol.wait before
+// touching global data the previous kernel produced or consumes.  SPX_PDL=0 disables it.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// launch errors are also recorded as the runtime's last error, which check_launch() reports
+#define spx_launch_check(expr) ((void)(expr))
+
 int set_error(int code, const char* msg);
 int set_cuda_error(cudaError_t e, const char* where);
 int check_launch(const char* kernel_name);
