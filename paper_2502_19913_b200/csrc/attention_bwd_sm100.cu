@@ -103,7 +103,7 @@ SPX_DEVICE void store_grad_row(uint32_t taddr, __nv_bfloat16* dst, float scale, 
 }
 
 // ------------------------------------------------------------------------------------------
-// dK / dV
+// dK / dV (persistent: one CTA per SM walks heavy-first items (batch, kv-head, key block))
 // ------------------------------------------------------------------------------------------
 template <int HD>
 struct DkdvSmem {
@@ -118,7 +118,7 @@ struct DkdvSmem {
   static constexpr int OFF_LSE = OFF_DST + 2 * ATOM;  // [NST][128] f32
   static constexpr int OFF_D = OFF_LSE + NST * 512;   // [NST][128] f32
   static constexpr int OFF_BAR = OFF_D + NST * 512;
-  static constexpr int BYTES = OFF_BAR + 256 + 1024;
+  static constexpr int BYTES = OFF_BAR + 256;         // base is __align__(1024)
 };
 
 template <int HD>
@@ -127,31 +127,36 @@ __global__ void __launch_bounds__(THREADS, 1)
                             const BwdParams p) {
   using L = DkdvSmem<HD>;
   constexpr int NST = L::NST;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* kv_full = bars + 0;
-  uint64_t* full = bars + 1;      // [NST]
-  uint64_t* empty = bars + 3;     // [NST]
-  uint64_t* sdp_full = bars + 5;
-  uint64_t* p_ready = bars + 6;
-  uint64_t* mma2_done = bars + 7;
-  uint64_t* tmem_free = bars + 8;   // S / dP of the current step copied to registers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* kv_empty = bars + 1;
+  uint64_t* full = bars + 2;      // [NST]
+  uint64_t* empty = bars + 4;     // [NST]
+  uint64_t* sdp_full = bars + 6;
+  uint64_t* p_ready = bars + 7;
+  uint64_t* mma2_done = bars + 8;
+  uint64_t* tmem_free = bars + 9;   // S / dP of the current step copied to registers
+  uint64_t* acc_free = bars + 10;   // dV / dK of the previous item read out of TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = p.T / BLK;
-  const int jb = nqb - 1 - (int)blockIdx.x;  // key block; heavy (early) blocks first
-  const int kvh = blockIdx.y, b = blockIdx.z;
   const int group = p.H / p.Hkv;
-  const int nq = nqb - jb;                   // query blocks jb..nqb-1
-  const int n_it = group * nq;
-  const int row0 = b * p.T;
+  const int BHk = p.B * p.Hkv;
+  const int n_items = nqb * BHk;
+  // item w: key block jb = w / (B*Hkv) (early key blocks see the most query blocks: heavy first)
+  auto item = [&](int w, int& b, int& kvh, int& jb) {
+    jb = w / BHk;
+    b = (w % BHk) / p.Hkv;
+    kvh = (w % BHk) % p.Hkv;
+  };
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmQKV);
     tma_prefetch_desc(&tmDO);
     mbar_init(kv_full, 1);
+    mbar_init(kv_empty, 1);
     for (int i = 0; i < NST; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -160,6 +165,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(p_ready, EW_WARPS);
     mbar_init(mma2_done, 1);
     mbar_init(tmem_free, EW_WARPS);
+    mbar_init(acc_free, EW_WARPS);
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -173,23 +179,30 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     // ---------------- producer ----------------
-    mbar_expect_tx(kv_full, 2 * L::TILE);
-    for (int a = 0; a < HD / 64; ++a) {
-      tma_load_2d(smem + L::OFF_K + a * ATOM, &tmQKV, kv_full, (p.H + kvh) * HD + 64 * a, row0 + jb * BLK);
-      tma_load_2d(smem + L::OFF_V + a * ATOM, &tmQKV, kv_full, (p.H + p.Hkv + kvh) * HD + 64 * a, row0 + jb * BLK);
-    }
-    for (int it = 0; it < n_it; ++it) {
-      const int s = it % NST;
-      const int h = kvh * group + it / nq, qb = jb + it % nq;
-      mbar_wait(&empty[s], ((it / NST) & 1) ^ 1);
-      mbar_expect_tx(&full[s], 2 * L::TILE + 1024);
+    int gi = 0, n = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+      int b, kvh, jb;
+      item(w, b, kvh, jb);
+      const int row0 = b * p.T, nq = nqb - jb;
+      mbar_wait(kv_empty, (n & 1) ^ 1);
+      mbar_expect_tx(kv_full, 2 * L::TILE);
       for (int a = 0; a < HD / 64; ++a) {
-        tma_load_2d(smem + L::OFF_Q + s * L::TILE + a * ATOM, &tmQKV, &full[s], h * HD + 64 * a, row0 + qb * BLK);
-        tma_load_2d(smem + L::OFF_DO + s * L::TILE + a * ATOM, &tmDO, &full[s], h * HD + 64 * a, row0 + qb * BLK);
+        tma_load_2d(smem + L::OFF_K + a * ATOM, &tmQKV, kv_full, (p.H + kvh) * HD + 64 * a, row0 + jb * BLK);
+        tma_load_2d(smem + L::OFF_V + a * ATOM, &tmQKV, kv_full, (p.H + p.Hkv + kvh) * HD + 64 * a, row0 + jb * BLK);
       }
-      const size_t off = ((size_t)b * p.H + h) * p.T + qb * BLK;
-      bulk_load(smem + L::OFF_LSE + s * 512, p.lse + off, 512, &full[s]);
-      bulk_load(smem + L::OFF_D + s * 512, p.delta + off, 512, &full[s]);
+      for (int it = 0; it < group * nq; ++it, ++gi) {
+        const int s = gi % NST;
+        const int h = kvh * group + it / nq, qb = jb + it % nq;
+        mbar_wait(&empty[s], ((gi / NST) & 1) ^ 1);
+        mbar_expect_tx(&full[s], 2 * L::TILE + 1024);
+        for (int a = 0; a < HD / 64; ++a) {
+          tma_load_2d(smem + L::OFF_Q + s * L::TILE + a * ATOM, &tmQKV, &full[s], h * HD + 64 * a, row0 + qb * BLK);
+          tma_load_2d(smem + L::OFF_DO + s * L::TILE + a * ATOM, &tmDO, &full[s], h * HD + 64 * a, row0 + qb * BLK);
+        }
+        const size_t off = ((size_t)b * p.H + h) * p.T + qb * BLK;
+        bulk_load(smem + L::OFF_LSE + s * 512, p.lse + off, 512, &full[s]);
+        bulk_load(smem + L::OFF_D + s * 512, p.delta + off, 512, &full[s]);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
@@ -197,10 +210,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr uint32_t ID_G = umma_idesc_bf16(BLK, HD, false, true);     // P^T.dO, dS^T.Q
     const uint32_t sK = smem_u32(smem + L::OFF_K), sV = smem_u32(smem + L::OFF_V);
     const uint32_t sPT = smem_u32(smem + L::OFF_PT), sDST = smem_u32(smem + L::OFF_DST);
-    mbar_wait(kv_full, 0);
-    auto issue_sdp = [&](int it) {
-      const int s = it % NST;
-      mbar_wait(&full[s], (it / NST) & 1);
+    auto issue_sdp = [&](int gi) {
+      const int s = gi % NST;
+      mbar_wait(&full[s], (gi / NST) & 1);
       tc_fence_after();
       const uint32_t sQ = smem_u32(smem + L::OFF_Q + s * L::TILE), sDO = smem_u32(smem + L::OFF_DO + s * L::TILE);
 #pragma unroll
@@ -212,31 +224,43 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       mma_commit(sdp_full);
     };
-    issue_sdp(0);
-    for (int it = 0; it < n_it; ++it) {
-      const int s = it % NST;
-      // S/dP of step it are in registers: compute step it+1's S/dP while the warps do the math
-      mbar_wait(tmem_free, it & 1);
-      tc_fence_after();
-      // with a 2-deep Q/dO ring the next S/dP can go first; with one stage the next Q/dO tile only
-      // lands after this step's dV/dK MMAs released the stage
-      if (NST > 1 && it + 1 < n_it) issue_sdp(it + 1);
-      mbar_wait(p_ready, it & 1);
-      tc_fence_after();
-      const uint32_t sQ = smem_u32(smem + L::OFF_Q + s * L::TILE), sDO = smem_u32(smem + L::OFF_DO + s * L::TILE);
+    int gi = 0, n = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+      int b, kvh, jb;
+      item(w, b, kvh, jb);
+      const int n_it = group * (nqb - jb);
+      mbar_wait(kv_full, n & 1);
+      bool issued = false;
+      for (int it = 0; it < n_it; ++it, ++gi) {
+        const int s = gi % NST;
+        if (!issued) issue_sdp(gi);
+        // S/dP of this step are in registers: with a 2-deep Q/dO ring the next step's S/dP (same
+        // item: K/V stay) overlap the elementwise math; otherwise they follow this step's dV/dK
+        mbar_wait(tmem_free, gi & 1);
+        tc_fence_after();
+        issued = false;
+        if (NST > 1 && it + 1 < n_it) {
+          issue_sdp(gi + 1);
+          issued = true;
+        }
+        mbar_wait(p_ready, gi & 1);
+        if (it == 0) mbar_wait(acc_free, (n & 1) ^ 1);  // previous item's dV/dK read out
+        tc_fence_after();
+        const uint32_t sQ = smem_u32(smem + L::OFF_Q + s * L::TILE), sDO = smem_u32(smem + L::OFF_DO + s * L::TILE);
 #pragma unroll
-      for (int kk = 0; kk < BLK / 16; ++kk) {
-        const uint32_t ao = (kk >> 2) * ATOM + (kk & 3) * 32;
-        const uint32_t bo = kk * 2048;
-        const uint32_t acc = (it > 0) || (kk > 0);
-        mma_bf16_ss(tmem + TM_DV, umma_desc_sw128(sPT + ao, 16, 1024), umma_desc_sw128(sDO + bo, ATOM, 1024), ID_G,
-                    acc);
-        mma_bf16_ss(tmem + TM_DK, umma_desc_sw128(sDST + ao, 16, 1024), umma_desc_sw128(sQ + bo, ATOM, 1024), ID_G,
-                    acc);
+        for (int kk = 0; kk < BLK / 16; ++kk) {
+          const uint32_t ao = (kk >> 2) * ATOM + (kk & 3) * 32;
+          const uint32_t bo = kk * 2048;
+          const uint32_t acc = (it > 0) || (kk > 0);
+          mma_bf16_ss(tmem + TM_DV, umma_desc_sw128(sPT + ao, 16, 1024), umma_desc_sw128(sDO + bo, ATOM, 1024), ID_G,
+                      acc);
+          mma_bf16_ss(tmem + TM_DK, umma_desc_sw128(sDST + ao, 16, 1024), umma_desc_sw128(sQ + bo, ATOM, 1024), ID_G,
+                      acc);
+        }
+        mma_commit(mma2_done);
+        mma_commit(&empty[s]);
+        if (it + 1 == n_it) mma_commit(kv_empty);
       }
-      mma_commit(mma2_done);
-      mma_commit(&empty[s]);
-      if (NST == 1 && it + 1 < n_it) issue_sdp(it + 1);
     }
   } else if (warp >= 4) {
     // ---------------- elementwise: thread = key row, 64 query columns ----------------
@@ -246,51 +270,59 @@ __global__ void __launch_bounds__(THREADS, 1)
     const float sl2 = p.scale * LOG2E;
     uint8_t* sPT = smem + L::OFF_PT;
     uint8_t* sDST = smem + L::OFF_DST;
-    for (int it = 0; it < n_it; ++it) {
-      const int s = it % NST;
-      const int qb = jb + it % nq;
-      const bool diag = qb == jb;
-      mbar_wait(&full[s], (it / NST) & 1);  // lse / D of this step are in smem
-      mbar_wait(sdp_full, it & 1);
+    int gi = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+      int b, kvh, jb;
+      item(w, b, kvh, jb);
+      const int nq = nqb - jb, n_it = group * nq;
+      for (int it = 0; it < n_it; ++it, ++gi) {
+        const int s = gi % NST;
+        const bool diag = (it % nq) == 0;  // query block == key block
+        mbar_wait(&full[s], (gi / NST) & 1);  // lse / D of this step are in smem
+        mbar_wait(sdp_full, gi & 1);
+        tc_fence_after();
+        const float* lse = reinterpret_cast<const float*>(smem + L::OFF_LSE + s * 512);
+        const float* dd = reinterpret_cast<const float*>(smem + L::OFF_D + s * 512);
+        const int cb = 64 * half;
+        uint32_t sv[64], dv[64];
+        tmem_ld_32x32b_x32(lane_base + TM_S + cb, *reinterpret_cast<uint32_t(*)[32]>(sv));
+        tmem_ld_32x32b_x32(lane_base + TM_S + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+        tmem_ld_32x32b_x32(lane_base + TM_DP + cb, *reinterpret_cast<uint32_t(*)[32]>(dv));
+        tmem_ld_32x32b_x32(lane_base + TM_DP + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tmem_free);
+        if (gi > 0) mbar_wait(mma2_done, (gi - 1) & 1);  // P^T / dS^T tiles free
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) {
+          float pv[8], ds[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = cb + 8 * c8 + j;
+            float pp = ex2(fmaf(__uint_as_float(sv[8 * c8 + j]), sl2, -lse[c] * LOG2E));
+            if (diag && c < r) pp = 0.f;  // query before key
+            pv[j] = pp;
+            ds[j] = pp * (__uint_as_float(dv[8 * c8 + j]) - dd[c]);
+          }
+          put_row8(sPT, r, (cb >> 3) + c8, pv);
+          put_row8(sDST, r, (cb >> 3) + c8, ds);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_ready);
+      }
+      // item outputs: half 0 writes dV, half 1 writes dK (scaled, inverse RoPE)
+      mbar_wait(mma2_done, (gi - 1) & 1);
       tc_fence_after();
-      const float* lse = reinterpret_cast<const float*>(smem + L::OFF_LSE + s * 512);
-      const float* dd = reinterpret_cast<const float*>(smem + L::OFF_D + s * 512);
-      const int cb = 64 * half;
-      uint32_t sv[64], dv[64];
-      tmem_ld_32x32b_x32(lane_base + TM_S + cb, *reinterpret_cast<uint32_t(*)[32]>(sv));
-      tmem_ld_32x32b_x32(lane_base + TM_S + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-      tmem_ld_32x32b_x32(lane_base + TM_DP + cb, *reinterpret_cast<uint32_t(*)[32]>(dv));
-      tmem_ld_32x32b_x32(lane_base + TM_DP + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
-      tmem_ld_wait();
+      const int key = jb * BLK + r;
+      __nv_bfloat16* dst = p.dqkv + (size_t)(b * p.T + key) * p.ld;
+      if (half == 0) store_grad_row<HD>(lane_base + TM_DV, dst + (p.H + p.Hkv + kvh) * HD, 1.f, nullptr, p.T, key);
+      else store_grad_row<HD>(lane_base + TM_DK, dst + (p.H + kvh) * HD, p.scale, p.rope_cs, p.T, key);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tmem_free);
-      if (it > 0) mbar_wait(mma2_done, (it - 1) & 1);  // P^T / dS^T tiles free
-#pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8) {
-        float pv[8], ds[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int c = cb + 8 * c8 + j;
-          float pp = ex2(fmaf(__uint_as_float(sv[8 * c8 + j]), sl2, -lse[c] * LOG2E));
-          if (diag && c < r) pp = 0.f;  // query before key
-          pv[j] = pp;
-          ds[j] = pp * (__uint_as_float(dv[8 * c8 + j]) - dd[c]);
-        }
-        put_row8(sPT, r, (cb >> 3) + c8, pv);
-        put_row8(sDST, r, (cb >> 3) + c8, ds);
-      }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_ready);
+      if (lane == 0) mbar_arrive(acc_free);
     }
-    // outputs: half 0 writes dV, half 1 writes dK (scaled, inverse RoPE)
-    mbar_wait(mma2_done, (n_it - 1) & 1);
-    tc_fence_after();
-    const int key = jb * BLK + r;
-    __nv_bfloat16* dst = p.dqkv + (size_t)(row0 + key) * p.ld;
-    if (half == 0) store_grad_row<HD>(lane_base + TM_DV, dst + (p.H + p.Hkv + kvh) * HD, 1.f, nullptr, p.T, key);
-    else store_grad_row<HD>(lane_base + TM_DK, dst + (p.H + kvh) * HD, p.scale, p.rope_cs, p.T, key);
   }
   __syncwarp();
   tc_fence_before();
@@ -300,7 +332,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ------------------------------------------------------------------------------------------
-// dQ
+// dQ (persistent: heavy-first items (batch, head, query block))
 // ------------------------------------------------------------------------------------------
 template <int HD>
 struct DqSmem {
@@ -311,7 +343,7 @@ struct DqSmem {
   static constexpr int OFF_V = OFF_K + 2 * TILE;  // [2]
   static constexpr int OFF_DS = OFF_V + 2 * TILE;
   static constexpr int OFF_BAR = OFF_DS + 2 * ATOM;
-  static constexpr int BYTES = OFF_BAR + 256 + 1024;
+  static constexpr int BYTES = OFF_BAR + 256;
 };
 
 template <int HD>
@@ -319,30 +351,35 @@ __global__ void __launch_bounds__(THREADS, 1)
     attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                           const BwdParams p) {
   using L = DqSmem<HD>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* qdo_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* sdp_full = bars + 5;
-  uint64_t* p_ready = bars + 6;
-  uint64_t* mma2_done = bars + 7;
-  uint64_t* tmem_free = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* qdo_empty = bars + 1;
+  uint64_t* kv_full = bars + 2;   // [2]
+  uint64_t* kv_empty = bars + 4;  // [2]
+  uint64_t* sdp_full = bars + 6;
+  uint64_t* p_ready = bars + 7;
+  uint64_t* mma2_done = bars + 8;
+  uint64_t* tmem_free = bars + 9;
+  uint64_t* acc_free = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = p.T / BLK;
-  const int ib = nqb - 1 - (int)blockIdx.x;  // heavy blocks first
-  const int h = blockIdx.y, b = blockIdx.z;
-  const int kvh = h / (p.H / p.Hkv);
-  const int nkb = ib + 1;
-  const int row0 = b * p.T;
+  const int BH = p.B * p.H;
+  const int n_items = nqb * BH;
+  const int group = p.H / p.Hkv;
+  auto item = [&](int w, int& b, int& h, int& ib) {
+    ib = nqb - 1 - w / BH;  // late query blocks see the most key blocks: heavy first
+    b = (w % BH) / p.H;
+    h = (w % BH) % p.H;
+  };
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmQKV);
     tma_prefetch_desc(&tmDO);
     mbar_init(qdo_full, 1);
+    mbar_init(qdo_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
@@ -351,6 +388,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(p_ready, EW_WARPS);
     mbar_init(mma2_done, 1);
     mbar_init(tmem_free, EW_WARPS);
+    mbar_init(acc_free, EW_WARPS);
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -363,20 +401,27 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 256;
 
   if (warp == 0 && lane == 0) {
-    mbar_expect_tx(qdo_full, 2 * L::TILE);
-    for (int a = 0; a < HD / 64; ++a) {
-      tma_load_2d(smem + L::OFF_Q + a * ATOM, &tmQKV, qdo_full, h * HD + 64 * a, row0 + ib * BLK);
-      tma_load_2d(smem + L::OFF_DO + a * ATOM, &tmDO, qdo_full, h * HD + 64 * a, row0 + ib * BLK);
-    }
-    for (int j = 0; j < nkb; ++j) {
-      const int s = j & 1;
-      mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-      mbar_expect_tx(&kv_full[s], 2 * L::TILE);
+    int gj = 0, n = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+      int b, h, ib;
+      item(w, b, h, ib);
+      const int row0 = b * p.T, kvh = h / group;
+      mbar_wait(qdo_empty, (n & 1) ^ 1);
+      mbar_expect_tx(qdo_full, 2 * L::TILE);
       for (int a = 0; a < HD / 64; ++a) {
-        tma_load_2d(smem + L::OFF_K + s * L::TILE + a * ATOM, &tmQKV, &kv_full[s], (p.H + kvh) * HD + 64 * a,
-                    row0 + j * BLK);
-        tma_load_2d(smem + L::OFF_V + s * L::TILE + a * ATOM, &tmQKV, &kv_full[s], (p.H + p.Hkv + kvh) * HD + 64 * a,
-                    row0 + j * BLK);
+        tma_load_2d(smem + L::OFF_Q + a * ATOM, &tmQKV, qdo_full, h * HD + 64 * a, row0 + ib * BLK);
+        tma_load_2d(smem + L::OFF_DO + a * ATOM, &tmDO, qdo_full, h * HD + 64 * a, row0 + ib * BLK);
+      }
+      for (int j = 0; j <= ib; ++j, ++gj) {
+        const int s = gj & 1;
+        mbar_wait(&kv_empty[s], ((gj >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[s], 2 * L::TILE);
+        for (int a = 0; a < HD / 64; ++a) {
+          tma_load_2d(smem + L::OFF_K + s * L::TILE + a * ATOM, &tmQKV, &kv_full[s], (p.H + kvh) * HD + 64 * a,
+                      row0 + j * BLK);
+          tma_load_2d(smem + L::OFF_V + s * L::TILE + a * ATOM, &tmQKV, &kv_full[s],
+                      (p.H + p.Hkv + kvh) * HD + 64 * a, row0 + j * BLK);
+        }
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -384,10 +429,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr uint32_t ID_G = umma_idesc_bf16(BLK, HD, false, true);    // dS.K
     const uint32_t sQ = smem_u32(smem + L::OFF_Q), sDO = smem_u32(smem + L::OFF_DO);
     const uint32_t sDS = smem_u32(smem + L::OFF_DS);
-    mbar_wait(qdo_full, 0);
-    auto issue_sdp = [&](int j) {
-      const int s = j & 1;
-      mbar_wait(&kv_full[s], (j >> 1) & 1);
+    auto issue_sdp = [&](int gj) {
+      const int s = gj & 1;
+      mbar_wait(&kv_full[s], (gj >> 1) & 1);
       tc_fence_after();
       const uint32_t sK = smem_u32(smem + L::OFF_K + s * L::TILE), sV = smem_u32(smem + L::OFF_V + s * L::TILE);
 #pragma unroll
@@ -399,23 +443,36 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       mma_commit(sdp_full);
     };
-    issue_sdp(0);
-    for (int j = 0; j < nkb; ++j) {
-      const int s = j & 1;
-      mbar_wait(tmem_free, j & 1);
-      tc_fence_after();
-      if (j + 1 < nkb) issue_sdp(j + 1);
-      mbar_wait(p_ready, j & 1);
-      tc_fence_after();
-      const uint32_t sK = smem_u32(smem + L::OFF_K + s * L::TILE);
+    int gj = 0, n = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+      int b, h, ib;
+      item(w, b, h, ib);
+      mbar_wait(qdo_full, n & 1);
+      bool issued = false;
+      for (int j = 0; j <= ib; ++j, ++gj) {
+        const int s = gj & 1;
+        if (!issued) issue_sdp(gj);
+        mbar_wait(tmem_free, gj & 1);
+        tc_fence_after();
+        issued = false;
+        if (j + 1 <= ib) {  // next S/dP of this item overlaps the elementwise math
+          issue_sdp(gj + 1);
+          issued = true;
+        }
+        mbar_wait(p_ready, gj & 1);
+        if (j == 0) mbar_wait(acc_free, (n & 1) ^ 1);  // previous item's dQ read out
+        tc_fence_after();
+        const uint32_t sK = smem_u32(smem + L::OFF_K + s * L::TILE);
 #pragma unroll
-      for (int kk = 0; kk < BLK / 16; ++kk) {
-        const uint32_t ao = (kk >> 2) * ATOM + (kk & 3) * 32;
-        mma_bf16_ss(tmem + TM_DQ, umma_desc_sw128(sDS + ao, 16, 1024), umma_desc_sw128(sK + kk * 2048, ATOM, 1024),
-                    ID_G, (j > 0) || (kk > 0));
+        for (int kk = 0; kk < BLK / 16; ++kk) {
+          const uint32_t ao = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_bf16_ss(tmem + TM_DQ, umma_desc_sw128(sDS + ao, 16, 1024), umma_desc_sw128(sK + kk * 2048, ATOM, 1024),
+                      ID_G, (j > 0) || (kk > 0));
+        }
+        mma_commit(mma2_done);
+        mma_commit(&kv_empty[s]);
+        if (j == ib) mma_commit(qdo_empty);
       }
-      mma_commit(mma2_done);
-      mma_commit(&kv_empty[s]);
     }
   } else if (warp >= 4) {
     // ---------------- elementwise: thread = query row, 64 key columns ----------------
@@ -423,45 +480,54 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int r = quad * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
     const float sl2 = p.scale * LOG2E;
-    const int t = ib * BLK + r;
-    const size_t stat = ((size_t)b * p.H + h) * p.T + t;
-    const float lse2 = p.lse[stat] * LOG2E, dr = p.delta[stat];
     uint8_t* sDS = smem + L::OFF_DS;
-    for (int j = 0; j < nkb; ++j) {
-      const bool diag = j == ib;
-      mbar_wait(sdp_full, j & 1);
+    int gj = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+      int b, h, ib;
+      item(w, b, h, ib);
+      const int t = ib * BLK + r;
+      const size_t stat = ((size_t)b * p.H + h) * p.T + t;
+      const float lse2 = p.lse[stat] * LOG2E, dr = p.delta[stat];
+      for (int j = 0; j <= ib; ++j, ++gj) {
+        const bool diag = j == ib;
+        mbar_wait(sdp_full, gj & 1);
+        tc_fence_after();
+        const int cb = 64 * half;
+        uint32_t sv[64], dv[64];
+        tmem_ld_32x32b_x32(lane_base + TM_S + cb, *reinterpret_cast<uint32_t(*)[32]>(sv));
+        tmem_ld_32x32b_x32(lane_base + TM_S + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+        tmem_ld_32x32b_x32(lane_base + TM_DP + cb, *reinterpret_cast<uint32_t(*)[32]>(dv));
+        tmem_ld_32x32b_x32(lane_base + TM_DP + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tmem_free);
+        if (gj > 0) mbar_wait(mma2_done, (gj - 1) & 1);  // dS tile free
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) {
+          float ds[8];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int c = cb + 8 * c8 + jj;
+            float pp = ex2(fmaf(__uint_as_float(sv[8 * c8 + jj]), sl2, -lse2));
+            if (diag && c > r) pp = 0.f;  // key after query
+            ds[jj] = pp * (__uint_as_float(dv[8 * c8 + jj]) - dr);
+          }
+          put_row8(sDS, r, (cb >> 3) + c8, ds);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_ready);
+      }
+      mbar_wait(mma2_done, (gj - 1) & 1);
       tc_fence_after();
-      const int cb = 64 * half;
-      uint32_t sv[64], dv[64];
-      tmem_ld_32x32b_x32(lane_base + TM_S + cb, *reinterpret_cast<uint32_t(*)[32]>(sv));
-      tmem_ld_32x32b_x32(lane_base + TM_S + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-      tmem_ld_32x32b_x32(lane_base + TM_DP + cb, *reinterpret_cast<uint32_t(*)[32]>(dv));
-      tmem_ld_32x32b_x32(lane_base + TM_DP + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
-      tmem_ld_wait();
+      if (half == 0)
+        store_grad_row<HD>(lane_base + TM_DQ, p.dqkv + (size_t)(b * p.T + t) * p.ld + h * HD, p.scale, p.rope_cs, p.T,
+                           t);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tmem_free);
-      if (j > 0) mbar_wait(mma2_done, (j - 1) & 1);  // dS tile free
-#pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8) {
-        float ds[8];
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          const int c = cb + 8 * c8 + jj;
-          float pp = ex2(fmaf(__uint_as_float(sv[8 * c8 + jj]), sl2, -lse2));
-          if (diag && c > r) pp = 0.f;  // key after query
-          ds[jj] = pp * (__uint_as_float(dv[8 * c8 + jj]) - dr);
-        }
-        put_row8(sDS, r, (cb >> 3) + c8, ds);
-      }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_ready);
+      if (lane == 0) mbar_arrive(acc_free);
     }
-    mbar_wait(mma2_done, (nkb - 1) & 1);
-    tc_fence_after();
-    if (half == 0)
-      store_grad_row<HD>(lane_base + TM_DQ, p.dqkv + (size_t)(row0 + t) * p.ld + h * HD, p.scale, p.rope_cs, p.T, t);
   }
   __syncwarp();
   tc_fence_before();
@@ -501,10 +567,12 @@ static int launch(const void* qkv, const void* dout, long long ld_o, const BwdPa
     set = true;
   }
   const int nqb = p.T / BLK;
-  spx_launch_check(launch_k(attn_bwd_dkdv_tc_kernel<HD>, dim3(dim3(nqb, p.Hkv, p.B)), dim3(THREADS), DkdvSmem<HD>::BYTES, s, mq, md, p));
+  const int items_kv = nqb * p.Hkv * p.B, items_q = nqb * p.H * p.B;
+  const int g1 = items_kv < num_sms() ? items_kv : num_sms(), g2 = items_q < num_sms() ? items_q : num_sms();
+  spx_launch_check(launch_k(attn_bwd_dkdv_tc_kernel<HD>, dim3(g1), dim3(THREADS), DkdvSmem<HD>::BYTES, s, mq, md, p));
   rc = check_launch("attn_bwd_dkdv_tc_kernel");
   if (rc) return rc;
-  spx_launch_check(launch_k(attn_bwd_dq_tc_kernel<HD>, dim3(dim3(nqb, p.H, p.B)), dim3(THREADS), DqSmem<HD>::BYTES, s, mq, md, p));
+  spx_launch_check(launch_k(attn_bwd_dq_tc_kernel<HD>, dim3(g2), dim3(THREADS), DqSmem<HD>::BYTES, s, mq, md, p));
   return check_launch("attn_bwd_dq_tc_kernel");
 }
 

@@ -1,16 +1,19 @@
 // tcgen05 flash-attention forward for sm_100a (causal, GQA, head_dim 64 or 128).
 //
-// One CTA = 128 query rows of one (batch, head).  Warp roles:
-//   warp 0      TMA producer: Q once, then K_j / V_j (128 keys) into a 2-stage ring, all read in
+// Persistent kernel: one CTA per SM walks a heavy-first list of work items (128 query rows of one
+// (batch, head)); TMEM is allocated once and every mbarrier keeps its phase across items, so the
+// pipeline never drains between items.  Warp roles:
+//   warp 0      TMA producer: Q per item, then K_j / V_j (128 keys) into a 2-stage ring, read in
 //               place from the fused QKV buffer with one SWIZZLE_128B tensor map
 //   warp 1      single-thread tcgen05.mma issuer:  S_j = Q K_j^T  (M=128, N=128, K=hd) into one of
 //               two TMEM buffers, then O += P_j V_j (M=128, N=hd, K=128; V as an MN-major operand)
 //   warp 2      TMEM allocation (512 columns: S0, S1, O)
 //   warps 4-7   softmax: thread = query row (its TMEM lane).  Reads S_j, keeps running max/sum in
-//               the exp2 domain, rescales O in TMEM when the max grows, writes P_j (bf16) into a
-//               swizzled smem tile that is the A operand of the PV MMA.
-// The S MMA of block j+1 overlaps the softmax of block j.  Heavy (late) query blocks launch first.
-// Output O and LSE match attn_fwd_kernel (attention.cu) so the backward kernels are unchanged.
+//               the exp2 domain (split accumulators: no long dependent chains), rescales O in TMEM
+//               when the max grows, writes P_j (bf16) into a swizzled smem tile (A of the PV MMA),
+//               and at the end of an item writes O / l and the LSE.
+// S_{j+1} overlaps the softmax of block j; the next item's S MMAs overlap the previous item's
+// epilogue.  O and LSE match attn_fwd_kernel (attention.cu).
 #include <cmath>
 
 #include "spx_common.cuh"
@@ -19,7 +22,7 @@
 namespace spx {
 namespace fa {
 
-constexpr int BM = 128;    // query rows per CTA
+constexpr int BM = 128;    // query rows per work item
 constexpr int BN = 128;    // keys per block
 constexpr int THREADS = 256;
 constexpr float LOG2E = 1.4426950408889634f;
@@ -51,6 +54,19 @@ struct FwdParams {
   float scale;
 };
 
+// work item w (heavy first): query block qb = nqb-1 - w / (B*H), (b, h) = w % (B*H)
+struct Item {
+  int b, h, qb;
+};
+SPX_DEVICE Item item_of(int w, int nqb, int BH, int H) {
+  Item it;
+  it.qb = nqb - 1 - w / BH;
+  const int bh = w % BH;
+  it.b = bh / H;
+  it.h = bh % H;
+  return it;
+}
+
 template <int HD>
 struct FwdSmem {
   static constexpr int ATOM = BM * 128;              // 128 rows x 128 B (64 bf16) swizzle atom block
@@ -61,8 +77,8 @@ struct FwdSmem {
   static constexpr int OFF_V = OFF_K + 2 * Q_BYTES;  // [2]
   static constexpr int OFF_P = OFF_V + 2 * Q_BYTES;
   static constexpr int OFF_BAR = OFF_P + P_BYTES;
-  // >= 116 KB so that only one CTA is resident per SM: each CTA allocates all 512 TMEM columns
-  static constexpr int RAW = OFF_BAR + 256 + 1024;
+  // >= 116 KB: one CTA per SM (it owns all 512 TMEM columns)
+  static constexpr int RAW = OFF_BAR + 256;
   static constexpr int BYTES = RAW > 116 * 1024 ? RAW : 116 * 1024;
 };
 
@@ -70,29 +86,29 @@ template <int HD>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const FwdParams p) {
   using L = FwdSmem<HD>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* v_full = bars + 3;   // [2]
-  uint64_t* kv_empty = bars + 5; // [2]
-  uint64_t* s_full = bars + 7;   // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* pv_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;   // [2]
+  uint64_t* v_full = bars + 4;   // [2]
+  uint64_t* kv_empty = bars + 6; // [2]
+  uint64_t* s_full = bars + 8;   // [2]
+  uint64_t* p_full = bars + 10;
+  uint64_t* pv_done = bars + 11;
+  uint64_t* o_free = bars + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = p.T / BM;
-  const int qb = nqb - 1 - (int)blockIdx.x;  // heavy blocks first
-  const int h = blockIdx.y, b = blockIdx.z;
-  const int kvh = h / (p.H / p.Hkv);
-  const int nkb = qb + 1;                    // causal, BM == BN
-  const int row0 = b * p.T;
+  const int BH = p.B * p.H;
+  const int n_items = nqb * BH;
+  const int group = p.H / p.Hkv;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmQKV);
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&v_full[i], 1);
@@ -101,6 +117,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     mbar_init(p_full, 4);
     mbar_init(pv_done, 1);
+    mbar_init(o_free, 4);
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -109,24 +126,31 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // upstream grid complete before any dependent global access
   constexpr uint32_t TM_O = 256;
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
-    mbar_expect_tx(q_full, L::Q_BYTES);
-    for (int a = 0; a < HD / 64; ++a)
-      tma_load_2d(smem + L::OFF_Q + a * L::ATOM, &tmQKV, q_full, h * HD + 64 * a, row0 + qb * BM);
-    for (int j = 0; j < nkb; ++j) {
-      const int s = j & 1;
-      mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-      mbar_expect_tx(&k_full[s], L::Q_BYTES);
+    int g = 0, n = 0;  // global K/V block counter, item counter
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+      const Item it = item_of(w, nqb, BH, p.H);
+      const int row0 = it.b * p.T, kvh = it.h / group;
+      mbar_wait(q_empty, (n & 1) ^ 1);
+      mbar_expect_tx(q_full, L::Q_BYTES);
       for (int a = 0; a < HD / 64; ++a)
-        tma_load_2d(smem + L::OFF_K + s * L::Q_BYTES + a * L::ATOM, &tmQKV, &k_full[s], (p.H + kvh) * HD + 64 * a,
-                    row0 + j * BN);
-      mbar_expect_tx(&v_full[s], L::Q_BYTES);
-      for (int a = 0; a < HD / 64; ++a)
-        tma_load_2d(smem + L::OFF_V + s * L::Q_BYTES + a * L::ATOM, &tmQKV, &v_full[s],
-                    (p.H + p.Hkv + kvh) * HD + 64 * a, row0 + j * BN);
+        tma_load_2d(smem + L::OFF_Q + a * L::ATOM, &tmQKV, q_full, it.h * HD + 64 * a, row0 + it.qb * BM);
+      for (int j = 0; j <= it.qb; ++j, ++g) {
+        const int s = g & 1;
+        mbar_wait(&kv_empty[s], ((g >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[s], L::Q_BYTES);
+        for (int a = 0; a < HD / 64; ++a)
+          tma_load_2d(smem + L::OFF_K + s * L::Q_BYTES + a * L::ATOM, &tmQKV, &k_full[s], (p.H + kvh) * HD + 64 * a,
+                      row0 + j * BN);
+        mbar_expect_tx(&v_full[s], L::Q_BYTES);
+        for (int a = 0; a < HD / 64; ++a)
+          tma_load_2d(smem + L::OFF_V + s * L::Q_BYTES + a * L::ATOM, &tmQKV, &v_full[s],
+                      (p.H + p.Hkv + kvh) * HD + 64 * a, row0 + j * BN);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
@@ -134,11 +158,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr uint32_t IDESC_O = umma_idesc_bf16(BM, HD, false, true);
     const uint32_t sQ = smem_u32(smem + L::OFF_Q);
     const uint32_t sP = smem_u32(smem + L::OFF_P);
-    mbar_wait(q_full, 0);
-    auto issue_pv = [&](int j) {
-      const int s = j & 1;
-      mbar_wait(p_full, j & 1);
-      mbar_wait(&v_full[s], (j >> 1) & 1);
+    int g = 0, n = 0;
+    // PV of block (global index gb, item-local j); the first PV of an item overwrites O, which
+    // the softmax warps must have read out for the previous item
+    auto issue_pv = [&](int gb, int j, int item_n) {
+      const int s = gb & 1;
+      if (j == 0) mbar_wait(o_free, (item_n & 1) ^ 1);
+      mbar_wait(p_full, gb & 1);
+      mbar_wait(&v_full[s], (gb >> 1) & 1);
       tc_fence_after();
       const uint32_t sV = smem_u32(smem + L::OFF_V + s * L::Q_BYTES);
 #pragma unroll
@@ -150,111 +177,133 @@ __global__ void __launch_bounds__(THREADS, 1)
       mma_commit(pv_done);
       mma_commit(&kv_empty[s]);
     };
-    for (int j = 0; j < nkb; ++j) {
-      const int s = j & 1;
-      mbar_wait(&k_full[s], (j >> 1) & 1);
-      tc_fence_after();
-      const uint32_t sK = smem_u32(smem + L::OFF_K + s * L::Q_BYTES);
+    int pend_g = -1, pend_j = 0, pend_n = 0;  // the PV lagging one block behind S
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+      const Item it = item_of(w, nqb, BH, p.H);
+      mbar_wait(q_full, n & 1);
+      for (int j = 0; j <= it.qb; ++j, ++g) {
+        const int s = g & 1;
+        mbar_wait(&k_full[s], (g >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(smem + L::OFF_K + s * L::Q_BYTES);
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const uint64_t ad = umma_desc_sw128(sQ + (kk >> 2) * L::ATOM + (kk & 3) * 32, 16, 1024);
-        const uint64_t bd = umma_desc_sw128(sK + (kk >> 2) * L::ATOM + (kk & 3) * 32, 16, 1024);
-        mma_bf16_ss(tmem + s * BN, ad, bd, IDESC_S, kk > 0);
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint64_t ad = umma_desc_sw128(sQ + (kk >> 2) * L::ATOM + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = umma_desc_sw128(sK + (kk >> 2) * L::ATOM + (kk & 3) * 32, 16, 1024);
+          mma_bf16_ss(tmem + s * BN, ad, bd, IDESC_S, kk > 0);
+        }
+        mma_commit(&s_full[s]);
+        if (j == it.qb) mma_commit(q_empty);  // last S of this item issued: Q reusable
+        if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_n);
+        pend_g = g;
+        pend_j = j;
+        pend_n = n;
       }
-      mma_commit(&s_full[s]);
-      if (j > 0) issue_pv(j - 1);
     }
-    issue_pv(nkb - 1);
+    if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_n);
   } else if (warp >= 4) {
     // ---------------- softmax (thread = query row) ----------------
     const int q = warp - 4;
     const int r = q * 32 + lane;  // row within the block
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     const float sl2 = p.scale * LOG2E;
-    float m = -INFINITY, l = 0.f;
     uint8_t* sP = smem + L::OFF_P;
-    for (int j = 0; j < nkb; ++j) {
-      const int s = j & 1;
-      mbar_wait(&s_full[s], (j >> 1) & 1);
-      tc_fence_after();
-      float x[BN];
-      {
-        uint32_t* xv = reinterpret_cast<uint32_t*>(x);
-#pragma unroll
-        for (int c = 0; c < BN; c += 32)
-          tmem_ld_32x32b_x32(lane_base + s * BN + c, *reinterpret_cast<uint32_t(*)[32]>(xv + c));
-        tmem_ld_wait();  // one wait for the four loads
-      }
-      if (j == qb) {
-#pragma unroll
-        for (int i = 0; i < BN; ++i)
-          if (i > r) x[i] = -INFINITY;
-      }
-      // running max on the raw scores (the scale is positive), exp2 via one FFMA per element
-      float mraw = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < BN; ++i) mraw = fmaxf(mraw, x[i]);
-      const float mx = fmaxf(m, mraw * sl2);
-      const float alpha = ex2(m - mx);  // 0 on the first block (m = -inf)
-      m = mx;
-      float rs = 0.f;
-#pragma unroll
-      for (int i = 0; i < BN; ++i) {
-        x[i] = ex2(fmaf(x[i], sl2, -m));
-        rs += x[i];
-      }
-      l = l * alpha + rs;
-      if (j > 0) {
-        mbar_wait(pv_done, (j - 1) & 1);  // O stable and the P tile free
+    int g = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+      const Item it = item_of(w, nqb, BH, p.H);
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j <= it.qb; ++j, ++g) {
+        const int s = g & 1;
+        mbar_wait(&s_full[s], (g >> 1) & 1);
         tc_fence_after();
-        // rescale O rows whose max grew (warp-uniform decision; tcgen05.ld/st are warp-collective)
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+        float x[BN];
+        {
+          uint32_t* xv = reinterpret_cast<uint32_t*>(x);
 #pragma unroll
-          for (int c = 0; c < HD; c += 32) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(lane_base + TM_O + c, v);
-            tmem_ld_wait();
+          for (int c = 0; c < BN; c += 32)
+            tmem_ld_32x32b_x32(lane_base + s * BN + c, *reinterpret_cast<uint32_t(*)[32]>(xv + c));
+          tmem_ld_wait();
+        }
+        if (j == it.qb) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-            tmem_st_32x32b_x32(lane_base + TM_O + c, v);
+          for (int i = 0; i < BN; ++i)
+            if (i > r) x[i] = -INFINITY;
+        }
+        // row max with 8 independent accumulators (raw scores; the scale is positive)
+        float mk[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mk[k] = x[k];
+#pragma unroll
+        for (int i = 8; i < BN; ++i) mk[i & 7] = fmaxf(mk[i & 7], x[i]);
+        const float mraw = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])),
+                                 fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
+        const float mx = fmaxf(m, mraw * sl2);
+        const float alpha = ex2(m - mx);  // 0 on the first block (m = -inf)
+        m = mx;
+        float sk[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < BN; ++i) {
+          x[i] = ex2(fmaf(x[i], sl2, -m));
+          sk[i & 7] += x[i];
+        }
+        l = l * alpha + (((sk[0] + sk[1]) + (sk[2] + sk[3])) + ((sk[4] + sk[5]) + (sk[6] + sk[7])));
+        if (j > 0) {
+          mbar_wait(pv_done, (g - 1) & 1);  // O stable and the P tile free
+          tc_fence_after();
+          // rescale O rows whose max grew (warp-uniform decision; tcgen05.ld/st are warp-collective)
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+            for (int c = 0; c < HD; c += 32) {
+              uint32_t v[32];
+              tmem_ld_32x32b_x32(lane_base + TM_O + c, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+              tmem_st_32x32b_x32(lane_base + TM_O + c, v);
+            }
+            tmem_st_wait();
           }
-          tmem_st_wait();
+        } else if (g > 0) {
+          mbar_wait(pv_done, (g - 1) & 1);  // previous item's last PV done: the P tile is free
+        }
+        // P (bf16) into the K-major SWIZZLE_128B A tile: row r, keys in two 64-key atoms
+#pragma unroll
+        for (int cch = 0; cch < BN / 8; ++cch) {
+          const int atom = cch >> 3, c16 = cch & 7;
+          uint4 v = make_uint4(pack_bf16(x[8 * cch], x[8 * cch + 1]), pack_bf16(x[8 * cch + 2], x[8 * cch + 3]),
+                               pack_bf16(x[8 * cch + 4], x[8 * cch + 5]), pack_bf16(x[8 * cch + 6], x[8 * cch + 7]));
+          *reinterpret_cast<uint4*>(sP + atom * L::ATOM + r * 128 + ((c16 ^ (r & 7)) << 4)) = v;
+        }
+        fence_proxy_async();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+      }
+      // item epilogue: O / l -> bf16, LSE; then hand O's TMEM back to the MMA warp
+      mbar_wait(pv_done, (g - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const int t = it.qb * BM + r;
+      __nv_bfloat16* orow = p.out + (size_t)(it.b * p.T + t) * p.ldo + it.h * HD;
+#pragma unroll
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(lane_base + TM_O + c, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          *reinterpret_cast<uint4*>(orow + c + i) =
+              make_uint4(pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv),
+                         pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv),
+                         pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv),
+                         pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv));
         }
       }
-      // P (bf16) into the K-major SWIZZLE_128B A tile: row r, keys in two 64-key atoms
-#pragma unroll
-      for (int cch = 0; cch < BN / 8; ++cch) {
-        const int atom = cch >> 3, c16 = cch & 7;
-        uint4 v = make_uint4(pack_bf16(x[8 * cch], x[8 * cch + 1]), pack_bf16(x[8 * cch + 2], x[8 * cch + 3]),
-                             pack_bf16(x[8 * cch + 4], x[8 * cch + 5]), pack_bf16(x[8 * cch + 6], x[8 * cch + 7]));
-        *reinterpret_cast<uint4*>(sP + atom * L::ATOM + r * 128 + ((c16 ^ (r & 7)) << 4)) = v;
-      }
-      fence_proxy_async();
+      p.lse[((size_t)it.b * p.H + it.h) * p.T + t] = (m + log2f(l)) / LOG2E;
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(o_free);
     }
-    // epilogue: O / l -> bf16, LSE
-    mbar_wait(pv_done, (nkb - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l;
-    const int t = qb * BM + r;
-    __nv_bfloat16* orow = p.out + (size_t)(row0 + t) * p.ldo + h * HD;
-#pragma unroll
-    for (int c = 0; c < HD; c += 32) {
-      uint32_t v[32];
-      tmem_ld_32x32b_x32(lane_base + TM_O + c, v);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        *reinterpret_cast<uint4*>(orow + c + i) =
-            make_uint4(pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv),
-                       pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv),
-                       pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv),
-                       pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv));
-      }
-    }
-    p.lse[((size_t)b * p.H + h) * p.T + t] = (m + log2f(l)) / LOG2E;
   }
   __syncwarp();
   tc_fence_before();
@@ -283,7 +332,9 @@ int launch_fwd(const void* qkv, const FwdParams& p, long long ld_qkv, cudaStream
     if (e != cudaSuccess) return set_cuda_error(e, "attn_fwd_tc attr");
     set = true;
   }
-  k<<<dim3(p.T / BM, p.H, p.B), THREADS, FwdSmem<HD>::BYTES, s>>>(map, p);
+  const int items = (p.T / BM) * p.B * p.H;
+  const int grid = items < num_sms() ? items : num_sms();
+  spx_launch_check(launch_k(k, dim3(grid), dim3(THREADS), FwdSmem<HD>::BYTES, s, map, p));
   return check_launch("attn_fwd_tc_kernel");
 }
 
