@@ -26,6 +26,10 @@ constexpr int THREADS = 128 + 32 * EW_WARPS;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr int ATOM = BLK * 128;          // 128 rows x 128 B swizzle atom block
 
+// Heavy-first item lists are dealt to CTAs in boustrophedon order (round k: CTA c takes item
+// k*G + c for even k, k*G + G-1-c for odd k), pairing heavy and light items per CTA.
+SPX_DEVICE int snake(int k, int c, int G) { return k * G + ((k & 1) ? (G - 1 - c) : c); }
+
 SPX_DEVICE float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -180,7 +184,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0 && lane == 0) {
     // ---------------- producer ----------------
     int gi = 0, n = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
+      if (w >= n_items) continue;
       int b, kvh, jb;
       item(w, b, kvh, jb);
       const int row0 = b * p.T, nq = nqb - jb;
@@ -225,7 +230,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       mma_commit(sdp_full);
     };
     int gi = 0, n = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
+      if (w >= n_items) continue;
       int b, kvh, jb;
       item(w, b, kvh, jb);
       const int n_it = group * (nqb - jb);
@@ -271,7 +277,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint8_t* sPT = smem + L::OFF_PT;
     uint8_t* sDST = smem + L::OFF_DST;
     int gi = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
+      if (w >= n_items) continue;
       int b, kvh, jb;
       item(w, b, kvh, jb);
       const int nq = nqb - jb, n_it = group * nq;
@@ -402,7 +409,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     int gj = 0, n = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
+      if (w >= n_items) continue;
       int b, h, ib;
       item(w, b, h, ib);
       const int row0 = b * p.T, kvh = h / group;
@@ -444,7 +452,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       mma_commit(sdp_full);
     };
     int gj = 0, n = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
+      if (w >= n_items) continue;
       int b, h, ib;
       item(w, b, h, ib);
       mbar_wait(qdo_full, n & 1);
@@ -482,7 +491,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const float sl2 = p.scale * LOG2E;
     uint8_t* sDS = smem + L::OFF_DS;
     int gj = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
+      if (w >= n_items) continue;
       int b, h, ib;
       item(w, b, h, ib);
       const int t = ib * BLK + r;

@@ -40,6 +40,10 @@ SPX_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
 }
 SPX_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// Heavy-first item lists are dealt to CTAs in boustrophedon order (round k: CTA c takes item
+// k*G + c for even k, k*G + G-1-c for odd k), pairing heavy and light items per CTA.
+SPX_DEVICE int snake(int k, int c, int G) { return k * G + ((k & 1) ? (G - 1 - c) : c); }
+
 SPX_DEVICE float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -132,7 +136,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
     int g = 0, n = 0;  // global K/V block counter, item counter
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
+      if (w >= n_items) continue;
       const Item it = item_of(w, nqb, BH, p.H);
       const int row0 = it.b * p.T, kvh = it.h / group;
       mbar_wait(q_empty, (n & 1) ^ 1);
@@ -178,7 +183,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       mma_commit(&kv_empty[s]);
     };
     int pend_g = -1, pend_j = 0, pend_n = 0;  // the PV lagging one block behind S
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
+      if (w >= n_items) continue;
       const Item it = item_of(w, nqb, BH, p.H);
       mbar_wait(q_full, n & 1);
       for (int j = 0; j <= it.qb; ++j, ++g) {
@@ -209,7 +215,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const float sl2 = p.scale * LOG2E;
     uint8_t* sP = smem + L::OFF_P;
     int g = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
+      if (w >= n_items) continue;
       const Item it = item_of(w, nqb, BH, p.H);
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j <= it.qb; ++j, ++g) {

@@ -183,35 +183,54 @@ class StageProgram:
         native.gemm(a.h, ps.w(f"l{i}.wdown"), y, M=n, N=d, K=f, lda=f, ldb=f, ldc=d,
                     epilogue=native.EPI_BF16_RESID, R=a.xmid, stream=s)
 
-    def layer_bwd(self, ps: ParamSet, i: int, x, a: LayerActs, dy, dx, sc: Scratch, s):
-        """dy: grad of the layer output; dx: grad of the layer input (may not alias dy)."""
+    def layer_bwd(self, ps: ParamSet, i: int, x, a: LayerActs, dy, dx, sc: Scratch, s, side=None):
+        """dy: grad of the layer output; dx: grad of the layer input (may not alias dy).
+
+        The four weight-gradient GEMMs (few output tiles, long K = tokens) go to ``side`` when given:
+        forked from ``s`` as soon as their inputs exist and joined at the end of the layer, so they
+        fill SMs the data-gradient chain leaves idle.  Everything they read (saved activations, and
+        scratch written once per layer) stays untouched until the join."""
         c, n = self.cfg, self.n
         d, f, qd, hd = c.d, c.ffn, c.qkv_dim, c.head_dim
         od = c.n_heads * hd
         F32E = native.EPI_F32
+
+        def wgrad(fn):
+            if side is None:
+                fn(s)
+                return
+            ev = torch.cuda.Event()
+            ev.record(s)
+            side.wait_event(ev)
+            fn(side)
+
         # MLP
+        wgrad(lambda st: native.gemm(dy, a.h, ps.gv(f"l{i}.wdown"), M=d, N=f, K=n, lda=d, ldb=f, ldc=f, a_mn=True,
+                                     b_mn=True, epilogue=F32E, beta=1.0, stream=st))
         native.gemm(dy, ps.w(f"l{i}.wdown"), sc.dh, M=n, N=f, K=d, lda=d, ldb=f, ldc=f, b_mn=True, stream=s)
-        native.gemm(dy, a.h, ps.gv(f"l{i}.wdown"), M=d, N=f, K=n, lda=d, ldb=f, ldc=f, a_mn=True, b_mn=True,
-                    epilogue=F32E, beta=1.0, stream=s)
         native.swiglu_bwd(a.gu, sc.dh, sc.dgu, rows=n, F=f, stream=s)
+        wgrad(lambda st: native.gemm(sc.dgu, a.xn2, ps.gv(f"l{i}.wgu"), M=2 * f, N=d, K=n, lda=2 * f, ldb=d, ldc=d,
+                                     a_mn=True, b_mn=True, epilogue=F32E, beta=1.0, stream=st))
         native.gemm(sc.dgu, ps.w(f"l{i}.wgu"), sc.dxn, M=n, N=d, K=2 * f, lda=2 * f, ldb=d, ldc=d, b_mn=True,
                     stream=s)
-        native.gemm(sc.dgu, a.xn2, ps.gv(f"l{i}.wgu"), M=2 * f, N=d, K=n, lda=2 * f, ldb=d, ldc=d, a_mn=True,
-                    b_mn=True, epilogue=F32E, beta=1.0, stream=s)
         native.rmsnorm_bwd(a.xmid, ps.w(f"l{i}.mlp_norm"), a.rstd2, sc.dxn, dy, sc.dxm, ps.gv(f"l{i}.mlp_norm"),
                            sc.rms_ws, rows=n, d=d, stream=s)
         # attention
+        wgrad(lambda st: native.gemm(sc.dxm, a.o, ps.gv(f"l{i}.wo"), M=d, N=od, K=n, lda=d, ldb=od, ldc=od, a_mn=True,
+                                     b_mn=True, epilogue=F32E, beta=1.0, stream=st))
         native.gemm(sc.dxm, ps.w(f"l{i}.wo"), sc.do, M=n, N=od, K=d, lda=d, ldb=od, ldc=od, b_mn=True, stream=s)
-        native.gemm(sc.dxm, a.o, ps.gv(f"l{i}.wo"), M=d, N=od, K=n, lda=d, ldb=od, ldc=od, a_mn=True, b_mn=True,
-                    epilogue=F32E, beta=1.0, stream=s)
         # dq, dk leave the attention backward already un-rotated (inverse RoPE fused)
         native.attn_bwd(a.qkv, a.o, sc.do, a.lse, sc.delta, sc.dqkv, B=self.b, T=self.T, H=c.n_heads,
                         Hkv=c.n_kv_heads, hd=hd, ld_qkv=qd, ld_o=od, scale=self.scale, rope_cs=sc.rope, stream=s)
+        wgrad(lambda st: native.gemm(sc.dqkv, a.xn1, ps.gv(f"l{i}.wqkv"), M=qd, N=d, K=n, lda=qd, ldb=d, ldc=d,
+                                     a_mn=True, b_mn=True, epilogue=F32E, beta=1.0, stream=st))
         native.gemm(sc.dqkv, ps.w(f"l{i}.wqkv"), sc.dxn, M=n, N=d, K=qd, lda=qd, ldb=d, ldc=d, b_mn=True, stream=s)
-        native.gemm(sc.dqkv, a.xn1, ps.gv(f"l{i}.wqkv"), M=qd, N=d, K=n, lda=qd, ldb=d, ldc=d, a_mn=True, b_mn=True,
-                    epilogue=F32E, beta=1.0, stream=s)
         native.rmsnorm_bwd(x, ps.w(f"l{i}.attn_norm"), a.rstd1, sc.dxn, sc.dxm, dx, ps.gv(f"l{i}.attn_norm"),
                            sc.rms_ws, rows=n, d=d, stream=s)
+        if side is not None:  # join: the next layer reuses the scratch buffers the wgrads read
+            ev = torch.cuda.Event()
+            ev.record(side)
+            s.wait_event(ev)
 
     # ---- node ops ----
     def fwd(self, ps: ParamSet, sb: SlotBuffers, sc: Scratch, origin: bool, s):
@@ -220,13 +239,13 @@ class StageProgram:
         for i, a in enumerate(sb.layers):
             self.layer_fwd(ps, i, sb.xs[i], a, sb.xs[i + 1], sc, s)
 
-    def bwd(self, ps: ParamSet, sb: SlotBuffers, sc: Scratch, origin: bool, s):
+    def bwd(self, ps: ParamSet, sb: SlotBuffers, sc: Scratch, origin: bool, s, side=None):
         """Returns the buffer holding the gradient w.r.t. the node's input."""
         dy = sb.gin
         k = 0
         for i in reversed(range(len(sb.layers))):
             dx = sc.dx[k]
-            self.layer_bwd(ps, i, sb.xs[i], sb.layers[i], dy, dx, sc, s)
+            self.layer_bwd(ps, i, sb.xs[i], sb.layers[i], dy, dx, sc, s, side)
             dy, k = dx, k ^ 1
         if origin:
             native.embed_bwd(sb.perm, sb.seg_start, sb.seg_id, sb.n_seg, self.n, dy, ps.gv("embed"), d=self.cfg.d,
@@ -373,6 +392,9 @@ class Trainer:
             native.gemm_set_workspace(self._gemm_sem)
             self.stream = torch.cuda.Stream(device=self.dev)
             self.recv_stream = torch.cuda.Stream(device=self.dev)
+            # weight-gradient GEMMs run here, forked/joined per layer inside the B graphs
+            self.side_stream = torch.cuda.Stream(device=self.dev) if os.environ.get("SPX_WGRAD_SIDE", "1") != "0" \
+                else None
             self.prog = StageProgram(cfg, self.n, b, self.T, self.M)
             self.mb_loss = torch.zeros(self.M, dtype=F32, device=self.dev)
             self._sumsq = torch.zeros(assignment.s, dtype=F32, device=self.dev)
@@ -431,7 +453,7 @@ class Trainer:
             return sb.xs[-1]
         if kind == L:
             return self.prog.loss(ps, sb, self.scratch, s)
-        return self.prog.bwd(ps, sb, self.scratch, origin, s)
+        return self.prog.bwd(ps, sb, self.scratch, origin, s, self.side_stream)
 
     def _key(self, op):
         return (op.kind, op.node, self.slot_of[(op.agent, op.node)])
