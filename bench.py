@@ -310,6 +310,7 @@ def run_ours_dist(args, rc):
                  rank=rank, world=world, device=local)
     native.record_gemms(False)
     launches = torch.tensor([tr.launches_per_step()], device=tr.dev)
+    placement = list(tr.placement)
     dist.all_reduce(launches)
     host = tr._stage_inputs(tokens)
     dev_inputs = {k: v.cuda() for k, v in host.items()}
@@ -361,7 +362,7 @@ def run_ours_dist(args, rc):
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": rc.name, "model": rc.model.name, "global_batch": rc.M * rc.b, "seq_len": rc.T,
                        "microbatches": rc.M, "tokens_per_step": tok, "stages": rc.s, "replicas": rc.sizes,
-                       "skip_pct": rc.k, "m": rc.m, "placement": tr.placement,
+                       "skip_pct": rc.k, "m": rc.m, "placement": placement,
                        "parallelism": f"pp-skip({rc.s}x{rc.sizes[0]} logical nodes over {world} GPUs)+dp-allreduce",
                        "l2_flush": "inputs+activations per step >> 126 MB L2", "kind": rc.kind},
             "loss": round(res["loss"], 5),

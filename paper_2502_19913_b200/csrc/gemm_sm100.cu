@@ -36,6 +36,7 @@ enum GemmEpilogue : int {
   EPI_SWIGLU = 3,      // H(bf16)[m, N/2] = silu(g)*u ; GU(bf16)[m, N] = (g,u) raw, 128-col interleave
   EPI_ROPE64 = 4,      // C(bf16) = acc with rotate-half RoPE on columns < rope_cols (head dim 64)
   EPI_ROPE128 = 5,     // same, head dim 128
+  EPI_SWIGLU_BWD = 6,  // D = dh [M, F]; R = gu [M, 2F] (128-col gate/up interleave) -> C2 = dgu [M, 2F]
 };
 
 template <int EPI>
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmC);
-    if (EPI == EPI_SWIGLU) tma_prefetch_desc(&tmC2);
+    if (EPI == EPI_SWIGLU || EPI == EPI_SWIGLU_BWD) tma_prefetch_desc(&tmC2);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -292,6 +293,49 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             else box_issue(&tmC2, n0 + BN / 2 + c, rbase, false);
           }
         }
+      } else if constexpr (EPI == EPI_SWIGLU_BWD) {
+        // dh tile columns [cb, cb+128) = one 128-column gate/up block of the interleaved layout:
+        //   dgate = dh * up * sig(g) * (1 + g (1 - sig(g))),  dup = dh * silu(g)
+        const int fc = n0 + cb;  // first dh column of this warp
+        if (fc < args.N) {
+          const int blk = fc >> 7;
+          const int row = rbase + lane;
+          const __nv_bfloat16* gur =
+              reinterpret_cast<const __nv_bfloat16*>(args.R) + (size_t)(row < args.M ? row : 0) * args.ldr + blk * 256;
+#pragma unroll 1
+          for (int c = 0; c < 128; c += 64) {
+#pragma unroll 1
+            for (int part = 0; part < 2; ++part) {  // 0: dgate box, 1: dup box
+              box_acquire();
+#pragma unroll 1
+              for (int q = 0; q < 2; ++q) {
+                float dh[32], o[32];
+                ld32(t_row + cb + c + 32 * q, dh);
+#pragma unroll
+                for (int j8 = 0; j8 < 4; ++j8) {
+                  const uint4 g4 = *reinterpret_cast<const uint4*>(gur + c + 32 * q + 8 * j8);
+                  const uint4 u4 = *reinterpret_cast<const uint4*>(gur + 128 + c + 32 * q + 8 * j8);
+                  const uint32_t gw[4] = {g4.x, g4.y, g4.z, g4.w}, uw[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float2 g2 = unpack_bf16(gw[e]), u2 = unpack_bf16(uw[e]);
+                    const int j = 8 * j8 + 2 * e;
+                    const float s0 = __frcp_rn(1.f + __expf(-g2.x)), s1 = __frcp_rn(1.f + __expf(-g2.y));
+                    if (part == 0) {
+                      o[j] = dh[j] * u2.x * s0 * (1.f + g2.x * (1.f - s0));
+                      o[j + 1] = dh[j + 1] * u2.y * s1 * (1.f + g2.y * (1.f - s1));
+                    } else {
+                      o[j] = dh[j] * g2.x * s0;
+                      o[j + 1] = dh[j + 1] * g2.y * s1;
+                    }
+                  }
+                }
+                put32(4 * q, o);
+              }
+              box_issue(&tmC2, blk * 256 + 128 * part + c, rbase, false);
+            }
+          }
+        }
       } else if constexpr (RopeHd<EPI>::value != 0) {
         // RoPE fused into the QKV projection.  The table is position-minor ([hd/2][T] of
         // (cos, sin)), so for a pair index j the warp's 32 consecutive rows read one contiguous
@@ -427,12 +471,14 @@ static int launch_gemm(const void* A, const void* B, long long lda, long long ld
   memset(&tc2, 0, sizeof tc2);
   if (EPI == EPI_F32) rc = make_tmap_2d(&tc, args.C, args.N, args.M, args.ldc, 32, 32, true);
   else if (EPI == EPI_SWIGLU) rc = make_tmap_2d(&tc, args.C, args.N / 2, args.M, args.ldc, 64, 32);
+  else if (EPI == EPI_SWIGLU_BWD) rc = make_tmap_2d(&tc, args.C2, 2 * args.N, args.M, args.ldc2, 64, 32);
   else rc = make_tmap_2d(&tc, args.C, args.N, args.M, args.ldc, 64, 32);
   if (rc) return rc;
   if (EPI == EPI_SWIGLU) {
     rc = make_tmap_2d(&tc2, args.C2, args.N, args.M, args.ldc2, 64, 32);
     if (rc) return rc;
   }
+  if (EPI == EPI_SWIGLU_BWD) tc2 = tc;
   auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, EPI>;
   static bool attr_set = false;  // one per template instantiation
   if (!attr_set) {
@@ -541,14 +587,17 @@ extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* 
   if (N % 32 != 0) return set_error(SPX_ERR_ARG, "gemm: N must be a multiple of 32");
   if (K % 8 != 0 || lda % 8 != 0 || ldb % 8 != 0) return set_error(SPX_ERR_ARG, "gemm: K/lda/ldb must be multiples of 8");
   if (((uintptr_t)A | (uintptr_t)B) & 15) return set_error(SPX_ERR_ARG, "gemm: A/B must be 16-byte aligned");
-  if (epilogue < 0 || epilogue > 3) return set_error(SPX_ERR_ARG, "gemm: bad epilogue");
+  if (epilogue < 0 || epilogue > 6 || epilogue == 4 || epilogue == 5) return set_error(SPX_ERR_ARG, "gemm: bad epilogue");
+  if (epilogue == EPI_SWIGLU_BWD && (N % 128 != 0 || C2 == nullptr || R == nullptr))
+    return set_error(SPX_ERR_ARG, "gemm: swiglu-bwd epilogue needs N % 128 == 0, gu (R) and dgu (C2)");
   if (epilogue == EPI_SWIGLU && (N % 256 != 0 || C2 == nullptr))
     return set_error(SPX_ERR_ARG, "gemm: swiglu epilogue needs N % 256 == 0 and a GU output");
   if (epilogue == EPI_BF16_RESID && R == nullptr) return set_error(SPX_ERR_ARG, "gemm: residual epilogue needs R");
-  GemmArgs args{(int)M, (int)N, (int)K, C, R, C2, (long long)ldc, (long long)ldc, (long long)ldc2, beta, nullptr, 0, 1,
-                1, nullptr};
+  GemmArgs args{(int)M, (int)N, (int)K, C, R, C2, (long long)ldc, (long long)(epilogue == EPI_SWIGLU_BWD ? ldc2 : ldc),
+                (long long)ldc2, beta, nullptr, 0, 1, 1, nullptr};
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int bn = (epilogue == EPI_SWIGLU || epilogue == EPI_F32) ? 256 : pick_bn((int)M, (int)N);
+  const int bn = (epilogue == EPI_SWIGLU || epilogue == EPI_F32 || epilogue == EPI_SWIGLU_BWD) ? 256
+                                                                                               : pick_bn((int)M, (int)N);
   if (epilogue == EPI_F32) pick_splits(args, bn);
   switch (epilogue) {
     case EPI_BF16:
@@ -560,6 +609,8 @@ extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* 
     case EPI_F32:
       return bn == 256 ? dispatch_major<256, EPI_F32>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s)
                        : dispatch_major<128, EPI_F32>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
+    case EPI_SWIGLU_BWD:
+      return dispatch_major<256, EPI_SWIGLU_BWD>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
     default:
       return dispatch_major<256, EPI_SWIGLU>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
   }

@@ -117,6 +117,9 @@ class SlotBuffers:
         self.xs = [torch.empty(n, cfg.d, **e) for _ in range(n_layers + 1)]  # residual stream
         self.layers = [LayerActs(cfg, n, b, T, device) for _ in range(n_layers)]
         self.gin = torch.empty(n, cfg.d, **e)           # gradient w.r.t. this node's output
+        # gradient w.r.t. this node's input (the B op's output, sent to the previous node); slot-
+        # owned so a cross-GPU send can drain asynchronously on the send stream
+        self.gout = torch.empty(n, cfg.d, **e) if not origin else None
         if origin:
             self.ids = torch.zeros(n, dtype=torch.int32, device=device)
             self.targets = torch.zeros(n, dtype=torch.int32, device=device)
@@ -125,6 +128,7 @@ class SlotBuffers:
             self.seg_id = torch.zeros(n, dtype=torch.int32, device=device)
             self.n_seg = torch.zeros(1, dtype=torch.int32, device=device)
             self.ret = torch.empty(n, cfg.d, **e)       # activation returned to the origin (L input)
+            self.dret = torch.empty(n, cfg.d, **e)      # L output: gradient sent to the last node
             self.loss = torch.zeros(1, dtype=F32, device=device)
 
 
@@ -150,7 +154,6 @@ class Scratch:
             self.logits = torch.empty(n, cfg.vocab, **e)
             self.row_loss = torch.empty(n, dtype=F32, device=device)
             self.dxf = torch.empty(n, d, **e)
-            self.dret = torch.empty(n, d, **e)
 
 
 # ---------------------------------------------------------------------------------------
@@ -207,6 +210,8 @@ class StageProgram:
         # MLP
         wgrad(lambda st: native.gemm(dy, a.h, ps.gv(f"l{i}.wdown"), M=d, N=f, K=n, lda=d, ldb=f, ldc=f, a_mn=True,
                                      b_mn=True, epilogue=F32E, beta=1.0, stream=st))
+        # (the fused EPI_SWIGLU_BWD epilogue exists but is slower than dgrad + swiglu_bwd today:
+        # its per-row gate/up reads make the epilogue the bottleneck)
         native.gemm(dy, ps.w(f"l{i}.wdown"), sc.dh, M=n, N=f, K=d, lda=d, ldb=f, ldc=f, b_mn=True, stream=s)
         native.swiglu_bwd(a.gu, sc.dh, sc.dgu, rows=n, F=f, stream=s)
         wgrad(lambda st: native.gemm(sc.dgu, a.xn2, ps.gv(f"l{i}.wgu"), M=2 * f, N=d, K=n, lda=2 * f, ldb=d, ldc=d,
@@ -244,7 +249,7 @@ class StageProgram:
         dy = sb.gin
         k = 0
         for i in reversed(range(len(sb.layers))):
-            dx = sc.dx[k]
+            dx = sb.gout if (i == 0 and sb.gout is not None) else sc.dx[k]
             self.layer_bwd(ps, i, sb.xs[i], sb.layers[i], dy, dx, sc, s, side)
             dy, k = dx, k ^ 1
         if origin:
@@ -263,9 +268,9 @@ class StageProgram:
         native.gemm(sc.logits, ps.w("head"), sc.dxf, M=n, N=d, K=V, lda=V, ldb=d, ldc=d, b_mn=True, stream=s)
         native.gemm(sc.logits, sc.xf, ps.gv("head"), M=V, N=d, K=n, lda=V, ldb=d, ldc=d, a_mn=True, b_mn=True,
                     epilogue=native.EPI_F32, beta=1.0, stream=s)
-        native.rmsnorm_bwd(sb.ret, ps.w("final_norm"), sc.rstdf, sc.dxf, None, sc.dret, ps.gv("final_norm"),
+        native.rmsnorm_bwd(sb.ret, ps.w("final_norm"), sc.rstdf, sc.dxf, None, sb.dret, ps.gv("final_norm"),
                            sc.rms_ws, rows=n, d=d, stream=s)
-        return sc.dret
+        return sb.dret
 
 
 # ---------------------------------------------------------------------------------------
@@ -392,6 +397,7 @@ class Trainer:
             native.gemm_set_workspace(self._gemm_sem)
             self.stream = torch.cuda.Stream(device=self.dev)
             self.recv_stream = torch.cuda.Stream(device=self.dev)
+            self.send_stream = torch.cuda.Stream(device=self.dev)
             # weight-gradient GEMMs run here, forked/joined per layer inside the B graphs
             self.side_stream = torch.cuda.Stream(device=self.dev) if os.environ.get("SPX_WGRAD_SIDE", "1") != "0" \
                 else None
@@ -510,6 +516,7 @@ class Trainer:
         t_iter0 = torch.cuda.Event(enable_timing=True)
         t_iter1 = torch.cuda.Event(enable_timing=True)
         pending: dict = {}
+        sends: list = []
         with torch.cuda.device(self.dev):
             s.wait_stream(torch.cuda.current_stream(self.dev))
             t_iter0.record(s)
@@ -565,9 +572,14 @@ class Trainer:
                 elif mine:
                     import torch.distributed as dist
 
-                    with torch.cuda.stream(s):
-                        w = dist.isend(out, dst_rank, group=self._pair[dst_rank])
-                        w.wait()                # the source buffer is reused by later ops
+                    # the source is slot-owned (F: last residual buffer, B: gout, L: dret) and is
+                    # rewritten only by this agent's next wave, which causally follows this send's
+                    # completion: drain it on the send stream without stalling compute
+                    ev_out = torch.cuda.Event()
+                    ev_out.record(s)
+                    self.send_stream.wait_event(ev_out)
+                    with torch.cuda.stream(self.send_stream):
+                        sends.append(dist.isend(out, dst_rank, group=self._pair[dst_rank]))
                 elif dst_mine:
                     import torch.distributed as dist
 
@@ -579,6 +591,11 @@ class Trainer:
                     with torch.cuda.stream(self.recv_stream):
                         w = dist.irecv(buf, self.placement[v], group=self._pair[self.placement[v]])
                     pending[(consumer, nv, op.agent, op.wave)] = w
+            if sends:
+                with torch.cuda.stream(s):
+                    for w in sends:
+                        w.wait()
+                s.wait_stream(self.send_stream)
             self.optimizer_step()
             t_iter1.record(s)
             torch.cuda.current_stream(self.dev).wait_stream(s)

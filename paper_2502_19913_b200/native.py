@@ -49,6 +49,7 @@ _RESTYPE = {"spx_last_error": ctypes.c_char_p, "spx_rmsnorm_ws_floats": ctypes.c
             "spx_sumsq_ws_floats": ctypes.c_int64}
 
 EPI_BF16, EPI_BF16_RESID, EPI_F32, EPI_SWIGLU = 0, 1, 2, 3
+EPI_SWIGLU_BWD = 6
 
 
 # kernel-launch accounting (bench.py "gpu_launches") and GEMM call recording (roofline timing)

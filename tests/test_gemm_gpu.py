@@ -106,3 +106,26 @@ def test_gemm_swiglu(M, F, K):
     gu = GU.view(M, F // 128, 2, 128)
     assert _rel(gu[:, :, 0].reshape(M, F), gate) < 1e-2
     assert _rel(gu[:, :, 1].reshape(M, F), up) < 1e-2
+
+
+@pytest.mark.parametrize("M,F,K", [(512, 768, 288), (4096, 2816, 1024)])
+def test_gemm_swiglu_bwd_epilogue(M, F, K):
+    """dh = dy . Wdown with the SwiGLU backward fused: dgu vs torch autograd of silu(g)*u."""
+    g = torch.Generator().manual_seed(5)
+    dy = _mk(M, K, gen=g)                      # grad of the down-projection output, K = d
+    wd = _mk(K, F, gen=g)                      # Wdown [d, F]
+    gate, up = torch.randn(M, F, generator=g), torch.randn(M, F, generator=g)
+    gu = torch.stack([gate.view(M, F // 128, 128), up.view(M, F // 128, 128)], dim=2).reshape(M, 2 * F)
+    gu = gu.to(torch.bfloat16).cuda()
+    dgu = torch.empty_like(gu)
+    native.gemm(dy, wd, None, M=M, N=F, K=K, lda=K, ldb=F, ldc=F, b_mn=True, epilogue=native.EPI_SWIGLU_BWD, R=gu,
+                C2=dgu, ldc2=2 * F)
+    torch.cuda.synchronize()
+    dh = dy.float() @ wd.float()
+    gr = gu.float().view(M, F // 128, 2, 128)
+    gt = gr[:, :, 0].reshape(M, F).requires_grad_()
+    ut = gr[:, :, 1].reshape(M, F).requires_grad_()
+    (torch.nn.functional.silu(gt) * ut).backward(dh)
+    d = dgu.float().view(M, F // 128, 2, 128)
+    assert _rel(d[:, :, 0].reshape(M, F), gt.grad) < 2e-2
+    assert _rel(d[:, :, 1].reshape(M, F), ut.grad) < 2e-2
