@@ -283,23 +283,35 @@ __global__ void __launch_bounds__(THREADS) attn_fwd_kernel(const Params p) {
 template <int HD>
 __global__ void attn_bwd_delta_kernel(const Params p) {
   pdl_wait();
-  // one warp per (row, head)
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  // 8 lanes per (row, head); lane j sums the 16-byte vectors j, j+8, ... of that head's row
+  const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const int j = threadIdx.x & 7;
   const long long rows = (long long)p.B * p.T;
-  if (gw >= rows * p.H) return;
-  const long long r = gw / p.H;
-  const int h = (int)(gw % p.H);
+  const bool live = g < rows * p.H;
+  const long long gg = live ? g : 0;
+  const long long r = gg / p.H;
+  const int h = (int)(gg % p.H);
   const __nv_bfloat16* o = p.o + r * p.ldo + h * HD;
   const __nv_bfloat16* d = p.dout + r * p.ldo + h * HD;
   float s = 0.f;
-  for (int i = lane * 2; i < HD; i += 64) {
-    float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + i));
-    float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(d + i));
-    s += a.x * c.x + a.y * c.y;
+  if (live) {
+#pragma unroll
+    for (int v = j; v < HD / 8; v += 8) {
+      const uint4 a = *reinterpret_cast<const uint4*>(o + v * 8);
+      const uint4 c = *reinterpret_cast<const uint4*>(d + v * 8);
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 fa = __bfloat1622float2(a2[i]), fc = __bfloat1622float2(c2[i]);
+        s += fa.x * fc.x + fa.y * fc.y;
+      }
+    }
   }
-  s = warp_sum(s);
-  if (lane == 0) {
+  s += __shfl_xor_sync(0xffffffffu, s, 4);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  if (live && j == 0) {
     const int b = (int)(r / p.T), t = (int)(r % p.T);
     p.delta[((long long)b * p.H + h) * p.T + t] = s;
   }
@@ -559,9 +571,9 @@ static int run_bwd(const Params& p, cudaStream_t s) {
   constexpr int LD = Tile<HD>::LD;
   constexpr int BQI = (HD > 64) ? 32 : 64;
   {
-    const long long warps = (long long)p.B * p.T * p.H;
+    const long long groups = (long long)p.B * p.T * p.H;  // 8 threads each
     const int threads = 256;
-    spx_launch_check(launch_k(attn_bwd_delta_kernel<HD>, dim3((unsigned)((warps * 32 + threads - 1) / threads)), dim3(threads), 0, s, p));
+    spx_launch_check(launch_k(attn_bwd_delta_kernel<HD>, dim3((unsigned)((groups * 8 + threads - 1) / threads)), dim3(threads), 0, s, p));
     int rc = check_launch("attn_bwd_delta_kernel");
     if (rc) return rc;
   }
@@ -644,6 +656,8 @@ extern "C" int spx_attn_bwd(const void* qkv, const void* o, const void* dout, co
                             int64_t ld_o, float scale, const float* rope_cos_sin, void* stream) {
   int rc = attn::check_args(B, T, H, Hkv, hd);
   if (rc) return rc;
+  if (ld_o % 8 != 0 || (((uintptr_t)o | (uintptr_t)dout) & 15))
+    return set_error(SPX_ERR_ARG, "attn_bwd: O/dO must be 16-byte aligned with ld_o % 8 == 0");
   attn::Params p{};
   p.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv);
   p.out = reinterpret_cast<__nv_bfloat16*>(dqkv);

@@ -129,13 +129,119 @@ __global__ void __launch_bounds__(128) rmsnorm_dg_partial_kernel(const __nv_bflo
   *reinterpret_cast<float2*>(part + (size_t)blockIdx.y * d + c) = make_float2(a0, a1);
 }
 
-__global__ void colsum_add_kernel(const float* __restrict__ part, float* __restrict__ out, int nsplit, int d) {
+// RMSNorm backward, dx and dg in one pass over x and dy.  Warp per row (a CTA owns a contiguous
+// block of rows, warp w takes rows w, w+8, ...); lane owns the 8-column vectors lane*8 + k*256
+// (k < NCH), so x and dy stay in registers between the row-dot pass and the dx pass, and the
+// lane's dg accumulators need no shuffles.  The CTA's dg partial is reduced over its warps in
+// fixed order through shared memory (deterministic), then colsum_add_kernel adds the partials.
+template <int NCH>
+__global__ void __launch_bounds__(256, NCH <= 4 ? 2 : 1) rmsnorm_bwd_fused_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd,
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx,
+    float* __restrict__ part, int rows, int d, int rows_per_cta) {
+  extern __shared__ float red[];  // [ROW_WARPS][d]
   pdl_wait();
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= d) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float acc[NCH][8];
+#pragma unroll
+  for (int k = 0; k < NCH; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[k][i] = 0.f;
+  const int r0 = blockIdx.x * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
+  for (int r = r0 + warp; r < r1; r += ROW_WARPS) {
+    const size_t off = (size_t)r * d;
+    const float s = rstd[r];
+    Vec8 xv[NCH], yv[NCH], rv[NCH];  // x, dy and dres of this row, loaded together up front
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const int c = lane * 8 + k * 256;
+      if (c < d) {
+        xv[k].u = *reinterpret_cast<const uint4*>(x + off + c);
+        yv[k].u = *reinterpret_cast<const uint4*>(dy + off + c);
+        rv[k].u = dres ? *reinterpret_cast<const uint4*>(dres + off + c) : make_uint4(0, 0, 0, 0);
+      }
+    }
+    float dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const int c = lane * 8 + k * 256;
+      if (c < d) {
+        float w[8];
+        load8(w, g + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 xf = __bfloat1622float2(xv[k].h[i]), gy = __bfloat1622float2(yv[k].h[i]);
+          dot += xf.x * w[2 * i] * gy.x + xf.y * w[2 * i + 1] * gy.y;
+        }
+      }
+    }
+    dot = warp_sum(dot) * s / d;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const int c = lane * 8 + k * 256;
+      if (c < d) {
+        float w[8], o[8];
+        load8(w, g + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 xf = __bfloat1622float2(xv[k].h[i]), gy = __bfloat1622float2(yv[k].h[i]);
+          const float2 rf = __bfloat1622float2(rv[k].h[i]);
+          o[2 * i] = rf.x + s * (w[2 * i] * gy.x - xf.x * s * dot);
+          o[2 * i + 1] = rf.y + s * (w[2 * i + 1] * gy.y - xf.y * s * dot);
+          acc[k][2 * i] += gy.x * xf.x * s;
+          acc[k][2 * i + 1] += gy.y * xf.y * s;
+        }
+        store8(dx + off + c, o);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    const int c = lane * 8 + k * 256;
+    if (c < d) {
+      float4* dst = reinterpret_cast<float4*>(red + (size_t)warp * d + c);
+      dst[0] = make_float4(acc[k][0], acc[k][1], acc[k][2], acc[k][3]);
+      dst[1] = make_float4(acc[k][4], acc[k][5], acc[k][6], acc[k][7]);
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < ROW_WARPS; ++w) t += red[(size_t)w * d + c];
+    part[(size_t)blockIdx.x * d + c] = t;
+  }
+}
+
+// rows per CTA of the fused RMSNorm backward: a multiple of 16 giving about two CTAs per SM
+static int rms_rows_per_cta(long long rows) {
+  const long long target = 2LL * num_sms();
+  long long rpc = (rows + target - 1) / target;
+  rpc = ((rpc + 15) / 16) * 16;
+  return (int)(rpc < 16 ? 16 : rpc);
+}
+
+// out[c] += sum_i part[i][c], deterministic: warp w sums partials w, w+8, ... of the CTA's 32
+// columns (coalesced 128-byte rows), then the 8 warp sums are added in warp order.
+__global__ void __launch_bounds__(256) colsum_add_kernel(const float* __restrict__ part, float* __restrict__ out,
+                                                         int nsplit, int d) {
+  __shared__ float red[ROW_WARPS][33];
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int i = 0; i < nsplit; ++i) s += part[(size_t)i * d + c];
-  out[c] += s;
+  if (c < d) {
+#pragma unroll 8
+    for (int i = warp; i < nsplit; i += ROW_WARPS) s += part[(size_t)i * d + c];
+  }
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && c < d) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < ROW_WARPS; ++w) t += red[w][lane];
+    out[c] += t;
+  }
 }
 
 // ---------------------------------------------------------------- RoPE (rotate-half convention)
@@ -395,6 +501,32 @@ extern "C" int spx_rmsnorm_fwd(const void* x, const void* g, void* y, float* rst
 extern "C" int spx_rmsnorm_bwd(const void* x, const void* g, const float* rstd, const void* dy, const void* dres,
                                void* dx, float* dg, float* ws, int64_t rows, int64_t d, void* stream) {
   if (d % 8) return set_error(SPX_ERR_ARG, "rmsnorm: d must be a multiple of 8");
+  if (rows <= 0) return SPX_OK;
+  if (dg != nullptr && d <= 2048) {
+    const int rpc = rms_rows_per_cta(rows);
+    const int grid = (int)((rows + rpc - 1) / rpc);
+    const size_t smem = (size_t)ROW_WARPS * d * sizeof(float);
+    const int nch = (int)((d + 255) / 256);
+    auto launch = [&](auto kern) {
+      static bool attr[4] = {false, false, false, false};  // per instantiation; 64 KB at d = 2048
+      const int slot = nch <= 1 ? 0 : nch <= 2 ? 1 : nch <= 4 ? 2 : 3;
+      if (!attr[slot]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2048 * 4);
+        if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(rmsnorm_bwd_fused)");
+        attr[slot] = true;
+      }
+      spx_launch_check(launch_k(kern, dim3((unsigned)grid), dim3(ROW_WARPS * 32), smem, SPX_S, CBF(x), CBF(g), rstd,
+                                CBF(dy), CBF(dres), BF(dx), ws, (int)rows, (int)d, rpc));
+      return check_launch("rmsnorm_bwd_fused_kernel");
+    };
+    int rc = nch <= 1 ? launch(rmsnorm_bwd_fused_kernel<1>)
+             : nch <= 2 ? launch(rmsnorm_bwd_fused_kernel<2>)
+             : nch <= 4 ? launch(rmsnorm_bwd_fused_kernel<4>)
+                        : launch(rmsnorm_bwd_fused_kernel<8>);
+    if (rc) return rc;
+    spx_launch_check(launch_k(colsum_add_kernel, dim3((unsigned)((d + 31) / 32)), dim3(256), 0, SPX_S, ws, dg, grid, (int)d));
+    return check_launch("colsum_add_kernel");
+  }
   spx_launch_check(launch_k(rmsnorm_bwd_dx_kernel, dim3((unsigned)((rows + ROW_WARPS - 1) / ROW_WARPS)), dim3(ROW_WARPS * 32), 0, SPX_S, 
       CBF(x), CBF(g), rstd, CBF(dy), CBF(dres), BF(dx), (int)rows, (int)d));
   int rc = check_launch("rmsnorm_bwd_dx_kernel");
@@ -404,11 +536,16 @@ extern "C" int spx_rmsnorm_bwd(const void* x, const void* g, const float* rstd, 
       CBF(x), rstd, CBF(dy), ws, (int)rows, (int)d));
   rc = check_launch("rmsnorm_dg_partial_kernel");
   if (rc) return rc;
-  spx_launch_check(launch_k(colsum_add_kernel, dim3((unsigned)((d + 255) / 256)), dim3(256), 0, SPX_S, ws, dg, chunks, (int)d));
+  spx_launch_check(launch_k(colsum_add_kernel, dim3((unsigned)((d + 31) / 32)), dim3(256), 0, SPX_S, ws, dg, chunks, (int)d));
   return check_launch("colsum_add_kernel");
 }
 
-extern "C" int64_t spx_rmsnorm_ws_floats(int64_t rows, int64_t d) { return ((rows + DG_ROWS - 1) / DG_ROWS) * d; }
+extern "C" int64_t spx_rmsnorm_ws_floats(int64_t rows, int64_t d) {
+  if (rows <= 0) return d;
+  const long long rpc = rms_rows_per_cta(rows);
+  const long long fused = (rows + rpc - 1) / rpc, split = (rows + DG_ROWS - 1) / DG_ROWS;
+  return (fused > split ? fused : split) * d;
+}
 
 extern "C" int spx_rope(void* qkv, const float* cos_sin, int64_t rows, int64_t T, int64_t n_heads, int64_t hd,
                         int64_t ld, int32_t inverse, void* stream) {
