@@ -43,6 +43,10 @@ extern "C" {
 int spx_abi_version(void);
 const char* spx_last_error(void);
 int spx_device_sm_count(void);
+
+/* Number of kernels libspx has launched (or recorded into a CUDA graph under capture) in this
+ * process; launch accounting for benchmarks. */
+int64_t spx_launch_count(void);
 int spx_enable_peer_access(int32_t dev, int32_t peer);
 
 /* Path hop: copy `bytes` from src (device src_dev) to dst (device dst_dev) on `stream`.
@@ -66,11 +70,13 @@ int spx_gemm_bf16(const void* A, const void* B, void* C, const void* R, void* C2
                   int64_t lda, int64_t ldb, int64_t ldc, int64_t ldc2, int32_t a_mn_major, int32_t b_mn_major,
                   int32_t epilogue, float beta, void* stream);
 
-/* Register a zero-initialised int32 buffer (>= max tiles of any GEMM, e.g. 65536) for the current
- * device.  When set, fp32-accumulating GEMMs (epilogue 2) with too few tiles for the SMs split K
- * and add their partial sums into C in split order (deterministic).  NULL disables split-K.  One
- * GEMM at a time may use the buffer on a device (the executor runs one compute stream per GPU). */
-int spx_gemm_set_workspace(int32_t* sem, int64_t n_ints);
+/* Register the split-K partials buffer of the current device (fp32, 16-byte aligned).  When set,
+ * fp32-accumulating GEMMs (epilogue 2) with too few tiles for the SMs split K: each split stores its
+ * partial product to the buffer and a reduce kernel adds the partials to C in split order
+ * (deterministic).  Split counts are capped so the partials fit in n_floats.  NULL disables
+ * split-K.  One split-K GEMM at a time may use the buffer on a device (the executor issues every
+ * weight-gradient GEMM on one stream). */
+int spx_gemm_set_workspace(float* partials, int64_t n_floats);
 
 /* QKV projection with RoPE fused into the epilogue: C = A.B^T, then rotate-half RoPE (position =
  * row % T, cos_sin [hd/2][T][2], position-minor) on columns [0, rope_cols) (the q and k heads).  head_dim 64 or 128. */

@@ -44,14 +44,19 @@ struct RopeHd {
   static constexpr int value = EPI == EPI_ROPE64 ? 64 : (EPI == EPI_ROPE128 ? 128 : 0);
 };
 
-template <int BN>
+// CG = 2: a CTA pair (cluster of 2 on one TPC) computes a 256 x BN tile with cta_group::2 MMAs;
+// each CTA stages its own 128 rows of A and half (BN/2 rows) of B, so per-SM operand traffic from
+// L2 drops from 48 KB to 32 KB per 64-deep k-block (the 1-CTA kernel is L2->SM bandwidth bound).
+// NBOX: 32-row x 128-byte staging boxes per epilogue warp (2 for the three-output SwiGLU epilogue).
+template <int BN, int CG = 1, int NBOX = 1>
 struct GemmCfg {
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
-  static constexpr int B_BYTES = BN * GEMM_BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int STAGING_BYTES = GEMM_EPI_WARPS * 4096 * NBOX;
+  static constexpr int FIT = (232448 - 1024 - 256 - STAGING_BYTES) / STAGE_BYTES;  // 227 KB opt-in limit
+  static constexpr int STAGES = FIT < 6 ? FIT : 6;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int STAGING_BYTES = GEMM_EPI_WARPS * 4096;  // one 32-row x 128-byte box per epilogue warp
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
@@ -65,16 +70,22 @@ struct GemmArgs {
   const float* rope_cs;  // [hd/2][T][2] (cos, sin), position-minor
   int rope_cols, rope_T;
   int splits;            // split-K factor (EPI_F32 only); units = tiles * splits
-  int* sem;              // per-tile split-order semaphores (zero between launches)
+  float* ws;             // split partials [splits][ws_rows][N] fp32 (tensor map tmC2)
+  long long ws_rows;     // rows per split in ws (M rounded up to whole tiles)
+  int probe;  // pipeline probe (SPX_GEMM_PROBE, benchmarking only): 1 no MMAs, 2 no loads, 3 no epilogue,
+              // 4 MMAs only, 5 no output stores, 6 loads only
+  int tma_store;  // bf16 outputs leave the staging box by TMA store (SPX_GEMM_TMA_STORE=1) instead of st.global
 };
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                      const GemmArgs args) {
-  using Cfg = GemmCfg<BN>;
+  constexpr int NBOX = EPI == EPI_SWIGLU ? 2 : 1;
+  using Cfg = GemmCfg<BN, CG, NBOX>;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int PAIR_M = GEMM_BM * CG;  // rows per work unit
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::STAGING_BYTES);
@@ -85,7 +96,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int num_m = (args.M + GEMM_BM - 1) / GEMM_BM;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // CTA within the pair; rank 0 issues the MMAs
+  const int unit0 = CG == 2 ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int ustep = CG == 2 ? (int)nclusters_x() : (int)gridDim.x;
+  const int num_m = (args.M + PAIR_M - 1) / PAIR_M;
   const int num_n = (args.N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
   const int num_kb = (args.K + GEMM_BK - 1) / GEMM_BK;
@@ -105,14 +119,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], GEMM_EPI_WARPS);
+      mbar_init(&tempty_bar[a], CG * GEMM_EPI_WARPS);  // epilogue warps of both CTAs release an accumulator
     }
     fence_barrier_init();
     fence_proxy_async();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == 2) {
+    if constexpr (CG == 2) tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
+    else tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // barrier inits visible to the peer before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();  // upstream grid complete before any dependent global access
@@ -121,43 +139,55 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ---------------- TMA producer ----------------
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+    // both CTAs of a pair count their bytes on the leader's full barrier
+    const uint32_t full0 = CG == 2 ? mapa_shared(smem_u32(&full_bar[0]), 0) : smem_u32(&full_bar[0]);
+    auto load = [&](void* dst, const CUtensorMap* m, int st, int c0, int c1) {
+      if constexpr (CG == 2) tma_load_2d_pair(dst, m, full0 + 8 * st, c0, c1);
+      else tma_load_2d(dst, m, &full_bar[st], c0, c1);
+    };
+    for (int u = unit0; u < num_units; u += ustep) {
       const int tile = u % num_tiles, kb0 = (u / num_tiles) * kbs, kb1 = min(num_kb, kb0 + kbs);
-      const int m0 = (tile % num_m) * GEMM_BM;
-      const int n0 = (tile / num_m) * BN;
+      const int m0 = (tile % num_m) * PAIR_M + (int)rank * GEMM_BM;
+      const int nb = (tile / num_m) * BN + (int)rank * (BN / CG);  // this CTA's B rows
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
         uint8_t* sb = sa + Cfg::A_BYTES;
-        mbar_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+        if (args.probe == 2 || args.probe == 4) {
+          if (rank == 0) mbar_arrive(&full_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          continue;
+        }
+        if (rank == 0) mbar_expect_tx(&full_bar[stage], CG * Cfg::STAGE_BYTES);
         const int k0 = kb * GEMM_BK;
         if (A_MN) {
 #pragma unroll
-          for (int a = 0; a < GEMM_BM / 64; ++a) tma_load_2d(sa + a * (GEMM_BK * 128), &tmA, &full_bar[stage], m0 + 64 * a, k0);
+          for (int a = 0; a < GEMM_BM / 64; ++a) load(sa + a * (GEMM_BK * 128), &tmA, stage, m0 + 64 * a, k0);
         } else {
-          tma_load_2d(sa, &tmA, &full_bar[stage], k0, m0);
+          load(sa, &tmA, stage, k0, m0);
         }
         if (B_MN) {
 #pragma unroll
-          for (int a = 0; a < BN / 64; ++a) tma_load_2d(sb + a * (GEMM_BK * 128), &tmB, &full_bar[stage], n0 + 64 * a, k0);
+          for (int a = 0; a < BN / CG / 64; ++a) load(sb + a * (GEMM_BK * 128), &tmB, stage, nb + 64 * a, k0);
         } else {
-          tma_load_2d(sb, &tmB, &full_bar[stage], k0, n0);
+          load(sb, &tmB, stage, k0, nb);
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
     pdl_trigger();  // all loads issued: let the next kernel launch and run its prologue
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (single thread) ----------------
-    constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, BN, A_MN, B_MN);
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ---------------- MMA issuer (single thread; the pair's leader for CG = 2) ----------------
+    constexpr uint32_t IDESC = umma_idesc_bf16(PAIR_M, BN, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+    for (int u = unit0; u < num_units; u += ustep, ++it) {
       const int kb0 = (u / num_tiles) * kbs, kb1 = min(num_kb, kb0 + kbs);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      if constexpr (CG == 2) mbar_wait_cluster(&tempty_bar[acc], acc_phase ^ 1);
+      else mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kb = kb0; kb < kb1; ++kb) {
@@ -167,16 +197,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const uint32_t sb = sa + Cfg::A_BYTES;
 #pragma unroll
         for (int kk = 0; kk < GEMM_BK / 16; ++kk) {
+          if (args.probe == 1 || args.probe == 6) break;
           const uint64_t ad = A_MN ? umma_desc_sw128(sa + kk * 2048, GEMM_BK * 128, 1024)
                                    : umma_desc_sw128(sa + kk * 32, 16, 1024);
           const uint64_t bd = B_MN ? umma_desc_sw128(sb + kk * 2048, GEMM_BK * 128, 1024)
                                    : umma_desc_sw128(sb + kk * 32, 16, 1024);
-          mma_bf16_ss(d_tmem, ad, bd, IDESC, (kb != kb0) || (kk != 0));
+          if constexpr (CG == 2) mma_bf16_ss_pair(d_tmem, ad, bd, IDESC, (kb != kb0) || (kk != 0));
+          else mma_bf16_ss(d_tmem, ad, bd, IDESC, (kb != kb0) || (kk != 0));
         }
-        mma_commit(&empty_bar[stage]);
+        if constexpr (CG == 2) mma_commit_pair(&empty_bar[stage]);
+        else mma_commit(&empty_bar[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      mma_commit(&tfull_bar[acc]);
+      if constexpr (CG == 2) mma_commit_pair(&tfull_bar[acc]);
+      else mma_commit(&tfull_bar[acc]);
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> fused op -> swizzled smem box -> TMA ----------
@@ -188,7 +222,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int wq = warp & 3;
     const int half = (warp - 4) >> 2;
     const int cb = half * (BN / 2);  // this warp's first tile column
-    uint8_t* box = smem + STAGES * Cfg::STAGE_BYTES + (warp - 4) * 4096;
+    uint8_t* const box0 = smem + STAGES * Cfg::STAGE_BYTES + (warp - 4) * 4096 * NBOX;
+    uint8_t* box = box0;  // the box the helpers below write / issue
     auto box_acquire = [&]() {
       if (lane == 0) bulk_wait_read<0>();  // the previous store from this buffer has read it
       __syncwarp();
@@ -203,10 +238,34 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
-        if (reduce) tma_reduce_add_2d(m, box, c0, c1);
+        if (args.probe == 5) {
+          // probe: output store skipped
+        } else if (reduce) tma_reduce_add_2d(m, box, c0, c1);
         else tma_store_2d(m, box, c0, c1);
         bulk_commit();
       }
+    };
+    // bf16 box -> global with coalesced 16-byte stores (8 lanes per 128-byte row); keeps the
+    // epilogue's output off the TMA unit, which the producer's operand loads keep busy
+    auto box_store = [&](void* base, long long ld, int ncols, int c0, int r0) {
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = i * 4 + (lane >> 3), j = lane & 7;
+        const int grow = r0 + r, gcol = c0 + 8 * j;
+        const uint4 v = *reinterpret_cast<const uint4*>(box + r * 128 + ((j ^ (r & 7)) << 4));
+        if (grow < args.M && gcol < ncols)
+          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(base) + (size_t)grow * ld + gcol) = v;
+      }
+      __syncwarp();
+    };
+    // output 0 = C (ncols0 columns), 1 = C2 (ncols1 columns)
+    const int ncols0 = EPI == EPI_SWIGLU ? args.N / 2 : args.N;
+    const int ncols1 = EPI == EPI_SWIGLU_BWD ? 2 * args.N : args.N;
+    auto box_out = [&](int which, int c0, int r0) {
+      if (args.tma_store || args.probe == 5) box_issue(which ? &tmC2 : &tmC, c0, r0, false);
+      else if (which == 0) box_store(args.C, args.ldc, ncols0, c0, r0);
+      else box_store(args.C2, args.ldc2, ncols1, c0, r0);
     };
     // 32 fp32 values -> 16-byte chunks j0..j0+3 of this lane's row (bf16)
     auto put32 = [&](int j0, const float* f) {
@@ -224,74 +283,87 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
     };
     int it = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+    const uint32_t tempty0 = CG == 2 ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : 0;
+    for (int u = unit0; u < num_units; u += ustep, ++it) {
       const int tile = u % num_tiles, split = u / num_tiles;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int m0 = (tile % num_m) * GEMM_BM;
+      const int m0 = (tile % num_m) * PAIR_M + (int)rank * GEMM_BM;
       const int n0 = (tile / num_m) * BN;
       const int rbase = m0 + wq * 32;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
-      if constexpr (EPI == EPI_F32) {
-        const bool ordered = args.splits > 1;
-        if (ordered) {
-          // deterministic split-K: split s adds into C only after split s-1 of this tile did
-          int v;
-          do {
-            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(args.sem + tile) : "memory");
-          } while (v != split);
-        }
-        const bool add = (split > 0) || (args.beta != 0.f);
+      if (args.probe == 3 || args.probe == 4 || args.probe == 6) {
+        // probe: accumulator released without reading it
+      } else if constexpr (EPI == EPI_F32) {
+        if (args.splits == 1) {
+          const bool add = args.beta != 0.f;
 #pragma unroll 1
-        for (int c = cb; c < cb + BN / 2 && n0 + c < args.N; c += 32) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(t_row + c, v);
-          tmem_ld_wait();
-          box_acquire();
+          for (int c = cb; c < cb + BN / 2 && n0 + c < args.N; c += 32) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_row + c, v);
+            tmem_ld_wait();
+            box_acquire();
 #pragma unroll
-          for (int j = 0; j < 8; ++j) box_put(lane, j, make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-          box_issue(&tmC, n0 + c, rbase, add);
-        }
-        if (ordered) {
-          if (lane == 0) bulk_wait<0>();  // this warp's adds have landed in global memory
-          __syncwarp();
-          __threadfence();
-          asm volatile("bar.sync 1, %0;" ::"n"(32 * GEMM_EPI_WARPS) : "memory");
-          if (threadIdx.x == 128) atomicExch(args.sem + tile, split + 1 == args.splits ? 0 : split + 1);
+            for (int j = 0; j < 8; ++j) box_put(lane, j, make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+            box_issue(&tmC, n0 + c, rbase, add);
+          }
+        } else {
+          // split-K: this split's partial goes to the workspace (plain store); splitk_reduce_kernel
+          // then adds the partials to C in split order (deterministic)
+#pragma unroll 1
+          for (int c = cb; c < cb + BN / 2 && n0 + c < args.N; c += 32) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_row + c, v);
+            tmem_ld_wait();
+            box_acquire();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) box_put(lane, j, make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+            box_issue(&tmC2, n0 + c, (int)(split * args.ws_rows) + rbase, false);
+          }
         }
       } else if constexpr (EPI == EPI_SWIGLU) {
         // tile columns [0,128) are gate, [128,256) the matching up rows of the interleaved weight;
-        // this warp handles gate/up columns [64*half, 64*half + 64)
+        // this warp handles gate/up columns [64*half, 64*half + 64).  Each accumulator column is
+        // read from TMEM once: the raw gate and up values go to boxes A and B, H = silu(g) * u is
+        // kept in registers and written through box A once the gate store has read it.
         const int c = 64 * half;
         if (n0 + c < args.N) {
-          float g[32], uu[32], h[32];
-#pragma unroll 1
-          for (int part = 0; part < 3; ++part) {  // 0: H, 1: gate, 2: up
-            box_acquire();
-#pragma unroll 1
-            for (int q = 0; q < 2; ++q) {
-              ld32(t_row + c + 32 * q, g);
-              ld32(t_row + BN / 2 + c + 32 * q, uu);
-              if (part == 0) {
+          uint8_t* const boxA = box0;
+          uint8_t* const boxB = box0 + 4096;
+          float h[2][32];
+          if (lane == 0) bulk_wait_read<0>();  // both boxes free (previous tile's stores have read them)
+          __syncwarp();
 #pragma unroll
-                for (int j = 0; j < 32; j += 2) {
-                  // silu from the bf16-rounded pre-activations the backward pass will see
-                  const float2 gr = unpack_bf16(pack_bf16(g[j], g[j + 1]));
-                  const float2 ur = unpack_bf16(pack_bf16(uu[j], uu[j + 1]));
-                  h[j] = gr.x * __frcp_rn(1.f + __expf(-gr.x)) * ur.x;
-                  h[j + 1] = gr.y * __frcp_rn(1.f + __expf(-gr.y)) * ur.y;
-                }
-                put32(4 * q, h);
-              } else {
-                put32(4 * q, part == 1 ? g : uu);
-              }
+          for (int q = 0; q < 2; ++q) {
+            float g[32], uu[32];
+            ld32(t_row + c + 32 * q, g);
+            ld32(t_row + BN / 2 + c + 32 * q, uu);
+            box = boxA;
+            put32(4 * q, g);
+            box = boxB;
+            put32(4 * q, uu);
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              // silu from the bf16-rounded pre-activations the backward pass will see
+              const float2 gr = unpack_bf16(pack_bf16(g[j], g[j + 1]));
+              const float2 ur = unpack_bf16(pack_bf16(uu[j], uu[j + 1]));
+              h[q][j] = gr.x * fast_sigmoid(gr.x) * ur.x;
+              h[q][j + 1] = gr.y * fast_sigmoid(gr.y) * ur.y;
             }
-            if (part == 0) box_issue(&tmC, n0 / 2 + c, rbase, false);
-            else if (part == 1) box_issue(&tmC2, n0 + c, rbase, false);
-            else box_issue(&tmC2, n0 + BN / 2 + c, rbase, false);
           }
+          box = boxA;
+          box_out(1, n0 + c, rbase);           // gate
+          box = boxB;
+          box_out(1, n0 + BN / 2 + c, rbase);  // up
+          if (lane == 0) bulk_wait_read<1>();                // the gate store has read box A
+          __syncwarp();
+          box = boxA;
+          put32(0, h[0]);
+          put32(4, h[1]);
+          box_out(0, n0 / 2 + c, rbase);       // H
+          box = box0;
         }
       } else if constexpr (EPI == EPI_SWIGLU_BWD) {
         // dh tile columns [cb, cb+128) = one 128-column gate/up block of the interleaved layout:
@@ -320,7 +392,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                   for (int e = 0; e < 4; ++e) {
                     const float2 g2 = unpack_bf16(gw[e]), u2 = unpack_bf16(uw[e]);
                     const int j = 8 * j8 + 2 * e;
-                    const float s0 = __frcp_rn(1.f + __expf(-g2.x)), s1 = __frcp_rn(1.f + __expf(-g2.y));
+                    const float s0 = fast_sigmoid(g2.x), s1 = fast_sigmoid(g2.y);
                     if (part == 0) {
                       o[j] = dh[j] * u2.x * s0 * (1.f + g2.x * (1.f - s0));
                       o[j + 1] = dh[j + 1] * u2.y * s1 * (1.f + g2.y * (1.f - s1));
@@ -332,7 +404,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 }
                 put32(4 * q, o);
               }
-              box_issue(&tmC2, blk * 256 + 128 * part + c, rbase, false);
+              box_out(1, blk * 256 + 128 * part + c, rbase);
             }
           }
         }
@@ -374,7 +446,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               }
               put32(4 * q, x1);
             }
-            box_issue(&tmC, n0 + hb + 64 * bx, rbase, false);
+            box_out(0, n0 + hb + 64 * bx, rbase);
           }
         }
       } else {
@@ -412,20 +484,52 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
             put32(4 * q, f);
           }
-          box_issue(&tmC, n0 + c, rbase, false);
+          box_out(0, n0 + c, rbase);
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster_relaxed(tempty0 + 8 * acc);
+        else mbar_arrive_relaxed(&tempty_bar[acc]);
+      }
     }
     if (lane == 0) bulk_wait<0>();  // staging smem must outlive the TMA reads
   }
   __syncwarp();
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // the peer's TMEM / smem / barriers are in use until both finish
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  if (warp == 2) {
+    if constexpr (CG == 2) tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+    else tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// C (+)= sum_s ws[s] over the split partials, in split order (deterministic); 4 columns per thread.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, float* __restrict__ C,
+                                                            int M, int N, long long ldc, long long ws_rows,
+                                                            int splits, int accumulate) {
+  pdl_wait();
+  const long long n4 = N / 4;
+  const long long total = (long long)M * n4;
+  const long long split_stride = ws_rows * N;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / n4, c = (i % n4) * 4;
+    const float* src = ws + r * N + c;
+    float4 acc = __ldcs(reinterpret_cast<const float4*>(src));
+    for (int sp = 1; sp < splits; ++sp) {
+      const float4 t = __ldcs(reinterpret_cast<const float4*>(src + sp * split_stride));
+      acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+    }
+    float4* dst = reinterpret_cast<float4*>(C + r * ldc + c);
+    if (accumulate) {
+      const float4 o = *dst;
+      acc.x = o.x + acc.x; acc.y = o.y + acc.y; acc.z = o.z + acc.z; acc.w = o.w + acc.w;
+    }
+    *dst = acc;
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -452,10 +556,10 @@ static int make_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint6
   return SPX_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG = 1>
 static int launch_gemm(const void* A, const void* B, long long lda, long long ldb, const GemmArgs& args,
                        cudaStream_t stream) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CG, EPI == EPI_SWIGLU ? 2 : 1>;
   CUtensorMap ta, tb;
   int rc;
   // A operand: rows = M, contraction = K
@@ -463,7 +567,7 @@ static int launch_gemm(const void* A, const void* B, long long lda, long long ld
   else rc = make_tmap_2d(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
   if (rc) return rc;
   if (B_MN) rc = make_tmap_2d(&tb, B, args.N, args.K, ldb, 64, GEMM_BK);
-  else rc = make_tmap_2d(&tb, B, args.K, args.N, ldb, GEMM_BK, BN);
+  else rc = make_tmap_2d(&tb, B, args.K, args.N, ldb, GEMM_BK, BN / CG);
   if (rc) return rc;
 
   // output boxes: 32 rows x 128 bytes (64 bf16 or 32 fp32 columns), SWIZZLE_128B
@@ -479,61 +583,125 @@ static int launch_gemm(const void* A, const void* B, long long lda, long long ld
     if (rc) return rc;
   }
   if (EPI == EPI_SWIGLU_BWD) tc2 = tc;
-  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, EPI>;
-  static bool attr_set = false;  // one per template instantiation
-  if (!attr_set) {
+  if (EPI == EPI_F32 && args.splits > 1) {
+    rc = make_tmap_2d(&tc2, args.ws, args.N, (uint64_t)args.splits * args.ws_rows, args.N, 32, 32, true);
+    if (rc) return rc;
+  }
+  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, EPI, CG>;
+  static int max_units = 0;  // co-resident CTAs (CG = 1) or CTA pairs (CG = 2); one per template instantiation
+  if (!max_units) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm)");
-    attr_set = true;
+    int n = num_sms();
+    if (CG == 2) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(2 * (num_sms() / 2));
+      cfg.blockDim = dim3(GEMM_THREADS);
+      cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      n = 0;
+      e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+      if (e != cudaSuccess || n <= 0) return set_cuda_error(e, "cudaOccupancyMaxActiveClusters(gemm)");
+    }
+    max_units = n;
   }
-  const int tiles = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + BN - 1) / BN) * args.splits;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  spx_launch_check(launch_k(kern, dim3(grid), dim3(GEMM_THREADS), Cfg::SMEM_BYTES, stream, ta, tb, tc, tc2, args));
-  return check_launch("gemm_bf16_kernel");
+  const int units = ((args.M + GEMM_BM * CG - 1) / (GEMM_BM * CG)) * ((args.N + BN - 1) / BN) * args.splits;
+  const int g = units < max_units ? units : max_units;
+  if (CG == 2)
+    spx_launch_check(launch_k_cluster(kern, 2, dim3(2 * g), dim3(GEMM_THREADS), Cfg::SMEM_BYTES, stream, ta, tb, tc, tc2, args));
+  else
+    spx_launch_check(launch_k(kern, dim3(g), dim3(GEMM_THREADS), Cfg::SMEM_BYTES, stream, ta, tb, tc, tc2, args));
+  rc = check_launch("gemm_bf16_kernel");
+  if (rc || EPI != EPI_F32 || args.splits == 1) return rc;
+  const long long work = (long long)args.M * (args.N / 4);
+  const long long want = (work + 255) / 256;
+  const int rg = (int)(want < 8LL * num_sms() ? want : 8LL * num_sms());
+  spx_launch_check(launch_k(splitk_reduce_kernel, dim3(rg), dim3(256), 0, stream, (const float*)args.ws, (float*)args.C,
+                            args.M, args.N, args.ldc, args.ws_rows, args.splits, args.beta != 0.f ? 1 : 0));
+  return check_launch("splitk_reduce_kernel");
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CG = 1>
 static int dispatch_major(const void* A, const void* B, long long lda, long long ldb, int a_mn, int b_mn,
                           const GemmArgs& args, cudaStream_t s) {
-  if (!a_mn && !b_mn) return launch_gemm<BN, false, false, EPI>(A, B, lda, ldb, args, s);
-  if (!a_mn && b_mn) return launch_gemm<BN, false, true, EPI>(A, B, lda, ldb, args, s);
-  if (a_mn && b_mn) return launch_gemm<BN, true, true, EPI>(A, B, lda, ldb, args, s);
-  return launch_gemm<BN, true, false, EPI>(A, B, lda, ldb, args, s);
+  if (!a_mn && !b_mn) return launch_gemm<BN, false, false, EPI, CG>(A, B, lda, ldb, args, s);
+  if (!a_mn && b_mn) return launch_gemm<BN, false, true, EPI, CG>(A, B, lda, ldb, args, s);
+  if (a_mn && b_mn) return launch_gemm<BN, true, true, EPI, CG>(A, B, lda, ldb, args, s);
+  return launch_gemm<BN, true, false, EPI, CG>(A, B, lda, ldb, args, s);
 }
 
-// Per-device split-K semaphores, registered once by the caller (no allocation in the GEMM path).
-static int* g_sem[64] = {nullptr};
-static int64_t g_sem_n[64] = {0};
+// Per-device split-K partials buffer, registered once by the caller (no allocation in the GEMM path).
+static float* g_ws[64] = {nullptr};
+static int64_t g_ws_n[64] = {0};
 
-// Split-K factor for the fp32 (wgrad) epilogue: maximise wave efficiency of tiles x splits on the
-// SMs, keeping >= 8 k-blocks per split; splits add into C in split order (deterministic).
+static int tma_store_mode() {
+  static const int t = [] {
+    const char* e = getenv("SPX_GEMM_TMA_STORE");
+    return e ? atoi(e) : 0;
+  }();
+  return t;
+}
+
+static int probe_mode() {
+  static const int p = [] {
+    const char* e = getenv("SPX_GEMM_PROBE");
+    return e ? atoi(e) : 0;
+  }();
+  return p;
+}
+
+// 256-row CTA-pair tiles (cta_group::2) for BN = 256 whenever M spans at least two 128-row
+// tiles; SPX_GEMM_PAIR=0 forces single-CTA tiles.
+static bool use_pair(int M) {
+  static const int enabled = [] {
+    const char* e = getenv("SPX_GEMM_PAIR");
+    return e ? atoi(e) : 1;
+  }();
+  return enabled && M > GEMM_BM;
+}
+
+// Split-K factor for the fp32 (wgrad) epilogue: the smallest split count within 5 % of the best
+// wave efficiency of tiles x splits on the SMs (CTA pairs), keeping >= 8 k-blocks per split and
+// the partials within the registered workspace (no workspace registered: no split-K).
 static void pick_splits(GemmArgs& a, int bn) {
   int dev = 0;
   cudaGetDevice(&dev);
-  const int tiles = ((a.M + GEMM_BM - 1) / GEMM_BM) * ((a.N + bn - 1) / bn);
+  if (dev < 0 || dev >= 64 || g_ws[dev] == nullptr) return;
+  if ((a.ldc & 3) || (reinterpret_cast<uintptr_t>(a.C) & 15)) return;  // the reduce kernel stores float4
+  const int cg = (bn == 256 && use_pair(a.M)) ? 2 : 1;
+  const int num_m = (a.M + GEMM_BM * cg - 1) / (GEMM_BM * cg);
+  const int tiles = num_m * ((a.N + bn - 1) / bn);
+  const long long ws_rows = (long long)num_m * GEMM_BM * cg;
   const int num_kb = (a.K + GEMM_BK - 1) / GEMM_BK;
-  if (dev < 0 || dev >= 64 || g_sem[dev] == nullptr || tiles > g_sem_n[dev]) return;
-  static const int enabled = [] {
-    const char* e = getenv("SPX_SPLITK");
-    return e ? atoi(e) : 0;
-  }();
-  if (!enabled) return;
-  const int sms = num_sms();
+  const int slots = num_sms() / cg;
+  double eff[9] = {0};
   double best = 0.0;
-  int best_s = 1;
-  for (int s = 1; s <= 8; ++s) {
-    const int kbs = (num_kb + s - 1) / s;
-    if (kbs < 8 && s > 1) break;
-    const int s_eff = (num_kb + kbs - 1) / kbs;
-    const long units = (long)tiles * s_eff;
-    const double eff = (double)units / (double)(((units + sms - 1) / sms) * sms);
-    if (eff > best + 0.05) {
-      best = eff;
-      best_s = s_eff;
-    }
+  for (int sp = 1; sp <= 8; ++sp) {
+    if (sp > 1 && (num_kb / sp < 8 || (long long)sp * ws_rows * a.N > g_ws_n[dev])) break;
+    const long units = (long)tiles * sp;
+    eff[sp] = (double)units / (double)(((units + slots - 1) / slots) * slots);
+    if (eff[sp] > best) best = eff[sp];
   }
-  a.splits = best_s;
-  a.sem = best_s > 1 ? g_sem[dev] : nullptr;
+  int pick = 1;
+  while (pick < 8 && eff[pick] < best - 0.05) ++pick;
+  a.splits = pick;
+  if (pick > 1) {
+    a.ws = g_ws[dev];
+    a.ws_rows = ws_rows;
+  }
+}
+
+template <int EPI>
+static int dispatch_256(const void* A, const void* B, long long lda, long long ldb, int a_mn, int b_mn,
+                        const GemmArgs& args, cudaStream_t s) {
+  if (use_pair(args.M)) return dispatch_major<256, EPI, 2>(A, B, lda, ldb, a_mn, b_mn, args, s);
+  return dispatch_major<256, EPI, 1>(A, B, lda, ldb, a_mn, b_mn, args, s);
 }
 
 static int pick_bn(int M, int N) {
@@ -549,19 +717,18 @@ static int pick_bn(int M, int N) {
 
 using namespace spx;
 
-extern "C" int spx_gemm_set_workspace(int32_t* sem, int64_t n_ints) {
+extern "C" int spx_gemm_set_workspace(float* partials, int64_t n_floats) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return set_error(SPX_ERR_ARG, "gemm workspace: bad device");
-  if (sem == nullptr || n_ints <= 0) {
-    g_sem[dev] = nullptr;
-    g_sem_n[dev] = 0;
+  if (partials == nullptr || n_floats <= 0) {
+    g_ws[dev] = nullptr;
+    g_ws_n[dev] = 0;
     return SPX_OK;
   }
-  cudaError_t e = cudaMemset(sem, 0, (size_t)n_ints * sizeof(int32_t));
-  if (e != cudaSuccess) return set_cuda_error(e, "gemm workspace memset");
-  g_sem[dev] = sem;
-  g_sem_n[dev] = n_ints;
+  if (((uintptr_t)partials) & 15) return set_error(SPX_ERR_ARG, "gemm workspace: partials must be 16-byte aligned");
+  g_ws[dev] = partials;
+  g_ws_n[dev] = n_floats;
   return SPX_OK;
 }
 
@@ -575,9 +742,11 @@ extern "C" int spx_gemm_bf16_rope(const void* A, const void* B, void* C, int64_t
   if (rope_cols % head_dim || T <= 0) return set_error(SPX_ERR_ARG, "gemm_rope: rope_cols must be whole heads");
   GemmArgs args{(int)M, (int)N, (int)K, C, nullptr, nullptr, (long long)ldc, (long long)ldc, 0, 0.f,
                 cos_sin, (int)rope_cols, (int)T, 1, nullptr};
+  args.probe = probe_mode();
+  args.tma_store = tma_store_mode();
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (head_dim == 64) return launch_gemm<256, false, false, EPI_ROPE64>(A, B, lda, ldb, args, s);
-  return launch_gemm<256, false, false, EPI_ROPE128>(A, B, lda, ldb, args, s);
+  if (head_dim == 64) return dispatch_256<EPI_ROPE64>(A, B, lda, ldb, 0, 0, args, s);
+  return dispatch_256<EPI_ROPE128>(A, B, lda, ldb, 0, 0, args, s);
 }
 
 extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* R, void* C2, int64_t M, int64_t N,
@@ -595,23 +764,25 @@ extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* 
   if (epilogue == EPI_BF16_RESID && R == nullptr) return set_error(SPX_ERR_ARG, "gemm: residual epilogue needs R");
   GemmArgs args{(int)M, (int)N, (int)K, C, R, C2, (long long)ldc, (long long)(epilogue == EPI_SWIGLU_BWD ? ldc2 : ldc),
                 (long long)ldc2, beta, nullptr, 0, 1, 1, nullptr};
+  args.probe = probe_mode();
+  args.tma_store = tma_store_mode();
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int bn = (epilogue == EPI_SWIGLU || epilogue == EPI_F32 || epilogue == EPI_SWIGLU_BWD) ? 256
                                                                                                : pick_bn((int)M, (int)N);
   if (epilogue == EPI_F32) pick_splits(args, bn);
   switch (epilogue) {
     case EPI_BF16:
-      return bn == 256 ? dispatch_major<256, EPI_BF16>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s)
+      return bn == 256 ? dispatch_256<EPI_BF16>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s)
                        : dispatch_major<128, EPI_BF16>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
     case EPI_BF16_RESID:
-      return bn == 256 ? dispatch_major<256, EPI_BF16_RESID>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s)
+      return bn == 256 ? dispatch_256<EPI_BF16_RESID>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s)
                        : dispatch_major<128, EPI_BF16_RESID>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
     case EPI_F32:
-      return bn == 256 ? dispatch_major<256, EPI_F32>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s)
+      return bn == 256 ? dispatch_256<EPI_F32>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s)
                        : dispatch_major<128, EPI_F32>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
     case EPI_SWIGLU_BWD:
-      return dispatch_major<256, EPI_SWIGLU_BWD>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
+      return dispatch_256<EPI_SWIGLU_BWD>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
     default:
-      return dispatch_major<256, EPI_SWIGLU>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
+      return dispatch_256<EPI_SWIGLU>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
   }
 }

@@ -3,6 +3,7 @@
 // different GPUs, a device-local copy otherwise).
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 
@@ -35,6 +36,9 @@ bool pdl_enabled() {
   }();
   return on;
 }
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int num_sms() {
   static int cached[64] = {0};
@@ -71,6 +75,8 @@ extern "C" int spx_abi_version(void) { return SPX_ABI_VERSION; }
 extern "C" const char* spx_last_error(void) { return g_err; }
 
 extern "C" int spx_device_sm_count(void) { return num_sms(); }
+
+extern "C" int64_t spx_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 extern "C" int spx_enable_peer_access(int32_t dev, int32_t peer) {
   int prev = 0;

@@ -393,8 +393,10 @@ class Trainer:
                     self.slots[(v, j)] = SlotBuffers(cfg, self.split[self.node_stage[v]], self.node_stage[v] == 0,
                                                      self.n, b, self.T, self.dev)
             self.scratch = Scratch(cfg, self.n, b, self.T, self.dev, with_head=0 in self.my_stages)
-            self._gemm_sem = torch.zeros(1 << 16, dtype=torch.int32, device=self.dev)
-            native.gemm_set_workspace(self._gemm_sem)
+            # No split-K workspace: the weight-gradient GEMMs run on a side stream next to the
+            # data-gradient chain, which uses the SMs a wgrad leaves idle; split-K's partial
+            # traffic costs more SM time than it saves there (spx_gemm_set_workspace, spx.h).
+            native.gemm_set_workspace(None)
             self.stream = torch.cuda.Stream(device=self.dev)
             self.recv_stream = torch.cuda.Stream(device=self.dev)
             self.send_stream = torch.cuda.Stream(device=self.dev)

@@ -24,6 +24,7 @@ SIGNATURES: dict[str, list] = {
     "spx_abi_version": [],
     "spx_last_error": [],
     "spx_device_sm_count": [],
+    "spx_launch_count": [],
     "spx_enable_peer_access": [_I32, _I32],
     "spx_hop": [_I32, _P, _I32, _P, _I64, _P],
     "spx_gemm_bf16": [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _F, _P],
@@ -45,7 +46,7 @@ SIGNATURES: dict[str, list] = {
     "spx_clip_scale": [_P, _I32, _F, _P, _P, _P],
     "spx_adamw": [_P, _P, _P, _P, _P, _I64, _I64, _F, _F, _F, _F, _F, _I64, _P, _P],
 }
-_RESTYPE = {"spx_last_error": ctypes.c_char_p, "spx_rmsnorm_ws_floats": ctypes.c_int64,
+_RESTYPE = {"spx_last_error": ctypes.c_char_p, "spx_rmsnorm_ws_floats": ctypes.c_int64, "spx_launch_count": ctypes.c_int64,
             "spx_sumsq_ws_floats": ctypes.c_int64}
 
 EPI_BF16, EPI_BF16_RESID, EPI_F32, EPI_SWIGLU = 0, 1, 2, 3
@@ -53,15 +54,12 @@ EPI_SWIGLU_BWD = 6
 
 
 # kernel-launch accounting (bench.py "gpu_launches") and GEMM call recording (roofline timing)
-_STATS = {"launches": 0, "record": False, "gemms": {}, "gemm_log": []}
+_STATS = {"record": False, "gemms": {}, "gemm_log": []}
 
 
 def launches() -> int:
-    return _STATS["launches"]
-
-
-def _count(n: int) -> None:
-    _STATS["launches"] += n
+    """Kernels libspx has launched (or recorded under graph capture) in this process."""
+    return int(load().spx_launch_count())
 
 
 def record_gemms(on: bool) -> None:
@@ -134,7 +132,6 @@ def gemm(A, B, C, *, M, N, K, lda, ldb, ldc, a_mn=False, b_mn=False, epilogue=EP
     rc = load().spx_gemm_bf16(_ptr(A), _ptr(B), _ptr(C), _ptr(R), _ptr(C2), M, N, K, lda, ldb, ldc, ldc2,
                               int(a_mn), int(b_mn), epilogue, float(beta), _stream(stream))
     _check(rc, "spx_gemm_bf16")
-    _count(1)
     if _STATS["record"]:
         key = (M, N, K, bool(a_mn), bool(b_mn), int(epilogue))
         cnt = _STATS["gemms"].get(key, (0, None))[0]
@@ -158,7 +155,6 @@ def gemm_rope(A, B, C, *, M, N, K, lda, ldb, ldc, cos_sin, rope_cols, T, head_di
     """QKV projection with RoPE fused into the epilogue (spx_gemm_bf16_rope)."""
     _check(load().spx_gemm_bf16_rope(_ptr(A), _ptr(B), _ptr(C), M, N, K, lda, ldb, ldc, _ptr(cos_sin), rope_cols, T,
                                      head_dim, _stream(stream)), "spx_gemm_bf16_rope")
-    _count(1)
     if _STATS["record"]:
         key = (M, N, K, False, False, 4)
         cnt = _STATS["gemms"].get(key, (0, None))[0]
@@ -176,9 +172,10 @@ def gemm_rope(A, B, C, *, M, N, K, lda, ldb, ldc, cos_sin, rope_cols, T, head_di
         _STATS["gemm_log"].append(key)
 
 
-def gemm_set_workspace(sem) -> None:
-    """Register the split-K semaphore buffer (int32 device tensor, zeroed) for the current device."""
-    _check(load().spx_gemm_set_workspace(_ptr(sem), 0 if sem is None else sem.numel()), "spx_gemm_set_workspace")
+def gemm_set_workspace(partials) -> None:
+    """Register the split-K partials buffer (fp32 device tensor) for the current device; None disables split-K."""
+    _check(load().spx_gemm_set_workspace(_ptr(partials), 0 if partials is None else partials.numel()),
+           "spx_gemm_set_workspace")
 
 
 def hop(dst, dst_dev: int, src, src_dev: int, nbytes: int, stream=None) -> None:
@@ -192,26 +189,22 @@ def enable_peer_access(dev: int, peer: int) -> None:
 def attn_fwd(qkv, o, lse, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, stream=None) -> None:
     _check(load().spx_attn_fwd(_ptr(qkv), _ptr(o), _ptr(lse), B, T, H, Hkv, hd, ld_qkv, ld_o, float(scale),
                                _stream(stream)), "spx_attn_fwd")
-    _count(1)
 
 
 def attn_bwd(qkv, o, dout, lse, delta_ws, dqkv, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, rope_cs=None,
              stream=None) -> None:
     _check(load().spx_attn_bwd(_ptr(qkv), _ptr(o), _ptr(dout), _ptr(lse), _ptr(delta_ws), _ptr(dqkv), B, T, H, Hkv,
                                hd, ld_qkv, ld_o, float(scale), _ptr(rope_cs), _stream(stream)), "spx_attn_bwd")
-    _count(3)  # delta + dK/dV + dQ
 
 
 def rmsnorm_fwd(x, g, y, rstd, *, rows, d, eps, stream=None) -> None:
     _check(load().spx_rmsnorm_fwd(_ptr(x), _ptr(g), _ptr(y), _ptr(rstd), rows, d, float(eps), _stream(stream)),
            "spx_rmsnorm_fwd")
-    _count(1)
 
 
 def rmsnorm_bwd(x, g, rstd, dy, dres, dx, dg, ws, *, rows, d, stream=None) -> None:
     _check(load().spx_rmsnorm_bwd(_ptr(x), _ptr(g), _ptr(rstd), _ptr(dy), _ptr(dres), _ptr(dx), _ptr(dg), _ptr(ws),
                                   rows, d, _stream(stream)), "spx_rmsnorm_bwd")
-    _count(3 if dg is not None else 1)
 
 
 def rmsnorm_ws_floats(rows: int, d: int) -> int:
@@ -221,24 +214,20 @@ def rmsnorm_ws_floats(rows: int, d: int) -> int:
 def rope(qkv, cos_sin, *, rows, T, n_heads, hd, ld, inverse=False, stream=None) -> None:
     _check(load().spx_rope(_ptr(qkv), _ptr(cos_sin), rows, T, n_heads, hd, ld, int(inverse), _stream(stream)),
            "spx_rope")
-    _count(1)
 
 
 def swiglu_bwd(gu, dh, dgu, *, rows, F, stream=None) -> None:
     _check(load().spx_swiglu_bwd(_ptr(gu), _ptr(dh), _ptr(dgu), rows, F, _stream(stream)), "spx_swiglu_bwd")
-    _count(1)
 
 
 def embed_fwd(ids, table, out, *, n, d, stream=None) -> None:
     _check(load().spx_embed_fwd(_ptr(ids), _ptr(table), _ptr(out), n, d, _stream(stream)), "spx_embed_fwd")
-    _count(1)
 
 
 def embed_bwd(perm, seg_start, seg_id, n_segments, max_segments, dout, dtable, *, d, stream=None) -> None:
     """n_segments: int32 device tensor holding the segment count (graph-capturable)."""
     _check(load().spx_embed_bwd(_ptr(perm), _ptr(seg_start), _ptr(seg_id), _ptr(n_segments), int(max_segments),
                                 _ptr(dout), _ptr(dtable), d, _stream(stream)), "spx_embed_bwd")
-    _count(1)
 
 
 def embed_segments(ids) -> tuple:
@@ -261,12 +250,10 @@ def embed_segments(ids) -> tuple:
 def xent_fwd_bwd(logits, targets, row_loss, *, n, V, ld, scale, stream=None) -> None:
     _check(load().spx_xent_fwd_bwd(_ptr(logits), _ptr(targets), _ptr(row_loss), n, V, ld, float(scale),
                                    _stream(stream)), "spx_xent_fwd_bwd")
-    _count(1)
 
 
 def sum_f32(x, n, out, *, scale=1.0, accumulate=False, stream=None) -> None:
     _check(load().spx_sum_f32(_ptr(x), n, _ptr(out), float(scale), int(accumulate), _stream(stream)), "spx_sum_f32")
-    _count(1)
 
 
 def sumsq_ws_floats() -> int:
@@ -275,13 +262,11 @@ def sumsq_ws_floats() -> int:
 
 def sumsq(x, n, ws, out, *, stream=None) -> None:
     _check(load().spx_sumsq(_ptr(x), n, _ptr(ws), _ptr(out), _stream(stream)), "spx_sumsq")
-    _count(2)
 
 
 def clip_scale(sumsq_vec, count, max_norm, scale_out, norm_out=None, *, stream=None) -> None:
     _check(load().spx_clip_scale(_ptr(sumsq_vec), count, float(max_norm), _ptr(scale_out), _ptr(norm_out),
                                  _stream(stream)), "spx_clip_scale")
-    _count(1)
 
 
 def adamw(p, g, m, v, p_bf16, *, n, n_decay, lr, beta1, beta2, eps, weight_decay, step, grad_scale=None,
@@ -289,4 +274,3 @@ def adamw(p, g, m, v, p_bf16, *, n, n_decay, lr, beta1, beta2, eps, weight_decay
     _check(load().spx_adamw(_ptr(p), _ptr(g), _ptr(m), _ptr(v), _ptr(p_bf16), n, n_decay, float(lr), float(beta1),
                             float(beta2), float(eps), float(weight_decay), int(step), _ptr(grad_scale),
                             _stream(stream)), "spx_adamw")
-    _count(1)

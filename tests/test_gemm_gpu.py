@@ -55,8 +55,8 @@ def test_gemm_residual(M, N, K):
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("M,N,K", [(288, 768, 512), (1024, 3072, 4096), (1024, 1024, 4096), (5632, 1024, 4096)])
 def test_gemm_f32_accumulate(M, N, K, split):
-    sem = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
-    native.gemm_set_workspace(sem if split else None)
+    ws = torch.empty(8 * (M + 256) * N, device="cuda")
+    native.gemm_set_workspace(ws if split else None)
     # wgrad form: dW[M=out,N=in] = dY^T X with both operands MN-major, accumulated twice.
     g = torch.Generator().manual_seed(2)
     dY, X = _mk(K, M, gen=g), _mk(K, N, gen=g)
@@ -68,15 +68,13 @@ def test_gemm_f32_accumulate(M, N, K, split):
     torch.cuda.synchronize()
     native.gemm_set_workspace(None)
     assert _rel(C, ref) < 5e-3
-    assert int(sem.abs().sum().item()) == 0       # semaphores self-reset
 
 
 def test_gemm_split_k_deterministic():
     M, N, K = 1024, 1024, 4096
     g = torch.Generator().manual_seed(9)
     dY, X = _mk(K, M, gen=g), _mk(K, N, gen=g)
-    sem = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
-    native.gemm_set_workspace(sem)
+    native.gemm_set_workspace(torch.empty(8 * (M + 256) * N, device="cuda"))
     outs = []
     for _ in range(3):
         C = torch.zeros(M, N, dtype=torch.float32, device="cuda")

@@ -1,6 +1,6 @@
 """Time spx_gemm_bf16 on the llama-500m (config C2) stage shapes; compare with torch.matmul (cuBLAS).
 
-Usage: python tools/gemm_bench.py   (prints one line per shape)
+Usage: python tools/gemm_bench.py [--only SUBSTRING] [--no-cublas]   (prints one line per shape)
 """
 
 import os
@@ -33,11 +33,17 @@ SHAPES = [
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default=None)
+    ap.add_argument("--no-cublas", action="store_true")
+    a = ap.parse_args()
     dev = torch.device("cuda")
-    sem = torch.zeros(1 << 16, dtype=torch.int32, device=dev)
-    native.gemm_set_workspace(sem)
+    native.gemm_set_workspace(torch.empty(64 << 20, device=dev))
     res = []
     for name, M, N, K, a_mn, b_mn, epi in SHAPES:
+        if a.only and a.only not in name:
+            continue
         A = torch.randn((K, M) if a_mn else (M, K), device=dev).to(torch.bfloat16)
         B = torch.randn((K, N) if b_mn else (N, K), device=dev).to(torch.bfloat16)
         if epi == native.EPI_F32:
@@ -68,15 +74,22 @@ def main():
             torch.matmul(Am, Bm.t())
 
         out = {}
-        for label, fn in (("spx", run), ("cublas", run_ref)):
+        out["cublas"] = (float("nan"), float("nan"))
+        for label, fn in (("spx", run),) + (() if a.no_cublas else (("cublas", run_ref),)):
             for _ in range(5):
                 fn()
             torch.cuda.synchronize()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            # launches captured in a CUDA graph (as in the training step): no host overhead in the timing
             iters = 20
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(iters):
+                    fn()
+            g.replay()
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
-            for _ in range(iters):
-                fn()
+            g.replay()
             e.record()
             torch.cuda.synchronize()
             ms = s.elapsed_time(e) / iters
