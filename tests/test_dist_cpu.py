@@ -1,4 +1,4 @@
-"""Multi-process host logic on CPU (gloo, world_size 2 and 4): every rank derives the same hop
+"""Multi-process host logic on CPU (gloo, world_size 2, 4 and 8): every rank derives the same hop
 plan from the same schedule and posts sends/receives in global op order, so each message lands on
 the intended receive — the property the NCCL P2P hops of the multi-GPU executor rely on."""
 
@@ -11,7 +11,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2502_19913_b200.configs import get_config
-from paper_2502_19913_b200.executor import default_placement, hop_plan, static_slots
+from paper_2502_19913_b200.executor import balanced_placement, hop_plan, static_slots
 from paper_2502_19913_b200.simulator import simulate
 
 
@@ -29,9 +29,10 @@ def _worker(rank, world, port, cfg_name, q):
     try:
         rc = get_config(cfg_name)
         sch = rc.schedule()
-        ops = simulate(sch, rc.topology(), rc.sim_config()).ops
+        rep = simulate(sch, rc.topology(), rc.sim_config())
+        ops = rep.ops
         paths = {a: sch.paths[a].nodes for a in sch.paths}
-        placement = default_placement(rc.topology().n, world)
+        placement = balanced_placement(rep, rc.topology().n, world)  # the Trainer's default
         plan = hop_plan(ops, paths, placement)
         got, sent, pending = [], 0, []
         for idx, (op, hop) in enumerate(zip(ops, plan)):
@@ -56,7 +57,7 @@ def _worker(rank, world, port, cfg_name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,cfg", [(2, "C2"), (4, "C2"), (2, "C1")])
+@pytest.mark.parametrize("world,cfg", [(2, "C2"), (4, "C2"), (8, "C2"), (2, "C1")])
 def test_cross_rank_hops_match(world, cfg):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
