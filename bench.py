@@ -158,8 +158,10 @@ def gemm_roofline(tr, peak_tflops: float, reps: int = 5) -> dict:
             e1.record(s)
         e1.synchronize()
         ms = e0.elapsed_time(e1) / reps
-        M, N, K = key[0], key[1], key[2]
-        fl = 2.0 * M * N * K
+        if key[0] == "group":  # grouped wgrad launch: ("group", ((M, N, K), ...), a_mn, b_mn)
+            fl = sum(2.0 * m * n * k for (m, n, k) in key[1])
+        else:
+            fl = 2.0 * key[0] * key[1] * key[2]
         total_flops += fl * count
         total_ms += ms * count
         per[str(key)] = {"launches_per_step": count, "us": round(ms * 1e3, 2), "tflops": round(fl / ms / 1e9, 1)}

@@ -78,6 +78,14 @@ int spx_gemm_bf16(const void* A, const void* B, void* C, const void* R, void* C2
  * weight-gradient GEMM on one stream). */
 int spx_gemm_set_workspace(float* partials, int64_t n_floats);
 
+/* Weight-gradient group: C_i (+)= A_i . B_i^T for i < count (1..4), fp32 accumulation exactly as
+ * epilogue 2 of spx_gemm_bf16 (beta_i != 0 adds into C_i), all problems sharing the operand majors,
+ * in ONE persistent launch so their tiles fill the SMs together (the four wgrads of a decoder
+ * layer).  Arrays are host arrays of length count.  No split-K. */
+int spx_gemm_f32_group(int32_t count, const void* const* A, const void* const* B, float* const* C, const int64_t* M,
+                       const int64_t* N, const int64_t* K, const int64_t* lda, const int64_t* ldb, const int64_t* ldc,
+                       const float* beta, int32_t a_mn_major, int32_t b_mn_major, void* stream);
+
 /* QKV projection with RoPE fused into the epilogue: C = A.B^T, then rotate-half RoPE (position =
  * row % T, cos_sin [hd/2][T][2], position-minor) on columns [0, rope_cols) (the q and k heads).  head_dim 64 or 128. */
 int spx_gemm_bf16_rope(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K, int64_t lda,

@@ -54,10 +54,10 @@ struct GemmCfg {
   static constexpr int B_BYTES = (BN / CG) * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGING_BYTES = GEMM_EPI_WARPS * 4096 * NBOX;
-  static constexpr int FIT = (232448 - 1024 - 256 - STAGING_BYTES) / STAGE_BYTES;  // 227 KB opt-in limit
+  static constexpr int FIT = (232448 - 1024 - 512 - STAGING_BYTES) / STAGE_BYTES;  // 227 KB opt-in limit
   static constexpr int STAGES = FIT < 6 ? FIT : 6;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 1024 /*align slack*/ + 512 /*barriers, problem table*/;
 };
 
 struct GemmArgs {
@@ -77,11 +77,31 @@ struct GemmArgs {
   int tma_store;  // bf16 outputs leave the staging box by TMA store (SPX_GEMM_TMA_STORE=1) instead of st.global
 };
 
+// Grouped launch (EPI_F32 only, no split-K): up to GEMM_GROUP_MAX independent problems share one
+// persistent launch -- the weight-gradient GEMMs of a decoder layer -- so their tiles fill the SMs
+// together instead of each leaving a partial last wave.  Problem 0 is described by the kernel's
+// own maps and GemmArgs; problems 1.. by this table.
+constexpr int GEMM_GROUP_MAX = 4;
+struct GemmProb {
+  int M, N, K;
+  float beta;
+};
+struct GemmGroup {
+  CUtensorMap ta[GEMM_GROUP_MAX - 1], tb[GEMM_GROUP_MAX - 1], tc[GEMM_GROUP_MAX - 1];
+  GemmProb prob[GEMM_GROUP_MAX - 1];
+  int count;  // extra problems
+};
+// per-problem tile geometry, built in shared memory by thread 0
+struct ProbInfo {
+  int M, N, num_m, num_kb, unit_end;
+  float beta;
+};
+
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
-                     const GemmArgs args) {
+                     const GemmArgs args, const __grid_constant__ GemmGroup grp) {
   constexpr int NBOX = EPI == EPI_SWIGLU ? 2 : 1;
   using Cfg = GemmCfg<BN, CG, NBOX>;
   constexpr int STAGES = Cfg::STAGES;
@@ -93,6 +113,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* tfull_bar = empty_bar + STAGES;   // [2]
   uint64_t* tempty_bar = tfull_bar + 2;       // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  ProbInfo* probs = reinterpret_cast<ProbInfo*>(tmem_slot + 4);  // [1 + grp.count]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -103,10 +124,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int num_n = (args.N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
   const int num_kb = (args.K + GEMM_BK - 1) / GEMM_BK;
-  // work unit u = split * num_tiles + tile: every CTA walks its units in increasing order, so a
-  // split only ever waits for a lower unit (no deadlock with all CTAs resident)
-  const int num_units = num_tiles * args.splits;
+  // work unit u = split * num_tiles + tile (problem 0), then the grouped problems' tiles
+  int num_units = num_tiles * args.splits;
+  for (int q = 0; q < grp.count; ++q)
+    num_units += ((grp.prob[q].M + PAIR_M - 1) / PAIR_M) * ((grp.prob[q].N + BN - 1) / BN);
   const int kbs = (num_kb + args.splits - 1) / args.splits;
+  // unit -> problem index (0 unless grouped); problem geometry from the shared table
+  auto prob_of = [&](int u) {
+    int q = 0;
+    while (u >= probs[q].unit_end) ++q;
+    return q;
+  };
+  auto map_a = [&](int q) { return q == 0 ? &tmA : &grp.ta[q - 1]; };
+  auto map_b = [&](int q) { return q == 0 ? &tmB : &grp.tb[q - 1]; };
+  auto map_c = [&](int q) { return q == 0 ? &tmC : &grp.tc[q - 1]; };
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
@@ -116,6 +147,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
+    }
+    probs[0] = ProbInfo{args.M, args.N, num_m, num_kb, num_tiles * args.splits, args.beta};
+    for (int q = 0; q < grp.count; ++q) {
+      const GemmProb& g = grp.prob[q];
+      const int nm = (g.M + PAIR_M - 1) / PAIR_M;
+      probs[q + 1] = ProbInfo{g.M, g.N, nm, (g.K + GEMM_BK - 1) / GEMM_BK,
+                              probs[q].unit_end + nm * ((g.N + BN - 1) / BN), g.beta};
+      tma_prefetch_desc(&grp.ta[q]);
+      tma_prefetch_desc(&grp.tb[q]);
+      tma_prefetch_desc(&grp.tc[q]);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
@@ -146,9 +187,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       else tma_load_2d(dst, m, &full_bar[st], c0, c1);
     };
     for (int u = unit0; u < num_units; u += ustep) {
-      const int tile = u % num_tiles, kb0 = (u / num_tiles) * kbs, kb1 = min(num_kb, kb0 + kbs);
-      const int m0 = (tile % num_m) * PAIR_M + (int)rank * GEMM_BM;
-      const int nb = (tile / num_m) * BN + (int)rank * (BN / CG);  // this CTA's B rows
+      const int q = prob_of(u);
+      const ProbInfo pi = probs[q];
+      const CUtensorMap* mA = map_a(q);
+      const CUtensorMap* mB = map_b(q);
+      const int lu = q == 0 ? u : u - probs[q - 1].unit_end;
+      const int tile = q == 0 ? u % num_tiles : lu;
+      const int kb0 = q == 0 ? (u / num_tiles) * kbs : 0;
+      const int kb1 = q == 0 ? min(num_kb, kb0 + kbs) : pi.num_kb;
+      const int m0 = (tile % pi.num_m) * PAIR_M + (int)rank * GEMM_BM;
+      const int nb = (tile / pi.num_m) * BN + (int)rank * (BN / CG);  // this CTA's B rows
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
@@ -162,15 +210,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int k0 = kb * GEMM_BK;
         if (A_MN) {
 #pragma unroll
-          for (int a = 0; a < GEMM_BM / 64; ++a) load(sa + a * (GEMM_BK * 128), &tmA, stage, m0 + 64 * a, k0);
+          for (int a = 0; a < GEMM_BM / 64; ++a) load(sa + a * (GEMM_BK * 128), mA, stage, m0 + 64 * a, k0);
         } else {
-          load(sa, &tmA, stage, k0, m0);
+          load(sa, mA, stage, k0, m0);
         }
         if (B_MN) {
 #pragma unroll
-          for (int a = 0; a < BN / CG / 64; ++a) load(sb + a * (GEMM_BK * 128), &tmB, stage, nb + 64 * a, k0);
+          for (int a = 0; a < BN / CG / 64; ++a) load(sb + a * (GEMM_BK * 128), mB, stage, nb + 64 * a, k0);
         } else {
-          load(sb, &tmB, stage, k0, nb);
+          load(sb, mB, stage, k0, nb);
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
@@ -183,7 +231,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t phase = 0;
     int it = 0;
     for (int u = unit0; u < num_units; u += ustep, ++it) {
-      const int kb0 = (u / num_tiles) * kbs, kb1 = min(num_kb, kb0 + kbs);
+      const int q = prob_of(u);
+      const int kb0 = q == 0 ? (u / num_tiles) * kbs : 0;
+      const int kb1 = q == 0 ? min(num_kb, kb0 + kbs) : probs[q].num_kb;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       if constexpr (CG == 2) mbar_wait_cluster(&tempty_bar[acc], acc_phase ^ 1);
@@ -285,11 +335,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int it = 0;
     const uint32_t tempty0 = CG == 2 ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : 0;
     for (int u = unit0; u < num_units; u += ustep, ++it) {
-      const int tile = u % num_tiles, split = u / num_tiles;
+      const int q = prob_of(u);
+      const ProbInfo pi = probs[q];
+      const int tile = q == 0 ? u % num_tiles : u - probs[q - 1].unit_end;
+      const int split = q == 0 ? u / num_tiles : 0;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int m0 = (tile % num_m) * PAIR_M + (int)rank * GEMM_BM;
-      const int n0 = (tile / num_m) * BN;
+      const int m0 = (tile % pi.num_m) * PAIR_M + (int)rank * GEMM_BM;
+      const int n0 = (tile / pi.num_m) * BN;
       const int rbase = m0 + wq * 32;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -298,16 +351,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // probe: accumulator released without reading it
       } else if constexpr (EPI == EPI_F32) {
         if (args.splits == 1) {
-          const bool add = args.beta != 0.f;
+          const bool add = pi.beta != 0.f;
+          const CUtensorMap* mC = map_c(q);
 #pragma unroll 1
-          for (int c = cb; c < cb + BN / 2 && n0 + c < args.N; c += 32) {
+          for (int c = cb; c < cb + BN / 2 && n0 + c < pi.N; c += 32) {
             uint32_t v[32];
             tmem_ld_32x32b_x32(t_row + c, v);
             tmem_ld_wait();
             box_acquire();
 #pragma unroll
             for (int j = 0; j < 8; ++j) box_put(lane, j, make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-            box_issue(&tmC, n0 + c, rbase, add);
+            box_issue(mC, n0 + c, rbase, add);
           }
         } else {
           // split-K: this split's partial goes to the workspace (plain store); splitk_reduce_kernel
@@ -556,9 +610,11 @@ static int make_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint6
   return SPX_OK;
 }
 
+static const GemmGroup kNoGroup{};
+
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG = 1>
 static int launch_gemm(const void* A, const void* B, long long lda, long long ldb, const GemmArgs& args,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, const GemmGroup& grp = kNoGroup) {
   using Cfg = GemmCfg<BN, CG, EPI == EPI_SWIGLU ? 2 : 1>;
   CUtensorMap ta, tb;
   int rc;
@@ -611,12 +667,14 @@ static int launch_gemm(const void* A, const void* B, long long lda, long long ld
     }
     max_units = n;
   }
-  const int units = ((args.M + GEMM_BM * CG - 1) / (GEMM_BM * CG)) * ((args.N + BN - 1) / BN) * args.splits;
+  int units = ((args.M + GEMM_BM * CG - 1) / (GEMM_BM * CG)) * ((args.N + BN - 1) / BN) * args.splits;
+  for (int q = 0; q < grp.count; ++q)
+    units += ((grp.prob[q].M + GEMM_BM * CG - 1) / (GEMM_BM * CG)) * ((grp.prob[q].N + BN - 1) / BN);
   const int g = units < max_units ? units : max_units;
   if (CG == 2)
-    spx_launch_check(launch_k_cluster(kern, 2, dim3(2 * g), dim3(GEMM_THREADS), Cfg::SMEM_BYTES, stream, ta, tb, tc, tc2, args));
+    spx_launch_check(launch_k_cluster(kern, 2, dim3(2 * g), dim3(GEMM_THREADS), Cfg::SMEM_BYTES, stream, ta, tb, tc, tc2, args, grp));
   else
-    spx_launch_check(launch_k(kern, dim3(g), dim3(GEMM_THREADS), Cfg::SMEM_BYTES, stream, ta, tb, tc, tc2, args));
+    spx_launch_check(launch_k(kern, dim3(g), dim3(GEMM_THREADS), Cfg::SMEM_BYTES, stream, ta, tb, tc, tc2, args, grp));
   rc = check_launch("gemm_bf16_kernel");
   if (rc || EPI != EPI_F32 || args.splits == 1) return rc;
   const long long work = (long long)args.M * (args.N / 4);
@@ -730,6 +788,59 @@ extern "C" int spx_gemm_set_workspace(float* partials, int64_t n_floats) {
   g_ws[dev] = partials;
   g_ws_n[dev] = n_floats;
   return SPX_OK;
+}
+
+// Weight-gradient group: C_i (+)= A_i . B_i^T (fp32 accumulate, epilogue 2) for up to four
+// independent problems in one persistent launch.  All share the operand majors.
+extern "C" int spx_gemm_f32_group(int32_t count, const void* const* A, const void* const* B, float* const* C,
+                                  const int64_t* M, const int64_t* N, const int64_t* K, const int64_t* lda,
+                                  const int64_t* ldb, const int64_t* ldc, const float* beta, int32_t a_mn_major,
+                                  int32_t b_mn_major, void* stream) {
+  if (count < 1 || count > GEMM_GROUP_MAX) return set_error(SPX_ERR_ARG, "gemm_f32_group: 1..4 problems");
+  int min_m = 1 << 30;
+  for (int i = 0; i < count; ++i) {
+    if (M[i] <= 0 || N[i] <= 0 || K[i] <= 0) return set_error(SPX_ERR_ARG, "gemm_f32_group: non-positive shape");
+    if (N[i] % 32 != 0 || K[i] % 8 != 0 || lda[i] % 8 != 0 || ldb[i] % 8 != 0)
+      return set_error(SPX_ERR_ARG, "gemm_f32_group: N % 32, K/lda/ldb % 8 required");
+    if (((uintptr_t)A[i] | (uintptr_t)B[i]) & 15) return set_error(SPX_ERR_ARG, "gemm_f32_group: A/B must be 16-byte aligned");
+    if (M[i] < min_m) min_m = (int)M[i];
+  }
+  GemmArgs args{(int)M[0], (int)N[0], (int)K[0], C[0], nullptr, nullptr, (long long)ldc[0], (long long)ldc[0], 0,
+                beta[0], nullptr, 0, 1, 1, nullptr};
+  args.probe = probe_mode();
+  args.tma_store = tma_store_mode();
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool pair = use_pair(min_m);
+  GemmGroup grp{};
+  grp.count = count - 1;
+  for (int i = 1; i < count; ++i) {
+    GemmProb& g = grp.prob[i - 1];
+    g.M = (int)M[i];
+    g.N = (int)N[i];
+    g.K = (int)K[i];
+    g.beta = beta[i];
+    int rc;
+    if (a_mn_major) rc = make_tmap_2d(&grp.ta[i - 1], A[i], M[i], K[i], lda[i], 64, GEMM_BK);
+    else rc = make_tmap_2d(&grp.ta[i - 1], A[i], K[i], M[i], lda[i], GEMM_BK, GEMM_BM);
+    if (rc) return rc;
+    const uint32_t bbox = pair ? 128 : 256;
+    if (b_mn_major) rc = make_tmap_2d(&grp.tb[i - 1], B[i], N[i], K[i], ldb[i], 64, GEMM_BK);
+    else rc = make_tmap_2d(&grp.tb[i - 1], B[i], K[i], N[i], ldb[i], GEMM_BK, bbox);
+    if (rc) return rc;
+    rc = make_tmap_2d(&grp.tc[i - 1], C[i], N[i], M[i], ldc[i], 32, 32, true);
+    if (rc) return rc;
+  }
+  const int am = a_mn_major ? 1 : 0, bm = b_mn_major ? 1 : 0;
+#define SPX_GRP(AM, BM)                                                                                     \
+  if (am == AM && bm == BM)                                                                                 \
+    return pair ? launch_gemm<256, AM, BM, EPI_F32, 2>(A[0], B[0], lda[0], ldb[0], args, s, grp)            \
+                : launch_gemm<256, AM, BM, EPI_F32, 1>(A[0], B[0], lda[0], ldb[0], args, s, grp);
+  SPX_GRP(true, true)
+  SPX_GRP(false, false)
+  SPX_GRP(false, true)
+  SPX_GRP(true, false)
+#undef SPX_GRP
+  return set_error(SPX_ERR_ARG, "gemm_f32_group: bad majors");
 }
 
 extern "C" int spx_gemm_bf16_rope(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K, int64_t lda,

@@ -138,13 +138,16 @@ class Scratch:
     def __init__(self, cfg: ModelConfig, n: int, b: int, T: int, device, with_head: bool):
         d, f = cfg.d, cfg.ffn
         e = dict(dtype=BF16, device=device)
-        self.dx = [torch.empty(n, d, **e) for _ in range(2)]
-        self.dxm = torch.empty(n, d, **e)
+        # Buffers read by a layer's weight-gradient group are double-buffered by layer parity (the
+        # group of layer i may still run while layer i-1 computes), and the layer-output gradients
+        # rotate through three buffers (layer i's dy is read by its group until layer i-2 starts).
+        self.dx = [torch.empty(n, d, **e) for _ in range(3)]
+        self.dxm2 = [torch.empty(n, d, **e) for _ in range(2)]
         self.dxn = torch.empty(n, d, **e)
         self.dh = torch.empty(n, f, **e)
-        self.dgu = torch.empty(n, 2 * f, **e)
+        self.dgu2 = [torch.empty(n, 2 * f, **e) for _ in range(2)]
         self.do = torch.empty(n, cfg.n_heads * cfg.head_dim, **e)
-        self.dqkv = torch.empty(n, cfg.qkv_dim, **e)
+        self.dqkv2 = [torch.empty(n, cfg.qkv_dim, **e) for _ in range(2)]
         self.delta = torch.empty(b, cfg.n_heads, T, dtype=F32, device=device)
         self.rms_ws = torch.empty(native.rmsnorm_ws_floats(n, d), dtype=F32, device=device)
         self.rope = rope_cos_sin(T, cfg.head_dim, cfg.rope_theta).to(device)
@@ -189,53 +192,47 @@ class StageProgram:
     def layer_bwd(self, ps: ParamSet, i: int, x, a: LayerActs, dy, dx, sc: Scratch, s, side=None):
         """dy: grad of the layer output; dx: grad of the layer input (may not alias dy).
 
-        The four weight-gradient GEMMs (few output tiles, long K = tokens) go to ``side`` when given:
-        forked from ``s`` as soon as their inputs exist and joined at the end of the layer, so they
-        fill SMs the data-gradient chain leaves idle.  Everything they read (saved activations, and
-        scratch written once per layer) stays untouched until the join."""
+        The data-gradient chain runs on ``s``.  The four weight-gradient GEMMs (few output tiles,
+        long K = tokens) form ONE grouped launch (spx_gemm_f32_group) issued as soon as their last
+        input (dqkv) exists: on ``side`` when given -- forked from ``s`` and returned as an event
+        the caller joins one layer later, so the group overlaps the next layer's data-gradient
+        chain -- else inline on ``s``.  The buffers it reads are per-parity scratch (Scratch)."""
         c, n = self.cfg, self.n
         d, f, qd, hd = c.d, c.ffn, c.qkv_dim, c.head_dim
         od = c.n_heads * hd
-        F32E = native.EPI_F32
-
-        def wgrad(fn):
-            if side is None:
-                fn(s)
-                return
+        par = i & 1
+        dgu, dxm, dqkv = sc.dgu2[par], sc.dxm2[par], sc.dqkv2[par]
+        # MLP
+        native.gemm(dy, ps.w(f"l{i}.wdown"), sc.dh, M=n, N=f, K=d, lda=d, ldb=f, ldc=f, b_mn=True, stream=s)
+        native.swiglu_bwd(a.gu, sc.dh, dgu, rows=n, F=f, stream=s)
+        native.gemm(dgu, ps.w(f"l{i}.wgu"), sc.dxn, M=n, N=d, K=2 * f, lda=2 * f, ldb=d, ldc=d, b_mn=True, stream=s)
+        native.rmsnorm_bwd(a.xmid, ps.w(f"l{i}.mlp_norm"), a.rstd2, sc.dxn, dy, dxm, ps.gv(f"l{i}.mlp_norm"),
+                           sc.rms_ws, rows=n, d=d, stream=s)
+        # attention; dq, dk leave the attention backward already un-rotated (inverse RoPE fused)
+        native.gemm(dxm, ps.w(f"l{i}.wo"), sc.do, M=n, N=od, K=d, lda=d, ldb=od, ldc=od, b_mn=True, stream=s)
+        native.attn_bwd(a.qkv, a.o, sc.do, a.lse, sc.delta, dqkv, B=self.b, T=self.T, H=c.n_heads,
+                        Hkv=c.n_kv_heads, hd=hd, ld_qkv=qd, ld_o=od, scale=self.scale, rope_cs=sc.rope, stream=s)
+        # weight gradients dW = dY^T X (both operands MN-major), accumulated in fp32
+        group = [
+            dict(A=dgu, B=a.xn2, C=ps.gv(f"l{i}.wgu"), M=2 * f, N=d, K=n, lda=2 * f, ldb=d, ldc=d, beta=1.0),
+            dict(A=dqkv, B=a.xn1, C=ps.gv(f"l{i}.wqkv"), M=qd, N=d, K=n, lda=qd, ldb=d, ldc=d, beta=1.0),
+            dict(A=dy, B=a.h, C=ps.gv(f"l{i}.wdown"), M=d, N=f, K=n, lda=d, ldb=f, ldc=f, beta=1.0),
+            dict(A=dxm, B=a.o, C=ps.gv(f"l{i}.wo"), M=d, N=od, K=n, lda=d, ldb=od, ldc=od, beta=1.0),
+        ]
+        done = None
+        if side is None:
+            native.gemm_f32_group(group, stream=s)
+        else:
             ev = torch.cuda.Event()
             ev.record(s)
             side.wait_event(ev)
-            fn(side)
-
-        # MLP
-        wgrad(lambda st: native.gemm(dy, a.h, ps.gv(f"l{i}.wdown"), M=d, N=f, K=n, lda=d, ldb=f, ldc=f, a_mn=True,
-                                     b_mn=True, epilogue=F32E, beta=1.0, stream=st))
-        # (the fused EPI_SWIGLU_BWD epilogue exists but is slower than dgrad + swiglu_bwd today:
-        # its per-row gate/up reads make the epilogue the bottleneck)
-        native.gemm(dy, ps.w(f"l{i}.wdown"), sc.dh, M=n, N=f, K=d, lda=d, ldb=f, ldc=f, b_mn=True, stream=s)
-        native.swiglu_bwd(a.gu, sc.dh, sc.dgu, rows=n, F=f, stream=s)
-        wgrad(lambda st: native.gemm(sc.dgu, a.xn2, ps.gv(f"l{i}.wgu"), M=2 * f, N=d, K=n, lda=2 * f, ldb=d, ldc=d,
-                                     a_mn=True, b_mn=True, epilogue=F32E, beta=1.0, stream=st))
-        native.gemm(sc.dgu, ps.w(f"l{i}.wgu"), sc.dxn, M=n, N=d, K=2 * f, lda=2 * f, ldb=d, ldc=d, b_mn=True,
-                    stream=s)
-        native.rmsnorm_bwd(a.xmid, ps.w(f"l{i}.mlp_norm"), a.rstd2, sc.dxn, dy, sc.dxm, ps.gv(f"l{i}.mlp_norm"),
+            native.gemm_f32_group(group, stream=side)
+            done = torch.cuda.Event()
+            done.record(side)
+        native.gemm(dqkv, ps.w(f"l{i}.wqkv"), sc.dxn, M=n, N=d, K=qd, lda=qd, ldb=d, ldc=d, b_mn=True, stream=s)
+        native.rmsnorm_bwd(x, ps.w(f"l{i}.attn_norm"), a.rstd1, sc.dxn, dxm, dx, ps.gv(f"l{i}.attn_norm"),
                            sc.rms_ws, rows=n, d=d, stream=s)
-        # attention
-        wgrad(lambda st: native.gemm(sc.dxm, a.o, ps.gv(f"l{i}.wo"), M=d, N=od, K=n, lda=d, ldb=od, ldc=od, a_mn=True,
-                                     b_mn=True, epilogue=F32E, beta=1.0, stream=st))
-        native.gemm(sc.dxm, ps.w(f"l{i}.wo"), sc.do, M=n, N=od, K=d, lda=d, ldb=od, ldc=od, b_mn=True, stream=s)
-        # dq, dk leave the attention backward already un-rotated (inverse RoPE fused)
-        native.attn_bwd(a.qkv, a.o, sc.do, a.lse, sc.delta, sc.dqkv, B=self.b, T=self.T, H=c.n_heads,
-                        Hkv=c.n_kv_heads, hd=hd, ld_qkv=qd, ld_o=od, scale=self.scale, rope_cs=sc.rope, stream=s)
-        wgrad(lambda st: native.gemm(sc.dqkv, a.xn1, ps.gv(f"l{i}.wqkv"), M=qd, N=d, K=n, lda=qd, ldb=d, ldc=d,
-                                     a_mn=True, b_mn=True, epilogue=F32E, beta=1.0, stream=st))
-        native.gemm(sc.dqkv, ps.w(f"l{i}.wqkv"), sc.dxn, M=n, N=d, K=qd, lda=qd, ldb=d, ldc=d, b_mn=True, stream=s)
-        native.rmsnorm_bwd(x, ps.w(f"l{i}.attn_norm"), a.rstd1, sc.dxn, sc.dxm, dx, ps.gv(f"l{i}.attn_norm"),
-                           sc.rms_ws, rows=n, d=d, stream=s)
-        if side is not None:  # join: the next layer reuses the scratch buffers the wgrads read
-            ev = torch.cuda.Event()
-            ev.record(side)
-            s.wait_event(ev)
+        return done
 
     # ---- node ops ----
     def fwd(self, ps: ParamSet, sb: SlotBuffers, sc: Scratch, origin: bool, s):
@@ -248,10 +245,17 @@ class StageProgram:
         """Returns the buffer holding the gradient w.r.t. the node's input."""
         dy = sb.gin
         k = 0
+        pending = {}  # layer -> its weight-gradient group's completion event (side stream)
         for i in reversed(range(len(sb.layers))):
+            if i + 2 in pending:  # layer i reuses the parity-(i & 1) scratch and dx buffer of layer i+2
+                s.wait_event(pending.pop(i + 2))
             dx = sb.gout if (i == 0 and sb.gout is not None) else sc.dx[k]
-            self.layer_bwd(ps, i, sb.xs[i], sb.layers[i], dy, dx, sc, s, side)
-            dy, k = dx, k ^ 1
+            done = self.layer_bwd(ps, i, sb.xs[i], sb.layers[i], dy, dx, sc, s, side)
+            if done is not None:
+                pending[i] = done
+            dy, k = dx, (k + 1) % 3
+        for ev in pending.values():  # join: all weight gradients of the node accumulated
+            s.wait_event(ev)
         if origin:
             native.embed_bwd(sb.perm, sb.seg_start, sb.seg_id, sb.n_seg, self.n, dy, ps.gv("embed"), d=self.cfg.d,
                              stream=s)

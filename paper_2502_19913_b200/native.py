@@ -31,6 +31,7 @@ SIGNATURES: dict[str, list] = {
     "spx_attn_fwd": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P],
     "spx_attn_bwd": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P, _P],
     "spx_gemm_set_workspace": [_P, _I64],
+    "spx_gemm_f32_group": [_I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P],
     "spx_gemm_bf16_rope": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _I64, _I64, _P],
     "spx_rmsnorm_fwd": [_P, _P, _P, _P, _I64, _I64, _F, _P],
     "spx_rmsnorm_bwd": [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _P],
@@ -144,6 +145,34 @@ def gemm(A, B, C, *, M, N, K, lda, ldb, ldc, a_mn=False, b_mn=False, epilogue=EP
             _STATS["record"] = False
             try:
                 gemm(*args, **kw)
+            finally:
+                _STATS["record"] = rec
+
+        _STATS["gemms"][key] = (cnt + 1, again)
+        _STATS["gemm_log"].append(key)
+
+
+def gemm_f32_group(problems, *, a_mn=True, b_mn=True, stream=None) -> None:
+    """Grouped fp32-accumulating GEMMs in one launch (spx_gemm_f32_group).  problems: list of dicts
+    with A, B, C (tensors) and M, N, K, lda, ldb, ldc, beta."""
+    k = len(problems)
+    P64 = ctypes.c_void_p * k
+    I64 = ctypes.c_int64 * k
+    arr = lambda key: I64(*[int(p[key]) for p in problems])  # noqa: E731
+    rc = load().spx_gemm_f32_group(k, P64(*[_ptr(p["A"]) for p in problems]), P64(*[_ptr(p["B"]) for p in problems]),
+                                   P64(*[_ptr(p["C"]) for p in problems]), arr("M"), arr("N"), arr("K"), arr("lda"),
+                                   arr("ldb"), arr("ldc"), (ctypes.c_float * k)(*[float(p["beta"]) for p in problems]),
+                                   int(a_mn), int(b_mn), _stream(stream))
+    _check(rc, "spx_gemm_f32_group")
+    if _STATS["record"]:
+        key = ("group", tuple((int(p["M"]), int(p["N"]), int(p["K"])) for p in problems), bool(a_mn), bool(b_mn))
+        cnt = _STATS["gemms"].get(key, (0, None))[0]
+
+        def again(pr=list(problems), kw=dict(a_mn=a_mn, b_mn=b_mn)):
+            rec = _STATS["record"]
+            _STATS["record"] = False
+            try:
+                gemm_f32_group(pr, **kw)
             finally:
                 _STATS["record"] = rec
 

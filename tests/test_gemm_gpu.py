@@ -127,3 +127,29 @@ def test_gemm_swiglu_bwd_epilogue(M, F, K):
     d = dgu.float().view(M, F // 128, 2, 128)
     assert _rel(d[:, :, 0].reshape(M, F), gt.grad) < 2e-2
     assert _rel(d[:, :, 1].reshape(M, F), ut.grad) < 2e-2
+
+
+@pytest.mark.parametrize("beta", [0.0, 1.0])
+def test_gemm_f32_group(beta):
+    """Four wgrad-shaped problems (incl. ragged M/N) in one grouped launch == four torch matmuls."""
+    g = torch.Generator().manual_seed(11)
+    shapes = [(768, 256, 512), (288, 512, 512), (1024, 2816, 1024), (320, 96, 1024)]
+    probs, refs = [], []
+    for (M, N, K) in shapes:
+        dY, X = _mk(K, M, gen=g), _mk(K, N, gen=g)
+        C = torch.randn(M, N, generator=g).cuda()
+        refs.append(beta * C + dY.float().t() @ X.float())
+        probs.append(dict(A=dY, B=X, C=C, M=M, N=N, K=K, lda=M, ldb=N, ldc=N, beta=beta))
+    native.gemm_f32_group(probs)
+    torch.cuda.synchronize()
+    for p, ref in zip(probs, refs):
+        assert _rel(p["C"], ref) < 5e-3
+    # one problem alone equals the single-GEMM path bit for bit
+    C1 = torch.zeros(768, 256, device="cuda")
+    C2 = torch.zeros(768, 256, device="cuda")
+    p0 = dict(probs[0], C=C1, beta=0.0)
+    native.gemm_f32_group([p0])
+    native.gemm(p0["A"], p0["B"], C2, M=768, N=256, K=512, lda=768, ldb=256, ldc=256, a_mn=True, b_mn=True,
+                epilogue=native.EPI_F32)
+    torch.cuda.synchronize()
+    assert torch.equal(C1, C2)
