@@ -97,9 +97,12 @@ int spx_gemm_bf16_rope(const void* A, const void* B, void* C, int64_t M, int64_t
  * o [B*T][ld_o] bf16, lse [B][H][T] f32 (natural log).  T % 64 == 0, hd in {48, 64, 128}. */
 int spx_attn_fwd(const void* qkv, void* o, float* lse, int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd,
                  int64_t ld_qkv, int64_t ld_o, float scale, void* stream);
-/* dqkv gets dq/dk/dv in the same layout as qkv.  delta_ws: B*H*T floats of workspace.
- * rope_cos_sin (may be NULL): when given, dq and dk are written back through the inverse RoPE
- * rotation (the gradient w.r.t. the pre-RoPE projections). */
+/* Workspace of spx_attn_bwd in floats: D = rowsum(dO*O) and lse*log2e (B*H*T each) and, on the
+ * tcgen05 path (hd 64/128, T % 128 == 0), the causal dS^T tiles the dQ GEMM reads. */
+int64_t spx_attn_bwd_ws_floats(int64_t B, int64_t H, int64_t T, int64_t hd);
+/* dqkv gets dq/dk/dv in the same layout as qkv.  delta_ws: spx_attn_bwd_ws_floats(B, H, T, hd)
+ * floats (16-byte aligned).  rope_cos_sin (may be NULL): when given, dq and dk are written back
+ * through the inverse RoPE rotation (the gradient w.r.t. the pre-RoPE projections). */
 int spx_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, float* delta_ws, void* dqkv,
                  int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv, int64_t ld_o, float scale,
                  const float* rope_cos_sin, void* stream);

@@ -313,7 +313,10 @@ __global__ void attn_bwd_delta_kernel(const Params p) {
   s += __shfl_xor_sync(0xffffffffu, s, 1);
   if (live && j == 0) {
     const int b = (int)(r / p.T), t = (int)(r % p.T);
-    p.delta[((long long)b * p.H + h) * p.T + t] = s;
+    const long long idx = ((long long)b * p.H + h) * p.T + t;
+    p.delta[idx] = s;
+    // second half of the workspace: lse in the exp2 domain for the tcgen05 dK/dV kernel
+    p.delta[(long long)p.B * p.H * p.T + idx] = p.lse[idx] * 1.4426950408889634f;
   }
 }
 
@@ -650,6 +653,15 @@ bool attn_use_legacy() {
   return legacy;
 }
 }  // namespace spx
+
+extern "C" int64_t spx_attn_bwd_ws_floats(int64_t B, int64_t H, int64_t T, int64_t hd) {
+  int64_t n = 2 * B * H * T;  // D and lse*log2e
+  if ((hd == 64 || hd == 128) && T % 128 == 0 && !attn_use_legacy()) {
+    const int64_t nqb = T / 128;
+    n += B * H * (nqb * (nqb + 1) / 2) * 128 * 128 / 2;  // dS^T tiles, bf16
+  }
+  return n;
+}
 
 extern "C" int spx_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, float* delta_ws,
                             void* dqkv, int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv,

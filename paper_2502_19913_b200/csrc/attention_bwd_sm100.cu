@@ -7,12 +7,14 @@
 //         P^T = exp2(S^T*scale*log2e - lse*log2e) and dS^T = P^T (dP^T - D) as bf16 swizzled
 //         smem tiles; then dV += P^T dO and dK += dS^T Q accumulate in TMEM (dO and Q tiles are
 //         re-used as MN-major B operands).
-//   dq:   CTA = 128 queries of one head; loops over key blocks 0..its own.  S = Q K^T and
-//         dP = dO V^T in TMEM, dS (bf16 smem) -> dQ += dS K (K re-used as MN-major B).
+//         The dK/dV kernel also stores each dS^T tile (bf16) to the workspace.
+//   dq:   dQ = dS K as a GEMM over those tiles (CTA = 128 queries of one head, key blocks
+//         0..its own), so S, dP and the softmax are computed once.
 // Both write bf16 gradients into the dQKV buffer (same layout as QKV) with the inverse RoPE
 // applied to dq/dk when a table is given, scale folded in.  D = rowsum(dO*O) comes from
 // attn_bwd_delta_kernel (attention.cu).
 #include <cmath>
+#include <type_traits>
 
 #include "spx_common.cuh"
 #include "spx_internal.h"
@@ -45,9 +47,10 @@ SPX_DEVICE void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* 
 
 struct BwdParams {
   __nv_bfloat16* dqkv;   // [B*T, ld]
-  const float* lse;      // [B, H, T]
+  const float* lse;      // [B, H, T] (dQ kernel; the dK/dV kernel reads lse*log2e from the workspace)
   const float* delta;    // [B, H, T]
   const float* rope_cs;  // [hd/2][T][2] or null
+  __nv_bfloat16* ds;     // dS^T tiles [B*H][tri(nqb)][128 keys][128 queries] (workspace)
   long long ld;
   int B, T, H, Hkv;
   float scale;
@@ -58,6 +61,11 @@ SPX_DEVICE void put_row8(uint8_t* tile, int r, int c8, const float* v) {
   const int atom = c8 >> 3, chunk = c8 & 7;
   *reinterpret_cast<uint4*>(tile + atom * ATOM + r * 128 + ((chunk ^ (r & 7)) << 4)) =
       make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+}
+
+SPX_DEVICE void put_row8p(uint8_t* tile, int r, int c8, const uint32_t* v) {
+  const int atom = c8 >> 3, chunk = c8 & 7;
+  *reinterpret_cast<uint4*>(tile + atom * ATOM + r * 128 + ((chunk ^ (r & 7)) << 4)) = make_uint4(v[0], v[1], v[2], v[3]);
 }
 
 // write a 128 x HD accumulator row (TMEM lane) as bf16, optionally through the inverse RoPE
@@ -128,7 +136,7 @@ struct DkdvSmem {
 template <int HD>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
-                            const BwdParams p) {
+                            const __grid_constant__ CUtensorMap tmDS, const BwdParams p) {
   using L = DkdvSmem<HD>;
   constexpr int NST = L::NST;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -142,6 +150,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* mma2_done = bars + 8;
   uint64_t* tmem_free = bars + 9;   // S / dP of the current step copied to registers
   uint64_t* acc_free = bars + 10;   // dV / dK of the previous item read out of TMEM
+  uint64_t* ds_read = bars + 11;    // the dS^T tile of the step has been read by its TMA store
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -170,6 +179,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(mma2_done, 1);
     mbar_init(tmem_free, EW_WARPS);
     mbar_init(acc_free, EW_WARPS);
+    mbar_init(ds_read, 1);
+    tma_prefetch_desc(&tmDS);
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -205,7 +216,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           tma_load_2d(smem + L::OFF_DO + s * L::TILE + a * ATOM, &tmDO, &full[s], h * HD + 64 * a, row0 + qb * BLK);
         }
         const size_t off = ((size_t)b * p.H + h) * p.T + qb * BLK;
-        bulk_load(smem + L::OFF_LSE + s * 512, p.lse + off, 512, &full[s]);
+        bulk_load(smem + L::OFF_LSE + s * 512, p.delta + (size_t)p.B * p.H * p.T + off, 512, &full[s]);  // lse*log2e
         bulk_load(smem + L::OFF_D + s * 512, p.delta + off, 512, &full[s]);
       }
     }
@@ -268,6 +279,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (it + 1 == n_it) mma_commit(kv_empty);
       }
     }
+  } else if (warp == 3 && lane == 0) {
+    // ---------------- dS^T tile -> workspace (b, h, qb, jb) for the dQ GEMM ----------------
+    int gi = 0;
+    const int ntri = nqb * (nqb + 1) / 2;
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
+      if (w >= n_items) continue;
+      int b, kvh, jb;
+      item(w, b, kvh, jb);
+      const int nq = nqb - jb, n_it = group * nq;
+      for (int it = 0; it < n_it; ++it, ++gi) {
+        const int h = kvh * group + it / nq, qb = jb + it % nq;
+        mbar_wait(p_ready, gi & 1);
+        const int row = ((b * p.H + h) * ntri + qb * (qb + 1) / 2 + jb) * BLK;
+        for (int a = 0; a < 2; ++a) tma_store_2d(&tmDS, smem + L::OFF_DST + a * ATOM, 64 * a, row);
+        bulk_commit();
+        bulk_wait_read<0>();
+        mbar_arrive(ds_read);
+      }
+    }
+    bulk_wait<0>();
   } else if (warp >= 4) {
     // ---------------- elementwise: thread = key row, 64 query columns ----------------
     const int quad = warp & 3, half = (warp - 4) >> 2;
@@ -291,30 +322,56 @@ __global__ void __launch_bounds__(THREADS, 1)
         const float* lse = reinterpret_cast<const float*>(smem + L::OFF_LSE + s * 512);
         const float* dd = reinterpret_cast<const float*>(smem + L::OFF_D + s * 512);
         const int cb = 64 * half;
-        uint32_t sv[64], dv[64];
-        tmem_ld_32x32b_x32(lane_base + TM_S + cb, *reinterpret_cast<uint32_t(*)[32]>(sv));
-        tmem_ld_32x32b_x32(lane_base + TM_S + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-        tmem_ld_32x32b_x32(lane_base + TM_DP + cb, *reinterpret_cast<uint32_t(*)[32]>(dv));
-        tmem_ld_32x32b_x32(lane_base + TM_DP + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tmem_free);
-        if (gi > 0) mbar_wait(mma2_done, (gi - 1) & 1);  // P^T / dS^T tiles free
+        // P^T and dS^T are formed in registers (bf16 pairs, 32 columns at a time) while the
+        // previous step's dV/dK MMAs still read the tiles; only the stores wait for them
+        uint32_t pk[32], dk[32];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t sv[32], dv[32];
+          tmem_ld_32x32b_x32(lane_base + TM_S + cb + 32 * hh, sv);
+          tmem_ld_32x32b_x32(lane_base + TM_DP + cb + 32 * hh, dv);
+          tmem_ld_wait();
+          if (hh == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tmem_free);
+          }
+          // lse2 = lse * log2e (precomputed by the delta kernel); the causal mask only on the
+          // diagonal block (separate code path: no per-element compare elsewhere)
+          auto body = [&](auto diag_c) {
+            constexpr bool DIAG = decltype(diag_c)::value;
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const int c8 = 4 * hh + c4;
+              float pv[8], ds[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int c = cb + 8 * c8 + j;
+                float pp = ex2(fmaf(__uint_as_float(sv[8 * c4 + j]), sl2, -lse[c]));
+                if (DIAG && c < r) pp = 0.f;  // query before key
+                pv[j] = pp;
+                ds[j] = pp * (__uint_as_float(dv[8 * c4 + j]) - dd[c]);
+              }
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                pk[4 * c8 + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
+                dk[4 * c8 + e] = pack_bf16(ds[2 * e], ds[2 * e + 1]);
+              }
+            }
+          };
+          if (diag) body(std::true_type{});
+          else body(std::false_type{});
+        }
+        if (gi > 0) {
+          mbar_wait(mma2_done, (gi - 1) & 1);  // P^T / dS^T tiles free
+          mbar_wait(ds_read, (gi - 1) & 1);    // the dS^T store has read its tile
+        }
 #pragma unroll
         for (int c8 = 0; c8 < 8; ++c8) {
-          float pv[8], ds[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int c = cb + 8 * c8 + j;
-            float pp = ex2(fmaf(__uint_as_float(sv[8 * c8 + j]), sl2, -lse[c] * LOG2E));
-            if (diag && c < r) pp = 0.f;  // query before key
-            pv[j] = pp;
-            ds[j] = pp * (__uint_as_float(dv[8 * c8 + j]) - dd[c]);
-          }
-          put_row8(sPT, r, (cb >> 3) + c8, pv);
-          put_row8(sDST, r, (cb >> 3) + c8, ds);
+          put_row8p(sPT, r, (cb >> 3) + c8, pk + 4 * c8);
+          put_row8p(sDST, r, (cb >> 3) + c8, dk + 4 * c8);
         }
+
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_ready);
@@ -339,40 +396,40 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ------------------------------------------------------------------------------------------
-// dQ (persistent: heavy-first items (batch, head, query block))
+// dQ = dS K as a GEMM over the dS^T tiles the dK/dV kernel stored (no recomputation of S, dP or
+// the softmax).  Persistent, heavy-first items (batch, head, query block ib); per key block j <= ib
+// the producer stages the dS^T tile (A, MN-major: rows = keys, columns = queries) and K_j (B,
+// MN-major); dQ accumulates in TMEM (double-buffered across items) and 4 epilogue warps write it
+// (scaled, inverse RoPE) while the next item accumulates.
 // ------------------------------------------------------------------------------------------
 template <int HD>
-struct DqSmem {
-  static constexpr int TILE = (HD / 64) * ATOM;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_DO = OFF_Q + TILE;
-  static constexpr int OFF_K = OFF_DO + TILE;     // [2]
-  static constexpr int OFF_V = OFF_K + 2 * TILE;  // [2]
-  static constexpr int OFF_DS = OFF_V + 2 * TILE;
-  static constexpr int OFF_BAR = OFF_DS + 2 * ATOM;
+struct DqmSmem {
+  static constexpr int DS_BYTES = 2 * ATOM;                 // 128 keys x 128 queries bf16
+  static constexpr int K_BYTES = (HD / 64) * ATOM;          // 128 keys x HD
+  static constexpr int STAGE = DS_BYTES + K_BYTES;
+  static constexpr int STAGES = HD == 64 ? 4 : 3;
+  static constexpr int OFF_BAR = STAGES * STAGE;
   static constexpr int BYTES = OFF_BAR + 256;
+  static constexpr int THREADS = 256;                       // producer, MMA, TMEM, spare, 4 epilogue warps
 };
 
 template <int HD>
-__global__ void __launch_bounds__(THREADS, 1)
-    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
-                          const BwdParams p) {
-  using L = DqSmem<HD>;
+__global__ void __launch_bounds__(DqmSmem<HD>::THREADS, 1)
+    attn_bwd_dq_mma_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDS,
+                           const BwdParams p) {
+  using L = DqmSmem<HD>;
+  constexpr int STAGES = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint64_t* qdo_full = bars + 0;
-  uint64_t* qdo_empty = bars + 1;
-  uint64_t* kv_full = bars + 2;   // [2]
-  uint64_t* kv_empty = bars + 4;  // [2]
-  uint64_t* sdp_full = bars + 6;
-  uint64_t* p_ready = bars + 7;
-  uint64_t* mma2_done = bars + 8;
-  uint64_t* tmem_free = bars + 9;
-  uint64_t* acc_free = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* full = bars;                // [STAGES]
+  uint64_t* empty = bars + STAGES;      // [STAGES]
+  uint64_t* acc_full = bars + 2 * STAGES;       // [2]
+  uint64_t* acc_empty = bars + 2 * STAGES + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = p.T / BLK;
+  const int ntri = nqb * (nqb + 1) / 2;
   const int BH = p.B * p.H;
   const int n_items = nqb * BH;
   const int group = p.H / p.Hkv;
@@ -384,169 +441,95 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmQKV);
-    tma_prefetch_desc(&tmDO);
-    mbar_init(qdo_full, 1);
-    mbar_init(qdo_empty, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+    tma_prefetch_desc(&tmDS);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
     }
-    mbar_init(sdp_full, 1);
-    mbar_init(p_ready, EW_WARPS);
-    mbar_init(mma2_done, 1);
-    mbar_init(tmem_free, EW_WARPS);
-    mbar_init(acc_free, EW_WARPS);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 4);
+    }
     fence_barrier_init();
     fence_proxy_async();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  constexpr uint32_t TMEM_COLS = 2 * HD;
+  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();  // upstream grid complete before any dependent global access
-  constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 256;
+  pdl_wait();  // the dK/dV kernel's dS^T tiles are complete
 
   if (warp == 0 && lane == 0) {
-    int gj = 0, n = 0;
-    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
-      if (w >= n_items) continue;
-      int b, h, ib;
-      item(w, b, h, ib);
-      const int row0 = b * p.T, kvh = h / group;
-      mbar_wait(qdo_empty, (n & 1) ^ 1);
-      mbar_expect_tx(qdo_full, 2 * L::TILE);
-      for (int a = 0; a < HD / 64; ++a) {
-        tma_load_2d(smem + L::OFF_Q + a * ATOM, &tmQKV, qdo_full, h * HD + 64 * a, row0 + ib * BLK);
-        tma_load_2d(smem + L::OFF_DO + a * ATOM, &tmDO, qdo_full, h * HD + 64 * a, row0 + ib * BLK);
-      }
-      for (int j = 0; j <= ib; ++j, ++gj) {
-        const int s = gj & 1;
-        mbar_wait(&kv_empty[s], ((gj >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[s], 2 * L::TILE);
-        for (int a = 0; a < HD / 64; ++a) {
-          tma_load_2d(smem + L::OFF_K + s * L::TILE + a * ATOM, &tmQKV, &kv_full[s], (p.H + kvh) * HD + 64 * a,
-                      row0 + j * BLK);
-          tma_load_2d(smem + L::OFF_V + s * L::TILE + a * ATOM, &tmQKV, &kv_full[s],
-                      (p.H + p.Hkv + kvh) * HD + 64 * a, row0 + j * BLK);
-        }
-      }
-    }
-  } else if (warp == 1 && lane == 0) {
-    constexpr uint32_t ID_S = umma_idesc_bf16(BLK, BLK, false, false);  // Q.K^T, dO.V^T
-    constexpr uint32_t ID_G = umma_idesc_bf16(BLK, HD, false, true);    // dS.K
-    const uint32_t sQ = smem_u32(smem + L::OFF_Q), sDO = smem_u32(smem + L::OFF_DO);
-    const uint32_t sDS = smem_u32(smem + L::OFF_DS);
-    auto issue_sdp = [&](int gj) {
-      const int s = gj & 1;
-      mbar_wait(&kv_full[s], (gj >> 1) & 1);
-      tc_fence_after();
-      const uint32_t sK = smem_u32(smem + L::OFF_K + s * L::TILE), sV = smem_u32(smem + L::OFF_V + s * L::TILE);
-#pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const uint32_t ko = (kk >> 2) * ATOM + (kk & 3) * 32;
-        mma_bf16_ss(tmem + TM_S, umma_desc_sw128(sQ + ko, 16, 1024), umma_desc_sw128(sK + ko, 16, 1024), ID_S, kk > 0);
-        mma_bf16_ss(tmem + TM_DP, umma_desc_sw128(sDO + ko, 16, 1024), umma_desc_sw128(sV + ko, 16, 1024), ID_S,
-                    kk > 0);
-      }
-      mma_commit(sdp_full);
-    };
-    int gj = 0, n = 0;
-    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
-      if (w >= n_items) continue;
-      int b, h, ib;
-      item(w, b, h, ib);
-      mbar_wait(qdo_full, n & 1);
-      bool issued = false;
-      for (int j = 0; j <= ib; ++j, ++gj) {
-        const int s = gj & 1;
-        if (!issued) issue_sdp(gj);
-        mbar_wait(tmem_free, gj & 1);
-        tc_fence_after();
-        issued = false;
-        if (j + 1 <= ib) {  // next S/dP of this item overlaps the elementwise math
-          issue_sdp(gj + 1);
-          issued = true;
-        }
-        mbar_wait(p_ready, gj & 1);
-        if (j == 0) mbar_wait(acc_free, (n & 1) ^ 1);  // previous item's dQ read out
-        tc_fence_after();
-        const uint32_t sK = smem_u32(smem + L::OFF_K + s * L::TILE);
-#pragma unroll
-        for (int kk = 0; kk < BLK / 16; ++kk) {
-          const uint32_t ao = (kk >> 2) * ATOM + (kk & 3) * 32;
-          mma_bf16_ss(tmem + TM_DQ, umma_desc_sw128(sDS + ao, 16, 1024), umma_desc_sw128(sK + kk * 2048, ATOM, 1024),
-                      ID_G, (j > 0) || (kk > 0));
-        }
-        mma_commit(mma2_done);
-        mma_commit(&kv_empty[s]);
-        if (j == ib) mma_commit(qdo_empty);
-      }
-    }
-  } else if (warp >= 4) {
-    // ---------------- elementwise: thread = query row, 64 key columns ----------------
-    const int quad = warp & 3, half = (warp - 4) >> 2;
-    const int r = quad * 32 + lane;
-    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
-    const float sl2 = p.scale * LOG2E;
-    uint8_t* sDS = smem + L::OFF_DS;
-    int gj = 0;
+    int g = 0;
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
       if (w >= n_items) continue;
       int b, h, ib;
       item(w, b, h, ib);
-      const int t = ib * BLK + r;
-      const size_t stat = ((size_t)b * p.H + h) * p.T + t;
-      const float lse2 = p.lse[stat] * LOG2E, dr = p.delta[stat];
-      for (int j = 0; j <= ib; ++j, ++gj) {
-        const bool diag = j == ib;
-        mbar_wait(sdp_full, gj & 1);
-        tc_fence_after();
-        const int cb = 64 * half;
-        uint32_t sv[64], dv[64];
-        tmem_ld_32x32b_x32(lane_base + TM_S + cb, *reinterpret_cast<uint32_t(*)[32]>(sv));
-        tmem_ld_32x32b_x32(lane_base + TM_S + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-        tmem_ld_32x32b_x32(lane_base + TM_DP + cb, *reinterpret_cast<uint32_t(*)[32]>(dv));
-        tmem_ld_32x32b_x32(lane_base + TM_DP + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tmem_free);
-        if (gj > 0) mbar_wait(mma2_done, (gj - 1) & 1);  // dS tile free
-#pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) {
-          float ds[8];
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            const int c = cb + 8 * c8 + jj;
-            float pp = ex2(fmaf(__uint_as_float(sv[8 * c8 + jj]), sl2, -lse2));
-            if (diag && c > r) pp = 0.f;  // key after query
-            ds[jj] = pp * (__uint_as_float(dv[8 * c8 + jj]) - dr);
-          }
-          put_row8(sDS, r, (cb >> 3) + c8, ds);
-        }
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(p_ready);
+      const int kvh = h / group;
+      const int tile0 = (b * p.H + h) * ntri + ib * (ib + 1) / 2;
+      for (int j = 0; j <= ib; ++j, ++g) {
+        const int st = g % STAGES;
+        mbar_wait(&empty[st], ((g / STAGES) & 1) ^ 1);
+        mbar_expect_tx(&full[st], L::STAGE);
+        uint8_t* sd = smem + st * L::STAGE;
+        for (int a = 0; a < 2; ++a) tma_load_2d(sd + a * ATOM, &tmDS, &full[st], 64 * a, (tile0 + j) * BLK);
+        for (int a = 0; a < HD / 64; ++a)
+          tma_load_2d(sd + L::DS_BYTES + a * ATOM, &tmQKV, &full[st], (p.H + kvh) * HD + 64 * a, b * p.T + j * BLK);
       }
-      mbar_wait(mma2_done, (gj - 1) & 1);
+    }
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t ID = umma_idesc_bf16(BLK, HD, true, true);  // dS (MN-major) . K (MN-major)
+    int g = 0, n = 0;
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
+      if (w >= n_items) continue;
+      int b, h, ib;
+      item(w, b, h, ib);
+      const int acc = n & 1;
+      mbar_wait(&acc_empty[acc], ((n >> 1) & 1) ^ 1);
       tc_fence_after();
-      if (half == 0)
-        store_grad_row<HD>(lane_base + TM_DQ, p.dqkv + (size_t)(b * p.T + t) * p.ld + h * HD, p.scale, p.rope_cs, p.T,
-                           t);
+      for (int j = 0; j <= ib; ++j, ++g) {
+        const int st = g % STAGES;
+        mbar_wait(&full[st], (g / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sd = smem_u32(smem + st * L::STAGE), sk = sd + L::DS_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BLK / 16; ++kk)
+          mma_bf16_ss(tmem + acc * HD, umma_desc_sw128(sd + kk * 2048, ATOM, 1024),
+                      umma_desc_sw128(sk + kk * 2048, ATOM, 1024), ID, (j > 0) || (kk > 0));
+        mma_commit(&empty[st]);
+      }
+      mma_commit(&acc_full[acc]);
+    }
+  } else if (warp >= 4) {
+    const int quad = warp - 4;
+    const int r = quad * 32 + lane;
+    int n = 0;
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
+      if (w >= n_items) continue;
+      int b, h, ib;
+      item(w, b, h, ib);
+      const int acc = n & 1;
+      mbar_wait(&acc_full[acc], (n >> 1) & 1);
+      tc_fence_after();
+      const int t = ib * BLK + r;
+      store_grad_row<HD>(tmem + ((uint32_t)(quad * 32) << 16) + acc * HD,
+                         p.dqkv + (size_t)(b * p.T + t) * p.ld + h * HD, p.scale, p.rope_cs, p.T, t);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(acc_free);
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
     }
   }
   __syncwarp();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 512);
+  if (warp == 2) tmem_dealloc(tmem, TMEM_COLS);
 }
 
 static int make_map(CUtensorMap* m, const void* ptr, long long ld, long long rows) {
+  // 2D bf16 [rows][ld], 64 x 128 boxes, SWIZZLE_128B
   auto encode = get_tensor_map_encoder();
   if (!encode) return set_error(SPX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
@@ -571,19 +554,24 @@ static int launch(const void* qkv, const void* dout, long long ld_o, const BwdPa
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          DkdvSmem<HD>::BYTES);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               DqSmem<HD>::BYTES);
+      e = cudaFuncSetAttribute(attn_bwd_dq_mma_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               DqmSmem<HD>::BYTES);
     if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc attr");
     set = true;
   }
   const int nqb = p.T / BLK;
+  CUtensorMap mds;  // dS^T tiles [B*H*tri(nqb)*128][128] bf16
+  const long long ntiles = (long long)p.B * p.H * (nqb * (nqb + 1) / 2);
+  rc = make_map(&mds, p.ds, BLK, ntiles * BLK);
+  if (rc) return rc;
   const int items_kv = nqb * p.Hkv * p.B, items_q = nqb * p.H * p.B;
   const int g1 = items_kv < num_sms() ? items_kv : num_sms(), g2 = items_q < num_sms() ? items_q : num_sms();
-  spx_launch_check(launch_k(attn_bwd_dkdv_tc_kernel<HD>, dim3(g1), dim3(THREADS), DkdvSmem<HD>::BYTES, s, mq, md, p));
+  spx_launch_check(launch_k(attn_bwd_dkdv_tc_kernel<HD>, dim3(g1), dim3(THREADS), DkdvSmem<HD>::BYTES, s, mq, md, mds, p));
   rc = check_launch("attn_bwd_dkdv_tc_kernel");
   if (rc) return rc;
-  spx_launch_check(launch_k(attn_bwd_dq_tc_kernel<HD>, dim3(g2), dim3(THREADS), DqSmem<HD>::BYTES, s, mq, md, p));
-  return check_launch("attn_bwd_dq_tc_kernel");
+  spx_launch_check(launch_k(attn_bwd_dq_mma_kernel<HD>, dim3(g2), dim3(DqmSmem<HD>::THREADS), DqmSmem<HD>::BYTES, s,
+                            mq, mds, p));
+  return check_launch("attn_bwd_dq_mma_kernel");
 }
 
 }  // namespace fab
@@ -592,7 +580,9 @@ static int launch(const void* qkv, const void* dout, long long ld_o, const BwdPa
 int attn_bwd_tcgen05(const void* qkv, const void* dout, const float* lse, const float* delta, void* dqkv, int64_t B,
                      int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv, int64_t ld_o, float scale,
                      const float* rope_cs, cudaStream_t s) {
-  fab::BwdParams p{reinterpret_cast<__nv_bfloat16*>(dqkv), lse, delta, rope_cs, (long long)ld_qkv,
+  // workspace: delta [BHT] | lse*log2e [BHT] | dS^T tiles (bf16)
+  __nv_bfloat16* ds = reinterpret_cast<__nv_bfloat16*>(const_cast<float*>(delta) + 2 * B * H * T);
+  fab::BwdParams p{reinterpret_cast<__nv_bfloat16*>(dqkv), lse, delta, rope_cs, ds, (long long)ld_qkv,
                    (int)B, (int)T, (int)H, (int)Hkv, scale};
   if (hd == 64) return fab::launch<64>(qkv, dout, ld_o, p, s);
   return fab::launch<128>(qkv, dout, ld_o, p, s);

@@ -29,6 +29,7 @@ SIGNATURES: dict[str, list] = {
     "spx_hop": [_I32, _P, _I32, _P, _I64, _P],
     "spx_gemm_bf16": [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _F, _P],
     "spx_attn_fwd": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P],
+    "spx_attn_bwd_ws_floats": [_I64, _I64, _I64, _I64],
     "spx_attn_bwd": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P, _P],
     "spx_gemm_set_workspace": [_P, _I64],
     "spx_gemm_f32_group": [_I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P],
@@ -48,6 +49,7 @@ SIGNATURES: dict[str, list] = {
     "spx_adamw": [_P, _P, _P, _P, _P, _I64, _I64, _F, _F, _F, _F, _F, _I64, _P, _P],
 }
 _RESTYPE = {"spx_last_error": ctypes.c_char_p, "spx_rmsnorm_ws_floats": ctypes.c_int64, "spx_launch_count": ctypes.c_int64,
+            "spx_attn_bwd_ws_floats": ctypes.c_int64,
             "spx_sumsq_ws_floats": ctypes.c_int64}
 
 EPI_BF16, EPI_BF16_RESID, EPI_F32, EPI_SWIGLU = 0, 1, 2, 3
@@ -220,8 +222,17 @@ def attn_fwd(qkv, o, lse, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, stream=None)
                                _stream(stream)), "spx_attn_fwd")
 
 
+def attn_bwd_ws_floats(B: int, H: int, T: int, hd: int) -> int:
+    """Workspace of spx_attn_bwd in floats (spx_attn_bwd_ws_floats)."""
+    return int(load().spx_attn_bwd_ws_floats(B, H, T, hd))
+
+
 def attn_bwd(qkv, o, dout, lse, delta_ws, dqkv, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, rope_cs=None,
              stream=None) -> None:
+    """delta_ws: fp32 workspace of at least attn_bwd_ws_floats(B, H, T) elements."""
+    need = attn_bwd_ws_floats(B, H, T, hd)
+    if delta_ws.numel() < need:
+        raise ValueError(f"attn_bwd: workspace needs {need} floats, got {delta_ws.numel()}")
     _check(load().spx_attn_bwd(_ptr(qkv), _ptr(o), _ptr(dout), _ptr(lse), _ptr(delta_ws), _ptr(dqkv), B, T, H, Hkv,
                                hd, ld_qkv, ld_o, float(scale), _ptr(rope_cs), _stream(stream)), "spx_attn_bwd")
 

@@ -58,7 +58,7 @@ def test_attention_fwd_bwd(B, T, H, Hkv, hd):
     lse = torch.empty(B, H, T, dtype=torch.float32, device=dev)
     native.attn_fwd(qkv, o, lse, B=B, T=T, H=H, Hkv=Hkv, hd=hd, ld_qkv=W, ld_o=H * hd, scale=scale)
     dqkv = torch.zeros_like(qkv)
-    delta = torch.empty(B, H, T, dtype=torch.float32, device=dev)
+    delta = torch.empty(native.attn_bwd_ws_floats(B, H, T, hd), dtype=torch.float32, device=dev)
     native.attn_bwd(qkv, o, do, lse, delta, dqkv, B=B, T=T, H=H, Hkv=Hkv, hd=hd, ld_qkv=W, ld_o=H * hd, scale=scale)
     torch.cuda.synchronize()
 
@@ -89,7 +89,7 @@ def test_attention_deterministic():
         lse = torch.empty(B, H, T, device=dev)
         native.attn_fwd(qkv, o, lse, B=B, T=T, H=H, Hkv=H, hd=hd, ld_qkv=W, ld_o=H * hd, scale=0.125)
         d = torch.zeros_like(qkv)
-        native.attn_bwd(qkv, o, do, lse, torch.empty_like(lse), d, B=B, T=T, H=H, Hkv=H, hd=hd, ld_qkv=W,
+        native.attn_bwd(qkv, o, do, lse, torch.empty(native.attn_bwd_ws_floats(B, H, T, hd), device=dev), d, B=B, T=T, H=H, Hkv=H, hd=hd, ld_qkv=W,
                         ld_o=H * hd, scale=0.125)
         outs.append((o, d))
     torch.cuda.synchronize()
@@ -262,7 +262,7 @@ def test_attention_bwd_inverse_rope():
     native.attn_fwd(qkv, o, lse, B=B, T=T, H=H, Hkv=H, hd=hd, ld_qkv=W, ld_o=H * hd, scale=0.125)
     plain = torch.zeros_like(qkv)
     fused = torch.zeros_like(qkv)
-    delta = torch.empty_like(lse)
+    delta = torch.empty(native.attn_bwd_ws_floats(B, H, T, hd), device=dev)
     kw = dict(B=B, T=T, H=H, Hkv=H, hd=hd, ld_qkv=W, ld_o=H * hd, scale=0.125)
     native.attn_bwd(qkv, o, do, lse, delta, plain, **kw)
     native.attn_bwd(qkv, o, do, lse, delta, fused, rope_cs=cs, **kw)

@@ -17,7 +17,7 @@ def bench(B, T, H, Hkv, hd, iters=20):
     o = torch.empty(B * T, H * hd, device="cuda", dtype=torch.bfloat16)
     lse = torch.empty(B, H, T, device="cuda")
     dq = torch.empty_like(qkv)
-    delta = torch.empty_like(lse)
+    delta = torch.empty(native.attn_bwd_ws_floats(B, H, T, hd), device="cuda")
     cs = rope_cos_sin(T, hd, 10000.0).cuda()
     sc = 1 / math.sqrt(hd)
     f = lambda: native.attn_fwd(qkv, o, lse, B=B, T=T, H=H, Hkv=Hkv, hd=hd, ld_qkv=W, ld_o=H * hd, scale=sc)  # noqa

@@ -11,7 +11,7 @@ do = torch.randn(B * T, H * hd, device="cuda").to(torch.bfloat16)
 o = torch.empty(B * T, H * hd, device="cuda", dtype=torch.bfloat16)
 lse = torch.empty(B, H, T, device="cuda")
 dq = torch.empty_like(qkv)
-delta = torch.empty_like(lse)
+delta = torch.empty(native.attn_bwd_ws_floats(B, H, T, hd), device="cuda")
 cs = rope_cos_sin(T, hd, 10000.0).cuda()
 for _ in range(3):
     native.attn_fwd(qkv, o, lse, B=B, T=T, H=H, Hkv=H, hd=hd, ld_qkv=W, ld_o=H * hd, scale=0.125)
