@@ -879,7 +879,7 @@ extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* 
   args.tma_store = tma_store_mode();
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int bn = (epilogue == EPI_SWIGLU || epilogue == EPI_F32 || epilogue == EPI_SWIGLU_BWD) ? 256
-                                                                                               : pick_bn((int)M, (int)N);
+                 : (use_pair((int)M) ? 256 : pick_bn((int)M, (int)N));  // CTA pairs need 256-col tiles
   if (epilogue == EPI_F32) pick_splits(args, bn);
   switch (epilogue) {
     case EPI_BF16:
