@@ -76,10 +76,14 @@ struct FwdSmem {
   static constexpr int ATOM = BM * 128;              // 128 rows x 128 B (64 bf16) swizzle atom block
   static constexpr int Q_BYTES = (HD / 64) * ATOM;   // same for one K or V tile (128 rows)
   static constexpr int P_BYTES = 2 * ATOM;           // 128 x 128 bf16
+  // K and V have separate rings: a K tile is released as soon as its S MMA completes, a V tile
+  // only after its PV MMA, so K prefetch runs ahead of the softmax
+  static constexpr int NK = HD == 64 ? 3 : 2;
+  static constexpr int NV = HD == 64 ? 3 : 2;
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + Q_BYTES;      // [2]
-  static constexpr int OFF_V = OFF_K + 2 * Q_BYTES;  // [2]
-  static constexpr int OFF_P = OFF_V + 2 * Q_BYTES;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;        // [NK]
+  static constexpr int OFF_V = OFF_K + NK * Q_BYTES;   // [NV]
+  static constexpr int OFF_P = OFF_V + NV * Q_BYTES;
   static constexpr int OFF_BAR = OFF_P + P_BYTES;
   // >= 116 KB: one CTA per SM (it owns all 512 TMEM columns)
   static constexpr int RAW = OFF_BAR + 256;
@@ -92,16 +96,18 @@ __global__ void __launch_bounds__(THREADS, 1)
   using L = FwdSmem<HD>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  constexpr int NK = L::NK, NV = L::NV;
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
-  uint64_t* k_full = bars + 2;   // [2]
-  uint64_t* v_full = bars + 4;   // [2]
-  uint64_t* kv_empty = bars + 6; // [2]
-  uint64_t* s_full = bars + 8;   // [2]
-  uint64_t* p_full = bars + 10;
-  uint64_t* pv_done = bars + 11;
-  uint64_t* o_free = bars + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* s_full = bars + 2;   // [2]
+  uint64_t* p_full = bars + 4;
+  uint64_t* pv_done = bars + 5;
+  uint64_t* o_free = bars + 6;
+  uint64_t* k_full = bars + 8;            // [NK]
+  uint64_t* k_empty = bars + 8 + NK;      // [NK]
+  uint64_t* v_full = bars + 8 + 2 * NK;   // [NV]
+  uint64_t* v_empty = bars + 8 + 2 * NK + NV;  // [NV]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * NK + 2 * NV);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = p.T / BM;
@@ -113,11 +119,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     tma_prefetch_desc(&tmQKV);
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
+    for (int i = 0; i < NK; ++i) {
       mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < NV; ++i) {
       mbar_init(&v_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-      mbar_init(&s_full[i], 1);
+      mbar_init(&v_empty[i], 1);
     }
     mbar_init(p_full, 4);
     mbar_init(pv_done, 1);
@@ -134,8 +143,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr uint32_t TM_O = 256;
 
   if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer ----------------
-    int g = 0, n = 0;  // global K/V block counter, item counter
+    // ---------------- TMA producer: Q and K ----------------
+    int g = 0, n = 0;  // global key-block counter, item counter
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
       if (w >= n_items) continue;
       const Item it = item_of(w, nqb, BH, p.H);
@@ -145,12 +154,24 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int a = 0; a < HD / 64; ++a)
         tma_load_2d(smem + L::OFF_Q + a * L::ATOM, &tmQKV, q_full, it.h * HD + 64 * a, row0 + it.qb * BM);
       for (int j = 0; j <= it.qb; ++j, ++g) {
-        const int s = g & 1;
-        mbar_wait(&kv_empty[s], ((g >> 1) & 1) ^ 1);
+        const int s = g % NK;
+        mbar_wait(&k_empty[s], ((g / NK) & 1) ^ 1);
         mbar_expect_tx(&k_full[s], L::Q_BYTES);
         for (int a = 0; a < HD / 64; ++a)
           tma_load_2d(smem + L::OFF_K + s * L::Q_BYTES + a * L::ATOM, &tmQKV, &k_full[s], (p.H + kvh) * HD + 64 * a,
                       row0 + j * BN);
+      }
+    }
+  } else if (warp == 3 && lane == 0) {
+    // ---------------- TMA producer: V ----------------
+    int g = 0;
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
+      if (w >= n_items) continue;
+      const Item it = item_of(w, nqb, BH, p.H);
+      const int row0 = it.b * p.T, kvh = it.h / group;
+      for (int j = 0; j <= it.qb; ++j, ++g) {
+        const int s = g % NV;
+        mbar_wait(&v_empty[s], ((g / NV) & 1) ^ 1);
         mbar_expect_tx(&v_full[s], L::Q_BYTES);
         for (int a = 0; a < HD / 64; ++a)
           tma_load_2d(smem + L::OFF_V + s * L::Q_BYTES + a * L::ATOM, &tmQKV, &v_full[s],
@@ -167,10 +188,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     // PV of block (global index gb, item-local j); the first PV of an item overwrites O, which
     // the softmax warps must have read out for the previous item
     auto issue_pv = [&](int gb, int j, int item_n) {
-      const int s = gb & 1;
+      const int s = gb % NV;
       if (j == 0) mbar_wait(o_free, (item_n & 1) ^ 1);
       mbar_wait(p_full, gb & 1);
-      mbar_wait(&v_full[s], (gb >> 1) & 1);
+      mbar_wait(&v_full[s], (gb / NV) & 1);
       tc_fence_after();
       const uint32_t sV = smem_u32(smem + L::OFF_V + s * L::Q_BYTES);
 #pragma unroll
@@ -180,7 +201,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         mma_bf16_ss(tmem + TM_O, ad, bd, IDESC_O, (j > 0) || (kk > 0));
       }
       mma_commit(pv_done);
-      mma_commit(&kv_empty[s]);
+      mma_commit(&v_empty[s]);
     };
     int pend_g = -1, pend_j = 0, pend_n = 0;  // the PV lagging one block behind S
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
@@ -188,10 +209,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       const Item it = item_of(w, nqb, BH, p.H);
       mbar_wait(q_full, n & 1);
       for (int j = 0; j <= it.qb; ++j, ++g) {
-        const int s = g & 1;
-        mbar_wait(&k_full[s], (g >> 1) & 1);
+        const int s = g & 1;  // S buffer
+        const int sk = g % NK;
+        mbar_wait(&k_full[sk], (g / NK) & 1);
         tc_fence_after();
-        const uint32_t sK = smem_u32(smem + L::OFF_K + s * L::Q_BYTES);
+        const uint32_t sK = smem_u32(smem + L::OFF_K + sk * L::Q_BYTES);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint64_t ad = umma_desc_sw128(sQ + (kk >> 2) * L::ATOM + (kk & 3) * 32, 16, 1024);
@@ -199,6 +221,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           mma_bf16_ss(tmem + s * BN, ad, bd, IDESC_S, kk > 0);
         }
         mma_commit(&s_full[s]);
+        mma_commit(&k_empty[sk]);
         if (j == it.qb) mma_commit(q_empty);  // last S of this item issued: Q reusable
         if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_n);
         pend_g = g;
@@ -289,7 +312,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // item epilogue: O / l -> bf16, LSE; then hand O's TMEM back to the MMA warp
       mbar_wait(pv_done, (g - 1) & 1);
       tc_fence_after();
-      const float inv = 1.f / l;
+      const float inv = __frcp_rn(l);
       const int t = it.qb * BM + r;
       __nv_bfloat16* orow = p.out + (size_t)(it.b * p.T + t) * p.ldo + it.h * HD;
 #pragma unroll
@@ -306,7 +329,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                          pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv));
         }
       }
-      p.lse[((size_t)it.b * p.H + it.h) * p.T + t] = (m + log2f(l)) / LOG2E;
+      p.lse[((size_t)it.b * p.H + it.h) * p.T + t] = (m + __log2f(l)) * (1.f / LOG2E);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_free);

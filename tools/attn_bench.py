@@ -42,5 +42,7 @@ def bench(B, T, H, Hkv, hd, iters=20):
 
 if __name__ == "__main__":
     bench(4, 1024, 16, 16, 64)
+    bench(1, 4096, 16, 16, 64)
+    bench(16, 1024, 16, 16, 64)
     bench(1, 4096, 16, 16, 128)
     bench(1, 4096, 32, 8, 128)
