@@ -144,6 +144,13 @@ def gemm_roofline(tr, peak_tflops: float, reps: int = 5) -> dict:
 
     calls = native.recorded_gemms()
     counts = tr.gemm_counts_per_step()
+    # DRAM bytes per launch of each shape from the committed ncu capture (profiles/), if present
+    traffic_by_shape = {}
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_gemm_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic_by_shape = {k: v["dram_bytes_per_launch"] for k, v in json.load(f)["per_shape"].items()}
+    t_bytes, t_count = 0.0, 0
     s = tr.stream
     total_flops, total_ms = 0.0, 0.0
     per = {}
@@ -165,9 +172,17 @@ def gemm_roofline(tr, peak_tflops: float, reps: int = 5) -> dict:
         total_flops += fl * count
         total_ms += ms * count
         per[str(key)] = {"launches_per_step": count, "us": round(ms * 1e3, 2), "tflops": round(fl / ms / 1e9, 1)}
+        if str(key) in traffic_by_shape:
+            per[str(key)]["dram_bytes"] = traffic_by_shape[str(key)]
+            t_bytes += traffic_by_shape[str(key)] * count
+            t_count += count
     ach = total_flops / total_ms / 1e9 if total_ms else 0.0
     return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak_tflops, "unit": "TFLOP/s",
-            "frac": round(ach / peak_tflops, 4), "traffic": None, "kernel": "spx gemm_bf16_kernel (tcgen05, all shapes)",
+            "frac": round(ach / peak_tflops, 4),
+            "traffic": round(t_bytes / t_count) if t_count else None,
+            "traffic_note": "dram read+write bytes per GEMM launch, launch-weighted over the iteration's shapes "
+                            "(ncu capture profiles/r01_gemm_traffic.json; per shape in per_shape)",
+            "kernel": "spx gemm_bf16_kernel (tcgen05, all shapes)",
             "gemm_ms_per_step": round(total_ms, 3), "per_shape": per}
 
 
