@@ -21,6 +21,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # per-node compute streams (executor.py)
 import statistics
 import subprocess
 import sys
@@ -186,16 +188,17 @@ def gemm_roofline(tr, peak_tflops: float, reps: int = 5) -> dict:
             "gemm_ms_per_step": round(total_ms, 3), "per_shape": per}
 
 
-def time_full_pp(args, rc_name, rank=0, world=1, local=0):
+def time_full_pp(args, rc_name, rank=0, world=1, local=0, variant="-full"):
     """Same protocol on the full sequential pipeline (dtfm_full, k=0) of the same model on the same
-    GPUs — the metric's "vs full PP" comparison.  Returns ms/step (max over ranks)."""
+    GPUs — the metric's "vs full PP" comparison — or on another executable baseline variant
+    ("-dtfmskip", "-notc2"; configs.VARIANTS).  Returns ms/step (max over ranks)."""
     import torch
 
     from paper_2502_19913_b200.configs import get_config
     from paper_2502_19913_b200.executor import Trainer
     from paper_2502_19913_b200.model import synthetic_tokens
 
-    rf = get_config(rc_name + "-full")
+    rf = get_config(rc_name + variant)
     tokens = synthetic_tokens(rf.model, rf.M, rf.b, rf.T, seed=1234)
     tr = Trainer(rf.schedule(), rf.topology(), rf.sim_config(), rf.model, rf.assignment, b=rf.b, T=rf.T,
                  rank=rank, world=world, device=local)
@@ -223,6 +226,16 @@ def time_full_pp(args, rc_name, rank=0, world=1, local=0):
     del tr
     torch.cuda.empty_cache()
     return ms, rf
+
+
+def time_baselines(args, rc_name, ms, tok, rank=0, world=1, local=0):
+    """Executed DT-FM-skip and SkipPipe-without-TC2 schedules next to SkipPipe."""
+    out = {}
+    for variant, label in (("-dtfmskip", "dtfm_skip"), ("-notc2", "skippipe_no_tc2")):
+        bms, rb = time_full_pp(args, rc_name, rank=rank, world=world, local=local, variant=variant)
+        out[label] = {"workload": rb.name, "ms_per_step": round(bms, 3), "tokens_per_s": round(tok / (bms / 1e3), 1),
+                      "skippipe_speedup": round(bms / ms, 4)}
+    return out
 
 
 def run_ours(args, rc):
@@ -280,6 +293,7 @@ def run_ours(args, rc):
         full = {"workload": rf.name, "kind": "dtfm_full (k=0, disjoint sequential pipelines)",
                 "ms_per_step": round(fms, 3), "tokens_per_s": round(tok / (fms / 1e3), 1),
                 "skippipe_speedup": round(fms / ms, 4)}
+    bl = time_baselines(args, rc.name, ms, tok) if args.baselines and rc.kind == "skippipe" else None
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
@@ -297,6 +311,7 @@ def run_ours(args, rc):
         "roofline": {**roof, "peak_kind": f"{peak_kind} burst bf16 (GEMMs timed alone)"},
         "cpu_baseline": cb,
         "vs_full_pp": full,
+        "baselines": bl,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -364,6 +379,7 @@ def run_ours_dist(args, rc):
     sm = t.clone()
     dist.all_reduce(sm)
     flops = rc.train_flops()
+    roof = gemm_roofline(tr, burst) if rank == 0 else None
     full = None
     if not args.no_full_pp and rc.kind == "skippipe":
         del tr
@@ -372,6 +388,8 @@ def run_ours_dist(args, rc):
         full = {"workload": rf.name, "kind": "dtfm_full (k=0, disjoint sequential pipelines)",
                 "ms_per_step": round(fms, 3), "tokens_per_s": round(tok / (fms / 1e3), 1),
                 "skippipe_speedup": round(fms / ms, 4)}
+    bl = time_baselines(args, rc.name, ms, tok, rank, world, local) if args.baselines and rc.kind == "skippipe" \
+        else None
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(tok / (ms / 1e3), 1), "unit": "tokens/s", "n_gpus": world,
@@ -388,7 +406,9 @@ def run_ours_dist(args, rc):
             "gpu_launches": int(launches.item()),
             "step_tflops": round(flops / (ms / 1e3) / 1e12, 1),
             "step_tensor_frac": round(flops / (ms / 1e3) / 1e12 / (sustained * world), 4),
+            "roofline": {**roof, "peak_kind": f"{peak_kind} burst bf16 (GEMMs timed alone, rank 0)"},
             "vs_full_pp": full,
+            "baselines": bl,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -405,6 +425,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full-pp", action="store_true", help="skip the full sequential pipeline comparison")
+    ap.add_argument("--baselines", action="store_true",
+                    help="also execute the DT-FM-skip and SkipPipe-without-TC2 schedules (same protocol)")
     args = ap.parse_args()
     from paper_2502_19913_b200.configs import get_config
 

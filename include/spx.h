@@ -140,6 +140,9 @@ int spx_xent_fwd_bwd(void* logits, const int32_t* targets, float* row_loss, int6
 
 /* ---- reductions / optimizer ---- */
 int spx_sum_f32(const float* x, int64_t n, float* out, float scale, int32_t accumulate, void* stream);
+/* dst += src, fp32, n elements (16-byte aligned): merges the gradient buffers of co-resident
+ * replicas of a stage before the replica all-reduce / optimizer. */
+int spx_add_f32(float* dst, const float* src, int64_t n, void* stream);
 int64_t spx_sumsq_ws_floats(void);
 int spx_sumsq(const float* x, int64_t n, float* ws, float* out, void* stream);
 /* scale[0] = min(1, max_norm / (sqrt(sum(sumsq[0:count])) + 1e-6))  (torch clip_grad_norm_) */

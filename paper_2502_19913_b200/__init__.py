@@ -7,4 +7,11 @@ Executor (drop-in for `simulate`, that runs real LLaMA stage comput
 Native compute path: libspx.so (csrc/, C-ABI in include/spx.h) bound by `native`.
 """
 
+import os as _os
+
+# The executor drives one compute stream (+ a weight-gradient side stream) per hosted logical node
+# plus hop streams; give the device enough hardware work queues that they do not falsely
+# serialise (effective only if set before the process creates its CUDA context).
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 __version__ = "0.1.0"

@@ -14,8 +14,8 @@ from dataclasses import dataclass, field
 
 from .allocation import StageAssignment
 from .model import ModelConfig, layer_split, model_config
-from .scheduler import Schedule, SchedulerConfig, path_length, schedule
-from .simulator import SimConfig
+from .scheduler import Schedule, SchedulerConfig, balance_replicas, path_length, schedule
+from .simulator import SimConfig, simulate
 from .topology import Topology, activation_bytes, b200_box
 
 PLAN_TFLOPS = 1000.0   # nominal sustained bf16 rate used only to derive planning times
@@ -34,6 +34,7 @@ class RunConfig:
     split: list[int] | None = None
     description: str = ""
     kind: str = "skippipe"          # or "full" (dtfm_full sequential pipelines)
+    balance_replicas: bool = True   # SkipPipe only: load-balance interchangeable replicas
     _cache: dict = field(default_factory=dict, repr=False)
 
     @property
@@ -86,8 +87,26 @@ class RunConfig:
 
                 self._cache["schedule"] = dtfm_full(self.topology(), self.s, msg_bytes=float(self.msg_bytes),
                                                     assignment=self.assignment)
+            elif self.kind == "dtfm_skip":
+                from .baselines import dtfm_skip
+
+                self._cache["schedule"] = dtfm_skip(self.topology(), self.assignment, self.scheduler_config())
+            elif self.kind == "no_tc2":
+                from .baselines import skippipe_no_tc2
+
+                self._cache["schedule"] = skippipe_no_tc2(self.topology(), self.assignment, self.scheduler_config())
             else:
-                self._cache["schedule"] = schedule(self.topology(), self.assignment, self.scheduler_config())
+                sch = schedule(self.topology(), self.assignment, self.scheduler_config())
+                if self.balance_replicas:
+                    # cost-neutral replica re-assignment on the uniform box, kept only when the
+                    # simulated iteration does not get slower (scheduler.balance_replicas)
+                    bal = balance_replicas(sch, self.topology(), self.assignment)
+                    if bal is not sch:
+                        sc = self.sim_config()
+                        if simulate(bal, self.topology(), sc).iteration_makespan <= \
+                                simulate(sch, self.topology(), sc).iteration_makespan:
+                            sch = bal
+                self._cache["schedule"] = sch
         return self._cache["schedule"]
 
     def path_len(self) -> int:
@@ -107,10 +126,17 @@ class RunConfig:
         return total
 
 
+# executable baseline variants of a config
+VARIANTS = {"-full": "full", "-dtfmskip": "dtfm_skip", "-notc2": "no_tc2"}
+
+
 def get_config(name: str, **over) -> RunConfig:
-    """C1..C5 (+ "-full" variants with k=0 disjoint sequential pipelines)."""
-    base = name.replace("-full", "")
-    full = name.endswith("-full")
+    """C1..C5, plus baseline variants: "-full" (DT-FM, k=0 disjoint sequential pipelines),
+    "-dtfmskip" (DT-FM-skip: topology-blind skip paths, no TC2) and "-notc2" (SkipPipe without the
+    throughput phase)."""
+    suffix = next((v for v in VARIANTS if name.endswith(v)), "")
+    base = name[: len(name) - len(suffix)] if suffix else name
+    full = suffix == "-full"
     if base == "C1":
         rc = RunConfig("C1", model_config("llama-50m"), [2, 2, 2, 2], 25, 2, 2, 256, 8,
                        description="tiny LLaMA SkipPipe iteration (4 stages x 2 replicas, 25% skip)")
@@ -130,6 +156,8 @@ def get_config(name: str, **over) -> RunConfig:
         raise KeyError(name)
     if full:
         rc.kind, rc.k, rc.name = "full", 0, rc.name + "-full"
+    elif suffix:
+        rc.kind, rc.name = VARIANTS[suffix], rc.name + suffix
     for k_, v in over.items():
         setattr(rc, k_, v)
     return rc

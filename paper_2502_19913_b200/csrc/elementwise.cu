@@ -404,6 +404,20 @@ __global__ void __launch_bounds__(XE_THREADS) xent_kernel(__nv_bfloat16* __restr
 
 // ---------------------------------------------------------------- reductions
 // out[0] (+)= scale * sum(x[0:n])   (single CTA, fixed order)
+// dst += src (fp32, float4 vectors when aligned): merges co-resident replicas' gradient buffers
+__global__ void add_f32_kernel(float* __restrict__ dst, const float* __restrict__ src, long long n) {
+  pdl_wait();
+  const long long n4 = n / 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 a = reinterpret_cast<float4*>(dst)[i];
+    const float4 b = reinterpret_cast<const float4*>(src)[i];
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    reinterpret_cast<float4*>(dst)[i] = a;
+  }
+  for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] += src[i];
+}
+
 __global__ void sum_kernel(const float* __restrict__ x, long long n, float* __restrict__ out, float scale,
                            int accumulate) {
   pdl_wait();
@@ -590,6 +604,16 @@ extern "C" int spx_xent_fwd_bwd(void* logits, const int32_t* targets, float* row
 extern "C" int spx_sum_f32(const float* x, int64_t n, float* out, float scale, int32_t accumulate, void* stream) {
   spx_launch_check(launch_k(sum_kernel, dim3(1), dim3(1024), 0, SPX_S, x, n, out, scale, accumulate));
   return check_launch("sum_kernel");
+}
+
+extern "C" int spx_add_f32(float* dst, const float* src, int64_t n, void* stream) {
+  if (n < 0) return set_error(SPX_ERR_ARG, "add_f32: negative size");
+  if (n == 0) return SPX_OK;
+  if (((uintptr_t)dst | (uintptr_t)src) & 15) return set_error(SPX_ERR_ARG, "add_f32: 16-byte aligned buffers required");
+  const long long want = (n / 4 + 255) / 256;
+  const int grid = (int)(want < 4LL * num_sms() ? (want > 0 ? want : 1) : 4LL * num_sms());
+  spx_launch_check(launch_k(add_f32_kernel, dim3(grid), dim3(256), 0, SPX_S, dst, src, (long long)n));
+  return check_launch("add_f32_kernel");
 }
 
 extern "C" int64_t spx_sumsq_ws_floats(void) { return SUMSQ_BLOCKS; }

@@ -91,6 +91,23 @@ class ParamSet:
         return self.lay.view(self.g, name)
 
 
+class NodeParams:
+    """A logical node's handle on its stage's parameter set with a private gradient buffer.
+
+    With one compute stream per logical node, co-resident replicas of a stage run concurrently, so
+    they accumulate into separate buffers; the optimizer adds them in node order (deterministic).
+    The first hosted node of a stage uses the parameter set's own gradient buffer."""
+
+    def __init__(self, ps: ParamSet, g: torch.Tensor):
+        self.ps, self.g, self.lay = ps, g, ps.lay
+
+    def w(self, name):
+        return self.ps.w(name)
+
+    def gv(self, name):
+        return self.lay.view(self.g, name)
+
+
 class LayerActs:
     """Saved activations of one decoder layer for one (node, slot)."""
 
@@ -396,7 +413,27 @@ class Trainer:
                 for j in range(self.n_slots[v]):
                     self.slots[(v, j)] = SlotBuffers(cfg, self.split[self.node_stage[v]], self.node_stage[v] == 0,
                                                      self.n, b, self.T, self.dev)
+            # One compute stream (+ weight-gradient side stream), scratch set and gradient buffer per
+            # hosted logical node: a node's ops wait only for their own inputs and concurrent nodes
+            # fill each other's kernel tails.  Default on a single GPU (the iteration is throughput
+            # bound: 289 vs 310 ms at C2).  Across GPUs the simulator's global order on one stream
+            # is faster (concurrency slows the pipeline's critical ops: 4 GPUs 124 vs 116 ms), so
+            # there every op of a rank is serialised on one stream.  SPX_NODE_STREAMS=0/1 forces.
+            env = os.environ.get("SPX_NODE_STREAMS")
+            self.node_streams = (world == 1) if env is None else env != "0"
+            side_on = os.environ.get("SPX_WGRAD_SIDE", "1") != "0"
             self.scratch = Scratch(cfg, self.n, b, self.T, self.dev, with_head=0 in self.my_stages)
+            self.nparams: dict[int, NodeParams] = {}
+            self.extra_grads: dict[int, list] = {st: [] for st in self.my_stages}
+            for v in self.my_nodes:
+                st = self.node_stage[v]
+                ps = self.psets[st]
+                if not self.node_streams or not any(self.nparams[u].ps is ps for u in self.nparams):
+                    self.nparams[v] = NodeParams(ps, ps.g)
+                else:
+                    g = torch.zeros_like(ps.g)
+                    self.extra_grads[st].append(g)
+                    self.nparams[v] = NodeParams(ps, g)
             # No split-K workspace: the weight-gradient GEMMs run on a side stream next to the
             # data-gradient chain, which uses the SMs a wgrad leaves idle; split-K's partial
             # traffic costs more SM time than it saves there (spx_gemm_set_workspace, spx.h).
@@ -404,9 +441,22 @@ class Trainer:
             self.stream = torch.cuda.Stream(device=self.dev)
             self.recv_stream = torch.cuda.Stream(device=self.dev)
             self.send_stream = torch.cuda.Stream(device=self.dev)
-            # weight-gradient GEMMs run here, forked/joined per layer inside the B graphs
-            self.side_stream = torch.cuda.Stream(device=self.dev) if os.environ.get("SPX_WGRAD_SIDE", "1") != "0" \
-                else None
+            # weight-gradient GEMMs run on a side stream, forked/joined per layer inside the B graphs
+            self.side_stream = torch.cuda.Stream(device=self.dev) if side_on else None
+            if self.node_streams:
+                self.nstream = {v: torch.cuda.Stream(device=self.dev) for v in self.my_nodes}
+                self.nside = {v: (torch.cuda.Stream(device=self.dev) if side_on else None) for v in self.my_nodes}
+                self.nscratch = {v: Scratch(cfg, self.n, b, self.T, self.dev, with_head=self.node_stage[v] == 0)
+                                 for v in self.my_nodes}
+                # hop streams per node too: a send / receive never queues behind another node's
+                self.nsend = {v: torch.cuda.Stream(device=self.dev) for v in self.my_nodes}
+                self.nrecv = {v: torch.cuda.Stream(device=self.dev) for v in self.my_nodes}
+            else:
+                self.nstream = {v: self.stream for v in self.my_nodes}
+                self.nside = {v: self.side_stream for v in self.my_nodes}
+                self.nscratch = {v: self.scratch for v in self.my_nodes}
+                self.nsend = {v: self.send_stream for v in self.my_nodes}
+                self.nrecv = {v: self.recv_stream for v in self.my_nodes}
             self.prog = StageProgram(cfg, self.n, b, self.T, self.M)
             self.mb_loss = torch.zeros(self.M, dtype=F32, device=self.dev)
             self._sumsq = torch.zeros(assignment.s, dtype=F32, device=self.dev)
@@ -457,15 +507,16 @@ class Trainer:
 
     # ---- graph capture ----
     def _run_op(self, kind: str, v: int, slot: int, s):
-        ps = self.psets[self.node_stage[v]]
+        ps = self.nparams[v]
         sb = self.slots[(v, slot)]
+        sc = self.nscratch[v]
         origin = self.node_stage[v] == 0
         if kind == F:
-            self.prog.fwd(ps, sb, self.scratch, origin, s)
+            self.prog.fwd(ps, sb, sc, origin, s)
             return sb.xs[-1]
         if kind == L:
-            return self.prog.loss(ps, sb, self.scratch, s)
-        return self.prog.bwd(ps, sb, self.scratch, origin, s, self.side_stream)
+            return self.prog.loss(ps, sb, sc, s)
+        return self.prog.bwd(ps, sb, sc, origin, s, self.nside[v])
 
     def _key(self, op):
         return (op.kind, op.node, self.slot_of[(op.agent, op.node)])
@@ -476,10 +527,11 @@ class Trainer:
             for key in keys:
                 kind, v, slot = key
                 g = torch.cuda.CUDAGraph()
-                self.stream.wait_stream(torch.cuda.current_stream())
+                cs = self.nstream[v]
+                cs.wait_stream(torch.cuda.current_stream())
                 n0 = native.launches()
                 native.take_gemm_log()
-                with torch.cuda.graph(g, stream=self.stream):
+                with torch.cuda.graph(g, stream=cs):
                     out = self._run_op(kind, v, slot, torch.cuda.current_stream())
                 self._graph_launches[key] = native.launches() - n0
                 self._graph_gemms[key] = native.take_gemm_log()
@@ -514,7 +566,11 @@ class Trainer:
 
     # ---- one iteration ----
     def step(self, tokens, *, timing: bool = False) -> dict:
-        """One synchronous training iteration over the M microbatches; returns the loss."""
+        """One synchronous training iteration over the M microbatches; returns the loss.
+
+        Ops are issued in the simulator's global order, each on its node's stream.  A node's op
+        waits only for its own inputs: an NCCL receive (remote hop) or the producer's completion
+        event followed by a D2D copy on the consumer's stream (local hop between nodes)."""
         host = tokens if isinstance(tokens, dict) else self._stage_inputs(tokens)
         self.step_count += 1
         s = self.stream
@@ -523,49 +579,64 @@ class Trainer:
         t_iter1 = torch.cuda.Event(enable_timing=True)
         pending: dict = {}
         sends: list = []
+        streams = list(dict.fromkeys(self.nstream[v] for v in self.my_nodes))
         with torch.cuda.device(self.dev):
             s.wait_stream(torch.cuda.current_stream(self.dev))
             t_iter0.record(s)
             with torch.cuda.stream(s):
                 for ps in self.psets.values():
                     ps.g.zero_()
+                for gl in self.extra_grads.values():
+                    for g in gl:
+                        g.zero_()
                 self.mb_loss.zero_()
+            for cs in streams:
+                if cs is not s:
+                    cs.wait_stream(s)
             executed = []
             for idx, op in enumerate(self.ops):
                 v, mb = op.node, op.mb
                 mine = self.placement[v] == self.rank
+                out = None
                 if mine:
+                    sv = self.nstream[v]
                     key = self._key(op)
                     sb = self.slots[(v, key[2])]
                     if op.kind == F and op.pos == 0:
-                        _h2d(sb.ids, host["ids"][mb], s)
+                        _h2d(sb.ids, host["ids"][mb], sv)
                     if op.kind == L:
-                        _h2d(sb.targets, host["tgt"][mb], s)
+                        _h2d(sb.targets, host["tgt"][mb], sv)
                     if op.kind == B and op.pos == 0:
-                        _h2d(sb.perm, host["perm"][mb], s)
-                        _h2d(sb.seg_start, host["seg_start"][mb], s)
-                        _h2d(sb.seg_id, host["seg_id"][mb], s)
-                        _h2d(sb.n_seg, host["n_seg"][mb], s)
+                        _h2d(sb.perm, host["perm"][mb], sv)
+                        _h2d(sb.seg_start, host["seg_start"][mb], sv)
+                        _h2d(sb.seg_id, host["seg_id"][mb], sv)
+                        _h2d(sb.n_seg, host["n_seg"][mb], sv)
                     w = pending.pop((op.kind, v, op.agent, op.wave), None)
                     if w is not None:
-                        with torch.cuda.stream(s):
-                            w.wait()           # input arrived from another rank
+                        if w[0] == "nccl":
+                            with torch.cuda.stream(sv):
+                                w[1].wait()        # input arrived from another rank
+                        else:                      # local hop from another node's stream
+                            _, src, src_ev, dst = w
+                            sv.wait_event(src_ev)
+                            native.hop(dst, self.dev.index, src, self.dev.index, src.numel() * src.element_size(),
+                                       stream=sv)
                     if timing:
                         e0 = torch.cuda.Event(enable_timing=True)
-                        e0.record(s)
+                        e0.record(sv)
                     if self.use_graphs:
-                        with torch.cuda.stream(s):
+                        with torch.cuda.stream(sv):
                             self._graphs[key].replay()   # replays on the current stream
                         out = self._outs[key]
                     else:
-                        out = self._run_op(op.kind, v, key[2], s)
+                        out = self._run_op(op.kind, v, key[2], sv)
                     if timing:
                         e1 = torch.cuda.Event(enable_timing=True)
-                        e1.record(s)
+                        e1.record(sv)
                         ev[idx] = (e0, e1)
                     executed.append((idx, op.kind, v, op.agent, op.wave))
                     if op.kind == L:
-                        with torch.cuda.stream(s):
+                        with torch.cuda.stream(sv):
                             self.mb_loss[mb:mb + 1].copy_(sb.loss, non_blocking=True)
                 hop = self.hops[idx]
                 if hop is None:
@@ -574,7 +645,18 @@ class Trainer:
                 dst_mine = dst_rank == self.rank
                 if mine and dst_mine:
                     buf = self._dst_buffer(op, nv, name)
-                    native.hop(buf, self.dev.index, out, self.dev.index, out.numel() * out.element_size(), stream=s)
+                    sv = self.nstream[v]
+                    if self.nstream[nv] is sv:
+                        native.hop(buf, self.dev.index, out, self.dev.index, out.numel() * out.element_size(),
+                                   stream=sv)
+                    else:
+                        # copied on the consumer's stream right before the consumer op: the
+                        # destination slot is then free (the consumer node's earlier ops are ahead
+                        # of it on that stream) and the source is slot-owned until the agent's next
+                        # wave, which causally follows the consumer
+                        done = torch.cuda.Event()
+                        done.record(sv)
+                        pending[(consumer, nv, op.agent, op.wave)] = ("local", out, done, buf)
                 elif mine:
                     import torch.distributed as dist
 
@@ -582,26 +664,31 @@ class Trainer:
                     # rewritten only by this agent's next wave, which causally follows this send's
                     # completion: drain it on the send stream without stalling compute
                     ev_out = torch.cuda.Event()
-                    ev_out.record(s)
-                    self.send_stream.wait_event(ev_out)
-                    with torch.cuda.stream(self.send_stream):
-                        sends.append(dist.isend(out, dst_rank, group=self._pair[dst_rank]))
+                    ev_out.record(self.nstream[v])
+                    ss = self.nsend[v]
+                    ss.wait_event(ev_out)
+                    with torch.cuda.stream(ss):
+                        sends.append((dist.isend(out, dst_rank, group=self._pair[dst_rank]), ss))
                 elif dst_mine:
                     import torch.distributed as dist
 
                     buf = self._dst_buffer(op, nv, name)
-                    # the destination slot was last read by this agent's previous wave, which is
-                    # earlier in the global order: let the receive start only after the compute
-                    # enqueued so far on this rank
-                    self.recv_stream.wait_stream(s)
-                    with torch.cuda.stream(self.recv_stream):
+                    # the destination slot was last read by this agent's previous wave on the
+                    # consumer node, whose ops so far are all on that node's stream
+                    rs = self.nrecv[nv]
+                    rs.wait_stream(self.nstream[nv])
+                    with torch.cuda.stream(rs):
                         w = dist.irecv(buf, self.placement[v], group=self._pair[self.placement[v]])
-                    pending[(consumer, nv, op.agent, op.wave)] = w
+                    pending[(consumer, nv, op.agent, op.wave)] = ("nccl", w)
+            for cs in streams:
+                if cs is not s:
+                    s.wait_stream(cs)
             if sends:
                 with torch.cuda.stream(s):
-                    for w in sends:
+                    for w, _ in sends:
                         w.wait()
-                s.wait_stream(self.send_stream)
+                for ss in dict.fromkeys(ss for _, ss in sends):
+                    s.wait_stream(ss)
             self.optimizer_step()
             t_iter1.record(s)
             torch.cuda.current_stream(self.dev).wait_stream(s)
@@ -622,7 +709,7 @@ class Trainer:
         """libspx kernel launches in one iteration on this rank (graph contents + optimizer)."""
         if not self.use_graphs:
             raise ValidationError("launch accounting needs use_graphs=True")
-        opt = 2 * len(self.psets) + 1 + len(self.psets)
+        opt = 2 * len(self.psets) + 1 + len(self.psets) + sum(len(gl) for gl in self.extra_grads.values())
         return sum(self._graph_launches[self._key(op)] for op in self.ops
                    if self.placement[op.node] == self.rank) + opt
 
@@ -641,6 +728,9 @@ class Trainer:
         o = self.optim
         s = self.stream
         with torch.cuda.stream(s):
+            for st, gl in self.extra_grads.items():  # co-resident replicas, in node order
+                for g in gl:
+                    native.add_f32(self.psets[st].g, g, self.psets[st].lay.numel, stream=s)
             if self.world > 1:
                 import torch.distributed as dist
 

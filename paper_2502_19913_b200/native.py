@@ -43,6 +43,7 @@ SIGNATURES: dict[str, list] = {
     "spx_embed_bwd": [_P, _P, _P, _P, _I64, _P, _P, _I64, _P],
     "spx_xent_fwd_bwd": [_P, _P, _P, _I64, _I64, _I64, _F, _P],
     "spx_sum_f32": [_P, _I64, _P, _F, _I32, _P],
+    "spx_add_f32": [_P, _P, _I64, _P],
     "spx_sumsq_ws_floats": [],
     "spx_sumsq": [_P, _I64, _P, _P, _P],
     "spx_clip_scale": [_P, _I32, _F, _P, _P, _P],
@@ -290,6 +291,11 @@ def embed_segments(ids) -> tuple:
 def xent_fwd_bwd(logits, targets, row_loss, *, n, V, ld, scale, stream=None) -> None:
     _check(load().spx_xent_fwd_bwd(_ptr(logits), _ptr(targets), _ptr(row_loss), n, V, ld, float(scale),
                                    _stream(stream)), "spx_xent_fwd_bwd")
+
+
+def add_f32(dst, src, n, *, stream=None) -> None:
+    """dst[:n] += src[:n] (fp32)."""
+    _check(load().spx_add_f32(_ptr(dst), _ptr(src), n, _stream(stream)), "spx_add_f32")
 
 
 def sum_f32(x, n, out, *, scale=1.0, accumulate=False, stream=None) -> None:

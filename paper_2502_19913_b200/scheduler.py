@@ -643,3 +643,64 @@ def schedule(topology: Topology, assignment: StageAssignment, config: SchedulerC
     pool = find_candidates(topology, assignment, None, config, pl)
     node, resolved = resolve_throughput(pool, topology, assignment, config, pl)
     return Schedule(config, agents, dict(node.paths), sorted(node.constraints), node.cost, resolved)
+
+
+def interchangeable_replicas(topology: Topology, assignment: StageAssignment) -> bool:
+    """True when, within every stage, the nodes have the same compute times and the same link costs
+    to every other node (a uniform box such as one NVSwitch domain): a path's cost then does not
+    depend on which replica of a stage it visits."""
+    lat, bw = topology.latency_ms, topology.bandwidth_bytes_per_ms
+    n = topology.n
+    for st in range(assignment.s):
+        mem = assignment.stage_nodes(st)
+        a = mem[0]
+        for b in mem[1:]:
+            if topology.compute_fwd_ms[a] != topology.compute_fwd_ms[b]:
+                return False
+            if topology.compute_bwd_ms(a) != topology.compute_bwd_ms(b):
+                return False
+            for x in range(n):
+                if x in (a, b):
+                    continue
+                if lat[a][x] != lat[b][x] or bw[a][x] != bw[b][x] or lat[x][a] != lat[x][b] or bw[x][a] != bw[x][b]:
+                    return False
+            if lat[a][b] != lat[b][a] or bw[a][b] != bw[b][a]:
+                return False
+    return True
+
+
+def balance_replicas(sch: Schedule, topology: Topology, assignment: StageAssignment) -> Schedule:
+    """Cost-neutral replica re-assignment for interchangeable replicas (B200 extension).
+
+    On a uniform topology A*'s ties go to the lowest node ids, so some replicas carry two paths
+    and others none (C2: node 7 never visited) -- harmless in the first-wave plan, but every wave
+    repeats it, so per-node work is uneven across the iteration.  Keeping each path's stage
+    sequence, the replica of every non-origin visit is re-chosen greedily (agents in id order)
+    as the least-loaded one, ties to the lower id.  Applied only when the replicas are
+    interchangeable (path costs unchanged) and the re-timed plan keeps CC3 and TC1; otherwise the
+    schedule is returned unchanged.  First-wave collisions (TC2) are left to the node queues; the
+    caller compares simulated iteration makespans before adopting the result."""
+    if not interchangeable_replicas(topology, assignment):
+        return sch
+    node_stage = assignment.node_stage()
+    load = [0] * topology.n
+    new_paths = {}
+    for a in sorted(sch.paths):
+        p = sch.paths[a]
+        nodes = [p.nodes[0]]
+        for v in p.nodes[1:]:
+            st = node_stage[v]
+            choice = min(assignment.stage_nodes(st), key=lambda u: (load[u], u))
+            nodes.append(choice)
+        for v in set(nodes[1:]):
+            load[v] += 1
+        new_paths[a] = time_fixed_path(a, nodes, topology, assignment, sch.config.msg_bytes)
+    cost = max(pp.e2e for pp in new_paths.values())
+    if cost > sch.cost_ms + 1e-9:
+        return sch
+    cand = SearchNode(frozenset(), new_paths, cost)
+    if any(not isinstance(c, Collision)
+           for c in detect_conflicts(cand, topology, assignment, topology.mem_capacity, k=sch.config.k)):
+        return sch
+    return Schedule(sch.config, sch.agents, new_paths, sch.constraints, cost, sch.resolved, kind=sch.kind)
+

@@ -222,3 +222,47 @@ def test_path_length_validation():
     assert S.path_length(6, 100 / 3) == 4
     with pytest.raises(ValidationError):
         S.path_length(8, 100 / 3)
+
+
+def test_balance_replicas_cost_neutral_and_spreads_load():
+    """B200 extension: on the uniform box the replica of each visit is re-chosen by load; stage
+    sequences, e2e costs, CC3 and TC1 are unchanged, no replica is left idle while another of the
+    same stage carries two paths, and the simulated iteration is not slower."""
+    from paper_2502_19913_b200.configs import get_config
+    from paper_2502_19913_b200.scheduler import (balance_replicas, interchangeable_replicas, node_path_counts,
+                                                 schedule, stage_visit_counts)
+    from paper_2502_19913_b200.simulator import simulate
+
+    rc = get_config("C2")
+    topo, asg = rc.topology(), rc.assignment
+    assert interchangeable_replicas(topo, asg)
+    raw = schedule(topo, asg, rc.scheduler_config())
+    bal = balance_replicas(raw, topo, asg)
+    assert bal is not raw
+    for a in raw.paths:
+        assert raw.paths[a].stages == bal.paths[a].stages
+        assert abs(raw.paths[a].e2e - bal.paths[a].e2e) < 1e-9 or bal.paths[a].e2e <= raw.paths[a].e2e
+    assert stage_visit_counts(raw.paths, asg) == stage_visit_counts(bal.paths, asg)
+    counts = node_path_counts(bal.paths, topo.n)
+    assert max(counts) <= topo.mem_capacity
+    for st in range(asg.s):
+        c = [counts[v] for v in asg.stage_nodes(st)]
+        assert max(c) - min(c) <= 1
+    sc = rc.sim_config()
+    assert simulate(bal, topo, sc).iteration_makespan <= simulate(raw, topo, sc).iteration_makespan
+    assert rc.schedule().path_nodes() == bal.path_nodes()   # what the executor runs
+
+
+def test_balance_replicas_skips_heterogeneous_topologies():
+    from paper_2502_19913_b200.configs import get_config
+    from paper_2502_19913_b200.scheduler import balance_replicas, interchangeable_replicas, schedule
+    from paper_2502_19913_b200.topology import Topology
+
+    rc = get_config("C2")
+    t = rc.topology()
+    fwd = list(t.compute_fwd_ms)
+    fwd[7] *= 1.5
+    het = Topology(t.n, t.latency_ms, t.bandwidth_bytes_per_ms, fwd, bwd_ratio=t.bwd_ratio, mem_capacity=t.mem_capacity)
+    assert not interchangeable_replicas(het, rc.assignment)
+    raw = schedule(het, rc.assignment, rc.scheduler_config())
+    assert balance_replicas(raw, het, rc.assignment) is raw
