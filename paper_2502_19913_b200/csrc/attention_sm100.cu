@@ -75,7 +75,6 @@ template <int HD>
 struct FwdSmem {
   static constexpr int ATOM = BM * 128;              // 128 rows x 128 B (64 bf16) swizzle atom block
   static constexpr int Q_BYTES = (HD / 64) * ATOM;   // same for one K or V tile (128 rows)
-  static constexpr int P_BYTES = 2 * ATOM;           // 128 x 128 bf16
   // K and V have separate rings: a K tile is released as soon as its S MMA completes, a V tile
   // only after its PV MMA, so K prefetch runs ahead of the softmax
   static constexpr int NK = HD == 64 ? 3 : 2;
@@ -83,8 +82,7 @@ struct FwdSmem {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;        // [NK]
   static constexpr int OFF_V = OFF_K + NK * Q_BYTES;   // [NV]
-  static constexpr int OFF_P = OFF_V + NV * Q_BYTES;
-  static constexpr int OFF_BAR = OFF_P + P_BYTES;
+  static constexpr int OFF_BAR = OFF_V + NV * Q_BYTES;
   // >= 116 KB: one CTA per SM (it owns all 512 TMEM columns)
   static constexpr int RAW = OFF_BAR + 256;
   static constexpr int BYTES = RAW > 116 * 1024 ? RAW : 116 * 1024;
@@ -100,14 +98,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
   uint64_t* s_full = bars + 2;   // [2]
-  uint64_t* p_full = bars + 4;
-  uint64_t* pv_done = bars + 5;
+  uint64_t* p_full = bars + 4;   // [2] by block parity (P is double-buffered in TMEM)
   uint64_t* o_free = bars + 6;
+  uint64_t* pv_done = bars + 14 + 2 * NK + 2 * NV;  // [2] by block parity
   uint64_t* k_full = bars + 8;            // [NK]
   uint64_t* k_empty = bars + 8 + NK;      // [NK]
   uint64_t* v_full = bars + 8 + 2 * NK;   // [NV]
   uint64_t* v_empty = bars + 8 + 2 * NK + NV;  // [NV]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * NK + 2 * NV);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * NK + 2 * NV);  // (+ 6 words spare)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = p.T / BM;
@@ -128,8 +126,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
     }
-    mbar_init(p_full, 4);
-    mbar_init(pv_done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_done[i], 1);
+    }
     mbar_init(o_free, 4);
     fence_barrier_init();
     fence_proxy_async();
@@ -140,7 +140,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // upstream grid complete before any dependent global access
-  constexpr uint32_t TM_O = 256;
+  // TMEM: S0 [0,128), S1 [128,256), O [256, 256+HD), P double buffer [384,448), [448,512): P
+  // (bf16 pairs, row = query) is the A operand of the PV MMA straight from TMEM, so it never
+  // touches shared memory (the kernel is otherwise shared-memory-bandwidth bound at hd=64)
+  constexpr uint32_t TM_O = 256, TM_P = 384;
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer: Q and K ----------------
@@ -183,24 +186,22 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr uint32_t IDESC_S = umma_idesc_bf16(BM, BN, false, false);
     constexpr uint32_t IDESC_O = umma_idesc_bf16(BM, HD, false, true);
     const uint32_t sQ = smem_u32(smem + L::OFF_Q);
-    const uint32_t sP = smem_u32(smem + L::OFF_P);
     int g = 0, n = 0;
     // PV of block (global index gb, item-local j); the first PV of an item overwrites O, which
     // the softmax warps must have read out for the previous item
     auto issue_pv = [&](int gb, int j, int item_n) {
       const int s = gb % NV;
       if (j == 0) mbar_wait(o_free, (item_n & 1) ^ 1);
-      mbar_wait(p_full, gb & 1);
+      mbar_wait(&p_full[gb & 1], (gb >> 1) & 1);
       mbar_wait(&v_full[s], (gb / NV) & 1);
       tc_fence_after();
       const uint32_t sV = smem_u32(smem + L::OFF_V + s * L::Q_BYTES);
 #pragma unroll
       for (int kk = 0; kk < BN / 16; ++kk) {
-        const uint64_t ad = umma_desc_sw128(sP + (kk >> 2) * L::ATOM + (kk & 3) * 32, 16, 1024);
         const uint64_t bd = umma_desc_sw128(sV + kk * 2048, L::ATOM, 1024);
-        mma_bf16_ss(tmem + TM_O, ad, bd, IDESC_O, (j > 0) || (kk > 0));
+        mma_bf16_ts(tmem + TM_O, tmem + TM_P + (gb & 1) * 64 + kk * 8, bd, IDESC_O, (j > 0) || (kk > 0));
       }
-      mma_commit(pv_done);
+      mma_commit(&pv_done[gb & 1]);
       mma_commit(&v_empty[s]);
     };
     int pend_g = -1, pend_j = 0, pend_n = 0;  // the PV lagging one block behind S
@@ -236,7 +237,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int r = q * 32 + lane;  // row within the block
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     const float sl2 = p.scale * LOG2E;
-    uint8_t* sP = smem + L::OFF_P;
     int g = 0;
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
       if (w >= n_items) continue;
@@ -277,11 +277,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           sk[i & 7] += x[i];
         }
         l = l * alpha + (((sk[0] + sk[1]) + (sk[2] + sk[3])) + ((sk[4] + sk[5]) + (sk[6] + sk[7])));
-        if (j > 0) {
-          mbar_wait(pv_done, (g - 1) & 1);  // O stable and the P tile free
+        // rescale O rows whose max grew (warp-uniform decision; tcgen05.ld/st are warp-collective);
+        // only then does this block wait for the previous block's PV
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
           tc_fence_after();
-          // rescale O rows whose max grew (warp-uniform decision; tcgen05.ld/st are warp-collective)
-          if (__any_sync(0xffffffffu, alpha != 1.f)) {
+          {
 #pragma unroll
             for (int c = 0; c < HD; c += 32) {
               uint32_t v[32];
@@ -293,24 +294,26 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             tmem_st_wait();
           }
-        } else if (g > 0) {
-          mbar_wait(pv_done, (g - 1) & 1);  // previous item's last PV done: the P tile is free
         }
-        // P (bf16) into the K-major SWIZZLE_128B A tile: row r, keys in two 64-key atoms
+        // P (bf16 pairs along the keys) into TMEM buffer g & 1, last read by the PV of block g-2
+        if (g >= 2) {
+          mbar_wait(&pv_done[g & 1], ((g - 2) >> 1) & 1);
+          tc_fence_after();
+        }
 #pragma unroll
-        for (int cch = 0; cch < BN / 8; ++cch) {
-          const int atom = cch >> 3, c16 = cch & 7;
-          uint4 v = make_uint4(pack_bf16(x[8 * cch], x[8 * cch + 1]), pack_bf16(x[8 * cch + 2], x[8 * cch + 3]),
-                               pack_bf16(x[8 * cch + 4], x[8 * cch + 5]), pack_bf16(x[8 * cch + 6], x[8 * cch + 7]));
-          *reinterpret_cast<uint4*>(sP + atom * L::ATOM + r * 128 + ((c16 ^ (r & 7)) << 4)) = v;
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) pk[e] = pack_bf16(x[64 * h2 + 2 * e], x[64 * h2 + 2 * e + 1]);
+          tmem_st_32x32b_x32(lane_base + TM_P + (g & 1) * 64 + 32 * h2, pk);
         }
-        fence_proxy_async();
+        tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(p_full);
+        if (lane == 0) mbar_arrive(&p_full[g & 1]);
       }
       // item epilogue: O / l -> bf16, LSE; then hand O's TMEM back to the MMA warp
-      mbar_wait(pv_done, (g - 1) & 1);
+      mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
       tc_fence_after();
       const float inv = __frcp_rn(l);
       const int t = it.qb * BM + r;
