@@ -422,44 +422,62 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       } else if constexpr (EPI == EPI_SWIGLU_BWD) {
         // dh tile columns [cb, cb+128) = one 128-column gate/up block of the interleaved layout:
         //   dgate = dh * up * sig(g) * (1 + g (1 - sig(g))),  dup = dh * silu(g)
+        // Per 32-column slice the warp stages gate and up (32 rows x 64 B each) through its
+        // swizzled box with coalesced 16-byte loads (8 lanes per 128-byte box row: chunks 0-3
+        // gate, 4-7 up), computes in place (lane = row) and writes dgate/dup back the same way;
+        // the next slice's gate/up loads are in flight while this one computes.
         const int fc = n0 + cb;  // first dh column of this warp
         if (fc < args.N) {
           const int blk = fc >> 7;
-          const int row = rbase + lane;
-          const __nv_bfloat16* gur =
-              reinterpret_cast<const __nv_bfloat16*>(args.R) + (size_t)(row < args.M ? row : 0) * args.ldr + blk * 256;
-#pragma unroll 1
-          for (int c = 0; c < 128; c += 64) {
-#pragma unroll 1
-            for (int part = 0; part < 2; ++part) {  // 0: dgate box, 1: dup box
-              box_acquire();
-#pragma unroll 1
-              for (int q = 0; q < 2; ++q) {
-                float dh[32], o[32];
-                ld32(t_row + cb + c + 32 * q, dh);
+          const __nv_bfloat16* GU = reinterpret_cast<const __nv_bfloat16*>(args.R);
+          __nv_bfloat16* DGU = reinterpret_cast<__nv_bfloat16*>(args.C2);
+          const int j = lane & 7;            // 16-byte chunk of a box row this lane moves
+          const int col_off = (j < 4 ? 0 : 128) + 8 * (j & 3);  // gate / up column within the block
+          auto load_slice = [&](int q, uint4 (&rv)[8]) {
 #pragma unroll
-                for (int j8 = 0; j8 < 4; ++j8) {
-                  const uint4 g4 = *reinterpret_cast<const uint4*>(gur + c + 32 * q + 8 * j8);
-                  const uint4 u4 = *reinterpret_cast<const uint4*>(gur + 128 + c + 32 * q + 8 * j8);
-                  const uint32_t gw[4] = {g4.x, g4.y, g4.z, g4.w}, uw[4] = {u4.x, u4.y, u4.z, u4.w};
-#pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    const float2 g2 = unpack_bf16(gw[e]), u2 = unpack_bf16(uw[e]);
-                    const int j = 8 * j8 + 2 * e;
-                    const float s0 = fast_sigmoid(g2.x), s1 = fast_sigmoid(g2.y);
-                    if (part == 0) {
-                      o[j] = dh[j] * u2.x * s0 * (1.f + g2.x * (1.f - s0));
-                      o[j + 1] = dh[j + 1] * u2.y * s1 * (1.f + g2.y * (1.f - s1));
-                    } else {
-                      o[j] = dh[j] * g2.x * s0;
-                      o[j + 1] = dh[j + 1] * g2.y * s1;
-                    }
-                  }
-                }
-                put32(4 * q, o);
-              }
-              box_out(1, blk * 256 + 128 * part + c, rbase);
+            for (int i = 0; i < 8; ++i) {
+              const int r = (lane >> 3) + 4 * i, grow = rbase + r;
+              rv[i] = grow < args.M
+                          ? *reinterpret_cast<const uint4*>(GU + (size_t)grow * args.ldr + blk * 256 + 32 * q + col_off)
+                          : make_uint4(0, 0, 0, 0);
             }
+          };
+          uint4 rv[8];
+          load_slice(0, rv);
+          box_acquire();
+#pragma unroll 1
+          for (int q = 0; q < 4; ++q) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) box_put((lane >> 3) + 4 * i, j, rv[i]);
+            __syncwarp();
+            if (q + 1 < 4) load_slice(q + 1, rv);
+            float dh[32];
+            ld32(t_row + cb + 32 * q, dh);
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const uint4 g4 = box_get(lane, c4), u4 = box_get(lane, 4 + c4);
+              const uint32_t gw[4] = {g4.x, g4.y, g4.z, g4.w}, uw[4] = {u4.x, u4.y, u4.z, u4.w};
+              uint32_t og[4], ou[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 g2 = unpack_bf16(gw[e]), u2 = unpack_bf16(uw[e]);
+                const float d0 = dh[8 * c4 + 2 * e], d1 = dh[8 * c4 + 2 * e + 1];
+                const float s0 = fast_sigmoid(g2.x), s1 = fast_sigmoid(g2.y);
+                og[e] = pack_bf16(d0 * u2.x * s0 * (1.f + g2.x * (1.f - s0)), d1 * u2.y * s1 * (1.f + g2.y * (1.f - s1)));
+                ou[e] = pack_bf16(d0 * g2.x * s0, d1 * g2.y * s1);
+              }
+              box_put(lane, c4, make_uint4(og[0], og[1], og[2], og[3]));
+              box_put(lane, 4 + c4, make_uint4(ou[0], ou[1], ou[2], ou[3]));
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = (lane >> 3) + 4 * i, grow = rbase + r;
+              const uint4 v = box_get(r, j);
+              if (grow < args.M)
+                *reinterpret_cast<uint4*>(DGU + (size_t)grow * args.ldc2 + blk * 256 + 32 * q + col_off) = v;
+            }
+            __syncwarp();
           }
         }
       } else if constexpr (RopeHd<EPI>::value != 0) {

@@ -28,6 +28,7 @@ SHAPES = [
     ("o wgrad", 1024, 1024, 4096, True, True, native.EPI_F32),
     ("o dgrad", 4096, 1024, 1024, False, True, native.EPI_BF16),
     ("down dgrad", 4096, 2816, 1024, False, True, native.EPI_BF16),
+    ("down dgrad+swiglu_bwd", 4096, 2816, 1024, False, True, native.EPI_SWIGLU_BWD),
     ("head wgrad", 32000, 1024, 4096, True, True, native.EPI_F32),
 ]
 
@@ -56,6 +57,9 @@ def main():
             C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
         C2 = torch.empty(M, N, device=dev, dtype=torch.bfloat16) if epi == native.EPI_SWIGLU else None
         R = torch.randn(M, N, device=dev).to(torch.bfloat16) if epi == native.EPI_BF16_RESID else None
+        if epi == native.EPI_SWIGLU_BWD:  # R = gu [M, 2N] (gate/up interleave), C2 = dgu [M, 2N]
+            R = torch.randn(M, 2 * N, device=dev).to(torch.bfloat16)
+            C2 = torch.empty(M, 2 * N, device=dev, dtype=torch.bfloat16)
         ldc = N // 2 if epi == native.EPI_SWIGLU else N
 
         cs = torch.randn(32, 1024, 2, device=dev)
@@ -65,7 +69,8 @@ def main():
                 return native.gemm_rope(A, B, C, M=M, N=N, K=K, lda=K, ldb=K, ldc=N, cos_sin=cs, rope_cols=2048, T=1024,
                                         head_dim=64)
             native.gemm(A, B, C, M=M, N=N, K=K, lda=A.shape[1], ldb=B.shape[1], ldc=ldc, a_mn=a_mn, b_mn=b_mn,
-                        epilogue=epi, R=R, C2=C2, ldc2=N, beta=1.0 if epi == native.EPI_F32 else 0.0)
+                        epilogue=epi, R=R, C2=C2, ldc2=2 * N if epi == native.EPI_SWIGLU_BWD else N,
+                        beta=1.0 if epi == native.EPI_F32 else 0.0)
 
         Am = A.t() if a_mn else A
         Bm = B.t() if b_mn else B
