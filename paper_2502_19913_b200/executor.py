@@ -422,7 +422,9 @@ class Trainer:
             env = os.environ.get("SPX_NODE_STREAMS")
             self.node_streams = (world == 1) if env is None else env != "0"
             side_on = os.environ.get("SPX_WGRAD_SIDE", "1") != "0"
-            self.scratch = Scratch(cfg, self.n, b, self.T, self.dev, with_head=0 in self.my_stages)
+            # one shared scratch set when every op of the rank is serialised on one stream
+            self.scratch = None if self.node_streams else \
+                Scratch(cfg, self.n, b, self.T, self.dev, with_head=0 in self.my_stages)
             self.nparams: dict[int, NodeParams] = {}
             self.extra_grads: dict[int, list] = {st: [] for st in self.my_stages}
             for v in self.my_nodes:
