@@ -38,6 +38,8 @@ from .model import (ModelConfig, StageLayout, init_params, layer_split, pack_sta
                     unpack_stage)
 from .scheduler import Schedule
 from .simulator import B, F, L, SimConfig, SimReport, simulate
+
+LW = "LW"  # graph key kind: the head weight gradient that follows an L op (off the backward chain)
 from .topology import Topology
 
 BF16 = torch.bfloat16
@@ -287,11 +289,18 @@ class StageProgram:
         native.xent_fwd_bwd(sc.logits, sb.targets, sc.row_loss, n=n, V=V, ld=V, scale=1.0 / (n * self.M), stream=s)
         native.sum_f32(sc.row_loss, n, sb.loss, scale=1.0 / n, stream=s)
         native.gemm(sc.logits, ps.w("head"), sc.dxf, M=n, N=d, K=V, lda=V, ldb=d, ldc=d, b_mn=True, stream=s)
-        native.gemm(sc.logits, sc.xf, ps.gv("head"), M=V, N=d, K=n, lda=V, ldb=d, ldc=d, a_mn=True, b_mn=True,
-                    epilogue=native.EPI_F32, beta=1.0, stream=s)
         native.rmsnorm_bwd(sb.ret, ps.w("final_norm"), sc.rstdf, sc.dxf, None, sb.dret, ps.gv("final_norm"),
                            sc.rms_ws, rows=n, d=d, stream=s)
         return sb.dret
+
+    def loss_wgrad(self, ps: ParamSet, sc: Scratch, s):
+        """The head's weight gradient from the L op's dlogits / normalised input.  Issued after the
+        L op's hop, so the returned gradient leaves for the path's last node without waiting for
+        this GEMM (it is off the backward chain; sc.logits / sc.xf are only rewritten by the node's
+        next L op, later on the same stream)."""
+        c, n = self.cfg, self.n
+        native.gemm(sc.logits, sc.xf, ps.gv("head"), M=c.vocab, N=c.d, K=n, lda=c.vocab, ldb=c.d, ldc=c.d,
+                    a_mn=True, b_mn=True, epilogue=native.EPI_F32, beta=1.0, stream=s)
 
 
 # ---------------------------------------------------------------------------------------
@@ -518,6 +527,9 @@ class Trainer:
             return sb.xs[-1]
         if kind == L:
             return self.prog.loss(ps, sb, sc, s)
+        if kind == LW:
+            self.prog.loss_wgrad(ps, sc, s)
+            return None
         return self.prog.bwd(ps, sb, sc, origin, s, self.nside[v])
 
     def _key(self, op):
@@ -525,6 +537,7 @@ class Trainer:
 
     def _capture_all(self):
         keys = sorted({self._key(op) for op in self.ops if self.placement[op.node] == self.rank})
+        keys += [(LW, v, slot) for (kind, v, slot) in keys if kind == L]
         with torch.cuda.device(self.dev):
             for key in keys:
                 kind, v, slot = key
@@ -641,57 +654,24 @@ class Trainer:
                         with torch.cuda.stream(sv):
                             self.mb_loss[mb:mb + 1].copy_(sb.loss, non_blocking=True)
                 hop = self.hops[idx]
-                if hop is None:
-                    continue
-                nv, name, _, dst_rank, consumer = hop
-                dst_mine = dst_rank == self.rank
-                if mine and dst_mine:
-                    buf = self._dst_buffer(op, nv, name)
+                if hop is not None:
+                    self._issue_hop(idx, op, hop, out, mine, pending, sends)
+                if mine and op.kind == L:  # the head wgrad, after the returned gradient left
                     sv = self.nstream[v]
-                    if self.nstream[nv] is sv:
-                        native.hop(buf, self.dev.index, out, self.dev.index, out.numel() * out.element_size(),
-                                   stream=sv)
+                    lw = (LW, v, self._key(op)[2])
+                    if self.use_graphs:
+                        with torch.cuda.stream(sv):
+                            self._graphs[lw].replay()
                     else:
-                        # copied on the consumer's stream right before the consumer op: the
-                        # destination slot is then free (the consumer node's earlier ops are ahead
-                        # of it on that stream) and the source is slot-owned until the agent's next
-                        # wave, which causally follows the consumer
-                        done = torch.cuda.Event()
-                        done.record(sv)
-                        pending[(consumer, nv, op.agent, op.wave)] = ("local", out, done, buf)
-                elif mine:
-                    import torch.distributed as dist
-
-                    # the source is slot-owned (F: last residual buffer, B: gout, L: dret) and is
-                    # rewritten only by this agent's next wave, which causally follows this send's
-                    # completion: drain it on the send stream without stalling compute
-                    ev_out = torch.cuda.Event()
-                    ev_out.record(self.nstream[v])
-                    ss = self.nsend[v]
-                    ss.wait_event(ev_out)
-                    with torch.cuda.stream(ss):
-                        sends.append((dist.isend(out, dst_rank, group=self._pair[dst_rank]), ss))
-                elif dst_mine:
-                    import torch.distributed as dist
-
-                    buf = self._dst_buffer(op, nv, name)
-                    # the destination slot was last read by this agent's previous wave on the
-                    # consumer node, whose ops so far are all on that node's stream
-                    rs = self.nrecv[nv]
-                    rs.wait_stream(self.nstream[nv])
-                    with torch.cuda.stream(rs):
-                        w = dist.irecv(buf, self.placement[v], group=self._pair[self.placement[v]])
-                    pending[(consumer, nv, op.agent, op.wave)] = ("nccl", w)
+                        self._run_op(LW, v, lw[2], sv)
+                    if timing:
+                        e1 = torch.cuda.Event(enable_timing=True)
+                        e1.record(sv)
+                        ev[idx] = (ev[idx][0], e1)
             for cs in streams:
                 if cs is not s:
                     s.wait_stream(cs)
-            if sends:
-                with torch.cuda.stream(s):
-                    for w, _ in sends:
-                        w.wait()
-                for ss in dict.fromkeys(ss for _, ss in sends):
-                    s.wait_stream(ss)
-            self.optimizer_step()
+            self._finish_step(sends)
             t_iter1.record(s)
             torch.cuda.current_stream(self.dev).wait_stream(s)
             if self.world > 1:
@@ -706,22 +686,81 @@ class Trainer:
             out["op_times"] = {i: (t_iter0.elapsed_time(a), t_iter0.elapsed_time(b_)) for i, (a, b_) in ev.items()}
         return out
 
+    def _issue_hop(self, idx, op, hop, out, mine, pending, sends):
+        """The path hop that follows op ``idx``: a local copy (or its deferred form), an NCCL send
+        from a slot-owned buffer, or the matching receive."""
+        v = op.node
+        nv, name, _, dst_rank, consumer = hop
+        dst_mine = dst_rank == self.rank
+        if mine and dst_mine:
+            buf = self._dst_buffer(op, nv, name)
+            sv = self.nstream[v]
+            if self.nstream[nv] is sv:
+                native.hop(buf, self.dev.index, out, self.dev.index, out.numel() * out.element_size(),
+                           stream=sv)
+            else:
+                # copied on the consumer's stream right before the consumer op: the
+                # destination slot is then free (the consumer node's earlier ops are ahead
+                # of it on that stream) and the source is slot-owned until the agent's next
+                # wave, which causally follows the consumer
+                done = torch.cuda.Event()
+                done.record(sv)
+                pending[(consumer, nv, op.agent, op.wave)] = ("local", out, done, buf)
+        elif mine:
+            import torch.distributed as dist
+
+            # the source is slot-owned (F: last residual buffer, B: gout, L: dret) and is
+            # rewritten only by this agent's next wave, which causally follows this send's
+            # completion: drain it on the send stream without stalling compute
+            ev_out = torch.cuda.Event()
+            ev_out.record(self.nstream[v])
+            ss = self.nsend[v]
+            ss.wait_event(ev_out)
+            with torch.cuda.stream(ss):
+                sends.append((dist.isend(out, dst_rank, group=self._pair[dst_rank]), ss))
+        elif dst_mine:
+            import torch.distributed as dist
+
+            buf = self._dst_buffer(op, nv, name)
+            # the destination slot was last read by this agent's previous wave on the
+            # consumer node, whose ops so far are all on that node's stream
+            rs = self.nrecv[nv]
+            rs.wait_stream(self.nstream[nv])
+            with torch.cuda.stream(rs):
+                w = dist.irecv(buf, self.placement[v], group=self._pair[self.placement[v]])
+            pending[(consumer, nv, op.agent, op.wave)] = ("nccl", w)
+
+    def _finish_step(self, sends):
+        """Drain the hop sends, then the replica sum / clip / AdamW on the rank's main stream."""
+        s = self.stream
+        if sends:
+            with torch.cuda.stream(s):
+                for w, _ in sends:
+                    w.wait()
+            for ss in dict.fromkeys(ss for _, ss in sends):
+                s.wait_stream(ss)
+        self.optimizer_step()
+
     # ---- optimizer ----
     def launches_per_step(self) -> int:
         """libspx kernel launches in one iteration on this rank (graph contents + optimizer)."""
         if not self.use_graphs:
             raise ValidationError("launch accounting needs use_graphs=True")
         opt = 2 * len(self.psets) + 1 + len(self.psets) + sum(len(gl) for gl in self.extra_grads.values())
-        return sum(self._graph_launches[self._key(op)] for op in self.ops
-                   if self.placement[op.node] == self.rank) + opt
+        mine = [self._key(op) for op in self.ops if self.placement[op.node] == self.rank]
+        return sum(self._graph_launches[k] + (self._graph_launches[(LW,) + k[1:]] if k[0] == L else 0)
+                   for k in mine) + opt
 
     def gemm_counts_per_step(self) -> dict:
         """GEMM key -> launches per iteration on this rank (needs native.record_gemms at setup)."""
         out: dict = {}
         for op in self.ops:
             if self.placement[op.node] == self.rank:
-                for key in self._graph_gemms.get(self._key(op), []):
-                    out[key] = out.get(key, 0) + 1
+                k = self._key(op)
+                keys = [k] + ([(LW,) + k[1:]] if k[0] == L else [])
+                for gk in keys:
+                    for key in self._graph_gemms.get(gk, []):
+                        out[key] = out.get(key, 0) + 1
         return out
 
     def optimizer_step(self):
