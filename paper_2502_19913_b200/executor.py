@@ -254,11 +254,24 @@ class StageProgram:
         return done
 
     # ---- node ops ----
-    def fwd(self, ps: ParamSet, sb: SlotBuffers, sc: Scratch, origin: bool, s):
+    def fwd(self, ps: ParamSet, sb: SlotBuffers, sc: Scratch, origin: bool, s, n_layers: int | None = None):
+        """Embedding (at the origin) and the stage's layers; ``n_layers`` runs only the first ones
+        (a partial stage, inference only).  Returns the output buffer."""
         if origin:
             native.embed_fwd(sb.ids, ps.w("embed"), sb.xs[0], n=self.n, d=self.cfg.d, stream=s)
-        for i, a in enumerate(sb.layers):
-            self.layer_fwd(ps, i, sb.xs[i], a, sb.xs[i + 1], sc, s)
+        k = len(sb.layers) if n_layers is None else n_layers
+        for i in range(k):
+            self.layer_fwd(ps, i, sb.xs[i], sb.layers[i], sb.xs[i + 1], sc, s)
+        return sb.xs[k]
+
+    def loss_fwd(self, ps: ParamSet, sb: SlotBuffers, sc: Scratch, s):
+        """Inference loss at the origin: final norm, head, token-mean cross-entropy into sb.loss
+        (the kernel's in-place dlogits are ignored; no gradient is touched)."""
+        c, n = self.cfg, self.n
+        native.rmsnorm_fwd(sb.ret, ps.w("final_norm"), sc.xf, sc.rstdf, rows=n, d=c.d, eps=c.eps, stream=s)
+        native.gemm(sc.xf, ps.w("head"), sc.logits, M=n, N=c.vocab, K=c.d, lda=c.d, ldb=c.d, ldc=c.vocab, stream=s)
+        native.xent_fwd_bwd(sc.logits, sb.targets, sc.row_loss, n=n, V=c.vocab, ld=c.vocab, scale=0.0, stream=s)
+        native.sum_f32(sc.row_loss, n, sb.loss, scale=1.0 / n, stream=s)
 
     def bwd(self, ps: ParamSet, sb: SlotBuffers, sc: Scratch, origin: bool, s, side=None):
         """Returns the buffer holding the gradient w.r.t. the node's input."""
@@ -805,6 +818,63 @@ class Trainer:
     def params(self) -> dict[int, dict[str, torch.Tensor]]:
         torch.cuda.synchronize(self.dev)
         return {st: unpack_stage(self.cfg, self.layouts[st], self.psets[st].p32) for st in self.my_stages}
+
+    # ---- skip-robust inference (§5) ----
+    def eval_loss(self, tokens: torch.Tensor, stages: list[int], partial: dict | None = None) -> float:
+        """Token-mean cross-entropy of one microbatch (tokens [b, T+1]) run forward through
+        ``stages`` (stage 0 first; any subset / order, as in training paths) and back to the
+        loss at the origin, with the current weights -- no gradients.  ``partial`` maps a stage
+        to the number of its first layers to execute (the paper's partial stage skips).  Uses
+        the first hosted node of each stage and its slot 0, so call it between iterations.  One
+        process holding every stage (world == 1)."""
+        if self.world != 1:
+            raise ValidationError("eval_loss runs on a single process that hosts every stage")
+        if not stages or stages[0] != 0:
+            raise ValidationError(f"an inference path starts at stage 0, got {stages}")
+        if tokens.shape != (self.b, self.T + 1):
+            raise ValidationError(f"tokens shape {tuple(tokens.shape)} != ({self.b}, {self.T + 1})")
+        partial = partial or {}
+        node_of = {}
+        for v in self.my_nodes:
+            node_of.setdefault(self.node_stage[v], v)
+        s = self.stream
+        with torch.cuda.device(self.dev), torch.cuda.stream(s):
+            s.wait_stream(torch.cuda.current_stream(self.dev))
+            for v in self.my_nodes:
+                s.wait_stream(self.nstream[v])
+            origin = self.slots[(node_of[0], 0)]
+            origin.ids.copy_(tokens[:, :-1].reshape(-1).to(torch.int32), non_blocking=True)
+            origin.targets.copy_(tokens[:, 1:].reshape(-1).to(torch.int32), non_blocking=True)
+            x = None
+            for st in stages:
+                v = node_of[st]
+                sb = self.slots[(v, 0)]
+                if x is not None:
+                    sb.xs[0].copy_(x)
+                x = self.prog.fwd(self.nparams[v], sb, self.nscratch[v], st == 0, s, partial.get(st))
+            origin.ret.copy_(x)
+            v0 = node_of[0]
+            self.prog.loss_fwd(self.nparams[v0], origin, self.nscratch[v0], s)
+            loss = float(origin.loss.item())
+        return loss
+
+    def skip_eval(self, tokens: torch.Tensor, skip_rate: float, seed: int = 0) -> float:
+        """Perplexity with ``skip_rate`` of the stages dropped at random per microbatch, never
+        stage 0; when the rate does not divide into whole stages the last dropped
+        stage is half-executed (its first half of layers).  tokens [M, b, T+1]."""
+        s_ = self.assignment.s
+        gen = torch.Generator().manual_seed(seed)
+        drop = skip_rate * s_
+        whole = int(math.floor(drop + 1e-9))
+        half = drop - whole > 1e-9
+        losses = []
+        for mb in range(tokens.shape[0]):
+            order = (torch.randperm(s_ - 1, generator=gen) + 1).tolist()
+            dropped, partial_st = set(order[:whole]), (order[whole] if half and whole < s_ - 1 else None)
+            stages = [st for st in range(s_) if st not in dropped]
+            partial = {partial_st: max(1, self.split[partial_st] // 2)} if partial_st is not None else None
+            losses.append(self.eval_loss(tokens[mb], stages, partial))
+        return math.exp(sum(losses) / len(losses))
 
     def grad_norm(self) -> float:
         torch.cuda.synchronize(self.dev)

@@ -91,3 +91,37 @@ def test_graphs_equal_eager():
                      use_graphs=graphs)
         losses.append([tr.step(tokens)["loss"] for _ in range(2)])
     assert losses[0] == losses[1]
+
+
+def test_skip_robust_inference_matches_oracle():
+    """eval_loss (forward-only path through any stage subset/order, §5) equals the CPU
+    fp32 oracle's loss for the same weights; skip_eval returns exp(mean loss)."""
+    import math
+
+    from oracle.train_ref import rms_norm, rope_tables, stage_forward
+
+    rc, sch, params, tokens = _setup()
+    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params)
+    tr.step(tokens)                                 # weights after one update
+    p = tr.params()
+    cfg = rc.model
+    cos, sin = rope_tables(rc.T, cfg.head_dim, cfg.rope_theta)
+    tok = tokens[0]
+
+    def ref(stages, partial=None):
+        x = p[0]["embed"][tok[:, :-1]]
+        for st in stages:
+            x = stage_forward(x, p[st], (partial or {}).get(st, rc.layers[st]), cfg, cos, sin)
+        x = rms_norm(x, p[0]["final_norm"], cfg.eps)
+        logits = x @ p[0]["head"].t()
+        return float(torch.nn.functional.cross_entropy(logits.reshape(-1, cfg.vocab), tok[:, 1:].reshape(-1)))
+
+    for stages, partial in (([0, 1, 2, 3], None), ([0, 2, 3], None), ([0, 2, 1, 3], None), ([0, 1], None),
+                            ([0, 1, 2, 3], {2: 1})):
+        got = tr.eval_loss(tok, stages, partial)
+        want = ref(stages, partial)
+        assert abs(got - want) / want < 2e-2, (stages, partial, got, want)
+    ppl = tr.skip_eval(tokens[:2], 0.25, seed=0)
+    assert math.isfinite(ppl) and ppl > 1.0
+    # the weights did not move and no gradient was written
+    assert all(torch.equal(tr.params()[st][k], p[st][k]) for st in p for k in p[st])
