@@ -81,3 +81,28 @@ def test_executor_requires_cuda():
     rc = get_config("C1")
     with pytest.raises(native.NativeError):
         Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T)
+
+
+def test_argument_validation_of_newer_entry_points(lib):
+    """Invalid arguments are rejected before any CUDA call (no GPU needed)."""
+    from paper_2502_19913_b200 import native
+
+    P64 = ctypes.c_void_p * 1
+    I64 = ctypes.c_int64 * 1
+    F1 = ctypes.c_float * 1
+    ptrs, ones = P64(None), I64(64)
+    rc = lib.spx_gemm_f32_group(0, ptrs, ptrs, ptrs, ones, ones, ones, ones, ones, ones, F1(1.0), 1, 1, None)
+    assert rc == -1 and b"1..4 problems" in lib.spx_last_error()
+    rc = lib.spx_gemm_f32_group(5, ptrs, ptrs, ptrs, ones, ones, ones, ones, ones, ones, F1(1.0), 1, 1, None)
+    assert rc == -1 and b"1..4 problems" in lib.spx_last_error()
+    rc = lib.spx_gemm_f32_group(1, ptrs, ptrs, ptrs, I64(64), I64(48), I64(64), ones, ones, ones, F1(1.0), 1, 1, None)
+    assert rc == -1 and b"N % 32" in lib.spx_last_error()
+    rc = lib.spx_add_f32(None, None, ctypes.c_int64(-1), None)
+    assert rc == -1 and b"negative" in lib.spx_last_error()
+    assert lib.spx_add_f32(None, None, ctypes.c_int64(0), None) == 0
+    # attention-backward workspace: D + lse*log2e, plus the causal dS^T tiles on the tcgen05 path
+    B, H, T = 2, 4, 512
+    nqb = T // 128
+    assert native.attn_bwd_ws_floats(B, H, T, 48) == 2 * B * H * T
+    assert native.attn_bwd_ws_floats(B, H, T, 64) == 2 * B * H * T + B * H * (nqb * (nqb + 1) // 2) * 128 * 128 // 2
+    assert lib.spx_launch_count() >= 0
