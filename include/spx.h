@@ -61,9 +61,9 @@ int spx_hop(int32_t dst_dev, void* dst, int32_t src_dev, const void* src, int64_
  *   0  C bf16 [M][ldc]  = D
  *   1  C bf16 [M][ldc]  = D + R (R bf16 [M][ldc], may alias C)
  *   2  C f32  [M][ldc]  = D + beta * C   (beta in {0,1}; wgrad accumulation)
- *   3  SwiGLU: N = 2F with gate/up interleaved in 128-column blocks;
- *      C bf16 [M][ldc] = silu(gate) * up  (F columns), C2 bf16 [M][ldc2] = raw gate/up (N columns)
- *   6  SwiGLU backward fused into the down-projection dgrad: D = dh [M][N=F]; R = gu [M][ldc2]
+ *   3  SwiGLU (forward layout: A and B K-major): N = 2F with gate/up interleaved in 128-column
+ *      blocks; C bf16 [M][ldc] = silu(gate) * up  (F columns), C2 bf16 [M][ldc2] = raw gate/up
+ *   6  SwiGLU backward fused into the down-projection dgrad (A K-major, B MN-major): D = dh [M][N=F]; R = gu [M][ldc2]
  *      (raw gate/up, 128-column interleave); C2 bf16 [M][ldc2] = dgu (dgate, dup interleaved)
  * Requires N % 32 == 0, K, lda, ldb multiples of 8, 16-byte aligned A/B. */
 int spx_gemm_bf16(const void* A, const void* B, void* C, const void* R, void* C2, int64_t M, int64_t N, int64_t K,

@@ -780,6 +780,14 @@ static int dispatch_256(const void* A, const void* B, long long lda, long long l
   return dispatch_major<256, EPI, 1>(A, B, lda, ldb, a_mn, b_mn, args, s);
 }
 
+// epilogues that exist for one operand layout only (fewer template instantiations)
+template <int EPI, bool A_MN, bool B_MN>
+static int dispatch_256_fixed(const void* A, const void* B, long long lda, long long ldb, const GemmArgs& args,
+                              cudaStream_t s) {
+  if (use_pair(args.M)) return launch_gemm<256, A_MN, B_MN, EPI, 2>(A, B, lda, ldb, args, s);
+  return launch_gemm<256, A_MN, B_MN, EPI, 1>(A, B, lda, ldb, args, s);
+}
+
 static int pick_bn(int M, int N) {
   auto eff = [&](int bn) {
     const long tiles = (long)((M + GEMM_BM - 1) / GEMM_BM) * ((N + bn - 1) / bn);
@@ -874,8 +882,8 @@ extern "C" int spx_gemm_bf16_rope(const void* A, const void* B, void* C, int64_t
   args.probe = probe_mode();
   args.tma_store = tma_store_mode();
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (head_dim == 64) return dispatch_256<EPI_ROPE64>(A, B, lda, ldb, 0, 0, args, s);
-  return dispatch_256<EPI_ROPE128>(A, B, lda, ldb, 0, 0, args, s);
+  if (head_dim == 64) return dispatch_256_fixed<EPI_ROPE64, false, false>(A, B, lda, ldb, args, s);
+  return dispatch_256_fixed<EPI_ROPE128, false, false>(A, B, lda, ldb, args, s);
 }
 
 extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* R, void* C2, int64_t M, int64_t N,
@@ -910,8 +918,10 @@ extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* 
       return bn == 256 ? dispatch_256<EPI_F32>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s)
                        : dispatch_major<128, EPI_F32>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
     case EPI_SWIGLU_BWD:
-      return dispatch_256<EPI_SWIGLU_BWD>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
+      if (a_mn_major || !b_mn_major) return set_error(SPX_ERR_ARG, "gemm: swiglu-bwd epilogue needs K-major A, MN-major B (dgrad)");
+      return dispatch_256_fixed<EPI_SWIGLU_BWD, false, true>(A, B, lda, ldb, args, s);
     default:
-      return dispatch_256<EPI_SWIGLU>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
+      if (a_mn_major || b_mn_major) return set_error(SPX_ERR_ARG, "gemm: swiglu epilogue needs K-major A and B (forward)");
+      return dispatch_256_fixed<EPI_SWIGLU, false, false>(A, B, lda, ldb, args, s);
   }
 }
