@@ -137,9 +137,10 @@ def run_reference(args, rc):
     print(json.dumps(line), flush=True)
 
 
-def gemm_roofline(tr, peak_tflops: float, reps: int = 5) -> dict:
-    """Per-launch timing of every tcgen05 GEMM of one iteration (same shapes, layouts and
-    epilogues as inside the captured graphs), on the executor's stream with CUDA events."""
+def gemm_roofline(tr, peak_tflops: float, reps: int = 10) -> dict:
+    """Per-launch timing of every tcgen05 GEMM of one iteration (same shapes, layouts, epilogues
+    and buffers as inside the captured graphs): ``reps`` back-to-back launches captured in a CUDA
+    graph and replayed on the executor's stream, timed with CUDA events."""
     import torch
 
     from paper_2502_19913_b200 import native
@@ -158,12 +159,20 @@ def gemm_roofline(tr, peak_tflops: float, reps: int = 5) -> dict:
     per = {}
     for key, (_, fn) in calls.items():
         count = counts.get(key, 0)
+        # the same launches replayed from a CUDA graph (as in the iteration): device time per
+        # launch without host launch gaps
         with torch.cuda.stream(s):
             fn()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(s)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
             for _ in range(reps):
                 fn()
+        with torch.cuda.stream(s):
+            g.replay()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            g.replay()
             e1.record(s)
         e1.synchronize()
         ms = e0.elapsed_time(e1) / reps
