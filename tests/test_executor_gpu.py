@@ -125,3 +125,29 @@ def test_skip_robust_inference_matches_oracle():
     assert math.isfinite(ppl) and ppl > 1.0
     # the weights did not move and no gradient was written
     assert all(torch.equal(tr.params()[st][k], p[st][k]) for st in p for k in p[st])
+
+
+@pytest.mark.parametrize("heads,kv", [(4, 2), (2, 1)])
+def test_gqa_config_matches_oracle(heads, kv):
+    """GQA models (query heads over half as many KV heads; head_dim 64 and 128: the tcgen05
+    attention paths with grouped K/V, RoPE on the KV heads, the fused QKV layout -- the C4 shape
+    family) train like the oracle."""
+    from paper_2502_19913_b200.configs import RunConfig
+    from paper_2502_19913_b200.model import model_config
+
+    cfg = model_config("llama-50m", d=256, n_heads=heads, n_kv_heads=kv, ffn=768)
+    rc = RunConfig("GQA", cfg, [2, 2, 2, 2], 25, 2, 2, 256, 8)
+    sch = rc.schedule()
+    params = init_params(cfg, rc.layers, seed=0)
+    tokens = synthetic_tokens(cfg, rc.M, rc.b, rc.T, seed=1234)
+    tr = Trainer(sch, rc.topology(), rc.sim_config(), cfg, rc.assignment, b=rc.b, T=rc.T, params=params)
+    res = tr.step(tokens)
+    agents = sorted(a.id for a in sch.agents)
+    mb_stages = train_ref.mb_stage_sequences({a: sch.paths[a].stages for a in agents}, agents, rc.M)
+    ref = train_ref.iteration(cfg, rc.layers, params, mb_stages, tokens, update=True)
+    assert abs(res["loss"] - ref["loss"]) / ref["loss"] < 2e-2
+    g = tr.grads()
+    for st in range(rc.s):
+        a, b = _flat(g[st]), _flat(ref["grads"][st])
+        cos = torch.nn.functional.cosine_similarity(a.double(), b.double(), dim=0).item()
+        assert cos >= 0.99, (st, cos)
