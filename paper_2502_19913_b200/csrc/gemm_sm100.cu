@@ -278,12 +278,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (lane == 0) bulk_wait_read<0>();  // the previous store from this buffer has read it
       __syncwarp();
     };
-    auto box_put = [&](int r, int j, uint4 v) {
-      *reinterpret_cast<uint4*>(box + r * 128 + ((j ^ (r & 7)) << 4)) = v;
-    };
-    auto box_get = [&](int r, int j) -> uint4 {
-      return *reinterpret_cast<const uint4*>(box + r * 128 + ((j ^ (r & 7)) << 4));
-    };
+    auto box_put = [&](int r, int j, uint4 v) { sts128(smem_u32(box) + r * 128 + ((j ^ (r & 7)) << 4), v); };
+    auto box_get = [&](int r, int j) -> uint4 { return lds128(smem_u32(box) + r * 128 + ((j ^ (r & 7)) << 4)); };
     auto box_issue = [&](const CUtensorMap* m, int c0, int c1, bool reduce) {
       fence_proxy_async();
       __syncwarp();
@@ -303,7 +299,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int i = 0; i < 8; ++i) {
         const int r = i * 4 + (lane >> 3), j = lane & 7;
         const int grow = r0 + r, gcol = c0 + 8 * j;
-        const uint4 v = *reinterpret_cast<const uint4*>(box + r * 128 + ((j ^ (r & 7)) << 4));
+        const uint4 v = box_get(r, j);
         if (grow < args.M && gcol < ncols)
           *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(base) + (size_t)grow * ld + gcol) = v;
       }
