@@ -472,6 +472,17 @@ __global__ void clip_scale_kernel(const float* __restrict__ sumsq, int count, fl
 }
 
 // ---------------------------------------------------------------- AdamW (torch.optim.AdamW math)
+// One AdamW element update with every rounding explicit (no compiler FMA contraction choices), so
+// the scalar and the 16-byte vector kernels are bit-identical.
+__device__ __forceinline__ void adamw_one(float& pi, float gi, float& mi, float& vi, bool decay, float lr, float b1,
+                                          float b2, float eps, float wd, float step, float rbc2) {
+  if (decay) pi = __fmul_rn(pi, __fsub_rn(1.f, __fmul_rn(lr, wd)));
+  mi = __fmaf_rn(b1, mi, __fmul_rn(__fsub_rn(1.f, b1), gi));
+  vi = __fmaf_rn(b2, vi, __fmul_rn(__fmul_rn(__fsub_rn(1.f, b2), gi), gi));
+  const float den = __fmaf_rn(__fsqrt_rn(vi), rbc2, eps);
+  pi = __fsub_rn(pi, __fdiv_rn(__fmul_rn(step, mi), den));
+}
+
 __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                              float* __restrict__ v, __nv_bfloat16* __restrict__ pb, long long n, long long n_decay,
                              float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
@@ -481,14 +492,52 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
   const float step = lr / bc1;
   const float rbc2 = rsqrtf(bc2);
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const float gi = g[i] * sc;
-    float pi = p[i];
-    if (i < n_decay) pi *= (1.f - lr * wd);
-    const float mi = b1 * m[i] + (1.f - b1) * gi;
-    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    float pi = p[i], mi = m[i], vi = v[i];
+    adamw_one(pi, __fmul_rn(g[i], sc), mi, vi, i < n_decay, lr, b1, b2, eps, wd, step, rbc2);
     m[i] = mi;
     v[i] = vi;
-    pi -= step * mi / (sqrtf(vi) * rbc2 + eps);
+    p[i] = pi;
+    pb[i] = __float2bfloat16(pi);
+  }
+}
+
+// 16-byte vector form: 4 elements per thread per iteration (p/g/m/v 16-byte, pb 8-byte aligned;
+// n % 4 by the scalar tail)
+__global__ void __launch_bounds__(256) adamw_vec_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                                        float* __restrict__ m, float* __restrict__ v,
+                                                        __nv_bfloat16* __restrict__ pb, long long n, long long n_decay,
+                                                        float lr, float b1, float b2, float eps, float wd, float bc1,
+                                                        float bc2, const float* __restrict__ gscale) {
+  pdl_wait();
+  const float sc = gscale ? gscale[0] : 1.f;
+  const float step = lr / bc1;
+  const float rbc2 = rsqrtf(bc2);
+  const long long n4 = n / 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 g4 = __ldcs(reinterpret_cast<const float4*>(g) + i);
+    float4 p4 = __ldcs(reinterpret_cast<const float4*>(p) + i);
+    float4 m4 = __ldcs(reinterpret_cast<const float4*>(m) + i);
+    float4 v4 = __ldcs(reinterpret_cast<const float4*>(v) + i);
+    const long long e = 4 * i;
+    adamw_one(p4.x, __fmul_rn(g4.x, sc), m4.x, v4.x, e + 0 < n_decay, lr, b1, b2, eps, wd, step, rbc2);
+    adamw_one(p4.y, __fmul_rn(g4.y, sc), m4.y, v4.y, e + 1 < n_decay, lr, b1, b2, eps, wd, step, rbc2);
+    adamw_one(p4.z, __fmul_rn(g4.z, sc), m4.z, v4.z, e + 2 < n_decay, lr, b1, b2, eps, wd, step, rbc2);
+    adamw_one(p4.w, __fmul_rn(g4.w, sc), m4.w, v4.w, e + 3 < n_decay, lr, b1, b2, eps, wd, step, rbc2);
+    __stcs(reinterpret_cast<float4*>(m) + i, m4);
+    __stcs(reinterpret_cast<float4*>(v) + i, v4);
+    __stcs(reinterpret_cast<float4*>(p) + i, p4);
+    __nv_bfloat162 lo = __floats2bfloat162_rn(p4.x, p4.y), hi = __floats2bfloat162_rn(p4.z, p4.w);
+    uint2 packed;
+    packed.x = *reinterpret_cast<uint32_t*>(&lo);
+    packed.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(pb)[i] = packed;
+  }
+  for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float pi = p[i], mi = m[i], vi = v[i];
+    adamw_one(pi, __fmul_rn(g[i], sc), mi, vi, i < n_decay, lr, b1, b2, eps, wd, step, rbc2);
+    m[i] = mi;
+    v[i] = vi;
     p[i] = pi;
     pb[i] = __float2bfloat16(pi);
   }
@@ -639,7 +688,8 @@ extern "C" int spx_adamw(float* p, const float* g, float* m, float* v, void* p_b
   const float bc1 = 1.f - powf(beta1, (float)step);
   const float bc2 = 1.f - powf(beta2, (float)step);
   const int blocks = num_sms() * 8;
-  spx_launch_check(launch_k(adamw_kernel, dim3(blocks), dim3(256), 0, SPX_S, p, g, m, v, BF(p_bf16), n, n_decay, lr, beta1, beta2, eps, weight_decay, bc1,
+  const bool vec = !((((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) | ((uintptr_t)p_bf16 & 7));
+  spx_launch_check(launch_k(vec ? adamw_vec_kernel : adamw_kernel, dim3(blocks), dim3(256), 0, SPX_S, p, g, m, v, BF(p_bf16), n, n_decay, lr, beta1, beta2, eps, weight_decay, bc1,
                                           bc2, grad_scale));
   return check_launch("adamw_kernel");
 }

@@ -233,6 +233,33 @@ def test_adamw_and_clip():
     assert torch.equal(pb, p.to(torch.bfloat16))
 
 
+def test_adamw_vector_path_bit_identical():
+    """16-byte vector AdamW (aligned buffers) == scalar AdamW (buffers offset by one element)."""
+    n, nd = 100_003, 61_001
+    g = torch.Generator().manual_seed(1)
+    base = [torch.randn(n + 1, generator=g).to(dev) for _ in range(2)]
+    grad = (torch.randn(n + 1, generator=g) * 2).to(dev)
+    sc = torch.full((1,), 0.7, device=dev)
+    outs = []
+    for off in (0, 1):  # off = 1 views every buffer at +4 bytes -> scalar kernel
+
+        def place(t):
+            buf = torch.empty(n + off, dtype=t.dtype, device=dev)
+            buf[off:] = t
+            return buf[off:]
+
+        p, m, v = place(base[0][1:]), place(torch.zeros(n, device=dev)), place(base[1][1:].abs())
+        pb, gg = place(torch.zeros(n, dtype=torch.bfloat16, device=dev)), place(grad[1:])
+        assert (p.data_ptr() % 16 == 0) == (off == 0)
+        for step in (1, 2, 3):
+            native.adamw(p, gg, m, v, pb, n=n, n_decay=nd, lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8,
+                         weight_decay=0.1, step=step, grad_scale=sc)
+        torch.cuda.synchronize()
+        outs.append((p.clone(), m.clone(), v.clone(), pb.clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("hd,H,Hkv", [(64, 16, 16), (128, 8, 2)])
 def test_gemm_rope_epilogue(hd, H, Hkv):
     B, T, d = 2, 256, 512
