@@ -133,6 +133,14 @@ int spx_embed_fwd(const int32_t* ids, const void* table, void* out, int64_t n, i
 int spx_embed_bwd(const int32_t* perm, const int32_t* seg_start, const int32_t* seg_id, const int32_t* n_segments,
                   int64_t max_segments, const void* dout, float* dtable, int64_t d, void* stream);
 
+/* ---- token batch preparation (the data format in front of S0): one microbatch's token block
+ *      tokens[b][ld_tokens] (int64, T+1 used per row) -> ids[n] = tokens[r][t], targets[n] =
+ *      tokens[r][t+1] (n = b*T, position r*T + t) and the embedding-backward grouping of
+ *      spx_embed_bwd (perm, seg_start, seg_id, *n_segments), computed on the device so a step's
+ *      only host->device input is the token block.  n <= 16384; ids must be < 2^31. */
+int spx_token_prep(const int64_t* tokens, int64_t b, int64_t T, int64_t ld_tokens, int32_t* ids, int32_t* targets,
+                   int32_t* perm, int32_t* seg_start, int32_t* seg_id, int32_t* n_segments, void* stream);
+
 /* ---- softmax cross-entropy: row_loss[r] = lse(z_r) - z_r[t_r]; logits overwritten by
  *      (softmax - onehot) * scale (bf16).  One pass pair per row, logits never re-materialised. */
 int spx_xent_fwd_bwd(void* logits, const int32_t* targets, float* row_loss, int64_t n, int64_t V, int64_t ld,

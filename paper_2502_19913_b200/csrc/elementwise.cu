@@ -331,6 +331,91 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ perm, const int32_t
   }
 }
 
+// ---------------------------------------------------------------- token batch preparation
+// One microbatch's token block [b, T+1] (int64, row stride ld) -> inputs ids[n] = tok[r, t],
+// targets[n] = tok[r, t+1] (n = b*T, position i = r*T + t), and the grouping the deterministic
+// embedding backward needs: positions sorted by (id, position), perm, segment starts and ids.
+// Keys (id << 32 | position) are unique, so the sorted order -- and with it the embedding
+// gradient's summation order -- is unique: a bitonic sort in shared memory (one CTA, n <= 16384)
+// gives exactly the host reference's stable argsort.  Runs on the device so a step's only
+// host->device input is the raw token block.
+constexpr int TP_THREADS = 1024;
+constexpr int TP_MAX_N = 16384;
+
+__global__ void __launch_bounds__(TP_THREADS) token_prep_kernel(const long long* __restrict__ tok, int T, long long ld,
+                                                                int n, int n2, int32_t* __restrict__ ids,
+                                                                int32_t* __restrict__ tgt, int32_t* __restrict__ perm,
+                                                                int32_t* __restrict__ seg_start,
+                                                                int32_t* __restrict__ seg_id,
+                                                                int32_t* __restrict__ n_seg) {
+  extern __shared__ unsigned long long keys[];  // n2 = next power of two >= n
+  __shared__ int wsum[TP_THREADS / 32];
+  pdl_wait();
+  const int tid = threadIdx.x;
+  for (int i = tid; i < n2; i += TP_THREADS) {
+    unsigned long long k = ~0ull;
+    if (i < n) {
+      const int r = i / T, t = i - r * T;
+      const long long id = tok[r * ld + t];
+      ids[i] = (int32_t)id;
+      tgt[i] = (int32_t)tok[r * ld + t + 1];
+      k = ((unsigned long long)(uint32_t)id << 32) | (uint32_t)i;
+    }
+    keys[i] = k;
+  }
+  __syncthreads();
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < n2; i += TP_THREADS) {
+        const int p = i ^ j;
+        if (p > i) {
+          const unsigned long long a = keys[i], c = keys[p];
+          if ((a > c) == ((i & k) == 0)) {
+            keys[i] = c;
+            keys[p] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // segment boundaries: a contiguous chunk of sorted positions per thread, block-wide scan
+  const int per = (n + TP_THREADS - 1) / TP_THREADS;
+  const int lo = min(n, tid * per), hi = min(n, lo + per);
+  int cnt = 0;
+  for (int i = lo; i < hi; ++i) cnt += (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32));
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((tid & 31) >= o) incl += y;
+  }
+  if ((tid & 31) == 31) wsum[tid >> 5] = incl;
+  __syncthreads();
+  if (tid < 32) {
+    int w = wsum[tid], wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (tid >= o) wi += y;
+    }
+    wsum[tid] = wi - w;  // exclusive prefix over warps
+  }
+  __syncthreads();
+  int seg = wsum[tid >> 5] + incl - cnt;
+  for (int i = lo; i < hi; ++i) {
+    const unsigned long long key = keys[i];
+    perm[i] = (int32_t)(uint32_t)key;
+    if (i == 0 || (key >> 32) != (keys[i - 1] >> 32)) {
+      seg_start[seg] = i;
+      seg_id[seg] = (int32_t)(key >> 32);
+      ++seg;
+    }
+  }
+  if (hi == n && lo < hi) {  // the thread holding the last position
+    seg_start[seg] = n;
+    n_seg[0] = seg;
+  }
+}
+
 // ---------------------------------------------------------------- softmax cross-entropy
 // One CTA per row: loss_r = logsumexp(z) - z[target]; dlogits = (softmax(z) - onehot) * scale
 // written in place over the bf16 logits.
@@ -641,6 +726,29 @@ extern "C" int spx_embed_bwd(const int32_t* perm, const int32_t* seg_start, cons
   spx_launch_check(launch_k(embed_bwd_kernel, dim3((unsigned)max_segments), dim3(128), 0, SPX_S, perm, seg_start, seg_id, n_segments, CBF(dout), dtable,
                                                               (int)d));
   return check_launch("embed_bwd_kernel");
+}
+
+extern "C" int spx_token_prep(const int64_t* tokens, int64_t b, int64_t T, int64_t ld_tokens, int32_t* ids,
+                              int32_t* targets, int32_t* perm, int32_t* seg_start, int32_t* seg_id, int32_t* n_segments,
+                              void* stream) {
+  const int64_t n = b * T;
+  if (b <= 0 || T <= 0) return set_error(SPX_ERR_ARG, "token_prep: b and T must be positive");
+  if (n > TP_MAX_N) return set_error(SPX_ERR_ARG, "token_prep: b*T must be <= 16384 (one-CTA sort)");
+  if (ld_tokens < T + 1) return set_error(SPX_ERR_ARG, "token_prep: ld_tokens must be >= T + 1");
+  int n2 = 1;
+  while (n2 < n) n2 <<= 1;
+  const size_t smem = (size_t)n2 * sizeof(unsigned long long);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(token_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         TP_MAX_N * (int)sizeof(unsigned long long));
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(token_prep)");
+    attr = true;
+  }
+  spx_launch_check(launch_k(token_prep_kernel, dim3(1), dim3(TP_THREADS), smem, SPX_S,
+                            reinterpret_cast<const long long*>(tokens), (int)T, (long long)ld_tokens, (int)n, n2, ids,
+                            targets, perm, seg_start, seg_id, n_segments));
+  return check_launch("token_prep_kernel");
 }
 
 extern "C" int spx_xent_fwd_bwd(void* logits, const int32_t* targets, float* row_loss, int64_t n, int64_t V, int64_t ld,

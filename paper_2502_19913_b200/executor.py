@@ -140,6 +140,7 @@ class SlotBuffers:
         # owned so a cross-GPU send can drain asynchronously on the send stream
         self.gout = torch.empty(n, cfg.d, **e) if not origin else None
         if origin:
+            self.tok = torch.zeros(b, T + 1, dtype=torch.int64, device=device)  # raw token block
             self.ids = torch.zeros(n, dtype=torch.int32, device=device)
             self.targets = torch.zeros(n, dtype=torch.int32, device=device)
             self.perm = torch.zeros(n, dtype=torch.int32, device=device)
@@ -419,6 +420,12 @@ class Trainer:
         self.paths = {a: schedule.paths[a].nodes for a in self.agents}
         self.slot_of, self.n_slots = static_slots(schedule, topology.n)
         self.hops = hop_plan(self.ops, self.paths, self.placement)
+        origin: dict = {}
+        for op in self.ops:  # token_prep at F pos 0 feeds the L and B pos 0 ops of the same origin slot
+            if (op.kind == F and op.pos == 0) or op.kind == L or (op.kind == B and op.pos == 0):
+                if origin.setdefault((op.agent, op.wave), op.node) != op.node:
+                    raise ValidationError(f"agent {op.agent} wave {op.wave}: embed, loss and embed-backward "
+                                          f"ops on different nodes")
         self.my_nodes = [v for v in range(topology.n) if self.placement[v] == rank]
         self.my_stages = sorted({self.node_stage[v] for v in self.my_nodes})
         self.stage_ranks = {st: sorted({self.placement[v] for v in range(topology.n) if self.node_stage[v] == st})
@@ -569,21 +576,17 @@ class Trainer:
 
     # ---- inputs ----
     def _stage_inputs(self, tokens: torch.Tensor):
-        """Pinned host copies of ids / targets / embedding-backward segments for every microbatch."""
+        """The step's host input: the token blocks [M, b, T+1] (int64) in pinned memory.  Inputs,
+        targets and the embedding-backward grouping are derived on the device (``token_prep``)."""
         M, b, T1 = tokens.shape
         if M != self.M or b != self.b or T1 != self.T + 1:
             raise ValidationError(f"tokens shape {tuple(tokens.shape)} != ({self.M}, {self.b}, {self.T + 1})")
-        ids = tokens[:, :, :-1].reshape(M, -1).to(torch.int32)
-        tgt = tokens[:, :, 1:].reshape(M, -1).to(torch.int32)
-        segs = [native.embed_segments(ids[mb]) for mb in range(M)]
-        pin = lambda t: t.contiguous().pin_memory()  # noqa: E731
-        return {"ids": pin(ids), "tgt": pin(tgt), "perm": pin(torch.stack([s_[0] for s_ in segs])),
-                "seg_start": pin(torch.stack([s_[1] for s_ in segs])), "seg_id": pin(torch.stack([s_[2] for s_ in segs])),
-                "n_seg": pin(torch.stack([s_[3] for s_ in segs]))}
+        t = tokens.to(torch.int64).contiguous()
+        return {"tokens": t if t.is_pinned() else t.pin_memory()}
 
     def h2d_bytes(self, tokens: torch.Tensor) -> int:
-        """Bytes of token-derived inputs this rank copies host->device per iteration."""
-        per = 4 * (self.n + self.n + self.n + (self.n + 1) + self.n + 1)
+        """Bytes of token blocks this rank copies host->device per iteration."""
+        per = 8 * self.b * (self.T + 1)
         mine = sum(1 for op in self.ops if op.kind == F and op.pos == 0 and self.placement[op.node] == self.rank)
         return mine * per
 
@@ -631,14 +634,11 @@ class Trainer:
                     key = self._key(op)
                     sb = self.slots[(v, key[2])]
                     if op.kind == F and op.pos == 0:
-                        _h2d(sb.ids, host["ids"][mb], sv)
-                    if op.kind == L:
-                        _h2d(sb.targets, host["tgt"][mb], sv)
-                    if op.kind == B and op.pos == 0:
-                        _h2d(sb.perm, host["perm"][mb], sv)
-                        _h2d(sb.seg_start, host["seg_start"][mb], sv)
-                        _h2d(sb.seg_id, host["seg_id"][mb], sv)
-                        _h2d(sb.n_seg, host["n_seg"][mb], sv)
+                        # the slot keeps ids / targets / grouping until this microbatch's L and B
+                        # ops at the origin (same node, same slot, same stream)
+                        _h2d(sb.tok, host["tokens"][mb], sv)
+                        native.token_prep(sb.tok, sb.ids, sb.targets, sb.perm, sb.seg_start, sb.seg_id, sb.n_seg,
+                                          b=self.b, T=self.T, stream=sv)
                     w = pending.pop((op.kind, v, op.agent, op.wave), None)
                     if w is not None:
                         if w[0] == "nccl":
@@ -761,7 +761,8 @@ class Trainer:
             raise ValidationError("launch accounting needs use_graphs=True")
         opt = 2 * len(self.psets) + 1 + len(self.psets) + sum(len(gl) for gl in self.extra_grads.values())
         mine = [self._key(op) for op in self.ops if self.placement[op.node] == self.rank]
-        return sum(self._graph_launches[k] + (self._graph_launches[(LW,) + k[1:]] if k[0] == L else 0)
+        prep = sum(1 for op in self.ops if op.kind == F and op.pos == 0 and self.placement[op.node] == self.rank)
+        return prep + sum(self._graph_launches[k] + (self._graph_launches[(LW,) + k[1:]] if k[0] == L else 0)
                    for k in mine) + opt
 
     def gemm_counts_per_step(self) -> dict:

@@ -41,6 +41,7 @@ SIGNATURES: dict[str, list] = {
     "spx_swiglu_bwd": [_P, _P, _P, _I64, _I64, _P],
     "spx_embed_fwd": [_P, _P, _P, _I64, _I64, _P],
     "spx_embed_bwd": [_P, _P, _P, _P, _I64, _P, _P, _I64, _P],
+    "spx_token_prep": [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P],
     "spx_xent_fwd_bwd": [_P, _P, _P, _I64, _I64, _I64, _F, _P],
     "spx_sum_f32": [_P, _I64, _P, _F, _I32, _P],
     "spx_add_f32": [_P, _P, _I64, _P],
@@ -271,9 +272,17 @@ def embed_bwd(perm, seg_start, seg_id, n_segments, max_segments, dout, dtable, *
                                 _ptr(dout), _ptr(dtable), d, _stream(stream)), "spx_embed_bwd")
 
 
+def token_prep(tokens, ids, targets, perm, seg_start, seg_id, n_segments, *, b, T, ld=None, stream=None) -> None:
+    """Device-side split of a [b, T+1] int64 token block into ids / targets and the embedding-
+    backward grouping (same values as ``embed_segments`` on the host)."""
+    _check(load().spx_token_prep(_ptr(tokens), b, T, T + 1 if ld is None else ld, _ptr(ids), _ptr(targets), _ptr(perm),
+                                 _ptr(seg_start), _ptr(seg_id), _ptr(n_segments), _stream(stream)), "spx_token_prep")
+
+
 def embed_segments(ids) -> tuple:
     """Host-side grouping of token positions by id for the deterministic embedding backward:
-    (perm, seg_start, seg_id, n_segments) as int32 CPU tensors padded to len(ids)."""
+    (perm, seg_start, seg_id, n_segments) as int32 CPU tensors padded to len(ids).  The executor
+    computes the same grouping on the device (``token_prep``); this is the tests' reference."""
     import torch
 
     ids = ids.reshape(-1).to(torch.int64).cpu()

@@ -182,6 +182,38 @@ def test_embedding():
     assert rel(dtab, ref) < 1e-5
 
 
+@pytest.mark.parametrize("b,T,V,pad", [(1, 1, 7, 0), (2, 5, 3, 1), (4, 1024, 32000, 0), (3, 700, 50, 3),
+                                       (1, 16384, 128256, 0), (16, 1024, 5, 0)])
+def test_token_prep_matches_host_grouping(b, T, V, pad):
+    """Device token split + (id, position) grouping == the host reference, incl. heavy collisions,
+    ragged n (not a power of two), row padding and the n = 16384 maximum."""
+    g = torch.Generator().manual_seed(b * 7 + T)
+    tok = torch.randint(0, V, (b, T + 1 + pad), generator=g, dtype=torch.int64)
+    n = b * T
+    dt = tok.to(dev)
+    ids, tgt, perm, sid = (torch.full((n,), -1, dtype=torch.int32, device=dev) for _ in range(4))
+    seg = torch.full((n + 1,), -1, dtype=torch.int32, device=dev)
+    nseg = torch.zeros(1, dtype=torch.int32, device=dev)
+    native.token_prep(dt, ids, tgt, perm, seg, sid, nseg, b=b, T=T, ld=T + 1 + pad)
+    torch.cuda.synchronize()
+    ref_ids = tok[:, :T].reshape(-1).to(torch.int32)
+    assert torch.equal(ids.cpu(), ref_ids)
+    assert torch.equal(tgt.cpu(), tok[:, 1:T + 1].reshape(-1).to(torch.int32))
+    rp, rs, ri, rn = native.embed_segments(ref_ids)
+    k = int(rn.item())
+    assert int(nseg.item()) == k
+    assert torch.equal(perm.cpu(), rp)
+    assert torch.equal(seg.cpu()[:k + 1], rs[:k + 1])
+    assert torch.equal(sid.cpu()[:k], ri[:k])
+
+
+def test_token_prep_rejects_oversize():
+    t = torch.zeros(1, 16386, dtype=torch.int64, device=dev)
+    z = torch.zeros(16386, dtype=torch.int32, device=dev)
+    with pytest.raises(native.NativeError, match="16384"):
+        native.token_prep(t, z, z, z, z, z, z, b=1, T=16385)
+
+
 @pytest.mark.parametrize("n,V", [(512, 32000), (300, 1024)])
 def test_xent(n, V):
     g = torch.Generator().manual_seed(V)
