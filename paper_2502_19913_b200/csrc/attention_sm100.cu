@@ -8,10 +8,11 @@
 //   warp 1      single-thread tcgen05.mma issuer:  S_j = Q K_j^T  (M=128, N=128, K=hd) into one of
 //               two TMEM buffers, then O += P_j V_j (M=128, N=hd, K=128; V as an MN-major operand)
 //   warp 2      TMEM allocation (512 columns: S0, S1, O)
-//   warps 4-7   softmax: thread = query row (its TMEM lane).  Reads S_j, keeps running max/sum in
-//               the exp2 domain (split accumulators: no long dependent chains), rescales O in TMEM
-//               when the max grows, writes P_j (bf16) into a swizzled smem tile (A of the PV MMA),
-//               and at the end of an item writes O / l and the LSE.
+//   warps 4-11  softmax: thread = query row (its TMEM lane), two warps per lane quadrant splitting
+//               the 128 keys of a block.  Reads S_j, keeps running max/sum in the exp2 domain
+//               (split accumulators: no long dependent chains; lazy rescaling), rescales O in TMEM
+//               when the max grows by more than 2^8, writes P_j (bf16 pairs) into TMEM (A of the PV
+//               MMA), and at the end of an item writes O / l and the LSE.
 // S_{j+1} overlaps the softmax of block j; the next item's S MMAs overlap the previous item's
 // epilogue.  O and LSE match attn_fwd_kernel (attention.cu).
 #include <cmath>
@@ -24,8 +25,9 @@ namespace fa {
 
 constexpr int BM = 128;    // query rows per work item
 constexpr int BN = 128;    // keys per block
-constexpr int THREADS = 256;
+constexpr int THREADS = 384;  // 4 role warps + 8 softmax warps (2 per TMEM lane quadrant)
 constexpr float LOG2E = 1.4426950408889634f;
+constexpr float RESCALE_LOG2 = 8.f;  // lazy-rescale threshold (log2 domain)
 
 SPX_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
@@ -39,6 +41,8 @@ SPX_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
       : "memory");
 }
 SPX_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// named barrier over the two softmax warps that share a TMEM lane quadrant
+SPX_DEVICE void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
 // Heavy-first item lists are dealt to CTAs in boustrophedon order (round k: CTA c takes item
 // k*G + c for even k, k*G + G-1-c for odd k), pairing heavy and light items per CTA.
@@ -83,8 +87,11 @@ struct FwdSmem {
   static constexpr int OFF_K = OFF_Q + Q_BYTES;        // [NK]
   static constexpr int OFF_V = OFF_K + NK * Q_BYTES;   // [NV]
   static constexpr int OFF_BAR = OFF_V + NV * Q_BYTES;
+  // row-max exchange between the two column halves of a row: [block parity][half][row], then the
+  // row-sum exchange at the end of an item: [half][row]
+  static constexpr int OFF_RED = OFF_BAR + 256;
   // >= 116 KB: one CTA per SM (it owns all 512 TMEM columns)
-  static constexpr int RAW = OFF_BAR + 256;
+  static constexpr int RAW = OFF_RED + 6 * BM * 4;
   static constexpr int BYTES = RAW > 116 * 1024 ? RAW : 116 * 1024;
 };
 
@@ -127,10 +134,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&v_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&p_full[i], 4);
+      mbar_init(&p_full[i], 8);
       mbar_init(&pv_done[i], 1);
     }
-    mbar_init(o_free, 4);
+    mbar_init(o_free, 8);
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -232,10 +239,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_n);
   } else if (warp >= 4) {
-    // ---------------- softmax (thread = query row) ----------------
-    const int q = warp - 4;
+    // ---------------- softmax (thread = query row, warp pair = column halves) ----------------
+    // warps 4-7 take keys [0, 64) of each block, warps 8-11 keys [64, 128), for the rows of TMEM
+    // lane quadrant warp % 4: two warps per SM sub-partition interleave their ex2 / FMA chains.
+    // The halves exchange their row maxima through shared memory each block (same running max m
+    // and rescale factor in both), keep separate row sums (added at the end of an item) and each
+    // rescales / normalises its own half of O's columns.
+    constexpr int HB = BN / 2;   // keys per half
+    constexpr int HO = HD / 2;   // O columns per half
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
     const int r = q * 32 + lane;  // row within the block
+    const int bar_id = 1 + q;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    float* red = reinterpret_cast<float*>(smem + L::OFF_RED);  // [2][2][BM] maxima, then [2][BM] sums
     const float sl2 = p.scale * LOG2E;
     int g = 0;
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
@@ -246,51 +263,61 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int s = g & 1;
         mbar_wait(&s_full[s], (g >> 1) & 1);
         tc_fence_after();
-        float x[BN];
+        float x[HB];
         {
           uint32_t* xv = reinterpret_cast<uint32_t*>(x);
 #pragma unroll
-          for (int c = 0; c < BN; c += 32)
-            tmem_ld_32x32b_x32(lane_base + s * BN + c, *reinterpret_cast<uint32_t(*)[32]>(xv + c));
+          for (int c = 0; c < HB; c += 32)
+            tmem_ld_32x32b_x32(lane_base + s * BN + half * HB + c, *reinterpret_cast<uint32_t(*)[32]>(xv + c));
           tmem_ld_wait();
         }
         if (j == it.qb) {
 #pragma unroll
-          for (int i = 0; i < BN; ++i)
-            if (i > r) x[i] = -INFINITY;
+          for (int i = 0; i < HB; ++i)
+            if (half * HB + i > r) x[i] = -INFINITY;
         }
-        // row max with 8 independent accumulators (raw scores; the scale is positive)
+        // half-row max with 8 independent accumulators (raw scores; the scale is positive)
         float mk[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) mk[k] = x[k];
 #pragma unroll
-        for (int i = 8; i < BN; ++i) mk[i & 7] = fmaxf(mk[i & 7], x[i]);
-        const float mraw = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])),
-                                 fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
-        const float mx = fmaxf(m, mraw * sl2);
-        const float alpha = ex2(m - mx);  // 0 on the first block (m = -inf)
-        m = mx;
+        for (int i = 8; i < HB; ++i) mk[i & 7] = fmaxf(mk[i & 7], x[i]);
+        float mraw = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])),
+                           fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
+        red[(s * 2 + half) * BM + r] = mraw;
+        pair_bar(bar_id);
+        mraw = fmaxf(mraw, red[(s * 2 + (half ^ 1)) * BM + r]);
+        // lazy rescaling: the running max m only moves when the block's max exceeds it by more
+        // than 2^8 (P <= 256 is exact enough in bf16 and O / l is invariant to the choice of m),
+        // so after the first block O is rarely rescaled and the softmax rarely has to wait for
+        // the previous block's PV
+        const float mx = mraw * sl2;
+        float alpha = 1.f;
+        if (mx > m + RESCALE_LOG2) {
+          alpha = ex2(m - mx);  // 0 on the first block (m = -inf)
+          m = mx;
+        }
         float sk[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int i = 0; i < BN; ++i) {
+        for (int i = 0; i < HB; ++i) {
           x[i] = ex2(fmaf(x[i], sl2, -m));
           sk[i & 7] += x[i];
         }
         l = l * alpha + (((sk[0] + sk[1]) + (sk[2] + sk[3])) + ((sk[4] + sk[5]) + (sk[6] + sk[7])));
-        // rescale O rows whose max grew (warp-uniform decision; tcgen05.ld/st are warp-collective);
-        // only then does this block wait for the previous block's PV
+        // rescale this half's O columns for rows whose max grew (warp-uniform decision, identical
+        // in both halves); only then does this block wait for the previous block's PV
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
           mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
           tc_fence_after();
           {
 #pragma unroll
-            for (int c = 0; c < HD; c += 32) {
+            for (int c = 0; c < HO; c += 32) {
               uint32_t v[32];
-              tmem_ld_32x32b_x32(lane_base + TM_O + c, v);
+              tmem_ld_32x32b_x32(lane_base + TM_O + half * HO + c, v);
               tmem_ld_wait();
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-              tmem_st_32x32b_x32(lane_base + TM_O + c, v);
+              tmem_st_32x32b_x32(lane_base + TM_O + half * HO + c, v);
             }
             tmem_st_wait();
           }
@@ -300,28 +327,30 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(&pv_done[g & 1], ((g - 2) >> 1) & 1);
           tc_fence_after();
         }
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
+        {
           uint32_t pk[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) pk[e] = pack_bf16(x[64 * h2 + 2 * e], x[64 * h2 + 2 * e + 1]);
-          tmem_st_32x32b_x32(lane_base + TM_P + (g & 1) * 64 + 32 * h2, pk);
+          for (int e = 0; e < 32; ++e) pk[e] = pack_bf16(x[2 * e], x[2 * e + 1]);
+          tmem_st_32x32b_x32(lane_base + TM_P + (g & 1) * 64 + 32 * half, pk);
         }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[g & 1]);
       }
-      // item epilogue: O / l -> bf16, LSE; then hand O's TMEM back to the MMA warp
+      // item epilogue: O / l -> bf16 (each half its columns), LSE; then hand O back to the MMA warp
+      red[(4 + half) * BM + r] = l;
+      pair_bar(bar_id);
+      l += red[(4 + (half ^ 1)) * BM + r];
       mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
       tc_fence_after();
       const float inv = __frcp_rn(l);
       const int t = it.qb * BM + r;
-      __nv_bfloat16* orow = p.out + (size_t)(it.b * p.T + t) * p.ldo + it.h * HD;
+      __nv_bfloat16* orow = p.out + (size_t)(it.b * p.T + t) * p.ldo + it.h * HD + half * HO;
 #pragma unroll
-      for (int c = 0; c < HD; c += 32) {
+      for (int c = 0; c < HO; c += 32) {
         uint32_t v[32];
-        tmem_ld_32x32b_x32(lane_base + TM_O + c, v);
+        tmem_ld_32x32b_x32(lane_base + TM_O + half * HO + c, v);
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
@@ -332,7 +361,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                          pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv));
         }
       }
-      p.lse[((size_t)it.b * p.H + it.h) * p.T + t] = (m + __log2f(l)) * (1.f / LOG2E);
+      if (half == 0) p.lse[((size_t)it.b * p.H + it.h) * p.T + t] = (m + __log2f(l)) * (1.f / LOG2E);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_free);
