@@ -188,8 +188,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                       (p.H + p.Hkv + kvh) * HD + 64 * a, row0 + j * BN);
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer ----------------
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (whole warp; one elected lane issues) ----------------
     constexpr uint32_t IDESC_S = umma_idesc_bf16(BM, BN, false, false);
     constexpr uint32_t IDESC_O = umma_idesc_bf16(BM, HD, false, true);
     const uint32_t sQ = smem_u32(smem + L::OFF_Q);
@@ -203,13 +203,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(&v_full[s], (gb / NV) & 1);
       tc_fence_after();
       const uint32_t sV = smem_u32(smem + L::OFF_V + s * L::Q_BYTES);
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < BN / 16; ++kk) {
-        const uint64_t bd = umma_desc_sw128(sV + kk * 2048, L::ATOM, 1024);
-        mma_bf16_ts(tmem + TM_O, tmem + TM_P + (gb & 1) * 64 + kk * 8, bd, IDESC_O, (j > 0) || (kk > 0));
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint64_t bd = umma_desc_sw128(sV + kk * 2048, L::ATOM, 1024);
+          mma_bf16_ts(tmem + TM_O, tmem + TM_P + (gb & 1) * 64 + kk * 8, bd, IDESC_O, (j > 0) || (kk > 0));
+        }
+        mma_commit(&pv_done[gb & 1]);
+        mma_commit(&v_empty[s]);
       }
-      mma_commit(&pv_done[gb & 1]);
-      mma_commit(&v_empty[s]);
+      __syncwarp();
     };
     int pend_g = -1, pend_j = 0, pend_n = 0;  // the PV lagging one block behind S
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
@@ -222,15 +225,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(&k_full[sk], (g / NK) & 1);
         tc_fence_after();
         const uint32_t sK = smem_u32(smem + L::OFF_K + sk * L::Q_BYTES);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint64_t ad = umma_desc_sw128(sQ + (kk >> 2) * L::ATOM + (kk & 3) * 32, 16, 1024);
-          const uint64_t bd = umma_desc_sw128(sK + (kk >> 2) * L::ATOM + (kk & 3) * 32, 16, 1024);
-          mma_bf16_ss(tmem + s * BN, ad, bd, IDESC_S, kk > 0);
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint64_t ad = umma_desc_sw128(sQ + (kk >> 2) * L::ATOM + (kk & 3) * 32, 16, 1024);
+            const uint64_t bd = umma_desc_sw128(sK + (kk >> 2) * L::ATOM + (kk & 3) * 32, 16, 1024);
+            mma_bf16_ss(tmem + s * BN, ad, bd, IDESC_S, kk > 0);
+          }
+          mma_commit(&s_full[s]);
+          mma_commit(&k_empty[sk]);
+          if (j == it.qb) mma_commit(q_empty);  // last S of this item issued: Q reusable
         }
-        mma_commit(&s_full[s]);
-        mma_commit(&k_empty[sk]);
-        if (j == it.qb) mma_commit(q_empty);  // last S of this item issued: Q reusable
+        __syncwarp();
         if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_n);
         pend_g = g;
         pend_j = j;

@@ -65,6 +65,16 @@ SPX_DEVICE uint4 lds128(uint32_t addr) {
   return v;
 }
 
+// one lane of a converged warp (elect.sync): lets a whole warp run an issue loop with its
+// descriptors in uniform registers while a single lane issues the tcgen05 instructions
+SPX_DEVICE bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 SPX_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 SPX_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
