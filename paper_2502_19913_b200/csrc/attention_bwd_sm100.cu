@@ -220,8 +220,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         bulk_load(smem + L::OFF_D + s * 512, p.delta + off, 512, &full[s]);
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer ----------------
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (whole warp; one elected lane issues) ----------------
     constexpr uint32_t ID_S = umma_idesc_bf16(BLK, BLK, false, false);   // K.Q^T, V.dO^T
     constexpr uint32_t ID_G = umma_idesc_bf16(BLK, HD, false, true);     // P^T.dO, dS^T.Q
     const uint32_t sK = smem_u32(smem + L::OFF_K), sV = smem_u32(smem + L::OFF_V);
@@ -231,14 +231,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(&full[s], (gi / NST) & 1);
       tc_fence_after();
       const uint32_t sQ = smem_u32(smem + L::OFF_Q + s * L::TILE), sDO = smem_u32(smem + L::OFF_DO + s * L::TILE);
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const uint32_t ko = (kk >> 2) * ATOM + (kk & 3) * 32;
-        mma_bf16_ss(tmem + TM_S, umma_desc_sw128(sK + ko, 16, 1024), umma_desc_sw128(sQ + ko, 16, 1024), ID_S, kk > 0);
-        mma_bf16_ss(tmem + TM_DP, umma_desc_sw128(sV + ko, 16, 1024), umma_desc_sw128(sDO + ko, 16, 1024), ID_S,
-                    kk > 0);
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t ko = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_bf16_ss(tmem + TM_S, umma_desc_sw128(sK + ko, 16, 1024), umma_desc_sw128(sQ + ko, 16, 1024), ID_S,
+                      kk > 0);
+          mma_bf16_ss(tmem + TM_DP, umma_desc_sw128(sV + ko, 16, 1024), umma_desc_sw128(sDO + ko, 16, 1024), ID_S,
+                      kk > 0);
+        }
+        mma_commit(sdp_full);
       }
-      mma_commit(sdp_full);
+      __syncwarp();
     };
     int gi = 0, n = 0;
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
@@ -264,19 +268,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (it == 0) mbar_wait(acc_free, (n & 1) ^ 1);  // previous item's dV/dK read out
         tc_fence_after();
         const uint32_t sQ = smem_u32(smem + L::OFF_Q + s * L::TILE), sDO = smem_u32(smem + L::OFF_DO + s * L::TILE);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BLK / 16; ++kk) {
-          const uint32_t ao = (kk >> 2) * ATOM + (kk & 3) * 32;
-          const uint32_t bo = kk * 2048;
-          const uint32_t acc = (it > 0) || (kk > 0);
-          mma_bf16_ss(tmem + TM_DV, umma_desc_sw128(sPT + ao, 16, 1024), umma_desc_sw128(sDO + bo, ATOM, 1024), ID_G,
-                      acc);
-          mma_bf16_ss(tmem + TM_DK, umma_desc_sw128(sDST + ao, 16, 1024), umma_desc_sw128(sQ + bo, ATOM, 1024), ID_G,
-                      acc);
+          for (int kk = 0; kk < BLK / 16; ++kk) {
+            const uint32_t ao = (kk >> 2) * ATOM + (kk & 3) * 32;
+            const uint32_t bo = kk * 2048;
+            const uint32_t acc = (it > 0) || (kk > 0);
+            mma_bf16_ss(tmem + TM_DV, umma_desc_sw128(sPT + ao, 16, 1024), umma_desc_sw128(sDO + bo, ATOM, 1024),
+                        ID_G, acc);
+            mma_bf16_ss(tmem + TM_DK, umma_desc_sw128(sDST + ao, 16, 1024), umma_desc_sw128(sQ + bo, ATOM, 1024),
+                        ID_G, acc);
+          }
+          mma_commit(mma2_done);
+          mma_commit(&empty[s]);
+          if (it + 1 == n_it) mma_commit(kv_empty);
         }
-        mma_commit(mma2_done);
-        mma_commit(&empty[s]);
-        if (it + 1 == n_it) mma_commit(kv_empty);
+        __syncwarp();
       }
     }
   } else if (warp == 3 && lane == 0) {
@@ -479,7 +486,7 @@ __global__ void __launch_bounds__(DqmSmem<HD>::THREADS, 1)
           tma_load_2d(sd + L::DS_BYTES + a * ATOM, &tmQKV, &full[st], (p.H + kvh) * HD + 64 * a, b * p.T + j * BLK);
       }
     }
-  } else if (warp == 1 && lane == 0) {
+  } else if (warp == 1) {  // MMA issuer: whole warp, one elected lane issues
     constexpr uint32_t ID = umma_idesc_bf16(BLK, HD, true, true);  // dS (MN-major) . K (MN-major)
     int g = 0, n = 0;
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
@@ -494,13 +501,17 @@ __global__ void __launch_bounds__(DqmSmem<HD>::THREADS, 1)
         mbar_wait(&full[st], (g / STAGES) & 1);
         tc_fence_after();
         const uint32_t sd = smem_u32(smem + st * L::STAGE), sk = sd + L::DS_BYTES;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BLK / 16; ++kk)
-          mma_bf16_ss(tmem + acc * HD, umma_desc_sw128(sd + kk * 2048, ATOM, 1024),
-                      umma_desc_sw128(sk + kk * 2048, ATOM, 1024), ID, (j > 0) || (kk > 0));
-        mma_commit(&empty[st]);
+          for (int kk = 0; kk < BLK / 16; ++kk)
+            mma_bf16_ss(tmem + acc * HD, umma_desc_sw128(sd + kk * 2048, ATOM, 1024),
+                        umma_desc_sw128(sk + kk * 2048, ATOM, 1024), ID, (j > 0) || (kk > 0));
+          mma_commit(&empty[st]);
+        }
+        __syncwarp();
       }
-      mma_commit(&acc_full[acc]);
+      if (elect_one()) mma_commit(&acc_full[acc]);
+      __syncwarp();
     }
   } else if (warp >= 4) {
     const int quad = warp - 4;

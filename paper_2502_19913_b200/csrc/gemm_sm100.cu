@@ -224,8 +224,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
     pdl_trigger();  // all loads issued: let the next kernel launch and run its prologue
-  } else if (warp == 1 && lane == 0 && rank == 0) {
-    // ---------------- MMA issuer (single thread; the pair's leader for CG = 2) ----------------
+  } else if (warp == 1 && rank == 0) {
+    // ---------------- MMA issuer (the pair's leader CTA for CG = 2) ----------------
+    // the whole warp runs the loop (descriptors stay in uniform registers); one elected lane
+    // issues the tcgen05 instructions
     constexpr uint32_t IDESC = umma_idesc_bf16(PAIR_M, BN, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
@@ -245,22 +247,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
         const uint32_t sb = sa + Cfg::A_BYTES;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < GEMM_BK / 16; ++kk) {
-          if (args.probe == 1 || args.probe == 6) break;
-          const uint64_t ad = A_MN ? umma_desc_sw128(sa + kk * 2048, GEMM_BK * 128, 1024)
-                                   : umma_desc_sw128(sa + kk * 32, 16, 1024);
-          const uint64_t bd = B_MN ? umma_desc_sw128(sb + kk * 2048, GEMM_BK * 128, 1024)
-                                   : umma_desc_sw128(sb + kk * 32, 16, 1024);
-          if constexpr (CG == 2) mma_bf16_ss_pair(d_tmem, ad, bd, IDESC, (kb != kb0) || (kk != 0));
-          else mma_bf16_ss(d_tmem, ad, bd, IDESC, (kb != kb0) || (kk != 0));
+          for (int kk = 0; kk < GEMM_BK / 16; ++kk) {
+            if (args.probe == 1 || args.probe == 6) break;
+            const uint64_t ad = A_MN ? umma_desc_sw128(sa + kk * 2048, GEMM_BK * 128, 1024)
+                                     : umma_desc_sw128(sa + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? umma_desc_sw128(sb + kk * 2048, GEMM_BK * 128, 1024)
+                                     : umma_desc_sw128(sb + kk * 32, 16, 1024);
+            if constexpr (CG == 2) mma_bf16_ss_pair(d_tmem, ad, bd, IDESC, (kb != kb0) || (kk != 0));
+            else mma_bf16_ss(d_tmem, ad, bd, IDESC, (kb != kb0) || (kk != 0));
+          }
+          if constexpr (CG == 2) mma_commit_pair(&empty_bar[stage]);
+          else mma_commit(&empty_bar[stage]);
         }
-        if constexpr (CG == 2) mma_commit_pair(&empty_bar[stage]);
-        else mma_commit(&empty_bar[stage]);
+        __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if constexpr (CG == 2) mma_commit_pair(&tfull_bar[acc]);
-      else mma_commit(&tfull_bar[acc]);
+      if (elect_one()) {
+        if constexpr (CG == 2) mma_commit_pair(&tfull_bar[acc]);
+        else mma_commit(&tfull_bar[acc]);
+      }
+      __syncwarp();
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> fused op -> swizzled smem box -> TMA ----------
