@@ -176,8 +176,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();  // upstream grid complete before any dependent global access
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer ----------------
+  if (warp == 0) {
+    // ---------------- TMA producer (whole warp; one elected lane issues) ----------------
     int stage = 0;
     uint32_t phase = 0;
     // both CTAs of a pair count their bytes on the leader's full barrier
@@ -202,24 +202,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
         uint8_t* sb = sa + Cfg::A_BYTES;
         if (args.probe == 2 || args.probe == 4) {
-          if (rank == 0) mbar_arrive(&full_bar[stage]);
+          if (rank == 0 && elect_one()) mbar_arrive(&full_bar[stage]);
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           continue;
         }
-        if (rank == 0) mbar_expect_tx(&full_bar[stage], CG * Cfg::STAGE_BYTES);
         const int k0 = kb * GEMM_BK;
-        if (A_MN) {
+        if (elect_one()) {
+          if (rank == 0) mbar_expect_tx(&full_bar[stage], CG * Cfg::STAGE_BYTES);
+          if (A_MN) {
 #pragma unroll
-          for (int a = 0; a < GEMM_BM / 64; ++a) load(sa + a * (GEMM_BK * 128), mA, stage, m0 + 64 * a, k0);
-        } else {
-          load(sa, mA, stage, k0, m0);
-        }
-        if (B_MN) {
+            for (int a = 0; a < GEMM_BM / 64; ++a) load(sa + a * (GEMM_BK * 128), mA, stage, m0 + 64 * a, k0);
+          } else {
+            load(sa, mA, stage, k0, m0);
+          }
+          if (B_MN) {
 #pragma unroll
-          for (int a = 0; a < BN / CG / 64; ++a) load(sb + a * (GEMM_BK * 128), mB, stage, nb + 64 * a, k0);
-        } else {
-          load(sb, mB, stage, k0, nb);
+            for (int a = 0; a < BN / CG / 64; ++a) load(sb + a * (GEMM_BK * 128), mB, stage, nb + 64 * a, k0);
+          } else {
+            load(sb, mB, stage, k0, nb);
+          }
         }
+        __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
