@@ -75,6 +75,7 @@ struct GemmArgs {
   int probe;  // pipeline probe (SPX_GEMM_PROBE, benchmarking only): 1 no MMAs, 2 no loads, 3 no epilogue,
               // 4 MMAs only, 5 no output stores, 6 loads only
   int tma_store;  // bf16 outputs leave the staging box by TMA store (SPX_GEMM_TMA_STORE=1) instead of st.global
+  int n_major;    // problem 0's tiles walk N first (consecutive units share an A row block; pick_raster)
 };
 
 // Grouped launch (EPI_F32 only, no split-K): up to GEMM_GROUP_MAX independent problems share one
@@ -195,8 +196,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int tile = q == 0 ? u % num_tiles : lu;
       const int kb0 = q == 0 ? (u / num_tiles) * kbs : 0;
       const int kb1 = q == 0 ? min(num_kb, kb0 + kbs) : pi.num_kb;
-      const int m0 = (tile % pi.num_m) * PAIR_M + (int)rank * GEMM_BM;
-      const int nb = (tile / pi.num_m) * BN + (int)rank * (BN / CG);  // this CTA's B rows
+      const bool nmaj = q == 0 && args.n_major;
+      const int m0 = (nmaj ? tile / num_n : tile % pi.num_m) * PAIR_M + (int)rank * GEMM_BM;
+      const int nb = (nmaj ? tile % num_n : tile / pi.num_m) * BN + (int)rank * (BN / CG);  // this CTA's B rows
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
@@ -349,8 +351,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int split = q == 0 ? u / num_tiles : 0;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int m0 = (tile % pi.num_m) * PAIR_M + (int)rank * GEMM_BM;
-      const int n0 = (tile / pi.num_m) * BN;
+      const bool nmaj = q == 0 && args.n_major;
+      const int m0 = (nmaj ? tile / num_n : tile % pi.num_m) * PAIR_M + (int)rank * GEMM_BM;
+      const int n0 = (nmaj ? tile % num_n : tile / pi.num_m) * BN;
       const int rbase = m0 + wq * 32;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -894,6 +897,21 @@ extern "C" int spx_gemm_bf16_rope(const void* A, const void* B, void* C, int64_t
   return dispatch_256_fixed<EPI_ROPE128, false, false>(A, B, lda, ldb, args, s);
 }
 
+// Tile raster of a single-problem launch.  M-first (default): concurrent units share a B column
+// block and stream all of A once per column of tiles; N-first: they share an A row block and
+// stream B once per row.  When the grid takes more than one wave, pick the order whose re-streamed
+// operand fits L2 (or costs fewer DRAM bytes) -- e.g. the LM-head weight gradient (M = V = 32000,
+// N = d, K = tokens) re-read its 262 MB A operand once per N tile in M-first order.
+static int pick_raster(long long M, long long N, long long K, int bn, int cg) {
+  const long long nm = (M + 128LL * cg - 1) / (128LL * cg), nn = (N + bn - 1) / bn;
+  if (nm * nn <= num_sms() / cg) return 0;  // a single wave: all reuse is concurrent anyway
+  const double l2 = 40e6;                    // L2 bytes a wave can keep resident (two 63 MB halves)
+  const double a = 2.0 * M * K, b = 2.0 * N * K;
+  const double cost_m = (a > l2 ? a * nn : a) + b;
+  const double cost_n = (b > l2 ? b * nm : b) + a;
+  return cost_n < cost_m ? 1 : 0;
+}
+
 extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* R, void* C2, int64_t M, int64_t N,
                              int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int64_t ldc2, int32_t a_mn_major,
                              int32_t b_mn_major, int32_t epilogue, float beta, void* stream) {
@@ -915,6 +933,7 @@ extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* 
   const int bn = (epilogue == EPI_SWIGLU || epilogue == EPI_F32 || epilogue == EPI_SWIGLU_BWD) ? 256
                  : (use_pair((int)M) ? 256 : pick_bn((int)M, (int)N));  // CTA pairs need 256-col tiles
   if (epilogue == EPI_F32) pick_splits(args, bn);
+  args.n_major = pick_raster(M, N, K, bn, (bn == 256 && use_pair((int)M)) ? 2 : 1);
   switch (epilogue) {
     case EPI_BF16:
       return bn == 256 ? dispatch_256<EPI_BF16>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s)

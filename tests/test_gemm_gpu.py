@@ -70,6 +70,27 @@ def test_gemm_f32_accumulate(M, N, K, split):
     assert _rel(C, ref) < 5e-3
 
 
+@pytest.mark.parametrize("epi", ["f32", "bf16"])
+def test_gemm_n_major_raster(epi):
+    """A multi-wave grid whose A operand exceeds the L2 budget walks N first (pick_raster): the
+    LM-head weight-gradient form (large M, small N) and a K-major bf16 product of the same shape."""
+    M, N, K = 16384, 512, 2048
+    g = torch.Generator().manual_seed(5)
+    if epi == "f32":
+        A, B = _mk(K, M, gen=g), _mk(K, N, gen=g)
+        ref = A.float().t() @ B.float()
+        C = torch.zeros(M, N, dtype=torch.float32, device="cuda")
+        native.gemm(A, B, C, M=M, N=N, K=K, lda=M, ldb=N, ldc=N, a_mn=True, b_mn=True, epilogue=native.EPI_F32,
+                    beta=1.0)
+    else:
+        A, B = _mk(M, K, gen=g), _mk(N, K, gen=g)
+        ref = A.float() @ B.float().t()
+        C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        native.gemm(A, B, C, M=M, N=N, K=K, lda=K, ldb=K, ldc=N)
+    torch.cuda.synchronize()
+    assert _rel(C, ref) < 1e-2
+
+
 def test_gemm_split_k_deterministic():
     M, N, K = 1024, 1024, 4096
     g = torch.Generator().manual_seed(9)
