@@ -137,7 +137,10 @@ int spx_embed_bwd(const int32_t* perm, const int32_t* seg_start, const int32_t* 
  *      tokens[b][ld_tokens] (int64, T+1 used per row) -> ids[n] = tokens[r][t], targets[n] =
  *      tokens[r][t+1] (n = b*T, position r*T + t) and the embedding-backward grouping of
  *      spx_embed_bwd (perm, seg_start, seg_id, *n_segments), computed on the device so a step's
- *      only host->device input is the token block.  n <= 16384; ids must be < 2^31. */
+ *      only host->device input is the token block.  n <= 16384; ids must be < 2^31.  ids / targets
+ *      may be NULL (grouping only); perm == NULL (with the other grouping outputs NULL) splits ids /
+ *      targets only, with a fast many-CTA kernel -- the executor splits on the compute stream and
+ *      sorts on a side stream, since only the embedding backward needs the grouping. */
 int spx_token_prep(const int64_t* tokens, int64_t b, int64_t T, int64_t ld_tokens, int32_t* ids, int32_t* targets,
                    int32_t* perm, int32_t* seg_start, int32_t* seg_id, int32_t* n_segments, void* stream);
 

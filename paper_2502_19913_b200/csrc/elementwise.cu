@@ -357,8 +357,8 @@ __global__ void __launch_bounds__(TP_THREADS) token_prep_kernel(const long long*
     if (i < n) {
       const int r = i / T, t = i - r * T;
       const long long id = tok[r * ld + t];
-      ids[i] = (int32_t)id;
-      tgt[i] = (int32_t)tok[r * ld + t + 1];
+      if (ids) ids[i] = (int32_t)id;
+      if (tgt) tgt[i] = (int32_t)tok[r * ld + t + 1];
       k = ((unsigned long long)(uint32_t)id << 32) | (uint32_t)i;
     }
     keys[i] = k;
@@ -414,6 +414,17 @@ __global__ void __launch_bounds__(TP_THREADS) token_prep_kernel(const long long*
     seg_start[seg] = n;
     n_seg[0] = seg;
   }
+}
+
+// split only (no grouping): ids / targets of one token block, one thread per position
+__global__ void token_split_kernel(const long long* __restrict__ tok, int T, long long ld, int n,
+                                   int32_t* __restrict__ ids, int32_t* __restrict__ tgt) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int r = i / T, t = i - r * T;
+  if (ids) ids[i] = (int32_t)tok[r * ld + t];
+  if (tgt) tgt[i] = (int32_t)tok[r * ld + t + 1];
 }
 
 // ---------------------------------------------------------------- softmax cross-entropy
@@ -735,6 +746,14 @@ extern "C" int spx_token_prep(const int64_t* tokens, int64_t b, int64_t T, int64
   if (b <= 0 || T <= 0) return set_error(SPX_ERR_ARG, "token_prep: b and T must be positive");
   if (n > TP_MAX_N) return set_error(SPX_ERR_ARG, "token_prep: b*T must be <= 16384 (one-CTA sort)");
   if (ld_tokens < T + 1) return set_error(SPX_ERR_ARG, "token_prep: ld_tokens must be >= T + 1");
+  if (perm == nullptr) {  // split only: ids / targets, no embedding-backward grouping
+    if (seg_start || seg_id || n_segments) return set_error(SPX_ERR_ARG, "token_prep: grouping needs perm");
+    spx_launch_check(launch_k(token_split_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, SPX_S,
+                              reinterpret_cast<const long long*>(tokens), (int)T, (long long)ld_tokens, (int)n, ids,
+                              targets));
+    return check_launch("token_split_kernel");
+  }
+  if (!seg_start || !seg_id || !n_segments) return set_error(SPX_ERR_ARG, "token_prep: grouping outputs missing");
   int n2 = 1;
   while (n2 < n) n2 <<= 1;
   const size_t smem = (size_t)n2 * sizeof(unsigned long long);

@@ -474,6 +474,9 @@ class Trainer:
             self.send_stream = torch.cuda.Stream(device=self.dev)
             # weight-gradient GEMMs run on a side stream, forked/joined per layer inside the B graphs
             self.side_stream = torch.cuda.Stream(device=self.dev) if side_on else None
+            # embedding-backward grouping (token sort) of each microbatch, off the compute streams
+            self.prep_stream = torch.cuda.Stream(device=self.dev)
+            self._prep_done: dict = {}
             if self.node_streams:
                 self.nstream = {v: torch.cuda.Stream(device=self.dev) for v in self.my_nodes}
                 self.nside = {v: (torch.cuda.Stream(device=self.dev) if side_on else None) for v in self.my_nodes}
@@ -635,10 +638,22 @@ class Trainer:
                     sb = self.slots[(v, key[2])]
                     if op.kind == F and op.pos == 0:
                         # the slot keeps ids / targets / grouping until this microbatch's L and B
-                        # ops at the origin (same node, same slot, same stream)
+                        # ops at the origin (same node, same slot, same stream).  The embed needs
+                        # only ids: split them here, sort for the embedding backward on the prep
+                        # stream (joined before the B op at the origin)
                         _h2d(sb.tok, host["tokens"][mb], sv)
-                        native.token_prep(sb.tok, sb.ids, sb.targets, sb.perm, sb.seg_start, sb.seg_id, sb.n_seg,
-                                          b=self.b, T=self.T, stream=sv)
+                        native.token_prep(sb.tok, sb.ids, sb.targets, None, None, None, None, b=self.b, T=self.T,
+                                          stream=sv)
+                        staged = torch.cuda.Event()
+                        staged.record(sv)
+                        self.prep_stream.wait_event(staged)
+                        native.token_prep(sb.tok, None, None, sb.perm, sb.seg_start, sb.seg_id, sb.n_seg, b=self.b,
+                                          T=self.T, stream=self.prep_stream)
+                        grouped = torch.cuda.Event()
+                        grouped.record(self.prep_stream)
+                        self._prep_done[(v, key[2])] = grouped
+                    if op.kind == B and op.pos == 0:
+                        sv.wait_event(self._prep_done.pop((v, key[2])))
                     w = pending.pop((op.kind, v, op.agent, op.wave), None)
                     if w is not None:
                         if w[0] == "nccl":
@@ -684,6 +699,7 @@ class Trainer:
             for cs in streams:
                 if cs is not s:
                     s.wait_stream(cs)
+            s.wait_stream(self.prep_stream)
             self._finish_step(sends)
             t_iter1.record(s)
             torch.cuda.current_stream(self.dev).wait_stream(s)
@@ -761,7 +777,7 @@ class Trainer:
             raise ValidationError("launch accounting needs use_graphs=True")
         opt = 2 * len(self.psets) + 1 + len(self.psets) + sum(len(gl) for gl in self.extra_grads.values())
         mine = [self._key(op) for op in self.ops if self.placement[op.node] == self.rank]
-        prep = sum(1 for op in self.ops if op.kind == F and op.pos == 0 and self.placement[op.node] == self.rank)
+        prep = 2 * sum(1 for op in self.ops if op.kind == F and op.pos == 0 and self.placement[op.node] == self.rank)
         return prep + sum(self._graph_launches[k] + (self._graph_launches[(LW,) + k[1:]] if k[0] == L else 0)
                    for k in mine) + opt
 

@@ -184,9 +184,11 @@ def test_embedding():
 
 @pytest.mark.parametrize("b,T,V,pad", [(1, 1, 7, 0), (2, 5, 3, 1), (4, 1024, 32000, 0), (3, 700, 50, 3),
                                        (1, 16384, 128256, 0), (16, 1024, 5, 0)])
-def test_token_prep_matches_host_grouping(b, T, V, pad):
+@pytest.mark.parametrize("mode", ["fused", "split+group"])
+def test_token_prep_matches_host_grouping(b, T, V, pad, mode):
     """Device token split + (id, position) grouping == the host reference, incl. heavy collisions,
-    ragged n (not a power of two), row padding and the n = 16384 maximum."""
+    ragged n (not a power of two), row padding and the n = 16384 maximum; in one call, or as the
+    executor issues it (split on one stream, grouping-only call after it)."""
     g = torch.Generator().manual_seed(b * 7 + T)
     tok = torch.randint(0, V, (b, T + 1 + pad), generator=g, dtype=torch.int64)
     n = b * T
@@ -194,7 +196,11 @@ def test_token_prep_matches_host_grouping(b, T, V, pad):
     ids, tgt, perm, sid = (torch.full((n,), -1, dtype=torch.int32, device=dev) for _ in range(4))
     seg = torch.full((n + 1,), -1, dtype=torch.int32, device=dev)
     nseg = torch.zeros(1, dtype=torch.int32, device=dev)
-    native.token_prep(dt, ids, tgt, perm, seg, sid, nseg, b=b, T=T, ld=T + 1 + pad)
+    if mode == "fused":
+        native.token_prep(dt, ids, tgt, perm, seg, sid, nseg, b=b, T=T, ld=T + 1 + pad)
+    else:
+        native.token_prep(dt, ids, tgt, None, None, None, None, b=b, T=T, ld=T + 1 + pad)
+        native.token_prep(dt, None, None, perm, seg, sid, nseg, b=b, T=T, ld=T + 1 + pad)
     torch.cuda.synchronize()
     ref_ids = tok[:, :T].reshape(-1).to(torch.int32)
     assert torch.equal(ids.cpu(), ref_ids)
