@@ -8,7 +8,7 @@ replicas, 25% skip, M=32 microbatches of 4x1024 tokens = 131,072 tokens) — F, 
 every microbatch along its scheduled path, replica gradient sync, clip and AdamW.  Inputs are
 synthetic uniform token ids; weights random N(0, 0.02).  At N=1 all 8 logical nodes are
 resident on one GPU; at N>1 (torchrun, one process per GPU) the nodes are placed over the
-GPUs and hops go over NVLink (see dist_trainer.py).
+GPUs and hops go over NVLink (see executor.py; `hops` in the JSON line reports their bandwidth).
 
 `value` is tokens/s with the step's inputs already in HBM; `e2e` is the same metric through the
 public ``Trainer.step(tokens)`` call with host token buffers (H2D staging and the loss readback
@@ -197,7 +197,72 @@ def gemm_roofline(tr, peak_tflops: float, reps: int = 10) -> dict:
             "gemm_ms_per_step": round(total_ms, 3), "per_shape": per}
 
 
-def time_full_pp(args, rc_name, rank=0, world=1, local=0, variant="-full"):
+NVLINK_GBS = 900.0  # NVLink 5 per GPU per direction (18 links x 50 GB/s), nominal: no measured peak
+
+
+def hop_bandwidth(tr, ms_step: float, reps: int = 20) -> dict:
+    """Path-hop transport (north_star: "for the P2P hops as a fraction of NVLink bandwidth").
+
+    Counts the iteration's cross-GPU hops from the executor's hop plan (every rank derives the
+    same plan), then times one hop message (an [n, d] bf16 activation or activation gradient)
+    sent rank 0 -> rank 1 with the executor's own transport (a spx_hop_push into a rank-1 slot,
+    or NCCL send/recv on the pair communicator), alone on a side stream, ``reps`` back-to-back
+    messages bracketed by CUDA events on that stream.
+    All ranks must call it (collective barrier); only ranks 0 and 1 move data."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_19913_b200 import native
+
+    cross = sum(1 for h in tr.hops if h is not None and h[2] != h[3])
+    c = tr.cfg
+    n = tr.b * tr.T
+    msg = n * c.d * 2
+    out = {"cross_gpu_hops_per_step": cross, "msg_bytes": msg, "bytes_per_step": cross * msg,
+           "demand_gbs": round(cross * msg / (ms_step / 1e3) / 1e9, 2)}
+    buf = torch.empty(n, c.d, dtype=torch.bfloat16, device=tr.dev)
+    s = torch.cuda.Stream(tr.dev)
+    peer = tr.hop_transport == "peer"
+    dist.barrier()
+    torch.cuda.synchronize(tr.dev)
+    t = torch.zeros(1, device=tr.dev)
+    if tr.rank in (0, 1):
+        other = 1 - tr.rank
+        if peer:   # a hop-receive slot hosted on rank 1 (same choice on both ranks)
+            key = min(k for k in (tr._peer_addr if tr.rank == 0 else tr._flag_expect) if tr.placement[k[0]] == 1)
+        for it in range(2):                        # warm-up pass, then the timed pass
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(reps):
+                if peer and tr.rank == 0:
+                    native.hop_push(tr._peer_addr[key], buf, msg, tr._peer_flag[key], tr.hop_ctas, stream=s)
+                elif peer:
+                    tr._flag_expect[key] += tr.hop_ctas
+                    native.hop_wait(tr._flag_local[key], tr._flag_expect[key], stream=s)
+                else:
+                    with torch.cuda.stream(s):
+                        if tr.rank == 0:
+                            dist.send(buf, other, group=tr._pair[other])
+                        else:
+                            dist.recv(buf, other, group=tr._pair[other])
+            e1.record(s)
+            torch.cuda.synchronize(tr.dev)
+        if tr.rank == 0:
+            t[0] = e0.elapsed_time(e1) * 1e3 / reps
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    us = float(t.item())
+    gbs = msg / (us / 1e6) / 1e9
+    out.update({"hop_us": round(us, 2), "achieved_gbs": round(gbs, 1), "peak_gbs": NVLINK_GBS,
+                "peak_kind": "nominal NVLink 5 per direction", "frac": round(gbs / NVLINK_GBS, 4),
+                "hop_ms_per_step_if_serial": round(cross * us / 1e3, 3),
+                "transport": tr.hop_transport, "ctas": tr.hop_ctas if peer else None,
+                "how": ("rank0->rank1 spx_hop_push into a rank-1 slot over NVLink peer memory (sender stream)" if peer
+                        else "rank0->rank1 NCCL send/recv on the executor's pair group") +
+                       f", CUDA events, {reps} back-to-back messages after a warm-up pass"})
+    return out
+
+
+def time_full_pp(args, rc_name, rank=0, world=1, local=0, variant="-full", over=None):
     """Same protocol on the full sequential pipeline (dtfm_full, k=0) of the same model on the same
     GPUs — the metric's "vs full PP" comparison — or on another executable baseline variant
     ("-dtfmskip", "-notc2"; configs.VARIANTS).  Returns ms/step (max over ranks)."""
@@ -207,7 +272,7 @@ def time_full_pp(args, rc_name, rank=0, world=1, local=0, variant="-full"):
     from paper_2502_19913_b200.executor import Trainer
     from paper_2502_19913_b200.model import synthetic_tokens
 
-    rf = get_config(rc_name + variant)
+    rf = get_config(rc_name + variant, **(over or {}))
     tokens = synthetic_tokens(rf.model, rf.M, rf.b, rf.T, seed=1234)
     tr = Trainer(rf.schedule(), rf.topology(), rf.sim_config(), rf.model, rf.assignment, b=rf.b, T=rf.T,
                  rank=rank, world=world, device=local)
@@ -245,6 +310,20 @@ def time_baselines(args, rc_name, ms, tok, rank=0, world=1, local=0):
         out[label] = {"workload": rb.name, "ms_per_step": round(bms, 3), "tokens_per_s": round(tok / (bms / 1e3), 1),
                       "skippipe_speedup": round(bms / ms, 4)}
     return out
+
+
+def time_sweep(args, ms_c2, tok, rank=0, world=1, local=0):
+    """BASELINE.json configs[4]: LLaMa-500M skip-ratio sweep 0/25/50 % against the full sequential
+    pipeline, same GPUs, same protocol.  0 % is SkipPipe's scheduler with k=0 (paths may still
+    cross replicas); "full" is DT-FM's disjoint sequential pipelines.  25 % is the headline run."""
+    full_ms, _ = time_full_pp(args, "C2", rank=rank, world=world, local=local, variant="-full")
+    pts = []
+    for pct, name, over in ((0, "C2", {"k": 0}), (25, None, None), (50, "C5", None)):
+        ms = ms_c2 if name is None else time_full_pp(args, name, rank=rank, world=world, local=local, variant="",
+                                                     over=over)[0]
+        pts.append({"skip_pct": pct, "ms_per_step": round(ms, 3), "tokens_per_s": round(tok / (ms / 1e3), 1),
+                    "vs_full_pp_speedup": round(full_ms / ms, 4)})
+    return {"full_pp_ms_per_step": round(full_ms, 3), "points": pts}
 
 
 def run_ours(args, rc):
@@ -303,6 +382,7 @@ def run_ours(args, rc):
                 "ms_per_step": round(fms, 3), "tokens_per_s": round(tok / (fms / 1e3), 1),
                 "skippipe_speedup": round(fms / ms, 4)}
     bl = time_baselines(args, rc.name, ms, tok) if args.baselines and rc.kind == "skippipe" else None
+    sw = time_sweep(args, ms, tok) if args.sweep and rc.name == "C2" else None
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
@@ -321,6 +401,7 @@ def run_ours(args, rc):
         "cpu_baseline": cb,
         "vs_full_pp": full,
         "baselines": bl,
+        "skip_sweep": sw,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -389,6 +470,7 @@ def run_ours_dist(args, rc):
     dist.all_reduce(sm)
     flops = rc.train_flops()
     roof = gemm_roofline(tr, burst) if rank == 0 else None
+    hops = hop_bandwidth(tr, ms)
     full = None
     if not args.no_full_pp and rc.kind == "skippipe":
         del tr
@@ -397,6 +479,7 @@ def run_ours_dist(args, rc):
         full = {"workload": rf.name, "kind": "dtfm_full (k=0, disjoint sequential pipelines)",
                 "ms_per_step": round(fms, 3), "tokens_per_s": round(tok / (fms / 1e3), 1),
                 "skippipe_speedup": round(fms / ms, 4)}
+    sw = time_sweep(args, ms, tok, rank, world, local) if args.sweep and rc.name == "C2" else None
     bl = time_baselines(args, rc.name, ms, tok, rank, world, local) if args.baselines and rc.kind == "skippipe" \
         else None
     if rank == 0:
@@ -416,8 +499,10 @@ def run_ours_dist(args, rc):
             "step_tflops": round(flops / (ms / 1e3) / 1e12, 1),
             "step_tensor_frac": round(flops / (ms / 1e3) / 1e12 / (sustained * world), 4),
             "roofline": {**roof, "peak_kind": f"{peak_kind} burst bf16 (GEMMs timed alone, rank 0)"},
+            "hops": hops,
             "vs_full_pp": full,
             "baselines": bl,
+            "skip_sweep": sw,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -434,6 +519,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full-pp", action="store_true", help="skip the full sequential pipeline comparison")
+    ap.add_argument("--sweep", action="store_true",
+                    help="also run the C5 skip-ratio sweep (0/25/50%% vs full PP) on the same GPUs")
     ap.add_argument("--baselines", action="store_true",
                     help="also execute the DT-FM-skip and SkipPipe-without-TC2 schedules (same protocol)")
     args = ap.parse_args()

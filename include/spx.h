@@ -53,6 +53,22 @@ int spx_enable_peer_access(int32_t dev, int32_t peer);
  * Cross-device copies go peer-to-peer over NVLink.  Replaces comm_time (topology.py:128-136). */
 int spx_hop(int32_t dst_dev, void* dst, int32_t src_dev, const void* src, int64_t bytes, void* stream);
 
+/* Cross-process path hops over NVLink peer memory (one process per GPU).  Also replaces
+ * comm_time (topology.py:128-136) for hops between logical nodes on different GPUs.
+ *   spx_ipc_export: CUDA IPC handle (64 bytes into handle_out) of the allocation holding `ptr`,
+ *                   and ptr's byte offset inside it;
+ *   spx_ipc_open / spx_ipc_close: map / unmap a peer process's allocation (base pointer);
+ *   spx_hop_push: `ctas` CTAs copy `bytes` (multiple of 16, 16-byte aligned) from local src to
+ *                 the peer-mapped dst with 16-byte stores, then each CTA release-adds 1 to the
+ *                 peer-mapped *flag (system scope) once its stores are visible;
+ *   spx_hop_wait: the stream waits until *flag - target >= 0 (acquire, system scope); traps
+ *                 after 120 s so a lost hop fails loudly. */
+int spx_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out);
+int spx_ipc_open(const void* handle, void** base_out);
+int spx_ipc_close(void* base);
+int spx_hop_push(void* dst, const void* src, int64_t bytes, uint32_t* flag, int32_t ctas, void* stream);
+int spx_hop_wait(const uint32_t* flag, uint32_t target, void* stream);
+
 /* ---- GEMM (tcgen05 + TMEM + TMA) ----
  * D[m,n] = sum_k A(m,k) * B(n,k), fp32 accumulate.
  *   a_mn_major = 0: A stored [M][lda] (K contiguous); 1: A stored [K][lda] (M contiguous)

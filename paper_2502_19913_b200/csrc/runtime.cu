@@ -110,3 +110,116 @@ extern "C" int spx_hop(int32_t dst_dev, void* dst, int32_t src_dev, const void* 
   if (e != cudaSuccess) return set_cuda_error(e, "spx_hop");
   return SPX_OK;
 }
+
+// ---- cross-process path hops over NVLink peer memory ----
+//
+// Every rank exports the receive buffers of the logical nodes it hosts (the slot buffers a hop
+// writes: layer-0 input, returned activation, incoming gradient) and one int32 flag per buffer
+// (spx_ipc_export); the ranks that send to it map them (spx_ipc_open).  A hop is then a push:
+// `ctas` CTAs on the sender stream stream the activation into the peer's slot with 16-byte
+// stores over NVLink, and each CTA release-increments the peer's flag once its stores are
+// system-visible.  The consumer's stream runs spx_hop_wait (one thread, acquire loads at system
+// scope) until the flag reaches the count the host expects for that buffer, then the consumer
+// op.  Buffer reuse is safe without a receiver->sender handshake because slots are static per
+// (agent, node) and a slot's next write causally follows its last read (executor.py, DESIGN.md
+// §1 "Static activation slots").
+
+namespace {
+
+typedef int (*MemGetAddressRangeFn)(unsigned long long*, size_t*, unsigned long long);
+
+MemGetAddressRangeFn get_addr_range() {
+  static MemGetAddressRangeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<MemGetAddressRangeFn>(p);
+  });
+  return fn;
+}
+
+__global__ void __launch_bounds__(512) hop_push_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                                       int64_t n16, unsigned int* flag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    uint4 a = __ldg(src + i), b = __ldg(src + i + stride), c = __ldg(src + i + 2 * stride),
+          d = __ldg(src + i + 3 * stride);
+    dst[i] = a;
+    dst[i + stride] = b;
+    dst[i + 2 * stride] = c;
+    dst[i + 3 * stride] = d;
+  }
+  for (; i < n16; i += stride) dst[i] = __ldg(src + i);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
+}
+
+__global__ void hop_wait_kernel(const unsigned int* flag, unsigned int target) {
+  if (threadIdx.x != 0) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned int v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int)(v - target) >= 0) break;
+    __nanosleep(256);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 120ull * 1000000000ull) __trap();  // a lost hop fails loudly instead of hanging
+  }
+}
+
+}  // namespace
+
+extern "C" int spx_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out) {
+  if (!ptr || !handle_out || !offset_out) return set_error(SPX_ERR_ARG, "ipc_export: null argument");
+  MemGetAddressRangeFn range = get_addr_range();
+  if (!range) return set_error(SPX_ERR_CUDA, "ipc_export: cuMemGetAddressRange unavailable");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (unsigned long long)ptr) != 0) return set_error(SPX_ERR_CUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaIpcGetMemHandle");
+  memcpy(handle_out, &h, sizeof h);
+  *offset_out = (int64_t)((unsigned long long)ptr - base);
+  return SPX_OK;
+}
+
+extern "C" int spx_ipc_open(const void* handle, void** base_out) {
+  if (!handle || !base_out) return set_error(SPX_ERR_ARG, "ipc_open: null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  cudaError_t e = cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaIpcOpenMemHandle");
+  return SPX_OK;
+}
+
+extern "C" int spx_ipc_close(void* base) {
+  cudaError_t e = cudaIpcCloseMemHandle(base);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaIpcCloseMemHandle");
+  return SPX_OK;
+}
+
+extern "C" int spx_hop_push(void* dst, const void* src, int64_t bytes, uint32_t* flag, int32_t ctas, void* stream) {
+  if (bytes < 0 || (bytes & 15) || ctas <= 0 || ctas > 1024) return set_error(SPX_ERR_ARG, "hop_push: bad size or ctas");
+  if (!dst || !src || !flag) return set_error(SPX_ERR_ARG, "hop_push: null pointer");
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15)
+    return set_error(SPX_ERR_ARG, "hop_push: buffers must be 16-byte aligned");
+  hop_push_kernel<<<ctas, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), bytes / 16, flag);
+  count_launch();
+  return check_launch("hop_push_kernel");
+}
+
+extern "C" int spx_hop_wait(const uint32_t* flag, uint32_t target, void* stream) {
+  if (!flag) return set_error(SPX_ERR_ARG, "hop_wait: null flag");
+  hop_wait_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flag, target);
+  count_launch();
+  return check_launch("hop_wait_kernel");
+}

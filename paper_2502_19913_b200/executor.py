@@ -384,15 +384,18 @@ class Trainer:
     ``rank``/``world``: one process per GPU (torch.distributed, NCCL).  ``placement[v]`` is the
     rank that hosts logical node v.  Every rank builds the same schedule and simulator op list and
     walks it in the same global order: it runs the ops of its own nodes, sends a path hop to the
-    rank of the next node (NCCL P2P over NVLink; a local ``spx_hop`` copy when both nodes are
-    on this rank) and posts the matching receive for hops that target its nodes.  With world=1
-    (the default) everything is on cuda:<device> and every hop is a local copy."""
+    rank of the next node and posts the matching receive for hops that target its nodes; a local
+    ``spx_hop`` copy when both nodes are on this rank.  ``hop_transport`` (default "peer", env
+    SPX_HOP): "peer" pushes the activation straight into the consumer's slot over NVLink peer
+    memory (spx_hop_push / spx_hop_wait on CUDA-IPC-mapped buffers and arrival flags); "nccl"
+    uses NCCL send/recv on a per-rank-pair communicator.  With world=1 (the default) everything is
+    on cuda:<device> and every hop is a local copy."""
 
     def __init__(self, schedule: Schedule, topology: Topology, sim_config: SimConfig, cfg: ModelConfig,
                  assignment, *, b: int, T: int | None = None, split: list[int] | None = None,
                  placement: list[int] | None = None, seed: int = 0, optim: OptimConfig | None = None,
                  use_graphs: bool = True, params: list | None = None, rank: int = 0, world: int = 1,
-                 device: int | None = None):
+                 device: int | None = None, hop_transport: str | None = None):
         if not torch.cuda.is_available():
             raise native.NativeError("the executor needs a CUDA device (there is no CPU fallback)")
         native.load()
@@ -406,6 +409,11 @@ class Trainer:
         self.optim = optim or OptimConfig()
         self.node_stage = assignment.node_stage()
         self.rank, self.world = rank, world
+        self.hop_transport = hop_transport or os.environ.get("SPX_HOP", "peer")
+        if self.hop_transport not in ("peer", "nccl"):
+            raise ValidationError(f"hop_transport must be 'peer' or 'nccl', not {self.hop_transport!r}")
+        # CTAs per pushed hop (each adds 1 to the slot's arrival flag)
+        self.hop_ctas = int(os.environ.get("SPX_HOP_CTAS", "32"))
         self.report: SimReport = simulate(schedule, topology, sim_config)
         if placement is None:
             placement = balanced_placement(self.report, topology.n, world)
@@ -538,6 +546,60 @@ class Trainer:
                     dist.recv(buf, a, group=self._pair[a])
                     dist.send(buf, a, group=self._pair[a])
         torch.cuda.synchronize(self.dev)
+        if self.hop_transport == "peer":
+            self._init_peer_hops()
+
+    def _init_peer_hops(self):
+        """NVLink peer-memory hops: export this rank's hop-receive buffers (layer-0 input,
+        returned activation, incoming gradient of every hosted slot) and one int32 arrival flag
+        per buffer, map every peer's (spx_ipc_export / spx_ipc_open).  Dedupes allocations: a
+        CUDA IPC handle may be opened once per process."""
+        import torch.distributed as dist
+
+        recv = []
+        for (v, j), sb in sorted(self.slots.items()):
+            recv.append(((v, j, "xs0"), sb.xs[0]))
+            recv.append(((v, j, "gin"), sb.gin))
+            if getattr(sb, "ret", None) is not None:
+                recv.append(((v, j, "ret"), sb.ret))
+        self._flags = torch.zeros(max(1, len(recv)), dtype=torch.int32, device=self.dev)
+        self._flag_local = {k: self._flags.data_ptr() + 4 * i for i, (k, _) in enumerate(recv)}
+        self._flag_expect = {k: 0 for k, _ in recv}
+        mine = {"flags": native.ipc_export(self._flags),
+                "bufs": {k: native.ipc_export(t) for k, t in recv}}
+        allx = [None] * self.world
+        dist.all_gather_object(allx, mine)
+        self._ipc_bases: dict = {}
+        self._peer_addr: dict = {}
+        self._peer_flag: dict = {}
+
+        def addr(hoff):
+            h, off = hoff
+            if h not in self._ipc_bases:
+                self._ipc_bases[h] = native.ipc_open(h)
+            return self._ipc_bases[h] + off
+
+        for r, ex in enumerate(allx):
+            if r == self.rank:
+                continue
+            fbase = addr(ex["flags"])
+            for i, (k, hoff) in enumerate(ex["bufs"].items()):
+                self._peer_addr[k] = addr(hoff)
+                self._peer_flag[k] = fbase + 4 * i
+        torch.cuda.synchronize(self.dev)
+        dist.barrier()
+
+    def close(self):
+        """Unmap peer allocations (peer hop transport)."""
+        for base in getattr(self, "_ipc_bases", {}).values():
+            try:
+                native.ipc_close(base)
+            except Exception:
+                pass
+        self._ipc_bases = {}
+
+    def __del__(self):
+        self.close()
 
     # ---- graph capture ----
     def _run_op(self, kind: str, v: int, slot: int, s):
@@ -659,6 +721,8 @@ class Trainer:
                         if w[0] == "nccl":
                             with torch.cuda.stream(sv):
                                 w[1].wait()        # input arrived from another rank
+                        elif w[0] == "peer":       # pushed by another rank into this slot
+                            native.hop_wait(w[1], w[2], stream=sv)
                         else:                      # local hop from another node's stream
                             _, src, src_ev, dst = w
                             sv.wait_event(src_ev)
@@ -745,11 +809,24 @@ class Trainer:
             ev_out.record(self.nstream[v])
             ss = self.nsend[v]
             ss.wait_event(ev_out)
-            with torch.cuda.stream(ss):
-                sends.append((dist.isend(out, dst_rank, group=self._pair[dst_rank]), ss))
+            if self.hop_transport == "peer":
+                # push straight into the consumer's slot on the peer GPU (static slots: its last
+                # reader causally precedes this producer), then release the slot's arrival flag
+                k = (nv, self.slot_of[(op.agent, nv)], name)
+                native.hop_push(self._peer_addr[k], out, out.numel() * out.element_size(), self._peer_flag[k],
+                                self.hop_ctas, stream=ss)
+                sends.append((None, ss))
+            else:
+                with torch.cuda.stream(ss):
+                    sends.append((dist.isend(out, dst_rank, group=self._pair[dst_rank]), ss))
         elif dst_mine:
             import torch.distributed as dist
 
+            if self.hop_transport == "peer":
+                k = (nv, self.slot_of[(op.agent, nv)], name)
+                self._flag_expect[k] += self.hop_ctas
+                pending[(consumer, nv, op.agent, op.wave)] = ("peer", self._flag_local[k], self._flag_expect[k])
+                return
             buf = self._dst_buffer(op, nv, name)
             # the destination slot was last read by this agent's previous wave on the
             # consumer node, whose ops so far are all on that node's stream
@@ -765,7 +842,8 @@ class Trainer:
         if sends:
             with torch.cuda.stream(s):
                 for w, _ in sends:
-                    w.wait()
+                    if w is not None:
+                        w.wait()
             for ss in dict.fromkeys(ss for _, ss in sends):
                 s.wait_stream(ss)
         self.optimizer_step()

@@ -27,6 +27,11 @@ SIGNATURES: dict[str, list] = {
     "spx_launch_count": [],
     "spx_enable_peer_access": [_I32, _I32],
     "spx_hop": [_I32, _P, _I32, _P, _I64, _P],
+    "spx_ipc_export": [_P, _P, _P],
+    "spx_ipc_open": [_P, _P],
+    "spx_ipc_close": [_P],
+    "spx_hop_push": [_P, _P, _I64, _P, _I32, _P],
+    "spx_hop_wait": [_P, ctypes.c_uint32, _P],
     "spx_gemm_bf16": [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _F, _P],
     "spx_attn_fwd": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P],
     "spx_attn_bwd_ws_floats": [_I64, _I64, _I64, _I64],
@@ -213,6 +218,36 @@ def gemm_set_workspace(partials) -> None:
 
 def hop(dst, dst_dev: int, src, src_dev: int, nbytes: int, stream=None) -> None:
     _check(load().spx_hop(dst_dev, _ptr(dst), src_dev, _ptr(src), nbytes, _stream(stream)), "spx_hop")
+
+
+def ipc_export(t) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding tensor ``t``, byte offset of ``t`` in it)."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64(0)
+    _check(load().spx_ipc_export(_ptr(t), h, ctypes.byref(off)), "spx_ipc_export")
+    return h.raw, int(off.value)
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map a peer process's allocation; returns its base address in this process."""
+    base = ctypes.c_void_p(0)
+    _check(load().spx_ipc_open(ctypes.create_string_buffer(handle, 64), ctypes.byref(base)), "spx_ipc_open")
+    return int(base.value)
+
+
+def ipc_close(base: int) -> None:
+    _check(load().spx_ipc_close(ctypes.c_void_p(base)), "spx_ipc_close")
+
+
+def hop_push(dst_addr: int, src, nbytes: int, flag_addr: int, ctas: int, stream=None) -> None:
+    _check(load().spx_hop_push(ctypes.c_void_p(dst_addr), _ptr(src), nbytes, ctypes.c_void_p(flag_addr), ctas,
+                               _stream(stream)), "spx_hop_push")
+
+
+def hop_wait(flag, target: int, stream=None) -> None:
+    """``flag``: a device address (int) or tensor element pointer."""
+    addr = flag if isinstance(flag, int) else flag.data_ptr()
+    _check(load().spx_hop_wait(ctypes.c_void_p(addr), target & 0xFFFFFFFF, _stream(stream)), "spx_hop_wait")
 
 
 def enable_peer_access(dev: int, peer: int) -> None:

@@ -106,3 +106,20 @@ def test_argument_validation_of_newer_entry_points(lib):
     assert native.attn_bwd_ws_floats(B, H, T, 48) == 2 * B * H * T
     assert native.attn_bwd_ws_floats(B, H, T, 64) == 2 * B * H * T + B * H * (nqb * (nqb + 1) // 2) * 128 * 128 // 2
     assert lib.spx_launch_count() >= 0
+
+
+def test_peer_hop_argument_validation(lib):
+    """The NVLink peer-hop entry points reject bad arguments before touching CUDA."""
+    P = ctypes.c_void_p
+    rc = lib.spx_hop_push(P(16), P(32), ctypes.c_int64(24), P(64), 32, None)   # not a multiple of 16
+    assert rc == -1 and b"bad size" in lib.spx_last_error()
+    rc = lib.spx_hop_push(P(16), P(32), ctypes.c_int64(32), P(64), 0, None)    # no CTAs
+    assert rc == -1 and b"bad size" in lib.spx_last_error()
+    rc = lib.spx_hop_push(P(16), P(0), ctypes.c_int64(32), P(64), 8, None)     # null source
+    assert rc == -1 and b"null" in lib.spx_last_error()
+    rc = lib.spx_hop_push(P(24), P(32), ctypes.c_int64(32), P(64), 8, None)    # misaligned destination
+    assert rc == -1 and b"aligned" in lib.spx_last_error()
+    assert lib.spx_hop_wait(None, ctypes.c_uint32(1), None) == -1
+    off = ctypes.c_int64(0)
+    assert lib.spx_ipc_export(None, ctypes.create_string_buffer(64), ctypes.byref(off)) == -1
+    assert lib.spx_ipc_open(None, None) == -1
