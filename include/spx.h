@@ -60,7 +60,8 @@ int spx_hop(int32_t dst_dev, void* dst, int32_t src_dev, const void* src, int64_
  *   spx_ipc_open / spx_ipc_close: map / unmap a peer process's allocation (base pointer);
  *   spx_hop_push: `ctas` CTAs copy `bytes` (multiple of 16, 16-byte aligned) from local src to
  *                 the peer-mapped dst with 16-byte stores, then each CTA release-adds 1 to the
- *                 peer-mapped *flag (system scope) once its stores are visible;
+ *                 peer-mapped *flag (system scope) once its stores are visible (flag may be
+ *                 NULL: an unsignalled copy, for bandwidth probes);
  *   spx_hop_wait: the stream waits until *flag - target >= 0 (acquire, system scope); traps
  *                 after 120 s so a lost hop fails loudly. */
 int spx_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out);

@@ -154,7 +154,9 @@ __global__ void __launch_bounds__(512) hop_push_kernel(uint4* __restrict__ dst, 
     dst[i + 3 * stride] = d;
   }
   for (; i < n16; i += stride) dst[i] = __ldg(src + i);
-  __threadfence_system();
+  if (flag == nullptr) return;  // unsignalled copy (bandwidth probes)
+  // the CTA barrier orders every thread's stores before thread 0's release; the release at
+  // system scope is cumulative, so the peer's acquire of the flag sees the whole CTA's data
   __syncthreads();
   if (threadIdx.x == 0) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
 }
@@ -208,7 +210,7 @@ extern "C" int spx_ipc_close(void* base) {
 
 extern "C" int spx_hop_push(void* dst, const void* src, int64_t bytes, uint32_t* flag, int32_t ctas, void* stream) {
   if (bytes < 0 || (bytes & 15) || ctas <= 0 || ctas > 1024) return set_error(SPX_ERR_ARG, "hop_push: bad size or ctas");
-  if (!dst || !src || !flag) return set_error(SPX_ERR_ARG, "hop_push: null pointer");
+  if (!dst || !src) return set_error(SPX_ERR_ARG, "hop_push: null pointer");
   if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15)
     return set_error(SPX_ERR_ARG, "hop_push: buffers must be 16-byte aligned");
   hop_push_kernel<<<ctas, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(

@@ -55,13 +55,16 @@ def main():
     g = dist.new_group([0, 1])
     for nbytes in sizes:
         src = big[: nbytes // 2]
-        for mode, ctas in [("peer", c) for c in (8, 16, 32, 64, 128)] + [("nccl", None)]:
+        for mode, ctas in [("peer", c) for c in (16, 32, 64, 128)] + [("push_noflag", 32), ("nccl", None)]:
             dist.barrier()
             for it in range(2):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(s)
                 for _ in range(reps):
-                    if mode == "peer":
+                    if mode == "push_noflag":      # the copy alone, no arrival flag
+                        if rank == 0:
+                            native.hop_push(dst, src, nbytes, 0, ctas, stream=s)
+                    elif mode == "peer":
                         if rank == 0:
                             native.hop_push(dst, src, nbytes, flag, ctas, stream=s)
                         else:
