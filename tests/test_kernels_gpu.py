@@ -334,3 +334,20 @@ def test_attention_bwd_inverse_rope():
     native.rope(plain, cs, rows=B * T, T=T, n_heads=2 * H, hd=hd, ld=W, inverse=True)
     torch.cuda.synchronize()
     assert rel(fused, plain) < 1e-2
+
+
+@pytest.mark.parametrize("nbytes,ctas", [(16, 1), (4096 * 1024 * 2, 32), (294_912, 7), (1_000_000 - 1_000_000 % 16, 64)])
+def test_hop_push_wait_bit_exact(nbytes, ctas):
+    """spx_hop_push / spx_hop_wait (the cross-GPU hop, exercised here within one GPU): the copy
+    is bit-exact for ragged sizes and CTA counts, every CTA adds 1 to the arrival flag, and the
+    wait returns once the flag reaches its target."""
+    src = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev)
+    dst = torch.zeros_like(src)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    s = torch.cuda.current_stream()
+    for rep in range(1, 4):
+        native.hop_push(dst.data_ptr(), src, nbytes, flag.data_ptr(), ctas, stream=s)
+        native.hop_wait(flag, rep * ctas, stream=s)
+    torch.cuda.synchronize()
+    assert torch.equal(dst, src)
+    assert int(flag.item()) == 3 * ctas
