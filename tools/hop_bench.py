@@ -6,6 +6,8 @@ as a fraction of NVLink bandwidth".
 Rank 0 sends `reps` back-to-back messages of each size to rank 1 with
   * peer: spx_hop_push (SM stores into rank 1's CUDA-IPC-mapped buffer + release flag), per CTA
     count, rank 1 waiting on the flag with spx_hop_wait;
+  * push_noflag / ce_noflag: the copy alone (SM stores / copy-engine cudaMemcpyAsync into the
+    mapped peer buffer), no arrival flag;
   * nccl: torch.distributed send/recv on a two-rank NCCL communicator.
 Times are CUDA events on rank 0's stream (the push / send side) and on rank 1's stream (the
 receive side, from its first wait to its last); both reported.  One JSON line per point.
@@ -13,6 +15,7 @@ receive side, from its first wait to its last); both reported.  One JSON line pe
 
 from __future__ import annotations
 
+import ctypes
 import json
 import os
 import sys
@@ -48,6 +51,7 @@ def main():
             bases[h] = native.ipc_open(h)
         return bases[h] + off
 
+    lib = native.load()
     peer = allx[1 - rank]
     dst, flag = addr(peer["buf"]), addr(peer["flag"])
     s = torch.cuda.Stream(dev)
@@ -55,13 +59,17 @@ def main():
     g = dist.new_group([0, 1])
     for nbytes in sizes:
         src = big[: nbytes // 2]
-        for mode, ctas in [("peer", c) for c in (16, 32, 64, 128)] + [("push_noflag", 32), ("nccl", None)]:
+        for mode, ctas in [("peer", c) for c in (16, 32, 64, 128)] + [("push_noflag", 32), ("ce_noflag", None), ("nccl", None)]:
             dist.barrier()
             for it in range(2):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(s)
                 for _ in range(reps):
-                    if mode == "push_noflag":      # the copy alone, no arrival flag
+                    if mode == "ce_noflag":        # copy-engine memcpy into the mapped peer buffer
+                        if rank == 0:
+                            lib.spx_hop(local, ctypes.c_void_p(dst), local, ctypes.c_void_p(src.data_ptr()), nbytes,
+                                        ctypes.c_void_p(s.cuda_stream))
+                    elif mode == "push_noflag":    # the copy alone, no arrival flag
                         if rank == 0:
                             native.hop_push(dst, src, nbytes, 0, ctas, stream=s)
                     elif mode == "peer":
