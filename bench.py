@@ -235,9 +235,9 @@ def hop_bandwidth(tr, ms_step: float, reps: int = 20) -> dict:
             e0.record(s)
             for _ in range(reps):
                 if peer and tr.rank == 0:
-                    native.hop_push(tr._peer_addr[key], buf, msg, tr._peer_flag[key], tr.hop_ctas, stream=s)
+                    tr._push(tr._peer_addr[key], buf, tr._peer_flag[key], s)
                 elif peer:
-                    tr._flag_expect[key] += tr.hop_ctas
+                    tr._flag_expect[key] += tr.hop_inc
                     native.hop_wait(tr._flag_local[key], tr._flag_expect[key], stream=s)
                 else:
                     with torch.cuda.stream(s):
@@ -255,8 +255,10 @@ def hop_bandwidth(tr, ms_step: float, reps: int = 20) -> dict:
     out.update({"hop_us": round(us, 2), "achieved_gbs": round(gbs, 1), "peak_gbs": NVLINK_GBS,
                 "peak_kind": "nominal NVLink 5 per direction", "frac": round(gbs / NVLINK_GBS, 4),
                 "hop_ms_per_step_if_serial": round(cross * us / 1e3, 3),
-                "transport": tr.hop_transport, "ctas": tr.hop_ctas if peer else None,
-                "how": ("rank0->rank1 spx_hop_push into a rank-1 slot over NVLink peer memory (sender stream)" if peer
+                "transport": tr.hop_transport + (f"/{tr.hop_engine}" if peer else ""),
+                "ctas": tr.hop_ctas if peer and tr.hop_engine == "sm" else None,
+                "how": (f"rank0->rank1 {'spx_hop_push_ce' if tr.hop_engine == 'ce' else 'spx_hop_push'} into a "
+                        "rank-1 slot over NVLink peer memory + arrival flag, rank 1 waiting on it" if peer
                         else "rank0->rank1 NCCL send/recv on the executor's pair group") +
                        f", CUDA events, {reps} back-to-back messages after a warm-up pass"})
     return out

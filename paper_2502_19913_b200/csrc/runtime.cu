@@ -161,6 +161,12 @@ __global__ void __launch_bounds__(512) hop_push_kernel(uint4* __restrict__ dst, 
   if (threadIdx.x == 0) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
 }
 
+__global__ void hop_signal_kernel(unsigned int* flag) {
+  // runs after the copy engine finished the stream's preceding peer copy: the fence orders
+  // that completed copy before the flag update for the peer's acquire
+  asm volatile("fence.sc.sys;\n\tred.release.sys.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
+}
+
 __global__ void hop_wait_kernel(const unsigned int* flag, unsigned int target) {
   if (threadIdx.x != 0) return;
   unsigned long long t0;
@@ -224,4 +230,16 @@ extern "C" int spx_hop_wait(const uint32_t* flag, uint32_t target, void* stream)
   hop_wait_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flag, target);
   count_launch();
   return check_launch("hop_wait_kernel");
+}
+
+extern "C" int spx_hop_push_ce(void* dst, const void* src, int64_t bytes, uint32_t* flag, void* stream) {
+  if (bytes < 0) return set_error(SPX_ERR_ARG, "hop_push_ce: negative size");
+  if (!dst || !src) return set_error(SPX_ERR_ARG, "hop_push_ce: null pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return set_cuda_error(e, "hop_push_ce: cudaMemcpyAsync");
+  if (flag == nullptr) return SPX_OK;
+  hop_signal_kernel<<<1, 1, 0, s>>>(flag);
+  count_launch();
+  return check_launch("hop_signal_kernel");
 }

@@ -412,8 +412,14 @@ class Trainer:
         self.hop_transport = hop_transport or os.environ.get("SPX_HOP", "peer")
         if self.hop_transport not in ("peer", "nccl"):
             raise ValidationError(f"hop_transport must be 'peer' or 'nccl', not {self.hop_transport!r}")
-        # CTAs per pushed hop (each adds 1 to the slot's arrival flag)
+        # peer hops as an SM push kernel ("sm": SPX_HOP_CTAS CTAs, each +1 on the flag; 8 MiB in
+        # 21 us) or on the copy engine ("ce": no SMs, then a one-thread flag kernel; 27 us, the
+        # gap before the flag kernel costs more than the faster copy saves).  Same step time.
+        self.hop_engine = os.environ.get("SPX_HOP_ENGINE", "sm")
+        if self.hop_engine not in ("ce", "sm"):
+            raise ValidationError(f"SPX_HOP_ENGINE must be 'ce' or 'sm', not {self.hop_engine!r}")
         self.hop_ctas = int(os.environ.get("SPX_HOP_CTAS", "32"))
+        self.hop_inc = 1 if self.hop_engine == "ce" else self.hop_ctas
         self.report: SimReport = simulate(schedule, topology, sim_config)
         if placement is None:
             placement = balanced_placement(self.report, topology.n, world)
@@ -588,6 +594,14 @@ class Trainer:
                 self._peer_flag[k] = fbase + 4 * i
         torch.cuda.synchronize(self.dev)
         dist.barrier()
+
+    def _push(self, dst_addr: int, src, flag_addr: int, stream):
+        """One cross-GPU hop into a peer-mapped slot, then its arrival-flag update."""
+        nbytes = src.numel() * src.element_size()
+        if self.hop_engine == "ce":
+            native.hop_push_ce(dst_addr, src, nbytes, flag_addr, stream=stream)
+        else:
+            native.hop_push(dst_addr, src, nbytes, flag_addr, self.hop_ctas, stream=stream)
 
     def close(self):
         """Unmap peer allocations (peer hop transport)."""
@@ -813,8 +827,7 @@ class Trainer:
                 # push straight into the consumer's slot on the peer GPU (static slots: its last
                 # reader causally precedes this producer), then release the slot's arrival flag
                 k = (nv, self.slot_of[(op.agent, nv)], name)
-                native.hop_push(self._peer_addr[k], out, out.numel() * out.element_size(), self._peer_flag[k],
-                                self.hop_ctas, stream=ss)
+                self._push(self._peer_addr[k], out, self._peer_flag[k], ss)
                 sends.append((None, ss))
             else:
                 with torch.cuda.stream(ss):
@@ -824,7 +837,7 @@ class Trainer:
 
             if self.hop_transport == "peer":
                 k = (nv, self.slot_of[(op.agent, nv)], name)
-                self._flag_expect[k] += self.hop_ctas
+                self._flag_expect[k] += self.hop_inc
                 pending[(consumer, nv, op.agent, op.wave)] = ("peer", self._flag_local[k], self._flag_expect[k])
                 return
             buf = self._dst_buffer(op, nv, name)

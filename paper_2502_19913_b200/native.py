@@ -31,6 +31,7 @@ SIGNATURES: dict[str, list] = {
     "spx_ipc_open": [_P, _P],
     "spx_ipc_close": [_P],
     "spx_hop_push": [_P, _P, _I64, _P, _I32, _P],
+    "spx_hop_push_ce": [_P, _P, _I64, _P, _P],
     "spx_hop_wait": [_P, ctypes.c_uint32, _P],
     "spx_gemm_bf16": [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _F, _P],
     "spx_attn_fwd": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P],
@@ -242,6 +243,12 @@ def ipc_close(base: int) -> None:
 def hop_push(dst_addr: int, src, nbytes: int, flag_addr: int, ctas: int, stream=None) -> None:
     _check(load().spx_hop_push(ctypes.c_void_p(dst_addr), _ptr(src), nbytes, ctypes.c_void_p(flag_addr), ctas,
                                _stream(stream)), "spx_hop_push")
+
+
+def hop_push_ce(dst_addr: int, src, nbytes: int, flag_addr: int, stream=None) -> None:
+    """Copy-engine hop into a peer-mapped buffer, then +1 on the peer-mapped flag (0: no flag)."""
+    _check(load().spx_hop_push_ce(ctypes.c_void_p(dst_addr), _ptr(src), nbytes, ctypes.c_void_p(flag_addr),
+                                  _stream(stream)), "spx_hop_push_ce")
 
 
 def hop_wait(flag, target: int, stream=None) -> None:

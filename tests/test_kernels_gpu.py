@@ -351,3 +351,18 @@ def test_hop_push_wait_bit_exact(nbytes, ctas):
     torch.cuda.synchronize()
     assert torch.equal(dst, src)
     assert int(flag.item()) == 3 * ctas
+
+
+def test_hop_push_ce_bit_exact():
+    """spx_hop_push_ce (copy-engine hop + one flag increment), exercised within one GPU."""
+    nbytes = 4096 * 1024 * 2
+    src = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev)
+    dst = torch.zeros_like(src)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    s = torch.cuda.current_stream()
+    for rep in range(1, 4):
+        native.hop_push_ce(dst.data_ptr(), src, nbytes, flag.data_ptr(), stream=s)
+        native.hop_wait(flag, rep, stream=s)
+    torch.cuda.synchronize()
+    assert torch.equal(dst, src)
+    assert int(flag.item()) == 3

@@ -6,6 +6,7 @@ as a fraction of NVLink bandwidth".
 Rank 0 sends `reps` back-to-back messages of each size to rank 1 with
   * peer: spx_hop_push (SM stores into rank 1's CUDA-IPC-mapped buffer + release flag), per CTA
     count, rank 1 waiting on the flag with spx_hop_wait;
+  * ce: spx_hop_push_ce (copy-engine memcpy into the mapped buffer + flag kernel), rank 1 waiting;
   * push_noflag / ce_noflag: the copy alone (SM stores / copy-engine cudaMemcpyAsync into the
     mapped peer buffer), no arrival flag;
   * nccl: torch.distributed send/recv on a two-rank NCCL communicator.
@@ -59,7 +60,7 @@ def main():
     g = dist.new_group([0, 1])
     for nbytes in sizes:
         src = big[: nbytes // 2]
-        for mode, ctas in [("peer", c) for c in (16, 32, 64, 128)] + [("push_noflag", 32), ("ce_noflag", None), ("nccl", None)]:
+        for mode, ctas in [("peer", c) for c in (16, 32, 64, 128)] + [("ce", None), ("push_noflag", 32), ("ce_noflag", None), ("nccl", None)]:
             dist.barrier()
             for it in range(2):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -72,6 +73,12 @@ def main():
                     elif mode == "push_noflag":    # the copy alone, no arrival flag
                         if rank == 0:
                             native.hop_push(dst, src, nbytes, 0, ctas, stream=s)
+                    elif mode == "ce":             # the executor's default hop: CE copy + flag
+                        if rank == 0:
+                            native.hop_push_ce(dst, src, nbytes, flag, stream=s)
+                        else:
+                            expect += 1
+                            native.hop_wait(flags, expect, stream=s)
                     elif mode == "peer":
                         if rank == 0:
                             native.hop_push(dst, src, nbytes, flag, ctas, stream=s)
