@@ -162,9 +162,9 @@ __global__ void __launch_bounds__(512) hop_push_kernel(uint4* __restrict__ dst, 
 }
 
 __global__ void hop_signal_kernel(unsigned int* flag) {
-  // runs after the copy engine finished the stream's preceding peer copy: the fence orders
-  // that completed copy before the flag update for the peer's acquire
-  asm volatile("fence.sc.sys;\n\tred.release.sys.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
+  // runs after the copy engine finished the stream's preceding peer copy (its writes are
+  // acknowledged by the peer before the copy completes); the release publishes the flag
+  asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
 }
 
 __global__ void hop_wait_kernel(const unsigned int* flag, unsigned int target) {
