@@ -571,8 +571,14 @@ class Trainer:
         self._flags = torch.zeros(max(1, len(recv)), dtype=torch.int32, device=self.dev)
         self._flag_local = {k: self._flags.data_ptr() + 4 * i for i, (k, _) in enumerate(recv)}
         self._flag_expect = {k: 0 for k, _ in recv}
-        mine = {"flags": native.ipc_export(self._flags),
-                "bufs": {k: native.ipc_export(t) for k, t in recv}}
+        # every step below is collective-safe: a rank whose CUDA IPC export or mapping fails
+        # still takes part in the exchange, and then ALL ranks fall back to NCCL hops (loudly)
+        err = None
+        try:
+            mine = {"flags": native.ipc_export(self._flags),
+                    "bufs": {k: native.ipc_export(t) for k, t in recv}}
+        except native.NativeError as e:
+            mine, err = None, e
         allx = [None] * self.world
         dist.all_gather_object(allx, mine)
         self._ipc_bases: dict = {}
@@ -585,13 +591,26 @@ class Trainer:
                 self._ipc_bases[h] = native.ipc_open(h)
             return self._ipc_bases[h] + off
 
-        for r, ex in enumerate(allx):
-            if r == self.rank:
-                continue
-            fbase = addr(ex["flags"])
-            for i, (k, hoff) in enumerate(ex["bufs"].items()):
-                self._peer_addr[k] = addr(hoff)
-                self._peer_flag[k] = fbase + 4 * i
+        if all(ex is not None for ex in allx):
+            try:
+                for r, ex in enumerate(allx):
+                    if r == self.rank:
+                        continue
+                    fbase = addr(ex["flags"])
+                    for i, (k, hoff) in enumerate(ex["bufs"].items()):
+                        self._peer_addr[k] = addr(hoff)
+                        self._peer_flag[k] = fbase + 4 * i
+            except native.NativeError as e:
+                err = e
+        ok = torch.tensor([0 if err is not None or any(ex is None for ex in allx) else 1], device=self.dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not int(ok.item()):
+            import sys
+
+            print(f"[spx] rank {self.rank}: NVLink peer hops unavailable ({err or 'a peer failed'}); "
+                  "using NCCL send/recv hops", file=sys.stderr, flush=True)
+            self.close()
+            self.hop_transport = "nccl"
         torch.cuda.synchronize(self.dev)
         dist.barrier()
 
