@@ -65,13 +65,16 @@ int spx_hop(int32_t dst_dev, void* dst, int32_t src_dev, const void* src, int64_
  *   spx_hop_push_ce: the same hop on the copy engine (cudaMemcpyAsync into the peer-mapped dst,
  *                 no SMs), then one thread fences and release-adds 1 to *flag (NULL: no flag);
  *   spx_hop_wait: the stream waits until *flag - target >= 0 (acquire, system scope); traps
- *                 after 120 s so a lost hop fails loudly. */
+ *                 after the hop timeout (default 120 s) so a lost hop fails loudly;
+ *   spx_hop_set_timeout: process-wide hop_wait timeout in seconds (0 < s <= 86400), read at
+ *                 each spx_hop_wait launch (executor: SPX_HOP_TIMEOUT_S). */
 int spx_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out);
 int spx_ipc_open(const void* handle, void** base_out);
 int spx_ipc_close(void* base);
 int spx_hop_push(void* dst, const void* src, int64_t bytes, uint32_t* flag, int32_t ctas, void* stream);
 int spx_hop_push_ce(void* dst, const void* src, int64_t bytes, uint32_t* flag, void* stream);
 int spx_hop_wait(const uint32_t* flag, uint32_t target, void* stream);
+int spx_hop_set_timeout(double seconds);
 
 /* ---- GEMM (tcgen05 + TMEM + TMA) ----
  * D[m,n] = sum_k A(m,k) * B(n,k), fp32 accumulate.

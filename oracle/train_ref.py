@@ -30,10 +30,10 @@ import torch
 F32 = torch.float32
 
 
-def rope_tables(T: int, hd: int, theta: float):
+def rope_tables(T: int, hd: int, theta: float, device=None):
     inv = 1.0 / (theta ** (torch.arange(0, hd, 2, dtype=torch.float64) / hd))
     ang = torch.arange(T, dtype=torch.float64)[:, None] * inv[None, :]
-    return ang.cos().to(F32), ang.sin().to(F32)
+    return ang.cos().to(F32).to(device), ang.sin().to(F32).to(device)
 
 
 def rms_norm(x, g, eps):
@@ -62,7 +62,7 @@ def decoder_layer(x, p, i, cfg, cos, sin):
     k = k.repeat_interleave(rep, dim=1)
     v = v.repeat_interleave(rep, dim=1)
     s = (q @ k.transpose(-1, -2)) / math.sqrt(hd)
-    mask = torch.ones(T, T, dtype=torch.bool).triu(1)
+    mask = torch.ones(T, T, dtype=torch.bool, device=x.device).triu(1)
     s = s.masked_fill(mask, float("-inf"))
     o = (torch.softmax(s, dim=-1) @ v).permute(0, 2, 1, 3).reshape(b, T, H * hd)
     x = x + o @ p[f"l{i}.wo"].t()
@@ -94,20 +94,26 @@ def is_decayed(name: str) -> bool:
 
 
 def iteration(cfg, split, params, mb_stages, tokens, opt_state=None, *, lr=3e-4, betas=(0.9, 0.95), eps=1e-8,
-              weight_decay=0.1, max_norm=1.0, step=1, update=True, threads=None):
+              weight_decay=0.1, max_norm=1.0, step=1, update=True, threads=None, device=None):
     """One synchronous iteration.
 
     params: list (per stage) of dicts of canonical fp32 tensors (not modified).
     mb_stages: list over microbatches of stage sequences (len M).
     tokens: int64 [M, b, T+1].
-    Returns dict(loss, mb_loss, grads, grad_norm, params (updated), opt_state).
+    device: where the fp32 arithmetic runs (default: the CPU).  Tests at the C2-C4 shapes run
+    the same fp32 restatement on the GPU with TF32 off, as a checker (it is not the product).
+    Returns dict(loss, mb_loss, grads, grad_norm, params (updated), opt_state), on ``device``.
     """
     if threads:
         torch.set_num_threads(threads)
     M = len(mb_stages)
     T = tokens.shape[-1] - 1
-    cos, sin = rope_tables(T, cfg.d // cfg.n_heads, cfg.rope_theta)
-    leaves = [{k: v.detach().clone().requires_grad_(True) for k, v in p.items()} for p in params]
+    tokens = tokens.to(device)
+    cos, sin = rope_tables(T, cfg.d // cfg.n_heads, cfg.rope_theta, device)
+    leaves = [{k: v.detach().to(device, F32).clone().requires_grad_(True) for k, v in p.items()} for p in params]
+    if opt_state is not None:
+        opt_state = [{k: (m.to(device), v.to(device)) for k, (m, v) in s.items()} for s in opt_state]
+    params = [{k: v.detach().to(device, F32) for k, v in p.items()} for p in params]
     mb_loss = []
     for mb in range(M):
         loss = microbatch_loss(tokens[mb], mb_stages[mb], leaves, split, cfg, cos, sin)

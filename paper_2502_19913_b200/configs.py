@@ -35,6 +35,7 @@ class RunConfig:
     description: str = ""
     kind: str = "skippipe"          # or "full" (dtfm_full sequential pipelines)
     balance_replicas: bool = True   # SkipPipe only: load-balance interchangeable replicas
+    swap_every: int = 0             # >0: every swap_every-th agent (ids 1, 1+e, ...) must take one swap
     _cache: dict = field(default_factory=dict, repr=False)
 
     @property
@@ -72,8 +73,18 @@ class RunConfig:
         fwd, _ = self.planning_times()
         return b200_box(fwd, mem_capacity=self.m)
 
+    def swap_agents(self) -> tuple:
+        if self.swap_every <= 0 or self.kind != "skippipe":
+            return ()
+        n_agents = self.m * self.sizes[0]
+        return tuple(range(1, n_agents, self.swap_every))
+
     def scheduler_config(self) -> SchedulerConfig:
-        return SchedulerConfig(k=self.k, msg_bytes=float(self.msg_bytes))
+        return SchedulerConfig(k=self.k, msg_bytes=float(self.msg_bytes), swap_agents=self.swap_agents())
+
+    def swapped_paths(self) -> int:
+        """Number of first-wave paths whose stage sequence is reordered (one swap, CC2)."""
+        return sum(1 for p in self.schedule().paths.values() if p.swap_count > 0)
 
     def sim_config(self, record_trace: bool = False) -> SimConfig:
         _, loss_ms = self.planning_times()
@@ -144,8 +155,11 @@ def get_config(name: str, **over) -> RunConfig:
         rc = RunConfig("C2", model_config("llama-500m"), [2, 2, 2, 2], 25, 2, 4, 1024, 32,
                        description="LLaMa-500M, 4 stages x 2 replicas, 25% stage skip")
     elif base == "C3":
+        # every other agent takes one swap: on the uniform box swaps never lower a path's cost, so
+        # without this the scheduler picks none (BASELINE configs[2] names reordered paths)
         rc = RunConfig("C3", model_config("llama-1.5b"), [1] * 8, 25, 8, 1, 4096, 32,
-                       description="LLaMa-1.5B, 8 stages x 1, skip + swap")
+                       description="LLaMa-1.5B, 8 stages x 1, skip + swap (every other path reordered)",
+                       swap_every=2)
     elif base == "C4":
         rc = RunConfig("C4", model_config("llama-8b"), [1] * 8, 37.5, 8, 1, 4096, 64,
                        description="LLaMa-8B, 8 stages, 33% skip (l=5 -> effective 37.5%), long queue")

@@ -162,12 +162,14 @@ __global__ void __launch_bounds__(512) hop_push_kernel(uint4* __restrict__ dst, 
 }
 
 __global__ void hop_signal_kernel(unsigned int* flag) {
-  // runs after the copy engine finished the stream's preceding peer copy (its writes are
-  // acknowledged by the peer before the copy completes); the release publishes the flag
+  // runs after the copy engine finished the stream's preceding peer copy.  A release orders only
+  // this thread's own accesses and the copy engine's writes are not among them, so a full system
+  // fence precedes the flag update (opt-in path; the fence costs ~1 us per hop)
+  __threadfence_system();
   asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
 }
 
-__global__ void hop_wait_kernel(const unsigned int* flag, unsigned int target) {
+__global__ void hop_wait_kernel(const unsigned int* flag, unsigned int target, unsigned long long timeout_ns) {
   if (threadIdx.x != 0) return;
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -178,7 +180,7 @@ __global__ void hop_wait_kernel(const unsigned int* flag, unsigned int target) {
     __nanosleep(256);
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 120ull * 1000000000ull) __trap();  // a lost hop fails loudly instead of hanging
+    if (t - t0 > timeout_ns) __trap();  // a lost hop fails loudly instead of hanging
   }
 }
 
@@ -225,9 +227,17 @@ extern "C" int spx_hop_push(void* dst, const void* src, int64_t bytes, uint32_t*
   return check_launch("hop_push_kernel");
 }
 
+static std::atomic<unsigned long long> g_hop_timeout_ns{120ull * 1000000000ull};
+
+extern "C" int spx_hop_set_timeout(double seconds) {
+  if (!(seconds > 0.0) || seconds > 86400.0) return set_error(SPX_ERR_ARG, "hop_set_timeout: need 0 < seconds <= 86400");
+  g_hop_timeout_ns.store((unsigned long long)(seconds * 1e9));
+  return SPX_OK;
+}
+
 extern "C" int spx_hop_wait(const uint32_t* flag, uint32_t target, void* stream) {
   if (!flag) return set_error(SPX_ERR_ARG, "hop_wait: null flag");
-  hop_wait_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flag, target);
+  hop_wait_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flag, target, g_hop_timeout_ns.load());
   count_launch();
   return check_launch("hop_wait_kernel");
 }

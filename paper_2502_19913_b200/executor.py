@@ -419,6 +419,7 @@ class Trainer:
         if self.hop_engine not in ("ce", "sm"):
             raise ValidationError(f"SPX_HOP_ENGINE must be 'ce' or 'sm', not {self.hop_engine!r}")
         self.hop_ctas = int(os.environ.get("SPX_HOP_CTAS", "32"))
+        self.hop_timeout_s = float(os.environ.get("SPX_HOP_TIMEOUT_S", "120"))
         self.hop_inc = 1 if self.hop_engine == "ce" else self.hop_ctas
         self.report: SimReport = simulate(schedule, topology, sim_config)
         if placement is None:
@@ -521,11 +522,25 @@ class Trainer:
             self._init_comm()
         if use_graphs:
             self._capture_all()
+        if world > 1:
+            # no rank's first hop_wait may start while a slower rank is still capturing graphs
+            import torch.distributed as dist
+
+            dist.barrier()
 
     # ---- communication setup (multi-process) ----
     def _init_comm(self):
         import torch.distributed as dist
 
+        # the hop protocol assumes every rank uses the same transport, engine and CTA count (the
+        # receiver's expected flag count is hop_inc per hop): agree before anything branches on it
+        mine = (self.hop_transport, self.hop_engine, self.hop_ctas, self.hop_timeout_s)
+        allc = [None] * self.world
+        dist.all_gather_object(allc, mine)
+        if any(c != allc[0] for c in allc):
+            raise ValidationError(f"hop settings differ across ranks (SPX_HOP, SPX_HOP_ENGINE, SPX_HOP_CTAS, "
+                                  f"SPX_HOP_TIMEOUT_S): {allc}")
+        native.hop_set_timeout(self.hop_timeout_s)
         # one NCCL group per replicated stage, created in the same order on every rank
         for st in range(self.assignment.s):
             ranks = self.stage_ranks[st]

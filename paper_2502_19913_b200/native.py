@@ -33,6 +33,7 @@ SIGNATURES: dict[str, list] = {
     "spx_hop_push": [_P, _P, _I64, _P, _I32, _P],
     "spx_hop_push_ce": [_P, _P, _I64, _P, _P],
     "spx_hop_wait": [_P, ctypes.c_uint32, _P],
+    "spx_hop_set_timeout": [ctypes.c_double],
     "spx_gemm_bf16": [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _F, _P],
     "spx_attn_fwd": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P],
     "spx_attn_bwd_ws_floats": [_I64, _I64, _I64, _I64],
@@ -249,6 +250,11 @@ def hop_push_ce(dst_addr: int, src, nbytes: int, flag_addr: int, stream=None) ->
     """Copy-engine hop into a peer-mapped buffer, then +1 on the peer-mapped flag (0: no flag)."""
     _check(load().spx_hop_push_ce(ctypes.c_void_p(dst_addr), _ptr(src), nbytes, ctypes.c_void_p(flag_addr),
                                   _stream(stream)), "spx_hop_push_ce")
+
+
+def hop_set_timeout(seconds: float) -> None:
+    """Process-wide spx_hop_wait timeout (a lost hop traps after it)."""
+    _check(load().spx_hop_set_timeout(float(seconds)), "spx_hop_set_timeout")
 
 
 def hop_wait(flag, target: int, stream=None) -> None:

@@ -138,6 +138,10 @@ class SchedulerConfig:
     cc3_branching: int = 4
     resolve_tc2: bool = True
     max_expansions: int = 4000
+    # B200 extension (not in SPEC): agents whose path must contain exactly one swap.  On a uniform
+    # NVSwitch box a swap never lowers a path's cost, so A* (ties to the lowest stage) never picks
+    # one; listing agents here makes a config exercise reordered paths (BASELINE configs[2]).
+    swap_agents: tuple = ()
 
     def __post_init__(self):
         if self.pool_size < 1:
@@ -150,12 +154,13 @@ class SchedulerConfig:
             raise ValidationError("max_swaps is fixed at 1 (multiple swaps are a non-goal, SPEC.md:314)")
         if not self.msg_bytes > 0:
             raise ValidationError("msg_bytes must be positive")
+        object.__setattr__(self, "swap_agents", tuple(sorted(int(a) for a in self.swap_agents)))
 
     def to_dict(self) -> dict:
         return {"k": self.k, "msg_bytes": self.msg_bytes, "pool_size": self.pool_size,
                 "slow_exempt_fraction": self.slow_exempt_fraction, "delta_tie": self.delta_tie,
                 "max_swaps": self.max_swaps, "cc3_branching": self.cc3_branching, "resolve_tc2": self.resolve_tc2,
-                "max_expansions": self.max_expansions}
+                "max_expansions": self.max_expansions, "swap_agents": list(self.swap_agents)}
 
     @classmethod
     def from_dict(cls, d: dict) -> "SchedulerConfig":
@@ -327,6 +332,8 @@ def astar_path(agent: Agent, topology: Topology, assignment: StageAssignment, co
             return PathPlan(agent.id, fwd_visits, bwd_visits, swaps, cost)
         seq, swaps, visits = payload
         if len(seq) == l:
+            if swaps == 0 and agent.id in config.swap_agents:
+                continue
             t_ret = t + (tm.comm[u, o] if u != o else 0.0)
             ret = Visit(o, 0, t_ret, t_ret, t_ret)
             bwd_visits, e2e = backward(nodes, t_ret)

@@ -1,5 +1,11 @@
-"""Multi-GPU executor (one process per GPU, NCCL P2P hops over NVLink, per-stage replica
-all-reduce) on config C1 vs the CPU oracle; skipped on boxes with fewer than 2 GPUs."""
+"""Multi-GPU executor (one process per GPU, path hops over NVLink, per-stage replica all-reduce)
+vs the fp32 oracle; skipped on boxes with fewer GPUs than the world size.
+
+* every hop transport -- NVLink peer push on the SMs (default), on the copy engine, and NCCL
+  send/recv -- trains C1 like the oracle, and since hops are pure copies all three give
+  bit-identical weights after two steps (slot reuse across waves and steps included);
+* the headline shape (C2: hd=64 tcgen05 attention, d=1024, T=1024, b=4; two waves) at every
+  world size."""
 
 import json
 import os
@@ -13,19 +19,36 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_multi_gpu_parity(world):
+def _run(world, config="C1", M=None, hop="peer", engine="sm", port=0):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, SPX_CONFIG=config, SPX_HOP=hop, SPX_HOP_ENGINE=engine, SPX_HOP_TIMEOUT_S="300")
+    if M:
+        env["SPX_M"] = str(M)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world), os.path.join(ROOT, "tools", "dist_parity.py")]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + 10 * world + port),
+           os.path.join(ROOT, "tools", "dist_parity.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
-    line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1]
-    r = json.loads(line)
+    r = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert r["hop"] == hop and r["engine"] == engine
     assert r["order_ok"]
     assert abs(r["loss"] - r["ref_loss"]) / r["ref_loss"] < 2e-2
     assert r["loss2"] < r["loss"]
     for key, (cos, rel) in r["stage_cos_rel"].items():
         assert cos >= 0.99 and rel <= 6e-2, (key, cos, rel)
     assert abs(r["grad_norm"] - r["ref_grad_norm"]) / r["ref_grad_norm"] < 3e-2
+    return r
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_hop_transports_bit_identical(world):
+    runs = [_run(world, hop="peer", engine="sm", port=0), _run(world, hop="peer", engine="ce", port=1),
+            _run(world, hop="nccl", engine="sm", port=2)]
+    assert runs[0]["params_sha"] == runs[1]["params_sha"] == runs[2]["params_sha"]
+    assert runs[0]["loss2"] == runs[1]["loss2"] == runs[2]["loss2"]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_headline_shape_multi_gpu(world):
+    _run(world, config="C2", M=8, port=3)

@@ -123,3 +123,7 @@ def test_peer_hop_argument_validation(lib):
     off = ctypes.c_int64(0)
     assert lib.spx_ipc_export(None, ctypes.create_string_buffer(64), ctypes.byref(off)) == -1
     assert lib.spx_ipc_open(None, None) == -1
+    lib.spx_hop_set_timeout.argtypes = [ctypes.c_double]
+    assert lib.spx_hop_set_timeout(0.0) == -1 and b"seconds" in lib.spx_last_error()
+    assert lib.spx_hop_set_timeout(-5.0) == -1
+    assert lib.spx_hop_set_timeout(120.0) == 0

@@ -283,3 +283,26 @@ def test_scale_20_nodes_6_stages_under_60s():
     assert time.perf_counter() - t0 < 60.0
     assert len(sch.agents) == 10 and A.sizes == [5, 3, 3, 3, 3, 3]
     _check_schedule(sch, T, A, 100 / 3) if sch.resolved else None
+
+
+def test_swap_agents_take_exactly_one_swap():
+    """B200 extension (SchedulerConfig.swap_agents): listed agents' paths contain exactly one
+    CC2-legal swap; the others are unconstrained.  C3 uses it so reordered paths are executed."""
+    from paper_2502_19913_b200.configs import get_config
+
+    rc = get_config("C3")
+    sch = rc.schedule()
+    forced = set(rc.scheduler_config().swap_agents)
+    assert forced == {1, 3, 5, 7}
+    for a, p in sch.paths.items():
+        st = p.stages
+        assert st[0] == 0 and len(set(st)) == len(st) == rc.path_len()
+        descents = [i for i in range(1, len(st)) if st[i] < st[i - 1]]
+        assert len(descents) == p.swap_count <= 1
+        if a in forced:
+            assert p.swap_count == 1
+            i = descents[0]   # transposing the descent yields an increasing sequence (CC2)
+            fixed = list(st)
+            fixed[i - 1], fixed[i] = fixed[i], fixed[i - 1]
+            assert fixed == sorted(fixed)
+    assert rc.swapped_paths() == len(forced)
