@@ -22,6 +22,22 @@
 namespace spx {
 namespace fab {
 
+// benchmarking hooks (tools/ubench/attn_main.cu builds variants; libspx uses the defaults)
+#ifndef SPX_FAB_NST64
+#define SPX_FAB_NST64 2
+#endif
+#ifndef SPX_FAB_PT_TMEM
+#define SPX_FAB_PT_TMEM 1
+#endif
+#ifdef SPX_FAB_PROBE
+// per-step clock64 stamps of CTA 0: [event][step]
+__device__ long long g_fab_probe[8][256];
+#define FAB_PROBE(ev, step) \
+  do { if (blockIdx.x == 0 && (step) < 256) g_fab_probe[ev][step] = clock64(); } while (0)
+#else
+#define FAB_PROBE(ev, step) do { } while (0)
+#endif
+
 constexpr int BLK = 128;                 // rows per block (queries and keys)
 constexpr int EW_WARPS = 8;              // elementwise warps: 2 per TMEM lane quadrant
 constexpr int THREADS = 128 + 32 * EW_WARPS;
@@ -37,6 +53,19 @@ SPX_DEVICE float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+SPX_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+SPX_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 SPX_DEVICE void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -119,14 +148,17 @@ SPX_DEVICE void store_grad_row(uint32_t taddr, __nv_bfloat16* dst, float scale, 
 // ------------------------------------------------------------------------------------------
 template <int HD>
 struct DkdvSmem {
-  static constexpr int NST = HD == 64 ? 2 : 1;      // Q/dO ring depth
+  static constexpr int NST = HD == 64 ? SPX_FAB_NST64 : 1;      // Q/dO ring depth
   static constexpr int TILE = (HD / 64) * ATOM;     // 128 x HD bf16
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + TILE;
   static constexpr int OFF_Q = OFF_V + TILE;        // [NST]
   static constexpr int OFF_DO = OFF_Q + NST * TILE; // [NST]
+  // hd=64: P^T and dS^T are A operands straight from TMEM (TS MMAs), only dS^T is also staged in
+  // shared memory for its TMA store; hd=128 has no spare TMEM columns and stages both in smem
+  static constexpr bool PT_TMEM = HD == 64 && SPX_FAB_PT_TMEM;
   static constexpr int OFF_PT = OFF_DO + NST * TILE;
-  static constexpr int OFF_DST = OFF_PT + 2 * ATOM;
+  static constexpr int OFF_DST = OFF_PT + (PT_TMEM ? 0 : 2 * ATOM);
   static constexpr int OFF_LSE = OFF_DST + 2 * ATOM;  // [NST][128] f32
   static constexpr int OFF_D = OFF_LSE + NST * 512;   // [NST][128] f32
   static constexpr int OFF_BAR = OFF_D + NST * 512;
@@ -141,17 +173,18 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int NST = L::NST;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint64_t* kv_full = bars + 0;
-  uint64_t* kv_empty = bars + 1;
-  uint64_t* full = bars + 2;      // [NST]
+  static_assert(NST <= 4, "barrier layout holds up to 4 ring stages");
+  uint64_t* full = bars + 0;      // [NST]
   uint64_t* empty = bars + 4;     // [NST]
-  uint64_t* sdp_full = bars + 6;
-  uint64_t* p_ready = bars + 7;
-  uint64_t* mma2_done = bars + 8;
-  uint64_t* tmem_free = bars + 9;   // S / dP of the current step copied to registers
-  uint64_t* acc_free = bars + 10;   // dV / dK of the previous item read out of TMEM
-  uint64_t* ds_read = bars + 11;    // the dS^T tile of the step has been read by its TMA store
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* kv_full = bars + 8;
+  uint64_t* kv_empty = bars + 9;
+  uint64_t* sdp_full = bars + 10;
+  uint64_t* p_ready = bars + 11;
+  uint64_t* mma2_done = bars + 12;
+  uint64_t* tmem_free = bars + 13;  // S / dP of the current step copied to registers
+  uint64_t* acc_free = bars + 14;   // dV / dK of the previous item read out of TMEM
+  uint64_t* ds_read = bars + 15;    // the dS^T tile of the step has been read by its TMA store
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = p.T / BLK;
@@ -191,6 +224,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // upstream grid complete before any dependent global access
   constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DV = 256, TM_DK = 256 + HD;
+  constexpr bool PT_TMEM = L::PT_TMEM;
+  constexpr uint32_t TM_PT = 384, TM_DST = 448;  // hd=64 only: P^T, dS^T (bf16 pairs along queries)
 
   if (warp == 0 && lane == 0) {
     // ---------------- producer ----------------
@@ -210,6 +245,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int s = gi % NST;
         const int h = kvh * group + it / nq, qb = jb + it % nq;
         mbar_wait(&empty[s], ((gi / NST) & 1) ^ 1);
+        FAB_PROBE(0, gi);
         mbar_expect_tx(&full[s], 2 * L::TILE + 1024);
         for (int a = 0; a < HD / 64; ++a) {
           tma_load_2d(smem + L::OFF_Q + s * L::TILE + a * ATOM, &tmQKV, &full[s], h * HD + 64 * a, row0 + qb * BLK);
@@ -258,6 +294,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // S/dP of this step are in registers: with a 2-deep Q/dO ring the next step's S/dP (same
         // item: K/V stay) overlap the elementwise math; otherwise they follow this step's dV/dK
         mbar_wait(tmem_free, gi & 1);
+        if (lane == 0) FAB_PROBE(1, gi);
         tc_fence_after();
         issued = false;
         if (NST > 1 && it + 1 < n_it) {
@@ -265,6 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           issued = true;
         }
         mbar_wait(p_ready, gi & 1);
+        if (lane == 0) FAB_PROBE(2, gi);
         if (it == 0) mbar_wait(acc_free, (n & 1) ^ 1);  // previous item's dV/dK read out
         tc_fence_after();
         const uint32_t sQ = smem_u32(smem + L::OFF_Q + s * L::TILE), sDO = smem_u32(smem + L::OFF_DO + s * L::TILE);
@@ -274,10 +312,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t ao = (kk >> 2) * ATOM + (kk & 3) * 32;
             const uint32_t bo = kk * 2048;
             const uint32_t acc = (it > 0) || (kk > 0);
-            mma_bf16_ss(tmem + TM_DV, umma_desc_sw128(sPT + ao, 16, 1024), umma_desc_sw128(sDO + bo, ATOM, 1024),
-                        ID_G, acc);
-            mma_bf16_ss(tmem + TM_DK, umma_desc_sw128(sDST + ao, 16, 1024), umma_desc_sw128(sQ + bo, ATOM, 1024),
-                        ID_G, acc);
+            if constexpr (PT_TMEM) {
+              mma_bf16_ts(tmem + TM_DV, tmem + TM_PT + kk * 8, umma_desc_sw128(sDO + bo, ATOM, 1024), ID_G, acc);
+              mma_bf16_ts(tmem + TM_DK, tmem + TM_DST + kk * 8, umma_desc_sw128(sQ + bo, ATOM, 1024), ID_G, acc);
+            } else {
+              mma_bf16_ss(tmem + TM_DV, umma_desc_sw128(sPT + ao, 16, 1024), umma_desc_sw128(sDO + bo, ATOM, 1024),
+                          ID_G, acc);
+              mma_bf16_ss(tmem + TM_DK, umma_desc_sw128(sDST + ao, 16, 1024), umma_desc_sw128(sQ + bo, ATOM, 1024),
+                          ID_G, acc);
+            }
           }
           mma_commit(mma2_done);
           mma_commit(&empty[s]);
@@ -325,6 +368,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool diag = (it % nq) == 0;  // query block == key block
         mbar_wait(&full[s], (gi / NST) & 1);  // lse / D of this step are in smem
         mbar_wait(sdp_full, gi & 1);
+        if (warp == 4 && lane == 0) FAB_PROBE(3, gi);
         tc_fence_after();
         const float* lse = reinterpret_cast<const float*>(smem + L::OFF_LSE + s * 512);
         const float* dd = reinterpret_cast<const float*>(smem + L::OFF_D + s * 512);
@@ -369,18 +413,31 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (diag) body(std::true_type{});
           else body(std::false_type{});
         }
+        if (warp == 4 && lane == 0) FAB_PROBE(4, gi);
         if (gi > 0) {
           mbar_wait(mma2_done, (gi - 1) & 1);  // P^T / dS^T tiles free
           mbar_wait(ds_read, (gi - 1) & 1);    // the dS^T store has read its tile
         }
+        if (warp == 4 && lane == 0) FAB_PROBE(5, gi);
+        if constexpr (PT_TMEM) {
+          // P^T / dS^T of this thread's key row and 64 query columns -> TMEM (A of the TS MMAs)
+          tmem_st_32x32b_x32(lane_base + TM_PT + (cb >> 1), pk);
+          tmem_st_32x32b_x32(lane_base + TM_DST + (cb >> 1), dk);
 #pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) {
-          put_row8p(sPT, r, (cb >> 3) + c8, pk + 4 * c8);
-          put_row8p(sDST, r, (cb >> 3) + c8, dk + 4 * c8);
+          for (int c8 = 0; c8 < 8; ++c8) put_row8p(sDST, r, (cb >> 3) + c8, dk + 4 * c8);
+          tmem_st_wait();
+          tc_fence_before();
+        } else {
+#pragma unroll
+          for (int c8 = 0; c8 < 8; ++c8) {
+            put_row8p(sPT, r, (cb >> 3) + c8, pk + 4 * c8);
+            put_row8p(sDST, r, (cb >> 3) + c8, dk + 4 * c8);
+          }
         }
 
         fence_proxy_async();
         __syncwarp();
+        if (warp == 4 && lane == 0) FAB_PROBE(6, gi);
         if (lane == 0) mbar_arrive(p_ready);
       }
       // item outputs: half 0 writes dV, half 1 writes dK (scaled, inverse RoPE)
