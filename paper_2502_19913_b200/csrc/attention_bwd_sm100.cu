@@ -24,7 +24,7 @@ namespace fab {
 
 // benchmarking hooks (tools/ubench/attn_main.cu builds variants; libspx uses the defaults)
 #ifndef SPX_FAB_NST64
-#define SPX_FAB_NST64 2
+#define SPX_FAB_NST64 3
 #endif
 #ifndef SPX_FAB_PT_TMEM
 #define SPX_FAB_PT_TMEM 1

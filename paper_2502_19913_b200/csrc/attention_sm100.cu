@@ -54,6 +54,90 @@ SPX_DEVICE float ex2(float x) {
   return y;
 }
 
+#ifdef SPX_FA_PROBE
+__device__ long long g_fa_probe[8][256];
+#define FA_PROBE(ev, step) \
+  do { if (blockIdx.x == 0 && (step) < 256) g_fa_probe[ev][step] = clock64(); } while (0)
+#else
+#define FA_PROBE(ev, step) do { } while (0)
+#endif
+
+constexpr float EXTREME_LOG2 = 64.f;  // lagged-max overflow guard (P <= 2^64)
+
+// tcgen05.wait::ld that the compiler sees as redefining the loaded registers, so no use of them
+// is scheduled before the wait
+SPX_DEVICE void tmem_ld_wait_dep(uint32_t (&a)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+                 "+r"(a[8]), "+r"(a[9]), "+r"(a[10]), "+r"(a[11]), "+r"(a[12]), "+r"(a[13]), "+r"(a[14]),
+                 "+r"(a[15]), "+r"(a[16]), "+r"(a[17]), "+r"(a[18]), "+r"(a[19]), "+r"(a[20]), "+r"(a[21]),
+                 "+r"(a[22]), "+r"(a[23]), "+r"(a[24]), "+r"(a[25]), "+r"(a[26]), "+r"(a[27]), "+r"(a[28]),
+                 "+r"(a[29]), "+r"(a[30]), "+r"(a[31])::"memory");
+}
+SPX_DEVICE void tmem_ld_wait_dep(uint32_t (&a)[32], uint32_t (&b)[32]) {
+  tmem_ld_wait_dep(a);
+  // b completed with a (wait::ld covers every outstanding load); pin it after the wait as well
+  asm volatile(""
+               : "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7]),
+                 "+r"(b[8]), "+r"(b[9]), "+r"(b[10]), "+r"(b[11]), "+r"(b[12]), "+r"(b[13]), "+r"(b[14]),
+                 "+r"(b[15]), "+r"(b[16]), "+r"(b[17]), "+r"(b[18]), "+r"(b[19]), "+r"(b[20]), "+r"(b[21]),
+                 "+r"(b[22]), "+r"(b[23]), "+r"(b[24]), "+r"(b[25]), "+r"(b[26]), "+r"(b[27]), "+r"(b[28]),
+                 "+r"(b[29]), "+r"(b[30]), "+r"(b[31])::"memory");
+}
+
+SPX_DEVICE float max3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// causal mask on the diagonal block: scores of keys after query row r -> -inf
+SPX_DEVICE void mask_chunk(uint32_t (&v)[32], int col0, int r) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (col0 + i > r) v[i] = 0xff800000u;
+}
+
+// raw (unscaled) maximum of 32 scores
+SPX_DEVICE float chunk_max(const uint32_t (&v)[32]) {
+  float mk[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) mk[k] = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) mk[(i >> 1) & 3] = max3(mk[(i >> 1) & 3], __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+  return fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3]));
+}
+
+// P = 2^(s * sl2 - m) for 32 scores -> 16 bf16 pairs; adds to sum and tracks the raw maximum.
+// Scale-and-shift as packed FFMA2, sums as packed FADD2, maxima as 3-input FMNMX.
+SPX_DEVICE void exp_chunk(const uint32_t (&v)[32], float sl2, float m, uint32_t* pk, float& sum, float& bmax) {
+  float s2[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+  float mk[2] = {bmax, -INFINITY};
+  const float nm = -m;
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {
+    const float a = __uint_as_float(v[i]), b = __uint_as_float(v[i + 1]);
+    mk[(i >> 1) & 1] = max3(mk[(i >> 1) & 1], a, b);
+    float ya, yb;
+    asm("{\n\t.reg .b64 x, k, c, y;\n\t"
+        "mov.b64 x, {%2, %3};\n\tmov.b64 k, {%4, %4};\n\tmov.b64 c, {%5, %5};\n\t"
+        "fma.rn.f32x2 y, x, k, c;\n\tmov.b64 {%0, %1}, y;\n\t}"
+        : "=f"(ya), "=f"(yb)
+        : "f"(a), "f"(b), "f"(sl2), "f"(nm));
+    ya = ex2(ya);
+    yb = ex2(yb);
+    float* acc = s2[(i >> 1) & 3];
+    asm("{\n\t.reg .b64 x, y;\n\t"
+        "mov.b64 x, {%0, %1};\n\tmov.b64 y, {%2, %3};\n\t"
+        "add.rn.f32x2 x, x, y;\n\tmov.b64 {%0, %1}, x;\n\t}"
+        : "+f"(acc[0]), "+f"(acc[1])
+        : "f"(ya), "f"(yb));
+    pk[i >> 1] = pack_bf16(ya, yb);
+  }
+  bmax = fmaxf(mk[0], mk[1]);
+  sum += ((s2[0][0] + s2[0][1]) + (s2[1][0] + s2[1][1])) + ((s2[2][0] + s2[2][1]) + (s2[3][0] + s2[3][1]));
+}
+
 struct FwdParams {
   __nv_bfloat16* out;  // O [B*T, ldo]
   float* lse;          // [B, H, T]
@@ -201,6 +285,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (j == 0) mbar_wait(o_free, (item_n & 1) ^ 1);
       mbar_wait(&p_full[gb & 1], (gb >> 1) & 1);
       mbar_wait(&v_full[s], (gb / NV) & 1);
+      if (lane == 0) FA_PROBE(7, gb);
       tc_fence_after();
       const uint32_t sV = smem_u32(smem + L::OFF_V + s * L::Q_BYTES);
       if (elect_one()) {
@@ -223,6 +308,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int s = g & 1;  // S buffer
         const int sk = g % NK;
         mbar_wait(&k_full[sk], (g / NK) & 1);
+        if (lane == 0) FA_PROBE(6, g);
         tc_fence_after();
         const uint32_t sK = smem_u32(smem + L::OFF_K + sk * L::Q_BYTES);
         if (elect_one()) {
@@ -265,84 +351,106 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (w >= n_items) continue;
       const Item it = item_of(w, nqb, BH, p.H);
       float m = -INFINITY, l = 0.f;
+      float alpha_pend = 1.f;  // O rescale owed before the next PV (the running max moved)
       for (int j = 0; j <= it.qb; ++j, ++g) {
         const int s = g & 1;
+        const bool diag = j == it.qb;
         mbar_wait(&s_full[s], (g >> 1) & 1);
+        if (warp == 4 && lane == 0) FA_PROBE(0, g);
         tc_fence_after();
-        float x[HB];
-        {
-          uint32_t* xv = reinterpret_cast<uint32_t*>(x);
-#pragma unroll
-          for (int c = 0; c < HB; c += 32)
-            tmem_ld_32x32b_x32(lane_base + s * BN + half * HB + c, *reinterpret_cast<uint32_t(*)[32]>(xv + c));
-          tmem_ld_wait();
+        const uint32_t sb = lane_base + s * BN + half * HB;
+        uint32_t va[32], vb[32], pk[32];
+        float sum = 0.f, bmax = -INFINITY;
+        if (j == 0) {
+          // first block of an item: the running max must exist before any exponential
+          tmem_ld_32x32b_x32(sb, va);
+          tmem_ld_32x32b_x32(sb + 32, vb);
+          tmem_ld_wait_dep(va, vb);
+          if (diag) {
+            mask_chunk(va, half * HB, r);
+            mask_chunk(vb, half * HB + 32, r);
+          }
+          float mraw = fmaxf(chunk_max(va), chunk_max(vb));
+          red[(s * 2 + half) * BM + r] = mraw;
+          pair_bar(bar_id);
+          mraw = fmaxf(mraw, red[(s * 2 + (half ^ 1)) * BM + r]);
+          m = mraw * sl2;
         }
-        if (j == it.qb) {
-#pragma unroll
-          for (int i = 0; i < HB; ++i)
-            if (half * HB + i > r) x[i] = -INFINITY;
+        // Later blocks use the lagged max: exponentiate with the running max of the previous blocks
+        // (no max pass and no exchange before the exponentials) while the second chunk streams out
+        // of TMEM; the block maximum is tracked on the side and agreed with the other half after.
+        // Pass 1 (rare) redoes the block after an extreme max growth (P could overflow).  One copy
+        // of the exponential code serves every case (instruction-cache footprint).
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          sum = 0.f;
+          bmax = -INFINITY;
+          tmem_ld_32x32b_x32(sb, va);
+          tmem_ld_wait_dep(va);
+          tmem_ld_32x32b_x32(sb + 32, vb);
+          if (diag) mask_chunk(va, half * HB, r);
+          exp_chunk(va, sl2, m, pk, sum, bmax);
+          tmem_ld_wait_dep(vb);
+          if (diag) mask_chunk(vb, half * HB + 32, r);
+          exp_chunk(vb, sl2, m, pk + 16, sum, bmax);
+          if (warp == 4 && lane == 0) FA_PROBE(1, g);
+          if (j == 0 || pass == 1) break;
+          red[(s * 2 + half) * BM + r] = bmax;
+          pair_bar(bar_id);
+          bmax = fmaxf(bmax, red[(s * 2 + (half ^ 1)) * BM + r]);
+          const float mx = bmax * sl2;
+          const bool extreme = mx > m + EXTREME_LOG2;
+          if (warp == 4 && lane == 0) FA_PROBE(2, g);
+          if (!__any_sync(0xffffffffu, extreme)) break;
+          if (extreme) {  // rescale O (before this block's PV) and l, then redo the block
+            const float a = ex2(m - mx);
+            m = mx;
+            l *= a;
+            alpha_pend *= a;
+          }
         }
-        // half-row max with 8 independent accumulators (raw scores; the scale is positive)
-        float mk[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) mk[k] = x[k];
-#pragma unroll
-        for (int i = 8; i < HB; ++i) mk[i & 7] = fmaxf(mk[i & 7], x[i]);
-        float mraw = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])),
-                           fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
-        red[(s * 2 + half) * BM + r] = mraw;
-        pair_bar(bar_id);
-        mraw = fmaxf(mraw, red[(s * 2 + (half ^ 1)) * BM + r]);
-        // lazy rescaling: the running max m only moves when the block's max exceeds it by more
-        // than 2^8 (P <= 256 is exact enough in bf16 and O / l is invariant to the choice of m),
-        // so after the first block O is rarely rescaled and the softmax rarely has to wait for
-        // the previous block's PV
-        const float mx = mraw * sl2;
-        float alpha = 1.f;
-        if (mx > m + RESCALE_LOG2) {
-          alpha = ex2(m - mx);  // 0 on the first block (m = -inf)
-          m = mx;
-        }
-        float sk[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int i = 0; i < HB; ++i) {
-          x[i] = ex2(fmaf(x[i], sl2, -m));
-          sk[i & 7] += x[i];
-        }
-        l = l * alpha + (((sk[0] + sk[1]) + (sk[2] + sk[3])) + ((sk[4] + sk[5]) + (sk[6] + sk[7])));
-        // rescale this half's O columns for rows whose max grew (warp-uniform decision, identical
-        // in both halves); only then does this block wait for the previous block's PV
-        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        l += sum;
+        // O rescale owed by the previous block (its PV used the old max; this block's P uses the
+        // new one): wait for that PV, then scale this half's O columns
+        if (__any_sync(0xffffffffu, alpha_pend != 1.f)) {
           mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
           tc_fence_after();
-          {
 #pragma unroll
-            for (int c = 0; c < HO; c += 32) {
-              uint32_t v[32];
-              tmem_ld_32x32b_x32(lane_base + TM_O + half * HO + c, v);
-              tmem_ld_wait();
+          for (int c = 0; c < HO; c += 32) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(lane_base + TM_O + half * HO + c, v);
+            tmem_ld_wait_dep(v);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-              tmem_st_32x32b_x32(lane_base + TM_O + half * HO + c, v);
-            }
-            tmem_st_wait();
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha_pend);
+            tmem_st_32x32b_x32(lane_base + TM_O + half * HO + c, v);
           }
+          tmem_st_wait();
+          alpha_pend = 1.f;
         }
         // P (bf16 pairs along the keys) into TMEM buffer g & 1, last read by the PV of block g-2
         if (g >= 2) {
           mbar_wait(&pv_done[g & 1], ((g - 2) >> 1) & 1);
           tc_fence_after();
         }
-        {
-          uint32_t pk[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) pk[e] = pack_bf16(x[2 * e], x[2 * e + 1]);
-          tmem_st_32x32b_x32(lane_base + TM_P + (g & 1) * 64 + 32 * half, pk);
-        }
+        if (warp == 4 && lane == 0) FA_PROBE(4, g);
+        tmem_st_32x32b_x32(lane_base + TM_P + (g & 1) * 64 + 32 * half, pk);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
+        if (warp == 4 && lane == 0) FA_PROBE(5, g);
         if (lane == 0) mbar_arrive(&p_full[g & 1]);
+        // lazy rescaling: the running max only moves when a block's max exceeds it by more than
+        // 2^8 (P <= 256 is exact enough in bf16; O / l is invariant to the choice of m); O owes
+        // the factor until the next block (or the item epilogue)
+        if (j > 0) {
+          const float mx = bmax * sl2;
+          if (mx > m + RESCALE_LOG2) {
+            const float a = ex2(m - mx);
+            m = mx;
+            l *= a;
+            alpha_pend = a;
+          }
+        }
       }
       // item epilogue: O / l -> bf16 (each half its columns), LSE; then hand O back to the MMA warp
       red[(4 + half) * BM + r] = l;
@@ -350,7 +458,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       l += red[(4 + (half ^ 1)) * BM + r];
       mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
       tc_fence_after();
-      const float inv = __frcp_rn(l);
+      const float inv = alpha_pend * __frcp_rn(l);
       const int t = it.qb * BM + r;
       __nv_bfloat16* orow = p.out + (size_t)(it.b * p.T + t) * p.ldo + it.h * HD + half * HO;
 #pragma unroll

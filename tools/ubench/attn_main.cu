@@ -62,6 +62,22 @@ int main(int argc, char** argv) {
     printf("{\"pass\": \"%s\", \"B\": %d, \"T\": %d, \"H\": %d, \"Hkv\": %d, \"hd\": %d, \"us\": %.2f, \"tflops\": %.1f}\n",
            k == 0 ? "fwd" : "bwd", B, T, H, Hkv, hd, us, (k == 0 ? 1.0 : 2.5) * fl / us / 1e6);
   }
+#ifdef SPX_FA_PROBE
+  {
+    cudaDeviceSynchronize();
+    fwd();
+    cudaDeviceSynchronize();
+    static long long pr[8][256];
+    cudaMemcpyFromSymbol(pr, spx::fa::g_fa_probe, sizeof pr);
+    const char* ev[] = {"s_full", "chunk0", "exps", "bar", "p_ready", "p_arrive", "S_issue", "PV_issue"};
+    long long t0 = pr[0][0];
+    for (int st = 0; st < 24; ++st) {
+      printf("{\"fprobe\": %d", st);
+      for (int e = 0; e < 8; ++e) printf(", \"%s\": %lld", ev[e], pr[e][st] - t0);
+      printf("}\n");
+    }
+  }
+#endif
 #ifdef SPX_FAB_PROBE
   {
     // one more backward, then the per-step stamps of CTA 0 (cycles relative to its first S/dP)
