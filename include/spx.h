@@ -38,6 +38,11 @@ extern "C" {
 #define SPX_OK 0
 #define SPX_ERR_ARG -1
 #define SPX_ERR_CUDA -2
+#define SPX_ERR_NCCL -3
+
+/* element types for spx_allreduce */
+#define SPX_DTYPE_F32 0
+#define SPX_DTYPE_BF16 1
 
 /* ---- runtime ---- */
 int spx_abi_version(void);
@@ -75,6 +80,20 @@ int spx_hop_push(void* dst, const void* src, int64_t bytes, uint32_t* flag, int3
 int spx_hop_push_ce(void* dst, const void* src, int64_t bytes, uint32_t* flag, void* stream);
 int spx_hop_wait(const uint32_t* flag, uint32_t target, void* stream);
 int spx_hop_set_timeout(double seconds);
+
+/* Stage-replica gradient aggregation (replaces the replica sync PAPER.md:97 describes; SURVEY.md
+ * §8(b)).  NCCL communicators owned by libspx, one per replicated stage; NCCL is resolved at run
+ * time (the process's libnccl.so.2), so these return SPX_ERR_NCCL on a box without it.
+ *   spx_comm_unique_id: 128-byte ncclUniqueId into id_out (one rank creates it, the caller
+ *                       broadcasts it to the group);
+ *   spx_comm_init: join the group as `rank` of `nranks`, *comm_out = communicator handle;
+ *   spx_allreduce: in-place sum of `count` elements (SPX_DTYPE_F32 / SPX_DTYPE_BF16) over the
+ *                  group, enqueued on `stream`;
+ *   spx_comm_destroy: free a communicator. */
+int spx_comm_unique_id(void* id_out);
+int spx_comm_init(const void* id, int32_t nranks, int32_t rank, void** comm_out);
+int spx_allreduce(void* comm, void* buf, int64_t count, int32_t dtype, void* stream);
+int spx_comm_destroy(void* comm);
 
 /* ---- GEMM (tcgen05 + TMEM + TMA) ----
  * D[m,n] = sum_k A(m,k) * B(n,k), fp32 accumulate.
@@ -177,6 +196,9 @@ int spx_sum_f32(const float* x, int64_t n, float* out, float scale, int32_t accu
 /* dst += src, fp32, n elements (16-byte aligned): merges the gradient buffers of co-resident
  * replicas of a stage before the replica all-reduce / optimizer. */
 int spx_add_f32(float* dst, const float* src, int64_t n, void* stream);
+/* dst += src, then src = 0 (merges a co-resident replica's gradient and leaves its buffer ready
+ * for the next iteration) */
+int spx_add_f32_clear(float* dst, float* src, int64_t n, void* stream);
 int64_t spx_sumsq_ws_floats(void);
 int spx_sumsq(const float* x, int64_t n, float* ws, float* out, void* stream);
 /* scale[0] = min(1, max_norm / (sqrt(sum(sumsq[0:count])) + 1e-6))  (torch clip_grad_norm_) */
@@ -186,6 +208,11 @@ int spx_clip_scale(const float* sumsq, int32_t count, float max_norm, float* sca
 int spx_adamw(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n, int64_t n_decay, float lr,
               float beta1, float beta2, float eps, float weight_decay, int64_t step, const float* grad_scale,
               void* stream);
+/* spx_adamw that also clears the gradient it consumed (g = 0), so the next iteration accumulates
+ * from zero without a separate fill pass (bit-identical update) */
+int spx_adamw_clear(float* p, float* g, float* m, float* v, void* p_bf16, int64_t n, int64_t n_decay, float lr,
+                    float beta1, float beta2, float eps, float weight_decay, int64_t step, const float* grad_scale,
+                    void* stream);
 
 #ifdef __cplusplus
 }

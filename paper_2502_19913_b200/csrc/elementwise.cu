@@ -501,7 +501,9 @@ __global__ void __launch_bounds__(XE_THREADS) xent_kernel(__nv_bfloat16* __restr
 // ---------------------------------------------------------------- reductions
 // out[0] (+)= scale * sum(x[0:n])   (single CTA, fixed order)
 // dst += src (fp32, float4 vectors when aligned): merges co-resident replicas' gradient buffers
-__global__ void add_f32_kernel(float* __restrict__ dst, const float* __restrict__ src, long long n) {
+// CLEAR: src = 0 afterwards (the merged buffer starts the next iteration at zero, no fill pass)
+template <bool CLEAR>
+__global__ void add_f32_kernel(float* __restrict__ dst, float* __restrict__ src, long long n) {
   pdl_wait();
   const long long n4 = n / 4;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -510,8 +512,12 @@ __global__ void add_f32_kernel(float* __restrict__ dst, const float* __restrict_
     const float4 b = reinterpret_cast<const float4*>(src)[i];
     a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
     reinterpret_cast<float4*>(dst)[i] = a;
+    if (CLEAR) reinterpret_cast<float4*>(src)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] += src[i];
+  for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    dst[i] += src[i];
+    if (CLEAR) src[i] = 0.f;
+  }
 }
 
 __global__ void sum_kernel(const float* __restrict__ x, long long n, float* __restrict__ out, float scale,
@@ -579,7 +585,8 @@ __device__ __forceinline__ void adamw_one(float& pi, float gi, float& mi, float&
   pi = __fsub_rn(pi, __fdiv_rn(__fmul_rn(step, mi), den));
 }
 
-__global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+template <bool ZERO>
+__global__ void adamw_kernel(float* __restrict__ p, float* __restrict__ g, float* __restrict__ m,
                              float* __restrict__ v, __nv_bfloat16* __restrict__ pb, long long n, long long n_decay,
                              float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
                              const float* __restrict__ gscale) {
@@ -594,12 +601,15 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
     v[i] = vi;
     p[i] = pi;
     pb[i] = __float2bfloat16(pi);
+    if (ZERO) g[i] = 0.f;
   }
 }
 
 // 16-byte vector form: 4 elements per thread per iteration (p/g/m/v 16-byte, pb 8-byte aligned;
 // n % 4 by the scalar tail)
-__global__ void __launch_bounds__(256) adamw_vec_kernel(float* __restrict__ p, const float* __restrict__ g,
+// ZERO: the consumed gradient is cleared (the next iteration accumulates from zero without a fill)
+template <bool ZERO>
+__global__ void __launch_bounds__(256) adamw_vec_kernel(float* __restrict__ p, float* __restrict__ g,
                                                         float* __restrict__ m, float* __restrict__ v,
                                                         __nv_bfloat16* __restrict__ pb, long long n, long long n_decay,
                                                         float lr, float b1, float b2, float eps, float wd, float bc1,
@@ -628,6 +638,7 @@ __global__ void __launch_bounds__(256) adamw_vec_kernel(float* __restrict__ p, c
     packed.x = *reinterpret_cast<uint32_t*>(&lo);
     packed.y = *reinterpret_cast<uint32_t*>(&hi);
     reinterpret_cast<uint2*>(pb)[i] = packed;
+    if (ZERO) __stcs(reinterpret_cast<float4*>(g) + i, make_float4(0.f, 0.f, 0.f, 0.f));
   }
   for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     float pi = p[i], mi = m[i], vi = v[i];
@@ -636,6 +647,7 @@ __global__ void __launch_bounds__(256) adamw_vec_kernel(float* __restrict__ p, c
     v[i] = vi;
     p[i] = pi;
     pb[i] = __float2bfloat16(pi);
+    if (ZERO) g[i] = 0.f;
   }
 }
 
@@ -782,14 +794,23 @@ extern "C" int spx_sum_f32(const float* x, int64_t n, float* out, float scale, i
   return check_launch("sum_kernel");
 }
 
-extern "C" int spx_add_f32(float* dst, const float* src, int64_t n, void* stream) {
+static int add_f32(float* dst, float* src, int64_t n, bool clear, cudaStream_t s) {
   if (n < 0) return set_error(SPX_ERR_ARG, "add_f32: negative size");
   if (n == 0) return SPX_OK;
   if (((uintptr_t)dst | (uintptr_t)src) & 15) return set_error(SPX_ERR_ARG, "add_f32: 16-byte aligned buffers required");
   const long long want = (n / 4 + 255) / 256;
   const int grid = (int)(want < 4LL * num_sms() ? (want > 0 ? want : 1) : 4LL * num_sms());
-  spx_launch_check(launch_k(add_f32_kernel, dim3(grid), dim3(256), 0, SPX_S, dst, src, (long long)n));
+  spx_launch_check(launch_k(clear ? add_f32_kernel<true> : add_f32_kernel<false>, dim3(grid), dim3(256), 0, s, dst, src,
+                            (long long)n));
   return check_launch("add_f32_kernel");
+}
+
+extern "C" int spx_add_f32(float* dst, const float* src, int64_t n, void* stream) {
+  return add_f32(dst, const_cast<float*>(src), n, false, SPX_S);
+}
+
+extern "C" int spx_add_f32_clear(float* dst, float* src, int64_t n, void* stream) {
+  return add_f32(dst, src, n, true, SPX_S);
 }
 
 extern "C" int64_t spx_sumsq_ws_floats(void) { return SUMSQ_BLOCKS; }
@@ -808,15 +829,30 @@ extern "C" int spx_clip_scale(const float* sumsq, int32_t count, float max_norm,
   return check_launch("clip_scale_kernel");
 }
 
-extern "C" int spx_adamw(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n, int64_t n_decay,
-                         float lr, float beta1, float beta2, float eps, float weight_decay, int64_t step,
-                         const float* grad_scale, void* stream) {
+static int adamw(float* p, float* g, float* m, float* v, void* p_bf16, int64_t n, int64_t n_decay, float lr,
+                 float beta1, float beta2, float eps, float weight_decay, int64_t step, const float* grad_scale,
+                 bool zero, cudaStream_t s) {
   if (step < 1) return set_error(SPX_ERR_ARG, "adamw: step must be >= 1");
   const float bc1 = 1.f - powf(beta1, (float)step);
   const float bc2 = 1.f - powf(beta2, (float)step);
   const int blocks = num_sms() * 8;
   const bool vec = !((((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) | ((uintptr_t)p_bf16 & 7));
-  spx_launch_check(launch_k(vec ? adamw_vec_kernel : adamw_kernel, dim3(blocks), dim3(256), 0, SPX_S, p, g, m, v, BF(p_bf16), n, n_decay, lr, beta1, beta2, eps, weight_decay, bc1,
-                                          bc2, grad_scale));
+  auto k = vec ? (zero ? adamw_vec_kernel<true> : adamw_vec_kernel<false>)
+               : (zero ? adamw_kernel<true> : adamw_kernel<false>);
+  spx_launch_check(launch_k(k, dim3(blocks), dim3(256), 0, s, p, g, m, v, BF(p_bf16), n, n_decay, lr, beta1, beta2,
+                            eps, weight_decay, bc1, bc2, grad_scale));
   return check_launch("adamw_kernel");
+}
+
+extern "C" int spx_adamw(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n, int64_t n_decay,
+                         float lr, float beta1, float beta2, float eps, float weight_decay, int64_t step,
+                         const float* grad_scale, void* stream) {
+  return adamw(p, const_cast<float*>(g), m, v, p_bf16, n, n_decay, lr, beta1, beta2, eps, weight_decay, step,
+               grad_scale, false, SPX_S);
+}
+
+extern "C" int spx_adamw_clear(float* p, float* g, float* m, float* v, void* p_bf16, int64_t n, int64_t n_decay,
+                               float lr, float beta1, float beta2, float eps, float weight_decay, int64_t step,
+                               const float* grad_scale, void* stream) {
+  return adamw(p, g, m, v, p_bf16, n, n_decay, lr, beta1, beta2, eps, weight_decay, step, grad_scale, true, SPX_S);
 }

@@ -395,7 +395,7 @@ class Trainer:
                  assignment, *, b: int, T: int | None = None, split: list[int] | None = None,
                  placement: list[int] | None = None, seed: int = 0, optim: OptimConfig | None = None,
                  use_graphs: bool = True, params: list | None = None, rank: int = 0, world: int = 1,
-                 device: int | None = None, hop_transport: str | None = None):
+                 device: int | None = None, hop_transport: str | None = None, keep_grads: bool = False):
         if not torch.cuda.is_available():
             raise native.NativeError("the executor needs a CUDA device (there is no CPU fallback)")
         native.load()
@@ -407,6 +407,11 @@ class Trainer:
         self.M = sim_config.total_microbatches
         self.split = layer_split(cfg, assignment.s, split)
         self.optim = optim or OptimConfig()
+        # keep_grads=False (default): AdamW clears each gradient it consumed and co-resident
+        # replica buffers are cleared by their merge, so no fill pass runs per iteration.
+        # keep_grads=True keeps the last iteration's gradients readable (grads(); tests) and zeroes
+        # them at the start of the next step instead; the updates are bit-identical.
+        self.keep_grads = keep_grads
         self.node_stage = assignment.node_stage()
         self.rank, self.world = rank, world
         self.hop_transport = hop_transport or os.environ.get("SPX_HOP", "peer")
@@ -518,6 +523,7 @@ class Trainer:
         self._opt_launches = 0
         self._outs: dict = {}
         self._groups: dict = {}
+        self._ar_after: dict = {}
         if world > 1:
             self._init_comm()
         if use_graphs:
@@ -541,13 +547,25 @@ class Trainer:
             raise ValidationError(f"hop settings differ across ranks (SPX_HOP, SPX_HOP_ENGINE, SPX_HOP_CTAS, "
                                   f"SPX_HOP_TIMEOUT_S): {allc}")
         native.hop_set_timeout(self.hop_timeout_s)
-        # one NCCL group per replicated stage, created in the same order on every rank
+        # one libspx-owned NCCL communicator per replicated stage (spx_comm_init), created in stage
+        # order on every rank (a global order, so the blocking inits cannot deadlock); the group's
+        # lowest rank makes the unique id, every rank learns it from one all-gather
+        uids = {st: native.comm_unique_id() for st in range(self.assignment.s)
+                if len(self.stage_ranks[st]) > 1 and self.stage_ranks[st][0] == self.rank}
+        alluid = [None] * self.world
+        dist.all_gather_object(alluid, uids)
         for st in range(self.assignment.s):
             ranks = self.stage_ranks[st]
-            if len(ranks) > 1:
-                g = dist.new_group(ranks)
-                if self.rank in ranks:
-                    self._groups[st] = g
+            if len(ranks) > 1 and self.rank in ranks:
+                self._groups[st] = native.comm_init(alluid[ranks[0]][st], len(ranks), ranks.index(self.rank))
+        # the replica all-reduce of a stage is issued as soon as this rank's last op of that stage
+        # is enqueued, on its own stream, so it overlaps the rank's remaining ops
+        self._ar_after = {}
+        for st in self._groups:
+            last = max(i for i, op in enumerate(self.ops)
+                       if self.placement[op.node] == self.rank and self.node_stage[op.node] == st)
+            self._ar_after.setdefault(last, []).append(st)
+        self._ar_stream = {st: torch.cuda.Stream(device=self.dev) for st in self._groups}
         # one process group (own NCCL communicator and stream) per rank pair for the path hops, so
         # hops between different pairs, and the replica all-reduces, never serialise behind each
         # other; created and warmed up in one global (lexicographic) order on every rank
@@ -624,7 +642,7 @@ class Trainer:
 
             print(f"[spx] rank {self.rank}: NVLink peer hops unavailable ({err or 'a peer failed'}); "
                   "using NCCL send/recv hops", file=sys.stderr, flush=True)
-            self.close()
+            self._unmap_peers()
             self.hop_transport = "nccl"
         torch.cuda.synchronize(self.dev)
         dist.barrier()
@@ -638,7 +656,16 @@ class Trainer:
             native.hop_push(dst_addr, src, nbytes, flag_addr, self.hop_ctas, stream=stream)
 
     def close(self):
-        """Unmap peer allocations (peer hop transport)."""
+        """Unmap peer allocations (peer hop transport) and free the replica communicators."""
+        for comm in getattr(self, "_groups", {}).values():
+            try:
+                native.comm_destroy(comm)
+            except Exception:
+                pass
+        self._groups = {}
+        self._unmap_peers()
+
+    def _unmap_peers(self):
         for base in getattr(self, "_ipc_bases", {}).values():
             try:
                 native.ipc_close(base)
@@ -728,12 +755,14 @@ class Trainer:
             s.wait_stream(torch.cuda.current_stream(self.dev))
             t_iter0.record(s)
             with torch.cuda.stream(s):
-                for ps in self.psets.values():
-                    ps.g.zero_()
-                for gl in self.extra_grads.values():
-                    for g in gl:
-                        g.zero_()
-                self.mb_loss.zero_()
+                if self.keep_grads:
+                    for ps in self.psets.values():
+                        ps.g.zero_()
+                    for gl in self.extra_grads.values():
+                        for g in gl:
+                            g.zero_()
+                if self.world > 1:
+                    self.mb_loss.zero_()   # summed over ranks; every slot is rewritten on one rank
             for cs in streams:
                 if cs is not s:
                     cs.wait_stream(s)
@@ -796,6 +825,8 @@ class Trainer:
                 hop = self.hops[idx]
                 if hop is not None:
                     self._issue_hop(idx, op, hop, out, mine, pending, sends)
+                for st in self._ar_after.get(idx, ()):
+                    self._issue_allreduce(st, self.nstream[v])
                 if mine and op.kind == L:  # the head wgrad, after the returned gradient left
                     sv = self.nstream[v]
                     lw = (LW, v, self._key(op)[2])
@@ -883,6 +914,21 @@ class Trainer:
                 w = dist.irecv(buf, self.placement[v], group=self._pair[self.placement[v]])
             pending[(consumer, nv, op.agent, op.wave)] = ("nccl", w)
 
+    def _issue_allreduce(self, st: int, after):
+        """Sum stage st's flat fp32 gradient over the ranks holding it (spx_allreduce on the
+        stage's libspx communicator) on the stage's own stream, once ``after`` (the stream of the
+        rank's last op of the stage) has produced it."""
+        cs = self._ar_stream[st]
+        # every stream that ran an op of the stage on this rank (per-node streams) has finished it
+        for sv in dict.fromkeys([after] + [self.nstream[v] for v in self.my_nodes if self.node_stage[v] == st]):
+            ev = torch.cuda.Event()
+            ev.record(sv)
+            cs.wait_event(ev)
+        ps = self.psets[st]
+        for g in self.extra_grads[st]:  # co-resident replicas first, in node order
+            native.add_f32(ps.g, g, ps.lay.numel, clear=not self.keep_grads, stream=cs)
+        native.allreduce(self._groups[st], ps.g, ps.lay.numel, stream=cs)
+
     def _finish_step(self, sends):
         """Drain the hop sends, then the replica sum / clip / AdamW on the rank's main stream."""
         s = self.stream
@@ -901,6 +947,7 @@ class Trainer:
         if not self.use_graphs:
             raise ValidationError("launch accounting needs use_graphs=True")
         opt = 2 * len(self.psets) + 1 + len(self.psets) + sum(len(gl) for gl in self.extra_grads.values())
+        # (+ torch fills when keep_grads: not libspx launches)
         mine = [self._key(op) for op in self.ops if self.placement[op.node] == self.rank]
         prep = 2 * sum(1 for op in self.ops if op.kind == F and op.pos == 0 and self.placement[op.node] == self.rank)
         return prep + sum(self._graph_launches[k] + (self._graph_launches[(LW,) + k[1:]] if k[0] == L else 0)
@@ -925,14 +972,12 @@ class Trainer:
         s = self.stream
         with torch.cuda.stream(s):
             for st, gl in self.extra_grads.items():  # co-resident replicas, in node order
+                if st in self._groups:
+                    continue                          # merged before its all-reduce
                 for g in gl:
-                    native.add_f32(self.psets[st].g, g, self.psets[st].lay.numel, stream=s)
-            if self.world > 1:
-                import torch.distributed as dist
-
-                for st in self.my_stages:
-                    if st in self._groups:
-                        dist.all_reduce(self.psets[st].g, group=self._groups[st])
+                    native.add_f32(self.psets[st].g, g, self.psets[st].lay.numel, clear=not self.keep_grads, stream=s)
+            for st in self._groups:  # replica all-reduces, issued during the step (_issue_allreduce)
+                s.wait_stream(self._ar_stream[st])
             self._sumsq.zero_()
             for st in self.my_stages:
                 # each stage counted once: its lowest hosting rank contributes the squared norm
@@ -948,12 +993,14 @@ class Trainer:
                 ps = self.psets[st]
                 native.adamw(ps.p32, ps.g, ps.m, ps.v, ps.pbf, n=ps.lay.numel, n_decay=ps.lay.n_decay, lr=o.lr,
                              beta1=o.beta1, beta2=o.beta2, eps=o.eps, weight_decay=o.weight_decay,
-                             step=self.step_count, grad_scale=self._clip, stream=s)
+                             step=self.step_count, grad_scale=self._clip, clear_grad=not self.keep_grads, stream=s)
 
     # ---- inspection (tests) ----
     def grads(self) -> dict[int, dict[str, torch.Tensor]]:
         """Canonical fp32 gradients of the last iteration (post replica-sum, pre-clip) for the
-        stages hosted on this rank."""
+        stages hosted on this rank (needs keep_grads=True: otherwise AdamW cleared them)."""
+        if not self.keep_grads:
+            raise ValidationError("grads() needs Trainer(keep_grads=True): the optimizer clears consumed gradients")
         torch.cuda.synchronize(self.dev)
         return {st: unpack_stage(self.cfg, self.layouts[st], self.psets[st].g) for st in self.my_stages}
 

@@ -34,6 +34,10 @@ SIGNATURES: dict[str, list] = {
     "spx_hop_push_ce": [_P, _P, _I64, _P, _P],
     "spx_hop_wait": [_P, ctypes.c_uint32, _P],
     "spx_hop_set_timeout": [ctypes.c_double],
+    "spx_comm_unique_id": [_P],
+    "spx_comm_init": [_P, _I32, _I32, _P],
+    "spx_allreduce": [_P, _P, _I64, _I32, _P],
+    "spx_comm_destroy": [_P],
     "spx_gemm_bf16": [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _F, _P],
     "spx_attn_fwd": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P],
     "spx_attn_bwd_ws_floats": [_I64, _I64, _I64, _I64],
@@ -52,10 +56,12 @@ SIGNATURES: dict[str, list] = {
     "spx_xent_fwd_bwd": [_P, _P, _P, _I64, _I64, _I64, _F, _P],
     "spx_sum_f32": [_P, _I64, _P, _F, _I32, _P],
     "spx_add_f32": [_P, _P, _I64, _P],
+    "spx_add_f32_clear": [_P, _P, _I64, _P],
     "spx_sumsq_ws_floats": [],
     "spx_sumsq": [_P, _I64, _P, _P, _P],
     "spx_clip_scale": [_P, _I32, _F, _P, _P, _P],
     "spx_adamw": [_P, _P, _P, _P, _P, _I64, _I64, _F, _F, _F, _F, _F, _I64, _P, _P],
+    "spx_adamw_clear": [_P, _P, _P, _P, _P, _I64, _I64, _F, _F, _F, _F, _F, _I64, _P, _P],
 }
 _RESTYPE = {"spx_last_error": ctypes.c_char_p, "spx_rmsnorm_ws_floats": ctypes.c_int64, "spx_launch_count": ctypes.c_int64,
             "spx_attn_bwd_ws_floats": ctypes.c_int64,
@@ -252,6 +258,41 @@ def hop_push_ce(dst_addr: int, src, nbytes: int, flag_addr: int, stream=None) ->
                                   _stream(stream)), "spx_hop_push_ce")
 
 
+DTYPE_F32, DTYPE_BF16 = 0, 1
+
+
+def comm_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (one rank creates it and broadcasts it to its group)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load().spx_comm_unique_id(buf), "spx_comm_unique_id")
+    return buf.raw
+
+
+def comm_init(uid: bytes, nranks: int, rank: int) -> int:
+    """Join an NCCL group (libspx-owned communicator); returns the communicator handle."""
+    if len(uid) != 128:
+        raise NativeError("comm_init: the unique id must be 128 bytes")
+    out = ctypes.c_void_p()
+    _check(load().spx_comm_init(ctypes.create_string_buffer(uid, 128), nranks, rank, ctypes.byref(out)),
+           "spx_comm_init")
+    return out.value
+
+
+def allreduce(comm: int, buf, count: int | None = None, stream=None) -> None:
+    """In-place sum of a flat fp32 / bf16 device tensor over the communicator's group."""
+    import torch
+
+    dt = {torch.float32: DTYPE_F32, torch.bfloat16: DTYPE_BF16}.get(buf.dtype)
+    if dt is None:
+        raise NativeError(f"allreduce: unsupported dtype {buf.dtype}")
+    n = buf.numel() if count is None else count
+    _check(load().spx_allreduce(ctypes.c_void_p(comm), _ptr(buf), n, dt, _stream(stream)), "spx_allreduce")
+
+
+def comm_destroy(comm: int) -> None:
+    _check(load().spx_comm_destroy(ctypes.c_void_p(comm)), "spx_comm_destroy")
+
+
 def hop_set_timeout(seconds: float) -> None:
     """Process-wide spx_hop_wait timeout (a lost hop traps after it)."""
     _check(load().spx_hop_set_timeout(float(seconds)), "spx_hop_set_timeout")
@@ -350,9 +391,12 @@ def xent_fwd_bwd(logits, targets, row_loss, *, n, V, ld, scale, stream=None) -> 
                                    _stream(stream)), "spx_xent_fwd_bwd")
 
 
-def add_f32(dst, src, n, *, stream=None) -> None:
-    """dst[:n] += src[:n] (fp32)."""
-    _check(load().spx_add_f32(_ptr(dst), _ptr(src), n, _stream(stream)), "spx_add_f32")
+def add_f32(dst, src, n, *, clear=False, stream=None) -> None:
+    """dst[:n] += src[:n] (fp32); clear=True also zeroes src[:n]."""
+    if clear:
+        _check(load().spx_add_f32_clear(_ptr(dst), _ptr(src), n, _stream(stream)), "spx_add_f32_clear")
+    else:
+        _check(load().spx_add_f32(_ptr(dst), _ptr(src), n, _stream(stream)), "spx_add_f32")
 
 
 def sum_f32(x, n, out, *, scale=1.0, accumulate=False, stream=None) -> None:
@@ -373,7 +417,9 @@ def clip_scale(sumsq_vec, count, max_norm, scale_out, norm_out=None, *, stream=N
 
 
 def adamw(p, g, m, v, p_bf16, *, n, n_decay, lr, beta1, beta2, eps, weight_decay, step, grad_scale=None,
-          stream=None) -> None:
-    _check(load().spx_adamw(_ptr(p), _ptr(g), _ptr(m), _ptr(v), _ptr(p_bf16), n, n_decay, float(lr), float(beta1),
-                            float(beta2), float(eps), float(weight_decay), int(step), _ptr(grad_scale),
-                            _stream(stream)), "spx_adamw")
+          clear_grad=False, stream=None) -> None:
+    """torch.optim.AdamW step over a flat fp32 set; clear_grad=True zeroes g after reading it."""
+    fn = load().spx_adamw_clear if clear_grad else load().spx_adamw
+    _check(fn(_ptr(p), _ptr(g), _ptr(m), _ptr(v), _ptr(p_bf16), n, n_decay, float(lr), float(beta1),
+              float(beta2), float(eps), float(weight_decay), int(step), _ptr(grad_scale),
+              _stream(stream)), "spx_adamw_clear" if clear_grad else "spx_adamw")

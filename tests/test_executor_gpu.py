@@ -33,7 +33,8 @@ def _flat(gdict):
 @pytest.fixture(scope="module")
 def c1():
     rc, sch, params, tokens = _setup()
-    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params)
+    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params,
+                 keep_grads=True)
     res = tr.step(tokens, timing=True)
     g = tr.grads()
     grads = [g[st] for st in range(rc.s)]
@@ -101,7 +102,8 @@ def test_skip_robust_inference_matches_oracle():
     from oracle.train_ref import rms_norm, rope_tables, stage_forward
 
     rc, sch, params, tokens = _setup()
-    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params)
+    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params,
+                 keep_grads=True)
     tr.step(tokens)                                 # weights after one update
     p = tr.params()
     cfg = rc.model
@@ -140,7 +142,8 @@ def test_gqa_config_matches_oracle(heads, kv):
     sch = rc.schedule()
     params = init_params(cfg, rc.layers, seed=0)
     tokens = synthetic_tokens(cfg, rc.M, rc.b, rc.T, seed=1234)
-    tr = Trainer(sch, rc.topology(), rc.sim_config(), cfg, rc.assignment, b=rc.b, T=rc.T, params=params)
+    tr = Trainer(sch, rc.topology(), rc.sim_config(), cfg, rc.assignment, b=rc.b, T=rc.T, params=params,
+                 keep_grads=True)
     res = tr.step(tokens)
     agents = sorted(a.id for a in sch.agents)
     mb_stages = train_ref.mb_stage_sequences({a: sch.paths[a].stages for a in agents}, agents, rc.M)
@@ -151,3 +154,19 @@ def test_gqa_config_matches_oracle(heads, kv):
         a, b = _flat(g[st]), _flat(ref["grads"][st])
         cos = torch.nn.functional.cosine_similarity(a.double(), b.double(), dim=0).item()
         assert cos >= 0.99, (st, cos)
+
+
+def test_cleared_gradients_equal_kept_gradients():
+    """Default path (AdamW clears each consumed gradient, replica merges clear their source; no fill
+    pass) and keep_grads=True (zero fill at step start) give bit-identical iterations."""
+    rc, sch, params, tokens = _setup()
+    runs = []
+    for keep in (False, True):
+        tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params,
+                     keep_grads=keep)
+        losses = [tr.step(tokens)["loss"] for _ in range(3)]
+        runs.append((losses, tr.params()))
+    assert runs[0][0] == runs[1][0]
+    for st in runs[0][1]:
+        for k in runs[0][1][st]:
+            assert torch.equal(runs[0][1][st][k], runs[1][1][st][k]), (st, k)
