@@ -119,12 +119,38 @@ def cpu_baseline(rc, budget_s: float = 20.0) -> dict:
                       f"median of {len(times)}"}
 
 
+def c1_iteration() -> dict:
+    """A directly timed full training iteration of config C1 (BASELINE configs[0], the tiny
+    CPU-runnable case: M=8 microbatches of 2x256 tokens along the scheduled paths, loss, backward,
+    clip and AdamW) on the CPU fp32 oracle, all host threads -- no extrapolation."""
+    import torch
+
+    from oracle import train_ref
+    from paper_2502_19913_b200.configs import get_config
+    from paper_2502_19913_b200.model import init_params, synthetic_tokens
+
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    rc = get_config("C1")
+    sch = rc.schedule()
+    agents = sorted(a.id for a in sch.agents)
+    mbs = train_ref.mb_stage_sequences({a: sch.paths[a].stages for a in agents}, agents, rc.M)
+    params = init_params(rc.model, rc.layers, seed=0)
+    tokens = synthetic_tokens(rc.model, rc.M, rc.b, rc.T, seed=1234)
+    t0 = time.perf_counter()
+    out = train_ref.iteration(rc.model, rc.layers, params, mbs, tokens, update=True)
+    sec = time.perf_counter() - t0
+    return {"config": "C1", "ms": sec * 1e3, "tokens_per_s": rc.M * rc.tokens_per_mb / sec, "cores": threads,
+            "loss": out["loss"]}
+
+
 def run_reference(args, rc):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     t0 = time.time()
     cb = cpu_baseline(rc, budget_s=min(30.0, 10.0 * max(1, args.steps)))
+    c1 = c1_iteration()
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": rc.M * rc.tokens_per_mb / cb["value"] * 1e3, "higher_is_better": True, "scaling": "weak",
@@ -133,7 +159,7 @@ def run_reference(args, rc):
                        "parallelism": "cpu"},
             "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                                          "d2h_bytes_per_step": 0},
-            "wall_s": time.time() - t0}
+            "c1_iteration": c1, "wall_s": time.time() - t0}
     print(json.dumps(line), flush=True)
 
 
@@ -391,7 +417,7 @@ def run_ours(args, rc):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": rc.name, "model": rc.model.name, "global_batch": rc.M * rc.b, "seq_len": rc.T,
                    "microbatches": rc.M, "tokens_per_step": tok, "stages": rc.s, "replicas": rc.sizes,
-                   "skip_pct": rc.k, "m": rc.m, "parallelism": "pp-skip(4x2 logical nodes on 1 GPU)",
+                   "skip_pct": rc.k, "m": rc.m, "parallelism": f"pp-skip({rc.s}x{rc.sizes[0]} logical nodes on 1 GPU)",
                    "l2_flush": "inputs+activations per step >> 126 MB L2", "kind": rc.kind},
         "loss": round(res["loss"], 5),
         "e2e": {"value": round(tok / (e2e_ms / 1e3), 1), "unit": "tokens/s",

@@ -63,6 +63,7 @@ class ExecReport:
     iteration_makespan: float            # ms, first op issue -> optimizer done (CUDA events)
     microbatch_e2e: list[float]          # ms, F at origin start -> B at origin end
     total_collision_wait: float          # ms, sum over ops of (start - ready) on the device timeline
+                                         # (ops whose producer ran on this rank; see make_report)
     node_busy: list[float]
     node_idle: list[float]
     loss: float
@@ -745,7 +746,7 @@ class Trainer:
         host = tokens if isinstance(tokens, dict) else self._stage_inputs(tokens)
         self.step_count += 1
         s = self.stream
-        ev = {}
+        ev, ev_lw = {}, {}
         t_iter0 = torch.cuda.Event(enable_timing=True)
         t_iter1 = torch.cuda.Event(enable_timing=True)
         pending: dict = {}
@@ -838,7 +839,7 @@ class Trainer:
                     if timing:
                         e1 = torch.cuda.Event(enable_timing=True)
                         e1.record(sv)
-                        ev[idx] = (ev[idx][0], e1)
+                        ev_lw[idx] = e1
             for cs in streams:
                 if cs is not s:
                     s.wait_stream(cs)
@@ -856,6 +857,8 @@ class Trainer:
             torch.cuda.synchronize(self.dev)
             out["iter_ms"] = t_iter0.elapsed_time(t_iter1)
             out["op_times"] = {i: (t_iter0.elapsed_time(a), t_iter0.elapsed_time(b_)) for i, (a, b_) in ev.items()}
+            # an L op's head weight gradient (issued after the returned gradient left)
+            out["lw_end"] = {i: t_iter0.elapsed_time(e) for i, e in ev_lw.items()}
         return out
 
     def _issue_hop(self, idx, op, hop, out, mine, pending, sends):
@@ -1076,10 +1079,9 @@ class Trainer:
         order: dict[int, list] = {}
         trace, start_f0 = [], {}
         e2e = [0.0] * self.M
-        wait = 0.0
         for idx, kind, v, agent, wave in res["executed"]:
             t0, t1 = res["op_times"][idx]
-            busy[v] += t1 - t0
+            busy[v] += res.get("lw_end", {}).get(idx, t1) - t0
             order.setdefault(v, []).append((kind, agent, wave))
             dirn = {"F": "fwd", "L": "loss", "B": "bwd"}[kind]
             trace.append((t0, v, "start", agent, wave, dirn))
@@ -1089,6 +1091,30 @@ class Trainer:
                 start_f0[op.mb] = t0
             if kind == B and op.pos == 0:
                 e2e[op.mb] = t1 - start_f0[op.mb]
+        # collision wait = sum over ops of (start - ready) as in the simulator, where
+        # ready is the end of the op that produced the input (F at the origin: the end of the
+        # agent's previous wave, or the iteration start).  Exact for producers on this rank (all
+        # ops at one GPU); ops fed from another rank are left out (no common clock across GPUs).
+        wait, counted = 0.0, 0
+        key = {(op.agent, op.wave, op.kind, op.pos): i for i, op in enumerate(self.ops)}
+        for idx, kind, v, agent, wave in res["executed"]:
+            op = self.ops[idx]
+            last = len(self.paths[agent]) - 1
+            if kind == F:
+                prod = key.get((agent, wave, F, op.pos - 1)) if op.pos > 0 else key.get((agent, wave - 1, B, 0))
+            elif kind == L:
+                prod = key[(agent, wave, F, last)]
+            else:
+                prod = key[(agent, wave, L, 0)] if op.pos == last else key[(agent, wave, B, op.pos + 1)]
+            if prod is None:
+                ready = 0.0
+            elif prod in res["op_times"]:
+                ready = res["op_times"][prod][1]
+            else:
+                continue
+            wait += max(0.0, res["op_times"][idx][0] - ready)
+            counted += 1
+        self.collision_wait_ops = counted
         mk = res["iter_ms"]
         return ExecReport(iteration_makespan=mk, microbatch_e2e=e2e, total_collision_wait=wait, node_busy=busy,
                           node_idle=[mk - x for x in busy], loss=res["loss"], mb_loss=self.mb_loss.tolist(),

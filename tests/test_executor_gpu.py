@@ -50,6 +50,9 @@ def test_op_order_matches_simulator(c1):
         sim_order.setdefault(op.node, []).append((op.kind, op.agent, op.wave))
     rep = c1["tr"].make_report(c1["res"])
     assert rep.node_order == sim_order
+    # measured collision wait (start - ready on the device timeline), every op counted at one GPU
+    assert c1["tr"].collision_wait_ops == len(c1["tr"].report.ops)
+    assert 0.0 <= rep.total_collision_wait < 1e3 * rep.iteration_makespan
 
 
 def test_loss_matches_oracle(c1):
