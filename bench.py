@@ -417,7 +417,8 @@ def run_ours(args, rc):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": rc.name, "model": rc.model.name, "global_batch": rc.M * rc.b, "seq_len": rc.T,
                    "microbatches": rc.M, "tokens_per_step": tok, "stages": rc.s, "replicas": rc.sizes,
-                   "skip_pct": rc.k, "m": rc.m, "parallelism": f"pp-skip({rc.s}x{rc.sizes[0]} logical nodes on 1 GPU)",
+                   "skip_pct": rc.k, "m": rc.m, "layer_split": rc.layers,
+                   "swapped_paths": rc.swapped_paths(), "parallelism": f"pp-skip({rc.s}x{rc.sizes[0]} logical nodes on 1 GPU)",
                    "l2_flush": "inputs+activations per step >> 126 MB L2", "kind": rc.kind},
         "loss": round(res["loss"], 5),
         "e2e": {"value": round(tok / (e2e_ms / 1e3), 1), "unit": "tokens/s",
@@ -517,7 +518,8 @@ def run_ours_dist(args, rc):
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": rc.name, "model": rc.model.name, "global_batch": rc.M * rc.b, "seq_len": rc.T,
                        "microbatches": rc.M, "tokens_per_step": tok, "stages": rc.s, "replicas": rc.sizes,
-                       "skip_pct": rc.k, "m": rc.m, "placement": placement,
+                       "skip_pct": rc.k, "m": rc.m, "layer_split": rc.layers,
+                   "swapped_paths": rc.swapped_paths(), "placement": placement,
                        "parallelism": f"pp-skip({rc.s}x{rc.sizes[0]} logical nodes over {world} GPUs)+dp-allreduce",
                        "l2_flush": "inputs+activations per step >> 126 MB L2", "kind": rc.kind},
             "loss": round(res["loss"], 5),

@@ -139,15 +139,23 @@ class RunConfig:
 
 # executable baseline variants of a config
 VARIANTS = {"-full": "full", "-dtfmskip": "dtfm_skip", "-notc2": "no_tc2"}
+# rebalanced layer split: S0 also runs the embedding, the head and the loss of
+# every microbatch, so it gets fewer decoder layers; opt-in beside the equal split
+REBALANCED = {24: {4: [3, 7, 7, 7]}}
 
 
 def get_config(name: str, **over) -> RunConfig:
-    """C1..C5, plus baseline variants: "-full" (DT-FM, k=0 disjoint sequential pipelines),
-    "-dtfmskip" (DT-FM-skip: topology-blind skip paths, no TC2) and "-notc2" (SkipPipe without the
-    throughput phase)."""
-    suffix = next((v for v in VARIANTS if name.endswith(v)), "")
-    base = name[: len(name) - len(suffix)] if suffix else name
-    full = suffix == "-full"
+    """C1..C5, plus suffixes (combinable, e.g. "C2-rb-full"): "-rb" rebalanced layer split
+    (S0 lighter; REBALANCED), "-full" (DT-FM, k=0 disjoint sequential pipelines), "-dtfmskip"
+    (DT-FM-skip: topology-blind skip paths, no TC2) and "-notc2" (SkipPipe without the throughput
+    phase)."""
+    base, suffixes = name, []
+    while True:
+        suf = next((v for v in list(VARIANTS) + ["-rb"] if base.endswith(v)), None)
+        if suf is None:
+            break
+        suffixes.insert(0, suf)
+        base = base[: len(base) - len(suf)]
     if base == "C1":
         rc = RunConfig("C1", model_config("llama-50m"), [2, 2, 2, 2], 25, 2, 2, 256, 8,
                        description="tiny LLaMA SkipPipe iteration (4 stages x 2 replicas, 25% skip)")
@@ -168,10 +176,16 @@ def get_config(name: str, **over) -> RunConfig:
                        description="LLaMa-500M skip sweep point (50%)")
     else:
         raise KeyError(name)
-    if full:
-        rc.kind, rc.k, rc.name = "full", 0, rc.name + "-full"
-    elif suffix:
-        rc.kind, rc.name = VARIANTS[suffix], rc.name + suffix
+    for suf in suffixes:
+        if suf == "-rb":
+            split = REBALANCED.get(rc.model.n_layers, {}).get(rc.s)
+            if split is None:
+                raise KeyError(f"{name}: no rebalanced split for {rc.model.n_layers} layers x {rc.s} stages")
+            rc.split, rc.name = list(split), rc.name + suf
+        elif suf == "-full":
+            rc.kind, rc.k, rc.name = "full", 0, rc.name + suf
+        else:
+            rc.kind, rc.name = VARIANTS[suf], rc.name + suf
     for k_, v in over.items():
         setattr(rc, k_, v)
     return rc

@@ -57,7 +57,7 @@ def _worker(rank, world, port, cfg_name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,cfg", [(2, "C2"), (4, "C2"), (8, "C2"), (2, "C1")])
+@pytest.mark.parametrize("world,cfg", [(2, "C2"), (4, "C2"), (8, "C2"), (2, "C1"), (8, "C2-rb"), (4, "C2-rb")])
 def test_cross_rank_hops_match(world, cfg):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -83,3 +83,17 @@ def test_static_slots_respect_tc1():
     assert max(n_slots) <= rc.m                       # TC1 => at most m slots per node
     for (a, v), j in slot_of.items():
         assert 0 <= j < n_slots[v] and v in sch.paths[a].nodes
+
+
+def test_rebalanced_split_config():
+    """C2-rb: S0 gets 3 of the 24 layers (it also runs embedding, head and loss
+    for every microbatch); at 8 GPUs (one logical node per GPU) the busiest node's simulated load
+    drops below the equal split's, and the full-pipeline comparator uses the same split."""
+    eq, rb = get_config("C2"), get_config("C2-rb")
+    assert rb.layers == [3, 7, 7, 7] and sum(rb.layers) == rb.model.n_layers
+    assert get_config("C2-rb-full").layers == [3, 7, 7, 7] and get_config("C2-rb-full").kind == "full"
+    busy_eq = simulate(eq.schedule(), eq.topology(), eq.sim_config()).node_busy
+    busy_rb = simulate(rb.schedule(), rb.topology(), rb.sim_config()).node_busy
+    assert max(busy_rb) < max(busy_eq)
+    placement = balanced_placement(simulate(rb.schedule(), rb.topology(), rb.sim_config()), rb.topology().n, 8)
+    assert sorted(placement) == list(range(8))

@@ -52,3 +52,8 @@ def test_hop_transports_bit_identical(world):
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_headline_shape_multi_gpu(world):
     _run(world, config="C2", M=8, port=3)
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_rebalanced_split_multi_gpu(world):
+    _run(world, config="C2-rb", M=8, port=4)

@@ -95,6 +95,12 @@ def test_c2_two_waves_matches_oracle():
     check_parity(rc)
 
 
+def test_c2_rebalanced_split_matches_oracle():
+    """C2-rb: unequal layer split (3, 7, 7, 7) -- stage parameter sets of different sizes."""
+    rc = get_config("C2-rb", M=8)
+    check_parity(rc)
+
+
 def test_c3_shape_with_swap_matches_oracle():
     cfg = model_config("llama-1.5b", n_layers=8)
     rc = RunConfig("C3-shape", cfg, [1] * 8, 25, 2, 1, 4096, 4, swap_every=2)
