@@ -107,6 +107,9 @@ int spx_comm_destroy(void* comm);
  *      blocks; C bf16 [M][ldc] = silu(gate) * up  (F columns), C2 bf16 [M][ldc2] = raw gate/up
  *   6  SwiGLU backward fused into the down-projection dgrad (A K-major, B MN-major): D = dh [M][N=F]; R = gu [M][ldc2]
  *      (raw gate/up, 128-column interleave); C2 bf16 [M][ldc2] = dgu (dgate, dup interleaved)
+ *   7  cross-entropy head (A and B K-major, N % 128 == 0): C bf16 [M][ldc] = D (logits) and
+ *      C2 f32 [M][ldc2 >= 2*N/128] = per 128-column block (max, sum exp(z - max)) of the bf16
+ *      logits, consumed by spx_xent_from_parts (replaces spx_head_xent_fwd_bwd's loss pass)
  * Requires N % 32 == 0, K, lda, ldb multiples of 8, 16-byte aligned A/B. */
 int spx_gemm_bf16(const void* A, const void* B, void* C, const void* R, void* C2, int64_t M, int64_t N, int64_t K,
                   int64_t lda, int64_t ldb, int64_t ldc, int64_t ldc2, int32_t a_mn_major, int32_t b_mn_major,
@@ -188,6 +191,11 @@ int spx_token_prep(const int64_t* tokens, int64_t b, int64_t T, int64_t ld_token
 
 /* ---- softmax cross-entropy: row_loss[r] = lse(z_r) - z_r[t_r]; logits overwritten by
  *      (softmax - onehot) * scale (bf16).  One pass pair per row, logits never re-materialised. */
+/* From the head GEMM's epilogue-7 partials (nb >= V/128 (max, sum) pairs per row): combine them
+ * (fixed order), row_loss[r] = lse - z[t_r], and if scale != 0 rewrite the logits in place as
+ * (softmax - onehot) * scale -- a single read and write of the logits. */
+int spx_xent_from_parts(void* logits, const float* parts, int64_t nb, const int32_t* targets, float* row_loss,
+                        int64_t n, int64_t V, int64_t ld, float scale, void* stream);
 int spx_xent_fwd_bwd(void* logits, const int32_t* targets, float* row_loss, int64_t n, int64_t V, int64_t ld,
                      float scale, void* stream);
 

@@ -498,6 +498,74 @@ __global__ void __launch_bounds__(XE_THREADS) xent_kernel(__nv_bfloat16* __restr
   if (threadIdx.x == 0) row_loss[row] = logf(s) + m - zt;
 }
 
+// Cross-entropy from the head GEMM's per-128-column (max, sum exp) partials (EPI_XENT): one CTA
+// per row combines its nb partials in fixed order (deterministic) into the log-sum-exp, writes
+// the row loss lse - z[target] and, when scale != 0, rewrites the logits in place as
+// dlogits = (softmax - onehot) * scale -- one read and one write of the logits instead of the
+// online pass plus the dlogits pass of xent_kernel.
+__device__ __forceinline__ void lse_merge(float& m, float& s, float om, float os) {
+  const float nm = fmaxf(m, om);
+  s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+  m = nm;
+}
+
+__global__ void __launch_bounds__(XE_THREADS) xent_parts_kernel(__nv_bfloat16* __restrict__ logits,
+                                                                const float* __restrict__ parts, int nb,
+                                                                const int32_t* __restrict__ targets,
+                                                                float* __restrict__ row_loss, int V, long long ld,
+                                                                float scale) {
+  pdl_wait();
+  __shared__ float red_m[XE_THREADS / 32], red_s[XE_THREADS / 32];
+  const int row = blockIdx.x;
+  const float2* pr = reinterpret_cast<const float2*>(parts + (size_t)row * 2 * nb);
+  float m = -INFINITY, s = 0.f;
+  for (int b = threadIdx.x; b < nb; b += XE_THREADS) {
+    const float2 p = pr[b];
+    lse_merge(m, s, p.x, p.y);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
+    lse_merge(m, s, om, os);
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    red_m[w] = m;
+    red_s[w] = s;
+  }
+  __syncthreads();
+  if (w == 0) {
+    m = lane < XE_THREADS / 32 ? red_m[lane] : -INFINITY;
+    s = lane < XE_THREADS / 32 ? red_s[lane] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
+      lse_merge(m, s, om, os);
+    }
+    if (lane == 0) {
+      red_m[0] = m;
+      red_s[0] = s;
+    }
+  }
+  __syncthreads();
+  m = red_m[0];
+  s = red_s[0];
+  __nv_bfloat16* z = logits + (size_t)row * ld;
+  const int tgt = targets[row];
+  const float zt = __bfloat162float(z[tgt]);
+  if (threadIdx.x == 0) row_loss[row] = logf(s) + m - zt;
+  if (scale == 0.f) return;  // loss only (inference)
+  __syncthreads();           // every thread has read z[tgt] before it is overwritten
+  const float inv = 1.f / s;
+  for (int c = threadIdx.x * 8; c < V; c += XE_THREADS * 8) {
+    float f[8];
+    load8(f, z + c);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = (__expf(f[i] - m) * inv - (c + i == tgt ? 1.f : 0.f)) * scale;
+    store8(z + c, f);
+  }
+}
+
 // ---------------------------------------------------------------- reductions
 // out[0] (+)= scale * sum(x[0:n])   (single CTA, fixed order)
 // dst += src (fp32, float4 vectors when aligned): merges co-resident replicas' gradient buffers
@@ -780,6 +848,15 @@ extern "C" int spx_token_prep(const int64_t* tokens, int64_t b, int64_t T, int64
                             reinterpret_cast<const long long*>(tokens), (int)T, (long long)ld_tokens, (int)n, n2, ids,
                             targets, perm, seg_start, seg_id, n_segments));
   return check_launch("token_prep_kernel");
+}
+
+extern "C" int spx_xent_from_parts(void* logits, const float* parts, int64_t nb, const int32_t* targets,
+                                   float* row_loss, int64_t n, int64_t V, int64_t ld, float scale, void* stream) {
+  if (V % 8 || ld % 8) return set_error(SPX_ERR_ARG, "xent_from_parts: V and ld must be multiples of 8");
+  if (nb <= 0 || nb * 128 < V) return set_error(SPX_ERR_ARG, "xent_from_parts: need nb >= V / 128 partials per row");
+  spx_launch_check(launch_k(xent_parts_kernel, dim3((unsigned)n), dim3(XE_THREADS), 0, SPX_S, BF(logits), parts, (int)nb,
+                            targets, row_loss, (int)V, ld, scale));
+  return check_launch("xent_parts_kernel");
 }
 
 extern "C" int spx_xent_fwd_bwd(void* logits, const int32_t* targets, float* row_loss, int64_t n, int64_t V, int64_t ld,

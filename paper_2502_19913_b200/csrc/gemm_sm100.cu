@@ -37,6 +37,8 @@ enum GemmEpilogue : int {
   EPI_ROPE64 = 4,      // C(bf16) = acc with rotate-half RoPE on columns < rope_cols (head dim 64)
   EPI_ROPE128 = 5,     // same, head dim 128
   EPI_SWIGLU_BWD = 6,  // D = dh [M, F]; R = gu [M, 2F] (128-col gate/up interleave) -> C2 = dgu [M, 2F]
+  EPI_XENT = 7,        // C(bf16) = acc (logits) and C2(f32)[m, 2*(N/128)] = per 128-column block
+                       // (max, sum exp(x - max)) of the bf16-rounded logits (cross-entropy partials)
 };
 
 template <int EPI>
@@ -533,7 +535,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
       } else {
-        // plain bf16 store, optionally + residual R (read coalesced into the staging box first)
+        // plain bf16 store, optionally + residual R (read coalesced into the staging box first);
+        // EPI_XENT also folds the row's 128 rounded logits into (max, sum exp) partials
+        float xm = -INFINITY, xs = 0.f;
 #pragma unroll 1
         for (int c = cb; c < cb + BN / 2 && n0 + c < args.N; c += 64) {
           box_acquire();
@@ -565,9 +569,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 f[8 * j + 4] += a2.x; f[8 * j + 5] += a2.y; f[8 * j + 6] += a3.x; f[8 * j + 7] += a3.y;
               }
             }
+            if constexpr (EPI == EPI_XENT) {
+              // statistics of the values as stored (bf16), online over the 32-column chunks
+              float cm = -INFINITY;
+#pragma unroll
+              for (int j = 0; j < 32; j += 2) {
+                const float2 r2 = unpack_bf16(pack_bf16(f[j], f[j + 1]));
+                f[j] = r2.x;
+                f[j + 1] = r2.y;
+                cm = fmaxf(cm, fmaxf(r2.x, r2.y));
+              }
+              if (cm > xm) {
+                xs *= exp2f((xm - cm) * 1.4426950408889634f);
+                xm = cm;
+              }
+              const float nm = -xm * 1.4426950408889634f;
+              float sk[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+              for (int j = 0; j < 32; ++j) sk[j & 3] += exp2f(fmaf(f[j], 1.4426950408889634f, nm));
+              xs += (sk[0] + sk[1]) + (sk[2] + sk[3]);
+            }
             put32(4 * q, f);
           }
           box_out(0, n0 + c, rbase);
+        }
+        if constexpr (EPI == EPI_XENT) {
+          const int row = rbase + lane;
+          if (row < args.M && n0 + cb < args.N)
+            *reinterpret_cast<float2*>(reinterpret_cast<float*>(args.C2) + (size_t)row * args.ldc2 + 2 * ((n0 + cb) >> 7)) =
+                make_float2(xm, xs);
         }
       }
       tc_fence_before();
@@ -919,7 +949,9 @@ extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* 
   if (N % 32 != 0) return set_error(SPX_ERR_ARG, "gemm: N must be a multiple of 32");
   if (K % 8 != 0 || lda % 8 != 0 || ldb % 8 != 0) return set_error(SPX_ERR_ARG, "gemm: K/lda/ldb must be multiples of 8");
   if (((uintptr_t)A | (uintptr_t)B) & 15) return set_error(SPX_ERR_ARG, "gemm: A/B must be 16-byte aligned");
-  if (epilogue < 0 || epilogue > 6 || epilogue == 4 || epilogue == 5) return set_error(SPX_ERR_ARG, "gemm: bad epilogue");
+  if (epilogue < 0 || epilogue > 7 || epilogue == 4 || epilogue == 5) return set_error(SPX_ERR_ARG, "gemm: bad epilogue");
+  if (epilogue == EPI_XENT && (N % 128 != 0 || C2 == nullptr || ldc2 < 2 * (N / 128)))
+    return set_error(SPX_ERR_ARG, "gemm: xent epilogue needs N % 128 == 0 and a partials output C2 with ldc2 >= 2*N/128");
   if (epilogue == EPI_SWIGLU_BWD && (N % 128 != 0 || C2 == nullptr || R == nullptr))
     return set_error(SPX_ERR_ARG, "gemm: swiglu-bwd epilogue needs N % 128 == 0, gu (R) and dgu (C2)");
   if (epilogue == EPI_SWIGLU && (N % 256 != 0 || C2 == nullptr))
@@ -930,7 +962,7 @@ extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* 
   args.probe = probe_mode();
   args.tma_store = tma_store_mode();
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int bn = (epilogue == EPI_SWIGLU || epilogue == EPI_F32 || epilogue == EPI_SWIGLU_BWD) ? 256
+  const int bn = (epilogue == EPI_SWIGLU || epilogue == EPI_F32 || epilogue == EPI_SWIGLU_BWD || epilogue == EPI_XENT) ? 256
                  : (use_pair((int)M) ? 256 : pick_bn((int)M, (int)N));  // CTA pairs need 256-col tiles
   if (epilogue == EPI_F32) pick_splits(args, bn);
   args.n_major = pick_raster(M, N, K, bn, (bn == 256 && use_pair((int)M)) ? 2 : 1);
@@ -944,6 +976,9 @@ extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* 
     case EPI_F32:
       return bn == 256 ? dispatch_256<EPI_F32>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s)
                        : dispatch_major<128, EPI_F32>(A, B, lda, ldb, a_mn_major, b_mn_major, args, s);
+    case EPI_XENT:
+      if (a_mn_major || b_mn_major) return set_error(SPX_ERR_ARG, "gemm: xent epilogue needs K-major A and B (forward)");
+      return dispatch_256_fixed<EPI_XENT, false, false>(A, B, lda, ldb, args, s);
     case EPI_SWIGLU_BWD:
       if (a_mn_major || !b_mn_major) return set_error(SPX_ERR_ARG, "gemm: swiglu-bwd epilogue needs K-major A, MN-major B (dgrad)");
       return dispatch_256_fixed<EPI_SWIGLU_BWD, false, true>(A, B, lda, ldb, args, s);

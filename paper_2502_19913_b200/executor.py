@@ -176,6 +176,10 @@ class Scratch:
             self.xf = torch.empty(n, d, **e)
             self.rstdf = torch.empty(n, dtype=F32, device=device)
             self.logits = torch.empty(n, cfg.vocab, **e)
+            # cross-entropy partials of the head GEMM epilogue: per row, (max, sum exp) of each
+            # 128-column block of the logits (EPI_XENT; V % 128 == 0)
+            self.xent_nb = cfg.vocab // 128 if cfg.vocab % 128 == 0 else 0
+            self.xparts = torch.empty(n, 2 * max(1, self.xent_nb), dtype=F32, device=device)
             self.row_loss = torch.empty(n, dtype=F32, device=device)
             self.dxf = torch.empty(n, d, **e)
 
@@ -266,14 +270,29 @@ class StageProgram:
             self.layer_fwd(ps, i, sb.xs[i], sb.layers[i], sb.xs[i + 1], sc, s)
         return sb.xs[k]
 
+    def head_xent(self, ps: ParamSet, sb: SlotBuffers, sc: Scratch, s, scale: float):
+        """Head GEMM + cross-entropy: the GEMM epilogue (EPI_XENT) writes the
+        bf16 logits and per-128-column (max, sum exp) partials; one pass then forms each row's
+        log-sum-exp and loss and, for training (scale != 0), overwrites the logits with
+        dlogits = (softmax - onehot) * scale.  Vocabularies that are not a multiple of 128 take
+        the separate xent pass."""
+        c, n, V = self.cfg, self.n, self.cfg.vocab
+        if sc.xent_nb:
+            native.gemm(sc.xf, ps.w("head"), sc.logits, M=n, N=V, K=c.d, lda=c.d, ldb=c.d, ldc=V,
+                        epilogue=native.EPI_XENT, C2=sc.xparts, ldc2=2 * sc.xent_nb, stream=s)
+            native.xent_from_parts(sc.logits, sc.xparts, sb.targets, sc.row_loss, nb=sc.xent_nb, n=n, V=V, ld=V,
+                                   scale=scale, stream=s)
+        else:
+            native.gemm(sc.xf, ps.w("head"), sc.logits, M=n, N=V, K=c.d, lda=c.d, ldb=c.d, ldc=V, stream=s)
+            native.xent_fwd_bwd(sc.logits, sb.targets, sc.row_loss, n=n, V=V, ld=V, scale=scale, stream=s)
+        native.sum_f32(sc.row_loss, n, sb.loss, scale=1.0 / n, stream=s)
+
     def loss_fwd(self, ps: ParamSet, sb: SlotBuffers, sc: Scratch, s):
         """Inference loss at the origin: final norm, head, token-mean cross-entropy into sb.loss
-        (the kernel's in-place dlogits are ignored; no gradient is touched)."""
+        (no dlogits, no gradient is touched)."""
         c, n = self.cfg, self.n
         native.rmsnorm_fwd(sb.ret, ps.w("final_norm"), sc.xf, sc.rstdf, rows=n, d=c.d, eps=c.eps, stream=s)
-        native.gemm(sc.xf, ps.w("head"), sc.logits, M=n, N=c.vocab, K=c.d, lda=c.d, ldb=c.d, ldc=c.vocab, stream=s)
-        native.xent_fwd_bwd(sc.logits, sb.targets, sc.row_loss, n=n, V=c.vocab, ld=c.vocab, scale=0.0, stream=s)
-        native.sum_f32(sc.row_loss, n, sb.loss, scale=1.0 / n, stream=s)
+        self.head_xent(ps, sb, sc, s, 0.0)
 
     def bwd(self, ps: ParamSet, sb: SlotBuffers, sc: Scratch, origin: bool, s, side=None):
         """Returns the buffer holding the gradient w.r.t. the node's input."""
@@ -300,9 +319,7 @@ class StageProgram:
         c, n = self.cfg, self.n
         d, V = c.d, c.vocab
         native.rmsnorm_fwd(sb.ret, ps.w("final_norm"), sc.xf, sc.rstdf, rows=n, d=d, eps=c.eps, stream=s)
-        native.gemm(sc.xf, ps.w("head"), sc.logits, M=n, N=V, K=d, lda=d, ldb=d, ldc=V, stream=s)
-        native.xent_fwd_bwd(sc.logits, sb.targets, sc.row_loss, n=n, V=V, ld=V, scale=1.0 / (n * self.M), stream=s)
-        native.sum_f32(sc.row_loss, n, sb.loss, scale=1.0 / n, stream=s)
+        self.head_xent(ps, sb, sc, s, 1.0 / (n * self.M))
         native.gemm(sc.logits, ps.w("head"), sc.dxf, M=n, N=d, K=V, lda=V, ldb=d, ldc=d, b_mn=True, stream=s)
         native.rmsnorm_bwd(sb.ret, ps.w("final_norm"), sc.rstdf, sc.dxf, None, sb.dret, ps.gv("final_norm"),
                            sc.rms_ws, rows=n, d=d, stream=s)

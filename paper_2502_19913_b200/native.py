@@ -54,6 +54,7 @@ SIGNATURES: dict[str, list] = {
     "spx_embed_bwd": [_P, _P, _P, _P, _I64, _P, _P, _I64, _P],
     "spx_token_prep": [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P],
     "spx_xent_fwd_bwd": [_P, _P, _P, _I64, _I64, _I64, _F, _P],
+    "spx_xent_from_parts": [_P, _P, _I64, _P, _P, _I64, _I64, _I64, _F, _P],
     "spx_sum_f32": [_P, _I64, _P, _F, _I32, _P],
     "spx_add_f32": [_P, _P, _I64, _P],
     "spx_add_f32_clear": [_P, _P, _I64, _P],
@@ -69,6 +70,7 @@ _RESTYPE = {"spx_last_error": ctypes.c_char_p, "spx_rmsnorm_ws_floats": ctypes.c
 
 EPI_BF16, EPI_BF16_RESID, EPI_F32, EPI_SWIGLU = 0, 1, 2, 3
 EPI_SWIGLU_BWD = 6
+EPI_XENT = 7
 
 
 # kernel-launch accounting (bench.py "gpu_launches") and GEMM call recording (roofline timing)
@@ -384,6 +386,12 @@ def embed_segments(ids) -> tuple:
     seg_id = torch.zeros(n, dtype=torch.int32)
     seg_id[:len(uniq)] = uniq.to(torch.int32)
     return perm.to(torch.int32), seg_start, seg_id, torch.tensor([len(uniq)], dtype=torch.int32)
+
+
+def xent_from_parts(logits, parts, targets, row_loss, *, nb, n, V, ld, scale, stream=None) -> None:
+    """Cross-entropy from the EPI_XENT head GEMM's (max, sum) partials; dlogits in place if scale."""
+    _check(load().spx_xent_from_parts(_ptr(logits), _ptr(parts), nb, _ptr(targets), _ptr(row_loss), n, V, ld,
+                                      float(scale), _stream(stream)), "spx_xent_from_parts")
 
 
 def xent_fwd_bwd(logits, targets, row_loss, *, n, V, ld, scale, stream=None) -> None:

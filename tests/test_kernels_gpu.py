@@ -239,6 +239,41 @@ def test_xent(n, V):
     assert rel(zz, zr.grad) < 1e-2
 
 
+@pytest.mark.parametrize("n,V,d", [(512, 32000, 1024), (384, 128256, 256), (256, 384, 64)])
+def test_head_gemm_xent_epilogue(n, V, d):
+    """Head GEMM with the cross-entropy epilogue (EPI_XENT: logits + per-128-column (max, sum exp)
+    partials) followed by spx_xent_from_parts equals torch fp32 cross-entropy on the same bf16
+    logits, and the separate xent pass on the same logits (loss and dlogits)."""
+    g = torch.Generator().manual_seed(V + d)
+    x = bf(torch.randn(n, d, generator=g)).to(dev)
+    w = bf(torch.randn(V, d, generator=g) * d ** -0.5 * 3).to(dev)
+    t = torch.randint(0, V, (n,), generator=g, dtype=torch.int32).to(dev)
+    nb = V // 128
+    z = torch.empty(n, V, dtype=torch.bfloat16, device=dev)
+    parts = torch.empty(n, 2 * nb, device=dev)
+    native.gemm(x, w, z, M=n, N=V, K=d, lda=d, ldb=d, ldc=V, epilogue=native.EPI_XENT, C2=parts, ldc2=2 * nb)
+    z_ref = z.clone()
+    scale = 1.0 / n
+    rl = torch.empty(n, device=dev)
+    native.xent_from_parts(z, parts, t, rl, nb=nb, n=n, V=V, ld=V, scale=scale)
+    rl2 = torch.empty(n, device=dev)
+    z2 = z_ref.clone()
+    native.xent_fwd_bwd(z2, t, rl2, n=n, V=V, ld=V, scale=scale)
+    torch.cuda.synchronize()
+    zr = z_ref.float().requires_grad_()
+    loss = torch.nn.functional.cross_entropy(zr, t.long(), reduction="none")
+    loss.sum().mul(scale).backward()
+    assert (rl - loss.detach()).abs().max().item() < 1e-3 * max(1.0, loss.abs().max().item())
+    assert (rl - rl2).abs().max().item() < 1e-4 * max(1.0, rl2.abs().max().item())
+    assert rel(z, zr.grad) < 1e-2
+    assert rel(z, z2) < 1e-2
+    # inference form: loss only, logits untouched
+    z3 = z_ref.clone()
+    native.xent_from_parts(z3, parts, t, rl, nb=nb, n=n, V=V, ld=V, scale=0.0)
+    torch.cuda.synchronize()
+    assert torch.equal(z3, z_ref)
+
+
 def test_adamw_and_clip():
     n, nd = 10_000, 7_000
     g = torch.Generator().manual_seed(0)
