@@ -9,7 +9,15 @@ NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -shared --expt-rela
 SRCS := $(wildcard $(CSRC)/*.cu)
 HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/spx.h
 
-all: $(OUT)
+SCHED := paper_2502_19913_b200/libspx_sched.so
+
+all: $(OUT) $(SCHED)
+
+sched: $(SCHED)
+
+# native path planner (host C++, no CUDA; include/spx_sched.h)
+$(SCHED): paper_2502_19913_b200/native_sched/sched.cpp include/spx_sched.h
+	$(CXX) -O2 -std=c++17 -ffp-contract=off -fPIC -shared -o $@ $<
 
 $(OUT): $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -o $@ $(SRCS) -lcudart
@@ -18,6 +26,6 @@ ptxas-info: $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -o /tmp/spx_ptxas.so $(SRCS) -lcudart
 
 clean:
-	rm -f $(OUT)
+	rm -f $(OUT) $(SCHED)
 
-.PHONY: all clean ptxas-info
+.PHONY: all clean ptxas-info sched

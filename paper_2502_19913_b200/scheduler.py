@@ -22,11 +22,14 @@ Ambiguities of the spec are pinned here and in DESIGN.md:
 
 from __future__ import annotations
 
+import ctypes
 import heapq
 import itertools
 import json
 import math
+import os
 from dataclasses import dataclass, field
+from pathlib import Path
 from fractions import Fraction
 
 import numpy as np
@@ -252,6 +255,86 @@ class _Timing:
         self.fwd = topology.compute_fwd_ms.astype(float)
         self.bwd = self.fwd * float(topology.bwd_ratio)
         self.comm = comm_matrix(topology, msg_bytes)
+        self._native = {}
+
+    def native_problem(self, assignment: StageAssignment, l: int, max_swaps: int):
+        """The spx_sched_problem struct for libspx_sched (arrays kept alive on this object)."""
+        key = (tuple(assignment.node_stage()), l, max_swaps)
+        if key not in self._native:
+            ns = np.ascontiguousarray(assignment.node_stage(), dtype=np.int32)
+            fwd = np.ascontiguousarray(self.fwd, dtype=np.float64)
+            bwd = np.ascontiguousarray(self.bwd, dtype=np.float64)
+            comm = np.ascontiguousarray(self.comm, dtype=np.float64)
+            st = _SchedProblem(len(ns), assignment.s, l, max_swaps, ns.ctypes.data_as(_PI32),
+                               fwd.ctypes.data_as(_PF64), bwd.ctypes.data_as(_PF64), comm.ctypes.data_as(_PF64))
+            self._native[key] = (st, ns, fwd, bwd, comm)
+        return self._native[key][0]
+
+
+# ---------------------------------------------------------------------------------------
+# native planner (libspx_sched.so, include/spx_sched.h; SURVEY.md §8(f) f2)
+# ---------------------------------------------------------------------------------------
+_PI32 = ctypes.POINTER(ctypes.c_int32)
+_PF64 = ctypes.POINTER(ctypes.c_double)
+
+
+class _SchedProblem(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("s", ctypes.c_int32), ("l", ctypes.c_int32), ("max_swaps", ctypes.c_int32),
+                ("node_stage", _PI32), ("fwd", _PF64), ("bwd", _PF64), ("comm", _PF64)]
+
+
+_SCHED_LIB: list = []
+
+
+def native_lib():
+    """libspx_sched.so, or None when it is not built or SPX_SCHED_NATIVE=0 (Python planner).
+    Both planners give identical schedules (tests/test_scheduler_native.py)."""
+    if os.environ.get("SPX_SCHED_NATIVE", "1") == "0":
+        return None
+    if not _SCHED_LIB:
+        path = Path(__file__).resolve().parent / "libspx_sched.so"
+        lib = None
+        if path.exists():
+            lib = ctypes.CDLL(str(path))
+            lib.spx_sched_astar.argtypes = [ctypes.POINTER(_SchedProblem), ctypes.c_int32, ctypes.c_int32,
+                                            ctypes.c_int32, _PI32, _PF64, _PF64, _PI32, _PF64, _PF64, _PI32, _PI32,
+                                            _PF64]
+            lib.spx_sched_collisions.restype = ctypes.c_int64
+            lib.spx_sched_collisions.argtypes = [ctypes.c_int32, _PI32, _PI32, _PI32, _PF64, _PF64, ctypes.c_int32,
+                                                 ctypes.c_int64, _PI32, _PF64]
+        _SCHED_LIB.append(lib)
+    return _SCHED_LIB[0]
+
+
+def _astar_native(lib, agent: Agent, assignment: StageAssignment, l: int, constraints, config, tm: _Timing):
+    node_stage = assignment.node_stage()
+    mine = [c for c in constraints if c.agent == agent.id]
+    if any(c.permanent and c.node == agent.origin for c in mine):
+        raise InfeasibleError(f"agent {agent.id}: origin {agent.origin} is banned")
+    k = len(mine)
+    cn = (ctypes.c_int32 * max(1, k))(*[c.node for c in mine])
+    c0 = (ctypes.c_double * max(1, k))(*[c.t_start for c in mine])
+    c1 = (ctypes.c_double * max(1, k))(*[c.t_end for c in mine])
+    s = assignment.s
+    nodes = (ctypes.c_int32 * s)()
+    fw = (ctypes.c_double * (3 * (s + 1)))()
+    bw = (ctypes.c_double * (3 * s))()
+    ln, sw, e2e = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
+    rc = lib.spx_sched_astar(ctypes.byref(tm.native_problem(assignment, l, config.max_swaps)), agent.origin,
+                             int(agent.id in config.swap_agents), k, cn, c0, c1, nodes, fw, bw, ctypes.byref(ln),
+                             ctypes.byref(sw), ctypes.byref(e2e))
+    if rc == 1:
+        raise InfeasibleError(f"agent {agent.id}: no path satisfies its {k} constraints")
+    if rc != 0:
+        raise ValidationError(f"spx_sched_astar: bad arguments (rc={rc})")
+    n_ = ln.value
+    route = [nodes[i] for i in range(n_)]
+    visits = tuple(Visit(v, node_stage[v], fw[3 * i], fw[3 * i + 1], fw[3 * i + 2]) for i, v in enumerate(route))
+    visits += (Visit(agent.origin, 0, fw[3 * n_], fw[3 * n_ + 1], fw[3 * n_ + 2]),)
+    back = list(reversed(route[1:])) + [agent.origin]
+    bwd = tuple(Visit(v, node_stage[v] if i < n_ - 1 else 0, bw[3 * i], bw[3 * i + 1], bw[3 * i + 2])
+                for i, v in enumerate(back))
+    return PathPlan(agent.id, visits, bwd, sw.value, e2e.value)
 
 
 def _earliest_start(windows: list[tuple[float, float]], t: float, dur: float) -> float:
@@ -284,6 +367,10 @@ def astar_path(agent: Agent, topology: Topology, assignment: StageAssignment, co
     stage_nodes = [assignment.stage_nodes(i) for i in range(s)]
     if node_stage[agent.origin] != 0:
         raise ValidationError(f"agent {agent.id} origin {agent.origin} is not in S0", row=agent.id)
+
+    lib = native_lib()
+    if lib is not None:
+        return _astar_native(lib, agent, assignment, l, constraints, config, tm)
 
     banned: set[int] = set()
     windows: dict[int, list[tuple[float, float]]] = {}
@@ -419,6 +506,11 @@ def detect_conflicts(node: SearchNode, topology: Topology, assignment: StageAssi
         if c > m:
             out.append(NodeOveruse(v, c, m))
     crit = critical_agent(paths) if paths else -1
+    lib = native_lib()
+    if lib is not None and paths:
+        cols = _collisions_native(lib, paths, topology.n)
+        cols.sort(key=lambda c: (0 if crit in (c.path_i, c.path_j) else 1, c.overlap[0], c.node, c.path_i, c.path_j))
+        return out + cols
     by_node: dict[int, list] = {}
     for a in sorted(paths):
         for v, s0, e0 in paths[a].fwd_intervals():
@@ -436,6 +528,29 @@ def detect_conflicts(node: SearchNode, topology: Topology, assignment: StageAssi
                 cols.append(Collision(i, j, v, (lo, hi), ii, jj))
     cols.sort(key=lambda c: (0 if crit in (c.path_i, c.path_j) else 1, c.overlap[0], c.node, c.path_i, c.path_j))
     return out + cols
+
+
+def _collisions_native(lib, paths: dict, n: int) -> list:
+    agents = sorted(paths)
+    ivs = [paths[a].fwd_intervals() for a in agents]
+    tot = sum(len(x) for x in ivs)
+    ids = (ctypes.c_int32 * len(agents))(*agents)
+    cnt = (ctypes.c_int32 * len(agents))(*[len(x) for x in ivs])
+    vn = (ctypes.c_int32 * tot)(*[v for x in ivs for v, _, _ in x])
+    vs = (ctypes.c_double * tot)(*[s0 for x in ivs for _, s0, _ in x])
+    ve = (ctypes.c_double * tot)(*[e0 for x in ivs for _, _, e0 in x])
+    cap = 64
+    while True:
+        ijn = (ctypes.c_int32 * (3 * cap))()
+        tms = (ctypes.c_double * (6 * cap))()
+        found = lib.spx_sched_collisions(len(agents), ids, cnt, vn, vs, ve, n, cap, ijn, tms)
+        if found < 0:
+            raise ValidationError("spx_sched_collisions: bad arguments")
+        if found <= cap:
+            break
+        cap = int(found)
+    return [Collision(ijn[3 * i], ijn[3 * i + 1], ijn[3 * i + 2], (tms[6 * i], tms[6 * i + 1]),
+                      (tms[6 * i + 2], tms[6 * i + 3]), (tms[6 * i + 4], tms[6 * i + 5])) for i in range(found)]
 
 
 # ---------------------------------------------------------------------------------------
