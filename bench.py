@@ -302,7 +302,7 @@ def time_full_pp(args, rc_name, rank=0, world=1, local=0, variant="-full", over=
 
     rf = get_config(rc_name + variant, **(over or {}))
     tokens = synthetic_tokens(rf.model, rf.M, rf.b, rf.T, seed=1234)
-    tr = Trainer(rf.schedule(), rf.topology(), rf.sim_config(), rf.model, rf.assignment, b=rf.b, T=rf.T,
+    tr = Trainer(rf.schedule(), rf.topology(), rf.sim_config(), rf.model, rf.assignment, b=rf.b, T=rf.T, split=rf.split,
                  rank=rank, world=world, device=local)
     dev_inputs = {k: v.cuda() for k, v in tr._stage_inputs(tokens).items()}
     for _ in range(max(1, args.warmup)):
@@ -368,7 +368,7 @@ def run_ours(args, rc):
     burst, sustained, hbm, peak_kind = _peaks()
     tokens = synthetic_tokens(rc.model, rc.M, rc.b, rc.T, seed=1234)
     native.record_gemms(True)
-    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T)
+    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, split=rc.split)
     native.record_gemms(False)
     launches = tr.launches_per_step()
     host = tr._stage_inputs(tokens)
@@ -457,7 +457,7 @@ def run_ours_dist(args, rc):
     burst, sustained, hbm, peak_kind = _peaks()
     tokens = synthetic_tokens(rc.model, rc.M, rc.b, rc.T, seed=1234)
     native.record_gemms(True)
-    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T,
+    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, split=rc.split,
                  rank=rank, world=world, device=local)
     native.record_gemms(False)
     launches = torch.tensor([tr.launches_per_step()], device=tr.dev)

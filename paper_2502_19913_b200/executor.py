@@ -470,6 +470,11 @@ class Trainer:
                             for st in range(assignment.s)}
 
         with torch.cuda.device(self.dev):
+            if params is not None:
+                got = [sum(1 for k in p if k.endswith(".wq")) for p in params]
+                if got != list(self.split):
+                    raise ValidationError(f"params hold {got} layers per stage, the layer split is {self.split} "
+                                          f"(pass split=)")
             canon = params if params is not None else init_params(cfg, self.split, seed)
             self.layouts = [stage_layout(cfg, st, self.split) for st in range(assignment.s)]
             # one parameter set per stage hosted here (co-resident replicas share it)

@@ -33,7 +33,7 @@ def _flat(gdict):
 @pytest.fixture(scope="module")
 def c1():
     rc, sch, params, tokens = _setup()
-    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params,
+    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, split=rc.split, params=params,
                  keep_grads=True)
     res = tr.step(tokens, timing=True)
     g = tr.grads()
@@ -91,7 +91,7 @@ def test_graphs_equal_eager():
     rc, sch, params, tokens = _setup()
     losses = []
     for graphs in (False, True):
-        tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params,
+        tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, split=rc.split, params=params,
                      use_graphs=graphs)
         losses.append([tr.step(tokens)["loss"] for _ in range(2)])
     assert losses[0] == losses[1]
@@ -105,7 +105,7 @@ def test_skip_robust_inference_matches_oracle():
     from oracle.train_ref import rms_norm, rope_tables, stage_forward
 
     rc, sch, params, tokens = _setup()
-    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params,
+    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, split=rc.split, params=params,
                  keep_grads=True)
     tr.step(tokens)                                 # weights after one update
     p = tr.params()
@@ -145,7 +145,7 @@ def test_gqa_config_matches_oracle(heads, kv):
     sch = rc.schedule()
     params = init_params(cfg, rc.layers, seed=0)
     tokens = synthetic_tokens(cfg, rc.M, rc.b, rc.T, seed=1234)
-    tr = Trainer(sch, rc.topology(), rc.sim_config(), cfg, rc.assignment, b=rc.b, T=rc.T, params=params,
+    tr = Trainer(sch, rc.topology(), rc.sim_config(), cfg, rc.assignment, b=rc.b, T=rc.T, split=rc.split, params=params,
                  keep_grads=True)
     res = tr.step(tokens)
     agents = sorted(a.id for a in sch.agents)
@@ -165,7 +165,7 @@ def test_cleared_gradients_equal_kept_gradients():
     rc, sch, params, tokens = _setup()
     runs = []
     for keep in (False, True):
-        tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params,
+        tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, split=rc.split, params=params,
                      keep_grads=keep)
         losses = [tr.step(tokens)["loss"] for _ in range(3)]
         runs.append((losses, tr.params()))

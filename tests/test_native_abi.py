@@ -80,7 +80,7 @@ def test_executor_requires_cuda():
 
     rc = get_config("C1")
     with pytest.raises(native.NativeError):
-        Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T)
+        Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, split=rc.split)
 
 
 def test_argument_validation_of_newer_entry_points(lib):

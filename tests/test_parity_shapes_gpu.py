@@ -46,7 +46,7 @@ def check_parity(rc: RunConfig, sch=None, seed=0):
     sch = sch or rc.schedule()
     params = init_params(rc.model, rc.layers, seed=seed)
     tokens = synthetic_tokens(rc.model, rc.M, rc.b, rc.T, seed=1234)
-    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params,
+    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, split=rc.split, params=params,
                  keep_grads=True)
     res = tr.step(tokens, timing=True)
     rep = tr.make_report(res)

@@ -11,7 +11,7 @@ agents = sorted(a.id for a in sch.agents)
 mbs = train_ref.mb_stage_sequences({a: sch.paths[a].stages for a in agents}, agents, rc.M)
 ref = train_ref.iteration(rc.model, rc.layers, params, mbs, tokens, update=False)
 for graphs in (False, True):
-    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params, use_graphs=graphs)
+    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, split=rc.split, params=params, use_graphs=graphs)
     r = tr.step(tokens)
     print("graphs", graphs, "loss", r["loss"], "ref", ref["loss"])
     print(" mb", [round(x, 4) for x in tr.mb_loss.tolist()])

@@ -32,7 +32,7 @@ def main():
     sch = rc.schedule()
     params = init_params(rc.model, rc.layers, seed=0)
     tokens = synthetic_tokens(rc.model, rc.M, rc.b, rc.T, seed=1234)
-    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, params=params,
+    tr = Trainer(sch, rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, split=rc.split, params=params,
                  rank=rank, world=world, device=local, keep_grads=True)
     res = tr.step(tokens, timing=True)
     rep = tr.make_report(res)

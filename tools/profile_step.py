@@ -29,7 +29,7 @@ def main():
     a = ap.parse_args()
     rc = get_config(a.config, M=a.M)
     tokens = synthetic_tokens(rc.model, rc.M, rc.b, rc.T)
-    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T,
+    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, split=rc.split,
                  use_graphs=not a.eager)
     host = tr._stage_inputs(tokens)
     dev = {k: v.cuda() for k, v in host.items()}

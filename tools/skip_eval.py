@@ -27,7 +27,7 @@ def main():
     ap.add_argument("--rates", default="0,0.25,0.5")
     a = ap.parse_args()
     rc = get_config(a.config)
-    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T)
+    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, split=rc.split)
     tokens = synthetic_tokens(rc.model, rc.M, rc.b, rc.T)
     host = tr._stage_inputs(tokens)
     for i in range(a.steps):

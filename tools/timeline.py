@@ -44,7 +44,7 @@ def main():
             f.write(emit_gantt(plan, rc.topology().n, f"{a.config} planned (simulator, planning times): "
                                                        f"{plan.iteration_makespan:.1f} ms"))
     tokens = synthetic_tokens(rc.model, rc.M, rc.b, rc.T)
-    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T,
+    tr = Trainer(rc.schedule(), rc.topology(), rc.sim_config(), rc.model, rc.assignment, b=rc.b, T=rc.T, split=rc.split,
                  rank=rank, world=world, device=local)
     host = tr._stage_inputs(tokens)
     for _ in range(a.warmup):
