@@ -283,14 +283,18 @@ __global__ void __launch_bounds__(THREADS) attn_fwd_kernel(const Params p) {
 template <int HD>
 __global__ void attn_bwd_delta_kernel(const Params p) {
   pdl_wait();
-  // 8 lanes per (row, head); lane j sums the 16-byte vectors j, j+8, ... of that head's row
+  // 8 lanes per (row, head); lane j sums the 16-byte vectors j, j+8, ... of that head's row.
+  // Groups are numbered in the [B, H, T] order of the outputs (position fastest), so the D and
+  // lse*log2e stores of a warp's four groups are contiguous
   const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
   const int j = threadIdx.x & 7;
   const long long rows = (long long)p.B * p.T;
   const bool live = g < rows * p.H;
   const long long gg = live ? g : 0;
-  const long long r = gg / p.H;
-  const int h = (int)(gg % p.H);
+  const int t_ = (int)(gg % p.T);
+  const long long bh = gg / p.T;
+  const int h = (int)(bh % p.H);
+  const long long r = (bh / p.H) * p.T + t_;
   const __nv_bfloat16* o = p.o + r * p.ldo + h * HD;
   const __nv_bfloat16* d = p.dout + r * p.ldo + h * HD;
   float s = 0.f;
@@ -312,8 +316,7 @@ __global__ void attn_bwd_delta_kernel(const Params p) {
   s += __shfl_xor_sync(0xffffffffu, s, 2);
   s += __shfl_xor_sync(0xffffffffu, s, 1);
   if (live && j == 0) {
-    const int b = (int)(r / p.T), t = (int)(r % p.T);
-    const long long idx = ((long long)b * p.H + h) * p.T + t;
+    const long long idx = gg;  // ((b * H + h) * T + t)
     p.delta[idx] = s;
     // second half of the workspace: lse in the exp2 domain for the tcgen05 dK/dV kernel
     p.delta[(long long)p.B * p.H * p.T + idx] = p.lse[idx] * 1.4426950408889634f;

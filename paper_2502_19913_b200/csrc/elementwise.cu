@@ -68,6 +68,51 @@ __global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __
   if (lane == 0) rstd[row] = r;
 }
 
+// Register-resident form (d <= 256*NCH): the row's 16-byte vectors are loaded once, all in
+// flight together, kept in registers for the normalisation pass (no second read of x).
+template <int NCH>
+__global__ void rmsnorm_fwd_reg_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
+                                       __nv_bfloat16* __restrict__ y, float* __restrict__ rstd, int rows, int d,
+                                       float eps) {
+  pdl_wait();
+  const int row = blockIdx.x * ROW_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const size_t off = (size_t)row * d;
+  Vec8 xv[NCH];
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    const int c = lane * 8 + k * 256;
+    xv[k].u = c < d ? *reinterpret_cast<const uint4*>(x + off + c) : make_uint4(0, 0, 0, 0);
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < NCH; ++k)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(xv[k].h[i]);
+      ss += f.x * f.x + f.y * f.y;
+    }
+  ss = warp_sum(ss);
+  const float r = rsqrtf(ss / d + eps);
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    const int c = lane * 8 + k * 256;
+    if (c < d) {
+      float w[8], f[8];
+      load8(w, g + c);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 t = __bfloat1622float2(xv[k].h[i]);
+        f[2 * i] = t.x * r * w[2 * i];
+        f[2 * i + 1] = t.y * r * w[2 * i + 1];
+      }
+      store8(y + off + c, f);
+    }
+  }
+  if (lane == 0) rstd[row] = r;
+}
+
 // RMSNorm backward, dx:  dx = dres + rstd * (g*dy - xhat * mean(xhat*g*dy)), xhat = x*rstd.
 // One warp per row, 16-byte vectors (HBM-bound: reads x, dy, dres, writes dx).
 __global__ void rmsnorm_bwd_dx_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
@@ -732,8 +777,15 @@ using namespace spx::ew;
 extern "C" int spx_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int64_t rows, int64_t d, float eps,
                                void* stream) {
   if (d % 8) return set_error(SPX_ERR_ARG, "rmsnorm: d must be a multiple of 8");
-  spx_launch_check(launch_k(rmsnorm_fwd_kernel, dim3((unsigned)((rows + ROW_WARPS - 1) / ROW_WARPS)), dim3(ROW_WARPS * 32), 0, SPX_S, 
-      CBF(x), CBF(g), BF(y), rstd, (int)rows, (int)d, eps));
+  const dim3 grid((unsigned)((rows + ROW_WARPS - 1) / ROW_WARPS)), block(ROW_WARPS * 32);
+  if (d <= 4096) {
+    const int nch = (int)((d + 255) / 256);
+    auto k = nch <= 1 ? rmsnorm_fwd_reg_kernel<1> : nch <= 2 ? rmsnorm_fwd_reg_kernel<2>
+             : nch <= 4 ? rmsnorm_fwd_reg_kernel<4> : nch <= 8 ? rmsnorm_fwd_reg_kernel<8> : rmsnorm_fwd_reg_kernel<16>;
+    spx_launch_check(launch_k(k, grid, block, 0, SPX_S, CBF(x), CBF(g), BF(y), rstd, (int)rows, (int)d, eps));
+    return check_launch("rmsnorm_fwd_reg_kernel");
+  }
+  spx_launch_check(launch_k(rmsnorm_fwd_kernel, grid, block, 0, SPX_S, CBF(x), CBF(g), BF(y), rstd, (int)rows, (int)d, eps));
   return check_launch("rmsnorm_fwd_kernel");
 }
 
