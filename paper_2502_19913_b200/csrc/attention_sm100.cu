@@ -499,6 +499,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 // softmax states at the end of the item.
 //   TMEM: S_A [0,128)  S_B [128,256)  O_A [256,320)  O_B [320,384)  P_A [384,448)  P_B [448,512)
 // ------------------------------------------------------------------------------------------
+// three role warps (TMA Q/K, MMA, TMEM alloc + TMA V) and two softmax warpgroups: 352 threads,
+// so each thread may hold 184 registers (a softmax thread keeps a full 128-column row in flight)
+constexpr int G2_THREADS = 32 * 11;
+
 struct G2Smem {
   static constexpr int ATOM = BM * 128;
   static constexpr int Q_BYTES = ATOM;  // hd = 64
@@ -549,7 +553,7 @@ SPX_DEVICE float exp_store_row128(uint32_t sb, uint32_t pdst, int r, bool diag, 
   return sum;
 }
 
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __maxnreg__(184)
     attn_fwd_g2_kernel(const __grid_constant__ CUtensorMap tmQKV, const FwdParams p) {
   using L = G2Smem;
   constexpr int HD = 64;
@@ -624,8 +628,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma_load_2d(smem + L::OFF_K + s * L::Q_BYTES, &tmQKV, &k_full[s], (p.H + kvh) * HD, row0 + j * BN);
       }
     }
-  } else if (warp == 3 && lane == 0) {
-    // ---------------- TMA producer: V ----------------
+  } else if (warp == 2 && lane == 0) {
+    // ---------------- TMA producer: V (the TMEM-allocating warp, idle otherwise) ----------------
     int g = 0;
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
       if (w >= n_items) continue;
@@ -695,9 +699,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
     if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_n, pend_c);
-  } else if (warp >= 4) {
-    // ---------------- softmax: group x = (warp - 4) / 4, thread = query row ----------------
-    const int x = (warp - 4) >> 2;
+  } else if (warp >= 3) {
+    // ---------------- softmax: group x = (warp - 3) / 4 (warps 3-6, 7-10), thread = query row;
+    // the TMEM lane quadrant of a warp is warp % 4, so each group covers the four quadrants ----
+    const int x = (warp - 3) >> 2;
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
@@ -866,7 +871,7 @@ int launch_fwd(const void* qkv, const FwdParams& p, long long ld_qkv, cudaStream
       if (e != cudaSuccess) return set_cuda_error(e, "attn_fwd_g2 attr");
       set2 = true;
     }
-    spx_launch_check(launch_k(attn_fwd_g2_kernel, dim3(grid), dim3(THREADS), G2Smem::BYTES, s, map, p));
+    spx_launch_check(launch_k(attn_fwd_g2_kernel, dim3(grid), dim3(G2_THREADS), G2Smem::BYTES, s, map, p));
     return check_launch("attn_fwd_g2_kernel");
   }
   auto k = attn_fwd_tc_kernel<HD>;
