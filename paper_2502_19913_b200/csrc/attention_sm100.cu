@@ -488,367 +488,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
-// ------------------------------------------------------------------------------------------
-// hd = 64: two softmax warpgroups on alternate key blocks.  At hd=64 the per-block MMA work
-// (S 256 + PV 256 cycles) is half the MUFU work (16384 ex2 at 16/clk), so the softmax decides
-// the speed; with one warpgroup its non-exponential phases (TMEM reads, P store, barriers) run
-// in lockstep and leave the MUFU idle.  Here group A (warps 4-7) takes the even blocks of an item
-// and group B (warps 8-11) the odd ones, each thread a full 128-column row, each group with its
-// own lagged running max, row sum and O accumulator -- no per-block exchange between warps -- so
-// one group's overheads overlap the other's exponentials.  Group A merges the two partial
-// softmax states at the end of the item.
-//   TMEM: S_A [0,128)  S_B [128,256)  O_A [256,320)  O_B [320,384)  P_A [384,448)  P_B [448,512)
-// ------------------------------------------------------------------------------------------
-// three role warps (TMA Q/K, MMA, TMEM alloc + TMA V) and two softmax warpgroups: 352 threads,
-// so each thread may hold 184 registers (a softmax thread keeps a full 128-column row in flight)
-constexpr int G2_THREADS = 32 * 11;
-
-struct G2Smem {
-  static constexpr int ATOM = BM * 128;
-  static constexpr int Q_BYTES = ATOM;  // hd = 64
-  static constexpr int NK = 3, NV = 3;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + Q_BYTES;
-  static constexpr int OFF_V = OFF_K + NK * Q_BYTES;
-  static constexpr int OFF_BAR = OFF_V + NV * Q_BYTES;
-  static constexpr int OFF_ST = OFF_BAR + 256;  // group B's per-row (m, l, owed O factor) [2 items][3][BM]
-  static constexpr int RAW = OFF_ST + 2 * 3 * BM * 4;
-  static constexpr int BYTES = RAW > 116 * 1024 ? RAW : 116 * 1024;
-};
-
-// O row (HD fp32 columns in TMEM) *= a
-SPX_DEVICE void scale_o(uint32_t taddr, float a) {
-#pragma unroll 1
-  for (int c = 0; c < 64; c += 32) {
-    uint32_t v[32];
-    tmem_ld_32x32b_x32(taddr + c, v);
-    tmem_ld_wait_dep(v);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * a);
-    tmem_st_32x32b_x32(taddr + c, v);
-  }
-  tmem_st_wait();
-}
-
-// exponentiate one 128-column row of S (4 TMEM chunks of 32, each loaded while the previous
-// one is processed) with max m and store P (bf16 pairs) to TMEM at pdst, 32 columns per pair of
-// chunks; returns the row sum and tracks the raw maximum
-SPX_DEVICE float exp_store_row128(uint32_t sb, uint32_t pdst, int r, bool diag, float sl2, float m, float& bmax) {
-  uint32_t va[32], vb[32], pk[32];
-  float sum = 0.f;
-  tmem_ld_32x32b_x32(sb, va);
-  tmem_ld_wait_dep(va);
-#pragma unroll
-  for (int c = 0; c < 4; c += 2) {
-    tmem_ld_32x32b_x32(sb + 32 * (c + 1), vb);
-    if (diag) mask_chunk(va, 32 * c, r);
-    exp_chunk(va, sl2, m, pk, sum, bmax);
-    tmem_ld_wait_dep(vb);
-    if (c + 2 < 4) tmem_ld_32x32b_x32(sb + 32 * (c + 2), va);
-    if (diag) mask_chunk(vb, 32 * (c + 1), r);
-    exp_chunk(vb, sl2, m, pk + 16, sum, bmax);
-    tmem_st_32x32b_x32(pdst + 16 * c, pk);
-    if (c + 2 < 4) tmem_ld_wait_dep(va);
-  }
-  return sum;
-}
-
-__global__ void __maxnreg__(184)
-    attn_fwd_g2_kernel(const __grid_constant__ CUtensorMap tmQKV, const FwdParams p) {
-  using L = G2Smem;
-  constexpr int HD = 64;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  constexpr int NK = L::NK, NV = L::NV;
-  uint64_t* q_full = bars + 0;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* s_full = bars + 2;    // [group]
-  uint64_t* p_full = bars + 4;    // [group], 4 arrivals
-  uint64_t* pv_done = bars + 6;   // [group]
-  uint64_t* o_free = bars + 8;    // [group], 4 arrivals (group A after the item epilogue)
-  uint64_t* b_done = bars + 10;   // group B's state for the item is in smem, 4 arrivals
-  uint64_t* st_free = bars + 11;  // group A has read it, 4 arrivals
-  uint64_t* k_full = bars + 12;            // [NK]
-  uint64_t* k_empty = bars + 12 + NK;      // [NK]
-  uint64_t* v_full = bars + 12 + 2 * NK;   // [NV]
-  uint64_t* v_empty = bars + 12 + 2 * NK + NV;  // [NV]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12 + 2 * NK + 2 * NV);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqb = p.T / BM;
-  const int BH = p.B * p.H;
-  const int n_items = nqb * BH;
-  const int group = p.H / p.Hkv;
-
-  if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tmQKV);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
-      mbar_init(&pv_done[i], 1);
-      mbar_init(&o_free[i], 4);
-    }
-    mbar_init(b_done, 4);
-    mbar_init(st_free, 4);
-    for (int i = 0; i < NK; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-    }
-    for (int i = 0; i < NV; ++i) {
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
-    }
-    fence_barrier_init();
-    fence_proxy_async();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_wait();
-  constexpr uint32_t TM_O = 256, TM_P = 384;
-
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer: Q and K ----------------
-    int g = 0, n = 0;
-    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
-      if (w >= n_items) continue;
-      const Item it = item_of(w, nqb, BH, p.H);
-      const int row0 = it.b * p.T, kvh = it.h / group;
-      mbar_wait(q_empty, (n & 1) ^ 1);
-      mbar_expect_tx(q_full, L::Q_BYTES);
-      tma_load_2d(smem + L::OFF_Q, &tmQKV, q_full, it.h * HD, row0 + it.qb * BM);
-      for (int j = 0; j <= it.qb; ++j, ++g) {
-        const int s = g % NK;
-        mbar_wait(&k_empty[s], ((g / NK) & 1) ^ 1);
-        mbar_expect_tx(&k_full[s], L::Q_BYTES);
-        tma_load_2d(smem + L::OFF_K + s * L::Q_BYTES, &tmQKV, &k_full[s], (p.H + kvh) * HD, row0 + j * BN);
-      }
-    }
-  } else if (warp == 2 && lane == 0) {
-    // ---------------- TMA producer: V (the TMEM-allocating warp, idle otherwise) ----------------
-    int g = 0;
-    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
-      if (w >= n_items) continue;
-      const Item it = item_of(w, nqb, BH, p.H);
-      const int row0 = it.b * p.T, kvh = it.h / group;
-      for (int j = 0; j <= it.qb; ++j, ++g) {
-        const int s = g % NV;
-        mbar_wait(&v_empty[s], ((g / NV) & 1) ^ 1);
-        mbar_expect_tx(&v_full[s], L::Q_BYTES);
-        tma_load_2d(smem + L::OFF_V + s * L::Q_BYTES, &tmQKV, &v_full[s], (p.H + p.Hkv + kvh) * HD, row0 + j * BN);
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer: S_j into S_{j&1}, then PV_{j-1} into O_{(j-1)&1} ----------------
-    constexpr uint32_t IDESC_S = umma_idesc_bf16(BM, BN, false, false);
-    constexpr uint32_t IDESC_O = umma_idesc_bf16(BM, HD, false, true);
-    const uint32_t sQ = smem_u32(smem + L::OFF_Q);
-    int g = 0, n = 0;
-    int cnt0 = 0, cnt1 = 0;  // blocks issued per group (phase of p_full of that group)
-    // PV of block (global gb, item-local j) for group x = j & 1, its cx-th block overall
-    auto issue_pv = [&](int gb, int j, int item_n, int cx) {
-      const int x = j & 1, s = gb % NV;
-      if (j < 2) mbar_wait(&o_free[x], (item_n & 1) ^ 1);  // group's first PV of the item overwrites O_x
-      mbar_wait(&p_full[x], cx & 1);
-      mbar_wait(&v_full[s], (gb / NV) & 1);
-      tc_fence_after();
-      const uint32_t sV = smem_u32(smem + L::OFF_V + s * L::Q_BYTES);
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t bd = umma_desc_sw128(sV + kk * 2048, L::ATOM, 1024);
-          mma_bf16_ts(tmem + TM_O + x * HD, tmem + TM_P + x * 64 + kk * 8, bd, IDESC_O, (j >= 2) || (kk > 0));
-        }
-        mma_commit(&pv_done[x]);
-        mma_commit(&v_empty[s]);
-      }
-      __syncwarp();
-    };
-    int pend_g = -1, pend_j = 0, pend_n = 0, pend_c = 0;
-    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
-      if (w >= n_items) continue;
-      const Item it = item_of(w, nqb, BH, p.H);
-      mbar_wait(q_full, n & 1);
-      for (int j = 0; j <= it.qb; ++j, ++g) {
-        const int x = j & 1;
-        const int sk = g % NK;
-        mbar_wait(&k_full[sk], (g / NK) & 1);
-        tc_fence_after();
-        const uint32_t sK = smem_u32(smem + L::OFF_K + sk * L::Q_BYTES);
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk) {
-            const uint64_t ad = umma_desc_sw128(sQ + kk * 32, 16, 1024);
-            const uint64_t bd = umma_desc_sw128(sK + kk * 32, 16, 1024);
-            mma_bf16_ss(tmem + x * BN, ad, bd, IDESC_S, kk > 0);
-          }
-          mma_commit(&s_full[x]);
-          mma_commit(&k_empty[sk]);
-          if (j == it.qb) mma_commit(q_empty);
-        }
-        __syncwarp();
-        if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_n, pend_c);
-        pend_g = g;
-        pend_j = j;
-        pend_n = n;
-        pend_c = x ? cnt1++ : cnt0++;
-      }
-    }
-    if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_n, pend_c);
-  } else if (warp >= 3) {
-    // ---------------- softmax: group x = (warp - 3) / 4 (warps 3-6, 7-10), thread = query row;
-    // the TMEM lane quadrant of a warp is warp % 4, so each group covers the four quadrants ----
-    const int x = (warp - 3) >> 2;
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    float* st = reinterpret_cast<float*>(smem + L::OFF_ST);  // [item parity][m, l, owed][BM]
-    const float sl2 = p.scale * LOG2E;
-    int cx = 0;                 // this group's blocks so far (s_full / p_full / pv_done phases)
-    int cy = 0;                 // the other group's blocks so far (group A: pv_done of B)
-    int n = 0;                  // items so far
-    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
-      if (w >= n_items) continue;
-      const Item it = item_of(w, nqb, BH, p.H);
-      float m = -INFINITY, l = 0.f, alpha_pend = 1.f;
-      bool first = true;
-      for (int j = x; j <= it.qb; j += 2, ++cx) {
-        const bool diag = j == it.qb;
-        mbar_wait(&s_full[x], cx & 1);
-        const uint32_t sb = lane_base + x * BN, pdst = lane_base + TM_P + x * 64;
-        if (!first) {
-          // the group's previous PV has read P_x and finished O_x: P_x may be rewritten, and O_x
-          // pays the factor it owes from the last max move
-          mbar_wait(&pv_done[x], (cx - 1) & 1);
-          tc_fence_after();
-          if (__any_sync(0xffffffffu, alpha_pend != 1.f)) {
-            scale_o(lane_base + TM_O + x * HD, alpha_pend);
-            alpha_pend = 1.f;
-          }
-        } else {
-          // the group's first block of the item: P_x was last read by the group's final PV of the
-          // previous item; its running max exists only after a max pass
-          if (cx > 0) mbar_wait(&pv_done[x], (cx - 1) & 1);
-          tc_fence_after();
-          float mraw = -INFINITY;
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(sb + 32 * c, v);
-            tmem_ld_wait_dep(v);
-            if (diag) mask_chunk(v, 32 * c, r);
-            mraw = fmaxf(mraw, chunk_max(v));
-          }
-          m = mraw * sl2;
-        }
-        float bmax, sum;
-#pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
-          bmax = -INFINITY;
-          sum = exp_store_row128(sb, pdst, r, diag, sl2, m, bmax);
-          if (first || pass == 1) break;
-          const float mx = bmax * sl2;
-          const bool extreme = mx > m + EXTREME_LOG2;  // P could overflow: redo with the new max
-          if (!__any_sync(0xffffffffu, extreme)) break;
-          const float a = extreme ? ex2(m - mx) : 1.f;
-          if (extreme) {
-            m = mx;
-            l *= a;
-          }
-          tmem_st_wait();
-          scale_o(lane_base + TM_O + x * HD, a);  // O_x's previous PVs are done (waited above)
-        }
-        l += sum;
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[x]);
-        // lazy rescaling (the max moves only by > 2^8); O_x owes the factor until its next PV
-        if (!first) {
-          const float mx = bmax * sl2;
-          if (mx > m + RESCALE_LOG2) {
-            const float a = ex2(m - mx);
-            m = mx;
-            l *= a;
-            alpha_pend = a;
-          }
-        }
-        first = false;
-      }
-      const int nb_b = (it.qb + 1) / 2;  // group B's blocks in this item
-      float* sx = st + (n & 1) * 3 * BM;
-      if (x == 1) {
-        // hand the partial state (max, sum, factor O_B still owes) to group A
-        mbar_wait(st_free, (n & 1) ^ 1);
-        sx[r] = m;
-        sx[BM + r] = l;
-        sx[2 * BM + r] = alpha_pend;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(b_done);
-      } else {
-        // item epilogue: merge the two partial softmax states, O / l -> bf16, LSE
-        mbar_wait(b_done, n & 1);
-        const float mB = sx[r], lB = sx[BM + r], aB = sx[2 * BM + r];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(st_free);
-        mbar_wait(&pv_done[0], (cx - 1) & 1);  // group A's last PV of the item
-        if (nb_b > 0) mbar_wait(&pv_done[1], (cy + nb_b - 1) & 1);
-        tc_fence_after();
-        cy += nb_b;
-        const float mm = fmaxf(m, mB);
-        const float fa = (m == -INFINITY) ? 0.f : ex2(m - mm), fb = (mB == -INFINITY) ? 0.f : ex2(mB - mm);
-        const float lt = l * fa + lB * fb;
-        const float inv = __frcp_rn(lt);
-        const float ca = alpha_pend * fa * inv, cb = aB * fb * inv;
-        const int t = it.qb * BM + r;
-        __nv_bfloat16* orow = p.out + (size_t)(it.b * p.T + t) * p.ldo + it.h * HD;
-#pragma unroll 1
-        for (int c = 0; c < HD; c += 32) {
-          uint32_t va[32], vb[32];
-          tmem_ld_32x32b_x32(lane_base + TM_O + c, va);
-          if (nb_b > 0) tmem_ld_32x32b_x32(lane_base + TM_O + HD + c, vb);
-          tmem_ld_wait_dep(va, vb);
-#pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            float o8[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              o8[e] = __uint_as_float(va[i + e]) * ca + (nb_b > 0 ? __uint_as_float(vb[i + e]) * cb : 0.f);
-            *reinterpret_cast<uint4*>(orow + c + i) = make_uint4(pack_bf16(o8[0], o8[1]), pack_bf16(o8[2], o8[3]),
-                                                                 pack_bf16(o8[4], o8[5]), pack_bf16(o8[6], o8[7]));
-          }
-        }
-        p.lse[((size_t)it.b * p.H + it.h) * p.T + t] = (mm + __log2f(lt)) * (1.f / LOG2E);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&o_free[0]);
-          mbar_arrive(&o_free[1]);
-        }
-      }
-    }
-  }
-  __syncwarp();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 512);
-}
-
-// hd=64 uses the two-warpgroup kernel unless SPX_ATTN_FWD1=1 (A/B)
-static bool fwd_g2() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SPX_ATTN_FWD1");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 template <int HD>
 int launch_fwd(const void* qkv, const FwdParams& p, long long ld_qkv, cudaStream_t s) {
   auto encode = get_tensor_map_encoder();
@@ -862,18 +501,6 @@ int launch_fwd(const void* qkv, const FwdParams& p, long long ld_qkv, cudaStream
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(SPX_ERR_CUDA, "attn_fwd_tc: tensor map encode failed");
-  const int items = (p.T / BM) * p.B * p.H;
-  const int grid = items < num_sms() ? items : num_sms();
-  if (HD == 64 && fwd_g2()) {
-    static bool set2 = false;
-    if (!set2) {
-      cudaError_t e = cudaFuncSetAttribute(attn_fwd_g2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G2Smem::BYTES);
-      if (e != cudaSuccess) return set_cuda_error(e, "attn_fwd_g2 attr");
-      set2 = true;
-    }
-    spx_launch_check(launch_k(attn_fwd_g2_kernel, dim3(grid), dim3(G2_THREADS), G2Smem::BYTES, s, map, p));
-    return check_launch("attn_fwd_g2_kernel");
-  }
   auto k = attn_fwd_tc_kernel<HD>;
   static bool set = false;
   if (!set) {
@@ -881,6 +508,8 @@ int launch_fwd(const void* qkv, const FwdParams& p, long long ld_qkv, cudaStream
     if (e != cudaSuccess) return set_cuda_error(e, "attn_fwd_tc attr");
     set = true;
   }
+  const int items = (p.T / BM) * p.B * p.H;
+  const int grid = items < num_sms() ? items : num_sms();
   spx_launch_check(launch_k(k, dim3(grid), dim3(THREADS), FwdSmem<HD>::BYTES, s, map, p));
   return check_launch("attn_fwd_tc_kernel");
 }

@@ -266,25 +266,27 @@ static int rms_rows_per_cta(long long rows) {
   return (int)(rpc < 16 ? 16 : rpc);
 }
 
-// out[c] += sum_i part[i][c], deterministic: warp w sums partials w, w+8, ... of the CTA's 32
-// columns (coalesced 128-byte rows), then the 8 warp sums are added in warp order.
+// out[c] += sum_i part[i][c], deterministic.  A CTA owns 8 columns (one 32-byte sector per
+// partial row); thread t sums the partials i = t/8, t/8 + 32, ... of column t%8 (independent
+// loads, all in flight), then the 32 per-thread sums of a column are added in fixed order.  128
+// CTAs at d = 1024 (the previous 32-column CTAs left most SMs idle and serialised the loads).
 __global__ void __launch_bounds__(256) colsum_add_kernel(const float* __restrict__ part, float* __restrict__ out,
                                                          int nsplit, int d) {
-  __shared__ float red[ROW_WARPS][33];
+  __shared__ float red[32][9];
   pdl_wait();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * 32 + lane;
+  const int cl = threadIdx.x & 7, pr = threadIdx.x >> 3;
+  const int c = blockIdx.x * 8 + cl;
   float s = 0.f;
   if (c < d) {
 #pragma unroll 8
-    for (int i = warp; i < nsplit; i += ROW_WARPS) s += part[(size_t)i * d + c];
+    for (int i = pr; i < nsplit; i += 32) s += part[(size_t)i * d + c];
   }
-  red[warp][lane] = s;
+  red[pr][cl] = s;
   __syncthreads();
-  if (warp == 0 && c < d) {
+  if (threadIdx.x < 8 && c < d) {
     float t = 0.f;
 #pragma unroll
-    for (int w = 0; w < ROW_WARPS; ++w) t += red[w][lane];
+    for (int w = 0; w < 32; ++w) t += red[w][cl];
     out[c] += t;
   }
 }
@@ -815,7 +817,7 @@ extern "C" int spx_rmsnorm_bwd(const void* x, const void* g, const float* rstd, 
              : nch <= 4 ? launch(rmsnorm_bwd_fused_kernel<4>)
                         : launch(rmsnorm_bwd_fused_kernel<8>);
     if (rc) return rc;
-    spx_launch_check(launch_k(colsum_add_kernel, dim3((unsigned)((d + 31) / 32)), dim3(256), 0, SPX_S, ws, dg, grid, (int)d));
+    spx_launch_check(launch_k(colsum_add_kernel, dim3((unsigned)((d + 7) / 8)), dim3(256), 0, SPX_S, ws, dg, grid, (int)d));
     return check_launch("colsum_add_kernel");
   }
   spx_launch_check(launch_k(rmsnorm_bwd_dx_kernel, dim3((unsigned)((rows + ROW_WARPS - 1) / ROW_WARPS)), dim3(ROW_WARPS * 32), 0, SPX_S, 
@@ -827,7 +829,7 @@ extern "C" int spx_rmsnorm_bwd(const void* x, const void* g, const float* rstd, 
       CBF(x), rstd, CBF(dy), ws, (int)rows, (int)d));
   rc = check_launch("rmsnorm_dg_partial_kernel");
   if (rc) return rc;
-  spx_launch_check(launch_k(colsum_add_kernel, dim3((unsigned)((d + 31) / 32)), dim3(256), 0, SPX_S, ws, dg, chunks, (int)d));
+  spx_launch_check(launch_k(colsum_add_kernel, dim3((unsigned)((d + 7) / 8)), dim3(256), 0, SPX_S, ws, dg, chunks, (int)d));
   return check_launch("colsum_add_kernel");
 }
 
