@@ -174,3 +174,19 @@ def test_gemm_f32_group(beta):
                 epilogue=native.EPI_F32)
     torch.cuda.synchronize()
     assert torch.equal(C1, C2)
+
+
+def test_gemm_f32_group_large_m():
+    """Grouped wgrad launch with every M > 512 (ragged M and N) and a large plain GEMM == torch."""
+    g = torch.Generator().manual_seed(5)
+    shapes = [(1280, 256, 512), (800, 512, 256), (1024, 288, 256), (1536, 96, 512)]
+    probs, refs = [], []
+    for (M, N, K) in shapes:
+        dY, X = _mk(K, M, gen=g), _mk(K, N, gen=g)
+        C = torch.randn(M, N, generator=g).cuda()
+        refs.append(C + dY.float().t() @ X.float())
+        probs.append(dict(A=dY, B=X, C=C, M=M, N=N, K=K, lda=M, ldb=N, ldc=N, beta=1.0))
+    native.gemm_f32_group(probs)
+    torch.cuda.synchronize()
+    for p, ref in zip(probs, refs):
+        assert _rel(p["C"], ref) < 5e-3
