@@ -110,6 +110,35 @@ SPX_DEVICE float chunk_max(const uint32_t (&v)[32]) {
 
 // P = 2^(s * sl2 - m) for 32 scores -> 16 bf16 pairs; adds to sum and tracks the raw maximum.
 // Scale-and-shift as packed FFMA2, sums as packed FADD2, maxima as 3-input FMNMX.
+#ifndef SPX_FA_POLY
+#define SPX_FA_POLY 1
+#endif
+// 2^x for two arguments on the FMA / integer pipes (FA4-style MUFU relief): x = j + f with
+// j = round(x) from the 1.5*2^23 magic add, 2^f on [-0.5, 0.5] by a cubic with p(0) = 1 (max
+// relative error 1.0e-4, below bf16's 3.9e-3 half-ulp), 2^j added to the exponent bits.  x is
+// clamped at -127, where the result is exactly 0 (masked scores).
+SPX_DEVICE void ex2_poly2(float& ya, float& yb) {
+  constexpr float C1 = 0.693282932425875f, C2 = 0.24221100073552806f, C3 = 0.05500892622514074f;
+  const float xa = fmaxf(ya, -127.f), xb = fmaxf(yb, -127.f);
+  float ta, tb, fa, fb, pa, pb;
+  asm("{\n\t.reg .b64 x, m, t, j, f;\n\t"
+      "mov.b64 x, {%6, %7};\n\tmov.b64 m, {%8, %8};\n\t"
+      "add.rn.f32x2 t, x, m;\n\tsub.rn.f32x2 j, t, m;\n\tsub.rn.f32x2 f, x, j;\n\t"
+      "mov.b64 {%0, %1}, t;\n\tmov.b64 {%2, %3}, f;\n\t}"
+      : "=f"(ta), "=f"(tb), "=f"(fa), "=f"(fb), "=f"(pa), "=f"(pb)
+      : "f"(xa), "f"(xb), "f"(12582912.f));
+  asm("{\n\t.reg .b64 f, p, c;\n\t"
+      "mov.b64 f, {%2, %3};\n\t"
+      "mov.b64 c, {%5, %5};\n\tmov.b64 p, {%4, %4};\n\tfma.rn.f32x2 p, p, f, c;\n\t"
+      "mov.b64 c, {%6, %6};\n\tfma.rn.f32x2 p, p, f, c;\n\t"
+      "mov.b64 c, {%7, %7};\n\tfma.rn.f32x2 p, p, f, c;\n\t"
+      "mov.b64 {%0, %1}, p;\n\t}"
+      : "=f"(pa), "=f"(pb)
+      : "f"(fa), "f"(fb), "f"(C3), "f"(C2), "f"(C1), "f"(1.f));
+  ya = __int_as_float(__float_as_int(pa) + (__float_as_int(ta) << 23));
+  yb = __int_as_float(__float_as_int(pb) + (__float_as_int(tb) << 23));
+}
+
 SPX_DEVICE void exp_chunk(const uint32_t (&v)[32], float sl2, float m, uint32_t* pk, float& sum, float& bmax) {
   float s2[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
   float mk[2] = {bmax, -INFINITY};
@@ -124,8 +153,12 @@ SPX_DEVICE void exp_chunk(const uint32_t (&v)[32], float sl2, float m, uint32_t*
         "fma.rn.f32x2 y, x, k, c;\n\tmov.b64 {%0, %1}, y;\n\t}"
         : "=f"(ya), "=f"(yb)
         : "f"(a), "f"(b), "f"(sl2), "f"(nm));
-    ya = ex2(ya);
-    yb = ex2(yb);
+    if (SPX_FA_POLY && ((i >> 1) & 3) == 3) {
+      ex2_poly2(ya, yb);  // a quarter of the exponentials on the FMA pipe (MUFU relief)
+    } else {
+      ya = ex2(ya);
+      yb = ex2(yb);
+    }
     float* acc = s2[(i >> 1) & 3];
     asm("{\n\t.reg .b64 x, y;\n\t"
         "mov.b64 x, {%0, %1};\n\tmov.b64 y, {%2, %3};\n\t"
