@@ -111,7 +111,7 @@ SPX_DEVICE float chunk_max(const uint32_t (&v)[32]) {
 // P = 2^(s * sl2 - m) for 32 scores -> 16 bf16 pairs; adds to sum and tracks the raw maximum.
 // Scale-and-shift as packed FFMA2, sums as packed FADD2, maxima as 3-input FMNMX.
 #ifndef SPX_FA_POLY
-#define SPX_FA_POLY 1
+#define SPX_FA_POLY 1  // quarters of the exponentials computed by ex2_poly2 (0..4)
 #endif
 // 2^x for two arguments on the FMA / integer pipes (FA4-style MUFU relief): x = j + f with
 // j = round(x) from the 1.5*2^23 magic add, 2^f on [-0.5, 0.5] by a cubic with p(0) = 1 (max
@@ -153,7 +153,7 @@ SPX_DEVICE void exp_chunk(const uint32_t (&v)[32], float sl2, float m, uint32_t*
         "fma.rn.f32x2 y, x, k, c;\n\tmov.b64 {%0, %1}, y;\n\t}"
         : "=f"(ya), "=f"(yb)
         : "f"(a), "f"(b), "f"(sl2), "f"(nm));
-    if (SPX_FA_POLY && ((i >> 1) & 3) == 3) {
+    if (((i >> 1) & 3) >= 4 - SPX_FA_POLY) {
       ex2_poly2(ya, yb);  // a quarter of the exponentials on the FMA pipe (MUFU relief)
     } else {
       ya = ex2(ya);
