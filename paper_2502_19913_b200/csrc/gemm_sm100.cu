@@ -100,12 +100,7 @@ struct ProbInfo {
   float beta;
 };
 
-// MC = 2 (CG = 2 only): a cluster of two CTA pairs stacked in M computes a 512 x BN work unit;
-// the pairs share the B tile, so each CTA loads a quarter of B (its pair-half split in two) and
-// multicasts it to its counterpart in the other pair: per-SM operand traffic from L2 drops from
-// 32 KB to 24 KB per k-block (the pair kernel runs at the L2->SM feed limit on long-K GEMMs).  A
-// stage is refilled only when both pairs' MMAs have consumed it (empty barriers count 2).
-template <int BN, bool A_MN, bool B_MN, int EPI, int CG, int MC>
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
@@ -113,9 +108,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   constexpr int NBOX = EPI == EPI_SWIGLU ? 2 : 1;
   using Cfg = GemmCfg<BN, CG, NBOX>;
   constexpr int STAGES = Cfg::STAGES;
-  static_assert(MC == 1 || CG == 2, "multicast clusters are made of CTA pairs");
-  constexpr int PAIR_M = GEMM_BM * CG;  // rows per CTA pair
-  constexpr int UNIT_M = PAIR_M * MC;   // rows per work unit
+  constexpr int PAIR_M = GEMM_BM * CG;  // rows per work unit
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::STAGING_BYTES);
@@ -127,20 +120,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;  // CTA within the cluster
-  const uint32_t rank = crank & 1;                           // CTA within the pair; rank 0 issues the MMAs
-  const uint32_t pidx = crank >> 1;                          // pair within the cluster (MC = 2)
-  const uint32_t lead = crank & ~1u;                         // cluster rank of this pair's leader
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // CTA within the pair; rank 0 issues the MMAs
   const int unit0 = CG == 2 ? (int)cluster_id_x() : (int)blockIdx.x;
   const int ustep = CG == 2 ? (int)nclusters_x() : (int)gridDim.x;
-  const int num_m = (args.M + UNIT_M - 1) / UNIT_M;
+  const int num_m = (args.M + PAIR_M - 1) / PAIR_M;
   const int num_n = (args.N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
   const int num_kb = (args.K + GEMM_BK - 1) / GEMM_BK;
   // work unit u = split * num_tiles + tile (problem 0), then the grouped problems' tiles
   int num_units = num_tiles * args.splits;
   for (int q = 0; q < grp.count; ++q)
-    num_units += ((grp.prob[q].M + UNIT_M - 1) / UNIT_M) * ((grp.prob[q].N + BN - 1) / BN);
+    num_units += ((grp.prob[q].M + PAIR_M - 1) / PAIR_M) * ((grp.prob[q].N + BN - 1) / BN);
   const int kbs = (num_kb + args.splits - 1) / args.splits;
   // unit -> problem index (0 unless grouped); problem geometry from the shared table
   auto prob_of = [&](int u) {
@@ -159,12 +149,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (EPI == EPI_SWIGLU || EPI == EPI_SWIGLU_BWD) tma_prefetch_desc(&tmC2);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], MC);  // MC = 2: both pairs' MMAs release a stage
+      mbar_init(&empty_bar[s], 1);
     }
     probs[0] = ProbInfo{args.M, args.N, num_m, num_kb, num_tiles * args.splits, args.beta};
     for (int q = 0; q < grp.count; ++q) {
       const GemmProb& g = grp.prob[q];
-      const int nm = (g.M + UNIT_M - 1) / UNIT_M;
+      const int nm = (g.M + PAIR_M - 1) / PAIR_M;
       probs[q + 1] = ProbInfo{g.M, g.N, nm, (g.K + GEMM_BK - 1) / GEMM_BK,
                               probs[q].unit_end + nm * ((g.N + BN - 1) / BN), g.beta};
       tma_prefetch_desc(&grp.ta[q]);
@@ -194,7 +184,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     // both CTAs of a pair count their bytes on the leader's full barrier
-    const uint32_t full0 = CG == 2 ? mapa_shared(smem_u32(&full_bar[0]), lead) : smem_u32(&full_bar[0]);
+    const uint32_t full0 = CG == 2 ? mapa_shared(smem_u32(&full_bar[0]), 0) : smem_u32(&full_bar[0]);
     auto load = [&](void* dst, const CUtensorMap* m, int st, int c0, int c1) {
       if constexpr (CG == 2) tma_load_2d_pair(dst, m, full0 + 8 * st, c0, c1);
       else tma_load_2d(dst, m, &full_bar[st], c0, c1);
@@ -209,7 +199,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int kb0 = q == 0 ? (u / num_tiles) * kbs : 0;
       const int kb1 = q == 0 ? min(num_kb, kb0 + kbs) : pi.num_kb;
       const bool nmaj = q == 0 && args.n_major;
-      const int m0 = (nmaj ? tile / num_n : tile % pi.num_m) * UNIT_M + (int)pidx * PAIR_M + (int)rank * GEMM_BM;
+      const int m0 = (nmaj ? tile / num_n : tile % pi.num_m) * PAIR_M + (int)rank * GEMM_BM;
       const int nb = (nmaj ? tile % num_n : tile / pi.num_m) * BN + (int)rank * (BN / CG);  // this CTA's B rows
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -230,14 +220,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           } else {
             load(sa, mA, stage, k0, m0);
           }
-          if constexpr (MC == 2) {
-            // this CTA's quarter of B (its pair-half, split between the two pairs), multicast to the
-            // same-rank CTA of both pairs; a quarter is one 64-column MN atom or 64 K-major rows
-            const uint16_t mask = (uint16_t)((1u << rank) | (1u << (2 + rank)));
-            constexpr int QB = BN / CG / 2;
-            if (B_MN) tma_load_2d_pair_mc(sb + pidx * (GEMM_BK * 128), mB, &full_bar[stage], mask, nb + QB * pidx, k0);
-            else tma_load_2d_pair_mc(sb + pidx * (QB * 128), mB, &full_bar[stage], mask, k0, nb + QB * pidx);
-          } else if (B_MN) {
+          if (B_MN) {
 #pragma unroll
             for (int a = 0; a < BN / CG / 64; ++a) load(sb + a * (GEMM_BK * 128), mB, stage, nb + 64 * a, k0);
           } else {
@@ -283,15 +266,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if constexpr (CG == 2) mma_bf16_ss_pair(d_tmem, ad, bd, IDESC, (kb != kb0) || (kk != 0));
             else mma_bf16_ss(d_tmem, ad, bd, IDESC, (kb != kb0) || (kk != 0));
           }
-          if constexpr (MC == 2) mma_commit_pair_mask(&empty_bar[stage], (uint16_t)0xF);
-          else if constexpr (CG == 2) mma_commit_pair(&empty_bar[stage]);
+          if constexpr (CG == 2) mma_commit_pair(&empty_bar[stage]);
           else mma_commit(&empty_bar[stage]);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
       if (elect_one()) {
-        if constexpr (CG == 2) mma_commit_pair_mask(&tfull_bar[acc], (uint16_t)(3u << lead));
+        if constexpr (CG == 2) mma_commit_pair(&tfull_bar[acc]);
         else mma_commit(&tfull_bar[acc]);
       }
       __syncwarp();
@@ -363,7 +345,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
     };
     int it = 0;
-    const uint32_t tempty0 = CG == 2 ? mapa_shared(smem_u32(&tempty_bar[0]), lead) : 0;
+    const uint32_t tempty0 = CG == 2 ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : 0;
     for (int u = unit0; u < num_units; u += ustep, ++it) {
       const int q = prob_of(u);
       const ProbInfo pi = probs[q];
@@ -372,7 +354,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const bool nmaj = q == 0 && args.n_major;
-      const int m0 = (nmaj ? tile / num_n : tile % pi.num_m) * UNIT_M + (int)pidx * PAIR_M + (int)rank * GEMM_BM;
+      const int m0 = (nmaj ? tile / num_n : tile % pi.num_m) * PAIR_M + (int)rank * GEMM_BM;
       const int n0 = (nmaj ? tile % num_n : tile / pi.num_m) * BN;
       const int rbase = m0 + wq * 32;
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -689,7 +671,7 @@ static int make_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint6
 
 static const GemmGroup kNoGroup{};
 
-template <int BN, bool A_MN, bool B_MN, int EPI, int CG = 1, int MC = 1>
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG = 1>
 static int launch_gemm(const void* A, const void* B, long long lda, long long ldb, const GemmArgs& args,
                        cudaStream_t stream, const GemmGroup& grp = kNoGroup) {
   using Cfg = GemmCfg<BN, CG, EPI == EPI_SWIGLU ? 2 : 1>;
@@ -700,7 +682,7 @@ static int launch_gemm(const void* A, const void* B, long long lda, long long ld
   else rc = make_tmap_2d(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
   if (rc) return rc;
   if (B_MN) rc = make_tmap_2d(&tb, B, args.N, args.K, ldb, 64, GEMM_BK);
-  else rc = make_tmap_2d(&tb, B, args.K, args.N, ldb, GEMM_BK, BN / CG / MC);
+  else rc = make_tmap_2d(&tb, B, args.K, args.N, ldb, GEMM_BK, BN / CG);
   if (rc) return rc;
 
   // output boxes: 32 rows x 128 bytes (64 bf16 or 32 fp32 columns), SWIZZLE_128B
@@ -720,21 +702,20 @@ static int launch_gemm(const void* A, const void* B, long long lda, long long ld
     rc = make_tmap_2d(&tc2, args.ws, args.N, (uint64_t)args.splits * args.ws_rows, args.N, 32, 32, true);
     if (rc) return rc;
   }
-  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, EPI, CG, MC>;
-  constexpr int CL = CG * MC;  // CTAs per cluster
-  static int max_units = 0;  // co-resident CTAs (CG = 1) or clusters (CG = 2); one per template instantiation
+  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, EPI, CG>;
+  static int max_units = 0;  // co-resident CTAs (CG = 1) or CTA pairs (CG = 2); one per template instantiation
   if (!max_units) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm)");
     int n = num_sms();
     if (CG == 2) {
       cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(CL * (num_sms() / CL));
+      cfg.gridDim = dim3(2 * (num_sms() / 2));
       cfg.blockDim = dim3(GEMM_THREADS);
       cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = CL;
+      at[0].val.clusterDim.x = 2;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
@@ -745,12 +726,12 @@ static int launch_gemm(const void* A, const void* B, long long lda, long long ld
     }
     max_units = n;
   }
-  constexpr int UM = GEMM_BM * CG * MC;  // rows per work unit
-  int units = ((args.M + UM - 1) / UM) * ((args.N + BN - 1) / BN) * args.splits;
-  for (int q = 0; q < grp.count; ++q) units += ((grp.prob[q].M + UM - 1) / UM) * ((grp.prob[q].N + BN - 1) / BN);
+  int units = ((args.M + GEMM_BM * CG - 1) / (GEMM_BM * CG)) * ((args.N + BN - 1) / BN) * args.splits;
+  for (int q = 0; q < grp.count; ++q)
+    units += ((grp.prob[q].M + GEMM_BM * CG - 1) / (GEMM_BM * CG)) * ((grp.prob[q].N + BN - 1) / BN);
   const int g = units < max_units ? units : max_units;
   if (CG == 2)
-    spx_launch_check(launch_k_cluster(kern, CL, dim3(CL * g), dim3(GEMM_THREADS), Cfg::SMEM_BYTES, stream, ta, tb, tc, tc2, args, grp));
+    spx_launch_check(launch_k_cluster(kern, 2, dim3(2 * g), dim3(GEMM_THREADS), Cfg::SMEM_BYTES, stream, ta, tb, tc, tc2, args, grp));
   else
     spx_launch_check(launch_k(kern, dim3(g), dim3(GEMM_THREADS), Cfg::SMEM_BYTES, stream, ta, tb, tc, tc2, args, grp));
   rc = check_launch("gemm_bf16_kernel");
@@ -763,32 +744,9 @@ static int launch_gemm(const void* A, const void* B, long long lda, long long ld
   return check_launch("splitk_reduce_kernel");
 }
 
-// Multicast clusters of two CTA pairs (MC = 2) for the long-K GEMMs whose pair kernel runs at the
-// L2->SM feed limit: plain bf16 outputs (dgrads, the head) and fp32 weight gradients.
-// SPX_GEMM_MC=0 disables them.
-static bool mc_enabled() {
-  static const int v = [] {
-    const char* e = getenv("SPX_GEMM_MC");
-    return e ? atoi(e) : 1;
-  }();
-  return v != 0;
-}
-template <int EPI>
-constexpr bool mc_epilogue() {
-  return EPI == EPI_BF16 || EPI == EPI_F32;
-}
-
 template <int BN, int EPI, int CG = 1>
 static int dispatch_major(const void* A, const void* B, long long lda, long long ldb, int a_mn, int b_mn,
                           const GemmArgs& args, cudaStream_t s) {
-  if constexpr (CG == 2 && mc_epilogue<EPI>()) {
-    if (mc_enabled() && args.splits == 1 && args.M > 2 * GEMM_BM * CG) {
-      if (!a_mn && !b_mn) return launch_gemm<BN, false, false, EPI, CG, 2>(A, B, lda, ldb, args, s);
-      if (!a_mn && b_mn) return launch_gemm<BN, false, true, EPI, CG, 2>(A, B, lda, ldb, args, s);
-      if (a_mn && b_mn) return launch_gemm<BN, true, true, EPI, CG, 2>(A, B, lda, ldb, args, s);
-      return launch_gemm<BN, true, false, EPI, CG, 2>(A, B, lda, ldb, args, s);
-    }
-  }
   if (!a_mn && !b_mn) return launch_gemm<BN, false, false, EPI, CG>(A, B, lda, ldb, args, s);
   if (!a_mn && b_mn) return launch_gemm<BN, false, true, EPI, CG>(A, B, lda, ldb, args, s);
   if (a_mn && b_mn) return launch_gemm<BN, true, true, EPI, CG>(A, B, lda, ldb, args, s);
@@ -932,8 +890,7 @@ extern "C" int spx_gemm_f32_group(int32_t count, const void* const* A, const voi
     if (a_mn_major) rc = make_tmap_2d(&grp.ta[i - 1], A[i], M[i], K[i], lda[i], 64, GEMM_BK);
     else rc = make_tmap_2d(&grp.ta[i - 1], A[i], K[i], M[i], lda[i], GEMM_BK, GEMM_BM);
     if (rc) return rc;
-    const bool mcq = pair && mc_enabled() && min_m > 4 * GEMM_BM;
-    const uint32_t bbox = pair ? (mcq ? 64 : 128) : 256;
+    const uint32_t bbox = pair ? 128 : 256;
     if (b_mn_major) rc = make_tmap_2d(&grp.tb[i - 1], B[i], N[i], K[i], ldb[i], 64, GEMM_BK);
     else rc = make_tmap_2d(&grp.tb[i - 1], B[i], K[i], N[i], ldb[i], GEMM_BK, bbox);
     if (rc) return rc;
@@ -941,12 +898,10 @@ extern "C" int spx_gemm_f32_group(int32_t count, const void* const* A, const voi
     if (rc) return rc;
   }
   const int am = a_mn_major ? 1 : 0, bm = b_mn_major ? 1 : 0;
-  const bool mc = pair && mc_enabled() && min_m > 4 * GEMM_BM;
 #define SPX_GRP(AM, BM)                                                                                     \
   if (am == AM && bm == BM)                                                                                 \
-    return mc ? launch_gemm<256, AM, BM, EPI_F32, 2, 2>(A[0], B[0], lda[0], ldb[0], args, s, grp)            \
-              : pair ? launch_gemm<256, AM, BM, EPI_F32, 2>(A[0], B[0], lda[0], ldb[0], args, s, grp)        \
-                     : launch_gemm<256, AM, BM, EPI_F32, 1>(A[0], B[0], lda[0], ldb[0], args, s, grp);
+    return pair ? launch_gemm<256, AM, BM, EPI_F32, 2>(A[0], B[0], lda[0], ldb[0], args, s, grp)            \
+                : launch_gemm<256, AM, BM, EPI_F32, 1>(A[0], B[0], lda[0], ldb[0], args, s, grp);
   SPX_GRP(true, true)
   SPX_GRP(false, false)
   SPX_GRP(false, true)

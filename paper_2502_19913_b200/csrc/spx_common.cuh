@@ -293,25 +293,6 @@ SPX_DEVICE void mma_bf16_ss_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// arrive on the mbarrier at this smem offset in every CTA of `mask` (cluster ranks) once the pair's
-// MMAs complete
-SPX_DEVICE void mma_commit_pair_mask(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-// TMA load multicast to the CTAs of `mask` (same smem offset in each); the transaction bytes are
-// counted on the mbarrier at `bar`'s offset in the pair leader of each destination CTA
-SPX_DEVICE void tma_load_2d_pair_mc(void* dst, const CUtensorMap* m, uint64_t* bar, uint16_t mask, int32_t c0,
-                                    int32_t c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-      "[%0], [%1, {%4, %5}], [%2], %3;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "h"(mask), "r"(c0), "r"(c1)
-      : "memory");
-}
 // arrive on the mbarrier at this smem offset in both CTAs of the pair once the pair MMAs complete
 SPX_DEVICE void mma_commit_pair(uint64_t* bar) {
   asm volatile(
