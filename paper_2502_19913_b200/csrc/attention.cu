@@ -285,41 +285,54 @@ __global__ void attn_bwd_delta_kernel(const Params p) {
   pdl_wait();
   // 8 lanes per (row, head); lane j sums the 16-byte vectors j, j+8, ... of that head's row.
   // Groups are numbered in the [B, H, T] order of the outputs (position fastest), so the D and
-  // lse*log2e stores of a warp's four groups are contiguous
-  const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
-  const int j = threadIdx.x & 7;
+  // lse*log2e stores of a warp's four groups are contiguous; each thread takes DG groups a grid
+  // apart with all their loads in flight (the kernel is load-latency bound at one group each).
+  constexpr int DG = 4;
   const long long rows = (long long)p.B * p.T;
-  const bool live = g < rows * p.H;
-  const long long gg = live ? g : 0;
-  const int t_ = (int)(gg % p.T);
-  const long long bh = gg / p.T;
-  const int h = (int)(bh % p.H);
-  const long long r = (bh / p.H) * p.T + t_;
-  const __nv_bfloat16* o = p.o + r * p.ldo + h * HD;
-  const __nv_bfloat16* d = p.dout + r * p.ldo + h * HD;
-  float s = 0.f;
-  if (live) {
+  const long long total = rows * p.H;
+  const long long stride = ((long long)gridDim.x * blockDim.x) >> 3;
+  const long long g0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const int j = threadIdx.x & 7;
+  constexpr int NV = (HD / 8 + 7) / 8;  // 16-byte vectors per lane (hd 48: lanes 6, 7 idle)
+  uint4 a[DG][NV], c[DG][NV];
 #pragma unroll
-    for (int v = j; v < HD / 8; v += 8) {
-      const uint4 a = *reinterpret_cast<const uint4*>(o + v * 8);
-      const uint4 c = *reinterpret_cast<const uint4*>(d + v * 8);
-      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
-      const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c);
+  for (int k = 0; k < DG; ++k) {
+    const long long gg = g0 + k * stride < total ? g0 + k * stride : 0;
+    const int t_ = (int)(gg % p.T);
+    const long long bh = gg / p.T;
+    const int h = (int)(bh % p.H);
+    const long long r = (bh / p.H) * p.T + t_;
+    const __nv_bfloat16* o = p.o + r * p.ldo + h * HD;
+    const __nv_bfloat16* d = p.dout + r * p.ldo + h * HD;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const bool in = j + 8 * v < HD / 8;
+      a[k][v] = in ? *reinterpret_cast<const uint4*>(o + (j + 8 * v) * 8) : make_uint4(0, 0, 0, 0);
+      c[k][v] = in ? *reinterpret_cast<const uint4*>(d + (j + 8 * v) * 8) : make_uint4(0, 0, 0, 0);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < DG; ++k) {
+    float s = 0.f;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a[k][v]);
+      const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c[k][v]);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float2 fa = __bfloat1622float2(a2[i]), fc = __bfloat1622float2(c2[i]);
         s += fa.x * fc.x + fa.y * fc.y;
       }
     }
-  }
-  s += __shfl_xor_sync(0xffffffffu, s, 4);
-  s += __shfl_xor_sync(0xffffffffu, s, 2);
-  s += __shfl_xor_sync(0xffffffffu, s, 1);
-  if (live && j == 0) {
-    const long long idx = gg;  // ((b * H + h) * T + t)
-    p.delta[idx] = s;
-    // second half of the workspace: lse in the exp2 domain for the tcgen05 dK/dV kernel
-    p.delta[(long long)p.B * p.H * p.T + idx] = p.lse[idx] * 1.4426950408889634f;
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    const long long idx = g0 + k * stride;  // ((b * H + h) * T + t)
+    if (j == 0 && idx < total) {
+      p.delta[idx] = s;
+      // second half of the workspace: lse in the exp2 domain for the tcgen05 dK/dV kernel
+      p.delta[total + idx] = p.lse[idx] * 1.4426950408889634f;
+    }
   }
 }
 
@@ -577,9 +590,10 @@ static int run_bwd(const Params& p, cudaStream_t s) {
   constexpr int LD = Tile<HD>::LD;
   constexpr int BQI = (HD > 64) ? 32 : 64;
   {
-    const long long groups = (long long)p.B * p.T * p.H;  // 8 threads each
+    const long long groups = (long long)p.B * p.T * p.H;  // 8 threads each, 4 groups per thread
     const int threads = 256;
-    spx_launch_check(launch_k(attn_bwd_delta_kernel<HD>, dim3((unsigned)((groups * 8 + threads - 1) / threads)), dim3(threads), 0, s, p));
+    const long long per_block = threads / 8 * 4;
+    spx_launch_check(launch_k(attn_bwd_delta_kernel<HD>, dim3((unsigned)((groups + per_block - 1) / per_block)), dim3(threads), 0, s, p));
     int rc = check_launch("attn_bwd_delta_kernel");
     if (rc) return rc;
   }
