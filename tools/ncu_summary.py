@@ -1,5 +1,5 @@
 """Summarise an ncu --set full report (per kernel launch): duration, tensor-pipe and XU activity,
-issue activity, shared-pipe activity, DRAM bytes.  Reads `ncu -i <rep> --page raw --csv` output.
+issue activity, DRAM bytes.  Reads `ncu -i <rep> --page raw --csv` output.
 
     ncu -i rep.ncu-rep --page raw --csv > raw.csv; python tools/ncu_summary.py raw.csv [--md out.md]
 """
@@ -10,7 +10,6 @@ COLS = [("gpu__time_duration.sum", "us", 1e-3),
         ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor %", 1),
         ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU %", 1),
         ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue %", 1),
-        ("sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active", "shared pipe %", 1),
         ("dram__bytes_read.sum", "DRAM rd MB", 1e-6),
         ("dram__bytes_write.sum", "DRAM wr MB", 1e-6),
         ("gpc__cycles_elapsed.avg.per_second", "GHz", 1e-9)]
