@@ -175,7 +175,7 @@ def gemm_roofline(tr, peak_tflops: float, reps: int = 10) -> dict:
     counts = tr.gemm_counts_per_step()
     # DRAM bytes per launch of each shape from the committed ncu capture (profiles/), if present
     traffic_by_shape = {}
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_gemm_traffic.json")
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_gemm_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic_by_shape = {k: v["dram_bytes_per_launch"] for k, v in json.load(f)["per_shape"].items()}
@@ -218,7 +218,7 @@ def gemm_roofline(tr, peak_tflops: float, reps: int = 10) -> dict:
             "frac": round(ach / peak_tflops, 4),
             "traffic": round(t_bytes / t_count) if t_count else None,
             "traffic_note": "dram read+write bytes per GEMM launch, launch-weighted over the iteration's shapes "
-                            "(ncu capture profiles/r01_gemm_traffic.json; per shape in per_shape)",
+                            "(ncu capture profiles/r02_gemm_traffic.json; per shape in per_shape)",
             "kernel": "spx gemm_bf16_kernel (tcgen05, all shapes)",
             "gemm_ms_per_step": round(total_ms, 3), "per_shape": per}
 
