@@ -145,13 +145,13 @@ REBALANCED = {24: {4: [3, 7, 7, 7]}}
 
 
 def get_config(name: str, **over) -> RunConfig:
-    """C1..C5, plus suffixes (combinable, e.g. "C2-rb-full"): "-rb" rebalanced layer split
-    (S0 lighter; REBALANCED), "-full" (DT-FM, k=0 disjoint sequential pipelines), "-dtfmskip"
+    """C1..C5, plus suffixes (combinable, e.g. "C2-rb-full"): "-m4" memory capacity m = 4
+    (8 agents at C2), "-rb" rebalanced layer split (S0 lighter; REBALANCED), "-full" (DT-FM, k=0 disjoint sequential pipelines), "-dtfmskip"
     (DT-FM-skip: topology-blind skip paths, no TC2) and "-notc2" (SkipPipe without the throughput
     phase)."""
     base, suffixes = name, []
     while True:
-        suf = next((v for v in list(VARIANTS) + ["-rb"] if base.endswith(v)), None)
+        suf = next((v for v in list(VARIANTS) + ["-rb", "-m4"] if base.endswith(v)), None)
         if suf is None:
             break
         suffixes.insert(0, suf)
@@ -177,7 +177,11 @@ def get_config(name: str, **over) -> RunConfig:
     else:
         raise KeyError(name)
     for suf in suffixes:
-        if suf == "-rb":
+        if suf == "-m4":
+            # memory capacity m = 4 microbatches per node (TC1): twice the agents in
+            # flight -- B200's 180 GB hold them easily -- so fewer pipeline bubbles per wave
+            rc.m, rc.name = 4, rc.name + suf
+        elif suf == "-rb":
             split = REBALANCED.get(rc.model.n_layers, {}).get(rc.s)
             if split is None:
                 raise KeyError(f"{name}: no rebalanced split for {rc.model.n_layers} layers x {rc.s} stages")

@@ -57,7 +57,8 @@ def _worker(rank, world, port, cfg_name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,cfg", [(2, "C2"), (4, "C2"), (8, "C2"), (2, "C1"), (8, "C2-rb"), (4, "C2-rb")])
+@pytest.mark.parametrize("world,cfg", [(2, "C2"), (4, "C2"), (8, "C2"), (2, "C1"), (8, "C2-rb"), (4, "C2-rb"),
+                                       (4, "C2-m4"), (8, "C2-m4")])
 def test_cross_rank_hops_match(world, cfg):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -97,3 +98,17 @@ def test_rebalanced_split_config():
     assert max(busy_rb) < max(busy_eq)
     placement = balanced_placement(simulate(rb.schedule(), rb.topology(), rb.sim_config()), rb.topology().n, 8)
     assert sorted(placement) == list(range(8))
+
+
+def test_memory_capacity_variant():
+    """C2-m4: m = 4 microbatches per node (TC1) -> 8 agents; paths still satisfy TC1 (<= 4 per
+    node) and the plan's makespan drops against m = 2 (fewer bubbles per wave)."""
+    from paper_2502_19913_b200.scheduler import node_path_counts
+
+    m2, m4 = get_config("C2"), get_config("C2-m4")
+    assert m4.m == 4 and len(m4.schedule().agents) == 8 and m4.layers == m2.layers
+    assert max(node_path_counts(m4.schedule().paths, m4.topology().n)) <= 4
+    ms2 = simulate(m2.schedule(), m2.topology(), m2.sim_config()).iteration_makespan
+    ms4 = simulate(m4.schedule(), m4.topology(), m4.sim_config()).iteration_makespan
+    assert ms4 < ms2
+    assert get_config("C2-rb-m4").layers == [3, 7, 7, 7] and get_config("C2-rb-m4-full").kind == "full"

@@ -101,6 +101,14 @@ def test_c2_rebalanced_split_matches_oracle():
     check_parity(rc)
 
 
+def test_c2_m4_matches_oracle():
+    """C2-m4: memory capacity 4 -- 8 agents in flight, up to 4 activation slots per node; M = 16
+    is two waves."""
+    rc = get_config("C2-m4", M=16)
+    assert len(rc.schedule().agents) == 8
+    check_parity(rc)
+
+
 def test_c3_shape_with_swap_matches_oracle():
     cfg = model_config("llama-1.5b", n_layers=8)
     rc = RunConfig("C3-shape", cfg, [1] * 8, 25, 2, 1, 4096, 4, swap_every=2)
