@@ -360,6 +360,18 @@ def balanced_placement(report: SimReport, n_nodes: int, n_ranks: int) -> list[in
     return out
 
 
+def allreduce_points(ops, node_stage: list[int], stages) -> dict:
+    """Global op index -> replicated stages whose all-reduce is issued right after that op: the
+    stage's last op in the global order.  A function of the op list only, so every rank issues
+    its replica all-reduces (and, interleaved, its NCCL hops) in one consistent order -- NCCL
+    kernels of different communicators enqueued in different orders on two ranks can deadlock."""
+    out: dict = {}
+    for st in sorted(stages):
+        last = max(i for i, op in enumerate(ops) if node_stage[op.node] == st)
+        out.setdefault(last, []).append(st)
+    return out
+
+
 def static_slots(schedule: Schedule, n_nodes: int) -> tuple[dict, list[int]]:
     """Activation slot of every (agent, node): the agent's rank among the agents whose path visits
     the node.  A slot is then only ever reused by the *same* agent's next wave, which launches
@@ -581,13 +593,13 @@ class Trainer:
             ranks = self.stage_ranks[st]
             if len(ranks) > 1 and self.rank in ranks:
                 self._groups[st] = native.comm_init(alluid[ranks[0]][st], len(ranks), ranks.index(self.rank))
-        # the replica all-reduce of a stage is issued as soon as this rank's last op of that stage
-        # is enqueued, on its own stream, so it overlaps the rank's remaining ops
-        self._ar_after = {}
-        for st in self._groups:
-            last = max(i for i, op in enumerate(self.ops)
-                       if self.placement[op.node] == self.rank and self.node_stage[op.node] == st)
-            self._ar_after.setdefault(last, []).append(st)
+        # the replica all-reduce of a stage is issued, on its own stream, at the stage's last op in
+        # the global op order -- the same walk position on every rank, so all NCCL work (these
+        # all-reduces and NCCL hops) is enqueued in one consistent order across ranks (NCCL
+        # kernels of different communicators issued in different orders can deadlock each
+        # other); this rank's ops of the stage are all enqueued by then, and the all-reduce
+        # overlaps the remaining ops
+        self._ar_after = allreduce_points(self.ops, self.node_stage, self._groups)
         self._ar_stream = {st: torch.cuda.Stream(device=self.dev) for st in self._groups}
         # one process group (own NCCL communicator and stream) per rank pair for the path hops, so
         # hops between different pairs, and the replica all-reduces, never serialise behind each
@@ -849,7 +861,7 @@ class Trainer:
                 if hop is not None:
                     self._issue_hop(idx, op, hop, out, mine, pending, sends)
                 for st in self._ar_after.get(idx, ()):
-                    self._issue_allreduce(st, self.nstream[v])
+                    self._issue_allreduce(st, self.stream)
                 if mine and op.kind == L:  # the head wgrad, after the returned gradient left
                     sv = self.nstream[v]
                     lw = (LW, v, self._key(op)[2])

@@ -11,7 +11,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2502_19913_b200.configs import get_config
-from paper_2502_19913_b200.executor import balanced_placement, hop_plan, static_slots
+from paper_2502_19913_b200.executor import allreduce_points, balanced_placement, hop_plan, static_slots
 from paper_2502_19913_b200.simulator import simulate
 
 
@@ -112,3 +112,25 @@ def test_memory_capacity_variant():
     ms4 = simulate(m4.schedule(), m4.topology(), m4.sim_config()).iteration_makespan
     assert ms4 < ms2
     assert get_config("C2-rb-m4").layers == [3, 7, 7, 7] and get_config("C2-rb-m4-full").kind == "full"
+
+
+@pytest.mark.parametrize("cfg,world", [("C2", 2), ("C2-m4", 2), ("C2-m4", 4), ("C2-rb", 8)])
+def test_allreduce_order_is_global(cfg, world):
+    """Replica all-reduces are placed at each stage's last op in the global op order: the same
+    positions on every rank (independent of which stages a rank holds), every hosting rank has
+    all its ops of the stage before that point, and stages come out in one order."""
+    rc = get_config(cfg)
+    rep = simulate(rc.schedule(), rc.topology(), rc.sim_config())
+    node_stage = rc.assignment.node_stage()
+    placement = balanced_placement(rep, rc.topology().n, world)
+    cross = [st for st in range(rc.s) if len({placement[v] for v in range(rc.topology().n) if node_stage[v] == st}) > 1]
+    pts = allreduce_points(rep.ops, node_stage, cross)
+    order = [st for i in sorted(pts) for st in pts[i]]
+    assert sorted(order) == sorted(cross)
+    for r in range(world):
+        mine = [st for st in cross if any(placement[v] == r for v in range(rc.topology().n) if node_stage[v] == st)]
+        assert allreduce_points(rep.ops, node_stage, mine) == {i: [s for s in v if s in mine] for i, v in pts.items()
+                                                               if any(s in mine for s in v)}
+        for i, sts in pts.items():
+            for st in sts:
+                assert all(j <= i for j, op in enumerate(rep.ops) if node_stage[op.node] == st and placement[op.node] == r)

@@ -57,3 +57,10 @@ def test_headline_shape_multi_gpu(world):
 @pytest.mark.parametrize("world", [4, 8])
 def test_rebalanced_split_multi_gpu(world):
     _run(world, config="C2-rb", M=8, port=4)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_memory_capacity_m4_multi_gpu(world):
+    """C2-m4 spreads every stage's replicas over the ranks (four replica communicators between the
+    same two GPUs at world 2): the all-reduces must be enqueued in one global order."""
+    _run(world, config="C2-m4", M=16, port=5)
