@@ -1,3 +1,4 @@
+#include <cstdlib>
 // HBM-bound kernels of a LLaMA stage and of the optimizer step: RMSNorm fwd/bwd, RoPE,
 // SwiGLU backward, embedding gather / deterministic scatter, fused softmax cross-entropy
 // (loss + dlogits in one pass pair), deterministic sums, grad-norm clip and fused AdamW.
@@ -260,6 +261,12 @@ __global__ void __launch_bounds__(256, NCH <= 4 ? 2 : 1) rmsnorm_bwd_fused_kerne
 
 // rows per CTA of the fused RMSNorm backward: a multiple of 16 giving about two CTAs per SM
 static int rms_rows_per_cta(long long rows) {
+  static const int fixed = [] {  // SPX_RMS_RPC: rows per CTA, multiple of 8 (benchmarking)
+    const char* e = getenv("SPX_RMS_RPC");
+    const int v = e ? atoi(e) : 0;
+    return v >= 8 ? v / 8 * 8 : 0;
+  }();
+  if (fixed) return fixed;
   const long long target = 2LL * num_sms();
   long long rpc = (rows + target - 1) / target;
   rpc = ((rpc + 15) / 16) * 16;
