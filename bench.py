@@ -340,6 +340,20 @@ def time_baselines(args, rc_name, ms, tok, rank=0, world=1, local=0):
     return out
 
 
+def time_variants(args, rc, ms, tok, rank=0, world=1, local=0):
+    """Opt-in B200 settings of the headline config measured beside it, same protocol, same GPUs:
+    C2-m4 (memory capacity m = 4: 8 agents in flight).  Skipped with --no-variants
+    and for other configs."""
+    if args.no_variants or rc.name != "C2":
+        return None
+    out = {}
+    for variant, label in (("-m4", "C2-m4 (m=4)"),):
+        vms, rv = time_full_pp(args, rc.name, rank=rank, world=world, local=local, variant=variant)
+        out[rv.name] = {"what": label, "ms_per_step": round(vms, 3), "tokens_per_s": round(tok / (vms / 1e3), 1),
+                        "vs_headline": round(ms / vms, 4)}
+    return out
+
+
 def time_sweep(args, ms_c2, tok, rank=0, world=1, local=0):
     """BASELINE.json configs[4]: LLaMa-500M skip-ratio sweep 0/25/50 % against the full sequential
     pipeline, same GPUs, same protocol.  0 % is SkipPipe's scheduler with k=0 (paths may still
@@ -411,6 +425,7 @@ def run_ours(args, rc):
                 "skippipe_speedup": round(fms / ms, 4)}
     bl = time_baselines(args, rc.name, ms, tok) if args.baselines and rc.kind == "skippipe" else None
     sw = time_sweep(args, ms, tok) if args.sweep and rc.name == "C2" else None
+    var = time_variants(args, rc, ms, tok)
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
@@ -431,6 +446,7 @@ def run_ours(args, rc):
         "vs_full_pp": full,
         "baselines": bl,
         "skip_sweep": sw,
+        "variants": var,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -511,6 +527,7 @@ def run_ours_dist(args, rc):
     sw = time_sweep(args, ms, tok, rank, world, local) if args.sweep and rc.name == "C2" else None
     bl = time_baselines(args, rc.name, ms, tok, rank, world, local) if args.baselines and rc.kind == "skippipe" \
         else None
+    var = time_variants(args, rc, ms, tok, rank, world, local)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(tok / (ms / 1e3), 1), "unit": "tokens/s", "n_gpus": world,
@@ -533,6 +550,7 @@ def run_ours_dist(args, rc):
             "vs_full_pp": full,
             "baselines": bl,
             "skip_sweep": sw,
+            "variants": var,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -549,6 +567,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full-pp", action="store_true", help="skip the full sequential pipeline comparison")
+    ap.add_argument("--no-variants", action="store_true", help="skip the C2-m4 variant measured beside the headline")
     ap.add_argument("--sweep", action="store_true",
                     help="also run the C5 skip-ratio sweep (0/25/50%% vs full PP) on the same GPUs")
     ap.add_argument("--baselines", action="store_true",
