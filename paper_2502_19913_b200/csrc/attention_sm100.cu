@@ -521,6 +521,358 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
+// ------------------------------------------------------------------------------------------
+// hd = 64, T % 256 == 0: two query tiles per work item (query blocks 2i and 2i+1 of one (b, h))
+// with one softmax warpgroup each (warps 4-7 tile 0, warps 8-11 tile 1; thread = a full
+// 128-column query row, its own lagged running max, sum and O accumulator -- no exchange between
+// warps).  The groups work on different rows, so nothing is merged; each key / value block is
+// loaded once for both tiles; one group's TMEM reads, P stores and waits overlap the other's
+// exponentials.
+//   TMEM: S0 [0,128)  S1 [128,256)  O0 [256,320)  O1 [320,384)  P0 [384,448)  P1 [448,512)
+// ------------------------------------------------------------------------------------------
+struct Q2Smem {
+  static constexpr int ATOM = BM * 128;
+  static constexpr int TILE = ATOM;  // 128 x 64 bf16
+  static constexpr int NK = 3, NV = 3;
+  static constexpr int OFF_Q = 0;                       // [2]
+  static constexpr int OFF_K = OFF_Q + 2 * TILE;        // [NK]
+  static constexpr int OFF_V = OFF_K + NK * TILE;       // [NV]
+  static constexpr int OFF_BAR = OFF_V + NV * TILE;
+  static constexpr int RAW = OFF_BAR + 256;
+  static constexpr int BYTES = RAW > 116 * 1024 ? RAW : 116 * 1024;
+};
+
+// O row (64 fp32 columns in TMEM) *= a
+SPX_DEVICE void q2_scale_o(uint32_t taddr, float a) {
+#pragma unroll 1
+  for (int c = 0; c < 64; c += 32) {
+    uint32_t v[32];
+    tmem_ld_32x32b_x32(taddr + c, v);
+    tmem_ld_wait_dep(v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * a);
+    tmem_st_32x32b_x32(taddr + c, v);
+  }
+  tmem_st_wait();
+}
+
+SPX_DEVICE void q2_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+// exponentiate one 128-column row of S (4 chunks of 32, the next loading while one is processed)
+// with max m and store P (bf16 pairs) to TMEM at pdst; returns the row sum, tracks the raw max
+SPX_DEVICE float q2_exp_row(uint32_t sb, uint32_t pdst, int r, bool diag, float sl2, float m, float& bmax) {
+  uint32_t va[32], vb[32], pk[16];
+  float sum = 0.f;
+  tmem_ld_32x32b_x32(sb, va);
+  tmem_ld_wait_dep(va);
+#pragma unroll
+  for (int c = 0; c < 4; c += 2) {
+    tmem_ld_32x32b_x32(sb + 32 * (c + 1), vb);
+    if (diag) mask_chunk(va, 32 * c, r);
+    exp_chunk(va, sl2, m, pk, sum, bmax);
+    q2_st16(pdst + 16 * c, pk);
+    tmem_ld_wait_dep(vb);
+    if (c + 2 < 4) tmem_ld_32x32b_x32(sb + 32 * (c + 2), va);
+    if (diag) mask_chunk(vb, 32 * (c + 1), r);
+    exp_chunk(vb, sl2, m, pk, sum, bmax);
+    q2_st16(pdst + 16 * (c + 1), pk);
+    if (c + 2 < 4) tmem_ld_wait_dep(va);
+  }
+  return sum;
+}
+
+// work item w (heavy first): query-block pair pi = npair-1 - w / (B*H)
+SPX_DEVICE Item q2_item_of(int w, int npair, int BH, int H) {
+  Item it;
+  it.qb = npair - 1 - w / BH;  // pair index
+  const int bh = w % BH;
+  it.b = bh / H;
+  it.h = bh % H;
+  return it;
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_fwd_q2_kernel(const __grid_constant__ CUtensorMap tmQKV, const FwdParams p) {
+  using L = Q2Smem;
+  constexpr int HD = 64;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  constexpr int NK = L::NK, NV = L::NV;
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* s_full = bars + 2;   // [tile]
+  uint64_t* p_full = bars + 4;   // [tile], 4 arrivals
+  uint64_t* pv_done = bars + 6;  // [tile]
+  uint64_t* o_free = bars + 8;   // [tile], 4 arrivals
+  uint64_t* k_full = bars + 10;            // [NK]
+  uint64_t* k_empty = bars + 10 + NK;      // [NK]
+  uint64_t* v_full = bars + 10 + 2 * NK;   // [NV]
+  uint64_t* v_empty = bars + 10 + 2 * NK + NV;  // [NV]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10 + 2 * NK + 2 * NV);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int npair = p.T / (2 * BM);
+  const int BH = p.B * p.H;
+  const int n_items = npair * BH;
+  const int group = p.H / p.Hkv;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmQKV);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_done[i], 1);
+      mbar_init(&o_free[i], 4);
+    }
+    for (int i = 0; i < NK; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < NV; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    fence_barrier_init();
+    fence_proxy_async();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  constexpr uint32_t TM_O = 256, TM_P = 384;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer: the two Q tiles, then K_j ----------------
+    int g = 0, n = 0;
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
+      if (w >= n_items) continue;
+      const Item it = q2_item_of(w, npair, BH, p.H);
+      const int row0 = it.b * p.T, kvh = it.h / group, nb = 2 * it.qb + 2;
+      mbar_wait(q_empty, (n & 1) ^ 1);
+      mbar_expect_tx(q_full, 2 * L::TILE);
+      tma_load_2d(smem + L::OFF_Q, &tmQKV, q_full, it.h * HD, row0 + 2 * it.qb * BM);
+      tma_load_2d(smem + L::OFF_Q + L::TILE, &tmQKV, q_full, it.h * HD, row0 + (2 * it.qb + 1) * BM);
+      for (int j = 0; j < nb; ++j, ++g) {
+        const int s = g % NK;
+        mbar_wait(&k_empty[s], ((g / NK) & 1) ^ 1);
+        mbar_expect_tx(&k_full[s], L::TILE);
+        tma_load_2d(smem + L::OFF_K + s * L::TILE, &tmQKV, &k_full[s], (p.H + kvh) * HD, row0 + j * BN);
+      }
+    }
+  } else if (warp == 3 && lane == 0) {
+    // ---------------- TMA producer: V_j ----------------
+    int g = 0;
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
+      if (w >= n_items) continue;
+      const Item it = q2_item_of(w, npair, BH, p.H);
+      const int row0 = it.b * p.T, kvh = it.h / group, nb = 2 * it.qb + 2;
+      for (int j = 0; j < nb; ++j, ++g) {
+        const int s = g % NV;
+        mbar_wait(&v_empty[s], ((g / NV) & 1) ^ 1);
+        mbar_expect_tx(&v_full[s], L::TILE);
+        tma_load_2d(smem + L::OFF_V + s * L::TILE, &tmQKV, &v_full[s], (p.H + p.Hkv + kvh) * HD, row0 + j * BN);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: per key block j, for each tile t: S_t(j), then PV_t(j-1) ----------------
+    constexpr uint32_t IDESC_S = umma_idesc_bf16(BM, BN, false, false);
+    constexpr uint32_t IDESC_O = umma_idesc_bf16(BM, HD, false, true);
+    int g = 0, n = 0;
+    int cs0 = 0, cs1 = 0;  // S MMAs issued per tile (p_full phases)
+    auto issue_s = [&](int t, uint32_t sK) {
+      const uint32_t sQ = smem_u32(smem + L::OFF_Q + t * L::TILE);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          mma_bf16_ss(tmem + t * BN, umma_desc_sw128(sQ + kk * 32, 16, 1024), umma_desc_sw128(sK + kk * 32, 16, 1024),
+                      IDESC_S, kk > 0);
+        mma_commit(&s_full[t]);
+      }
+      __syncwarp();
+    };
+    // PV of tile t for the block whose V sits in ring slot vs; acc = 0 for the tile's first block
+    auto issue_pv = [&](int t, int vs, bool acc) {
+      tc_fence_after();
+      const uint32_t sV = smem_u32(smem + L::OFF_V + vs * L::TILE);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk)
+          mma_bf16_ts(tmem + TM_O + t * HD, tmem + TM_P + t * 64 + kk * 8, umma_desc_sw128(sV + kk * 2048, L::ATOM, 1024),
+                      IDESC_O, acc || (kk > 0));
+        mma_commit(&pv_done[t]);
+      }
+      __syncwarp();
+    };
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
+      if (w >= n_items) continue;
+      const Item it = q2_item_of(w, npair, BH, p.H);
+      const int last0 = 2 * it.qb, nb = 2 * it.qb + 2;
+      mbar_wait(q_full, n & 1);
+      for (int j = 0; j <= nb; ++j, ++g) {
+        const int sk = g % NK;
+        const int gp = g - 1;  // global index of block j-1 (V ring slot)
+        if (j < nb) {
+          mbar_wait(&k_full[sk], (g / NK) & 1);
+          tc_fence_after();
+        }
+        const uint32_t sK = smem_u32(smem + L::OFF_K + sk * L::TILE);
+        // tile 0
+        if (j > 0 && j - 1 <= last0) {
+          mbar_wait(&p_full[0], (cs0 - 1) & 1);  // softmax of S0(j-1) done: S0 free, P0(j-1) ready
+          if (j - 1 == 0) mbar_wait(&o_free[0], (n & 1) ^ 1);
+          mbar_wait(&v_full[gp % NV], (gp / NV) & 1);
+        }
+        if (j <= last0) {
+          issue_s(0, sK);
+          ++cs0;
+        }
+        if (j > 0 && j - 1 <= last0) issue_pv(0, gp % NV, j - 1 > 0);
+        // tile 1
+        if (j > 0) {
+          mbar_wait(&p_full[1], (cs1 - 1) & 1);
+          if (j - 1 == 0) mbar_wait(&o_free[1], (n & 1) ^ 1);
+          mbar_wait(&v_full[gp % NV], (gp / NV) & 1);
+        }
+        if (j < nb) {
+          issue_s(1, sK);
+          ++cs1;
+          if (elect_one()) {
+            mma_commit(&k_empty[sk]);
+            if (j == nb - 1) mma_commit(q_empty);
+          }
+          __syncwarp();
+        }
+        if (j > 0) {
+          issue_pv(1, gp % NV, j - 1 > 0);
+          if (elect_one()) mma_commit(&v_empty[gp % NV]);
+          __syncwarp();
+        }
+      }
+      --g;  // the j = nb pass only drained the last PVs
+    }
+  } else if (warp >= 4) {
+    // ---------------- softmax: tile t = (warp - 4) / 4, thread = query row ----------------
+    const int t = (warp - 4) >> 2;
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    const float sl2 = p.scale * LOG2E;
+    int cx = 0;  // this tile's blocks so far (s_full / pv_done phases)
+    for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
+      if (w >= n_items) continue;
+      const Item it = q2_item_of(w, npair, BH, p.H);
+      const int lastb = 2 * it.qb + t;  // this tile's diagonal block
+      float m = -INFINITY, l = 0.f, alpha_pend = 1.f;
+      for (int j = 0; j <= lastb; ++j, ++cx) {
+        const bool diag = j == lastb;
+        mbar_wait(&s_full[t], cx & 1);
+        const uint32_t sb = lane_base + t * BN, pdst = lane_base + TM_P + t * 64;
+        // the tile's previous PV has read P_t and finished O_t
+        if (cx > 0) mbar_wait(&pv_done[t], (cx - 1) & 1);
+        tc_fence_after();
+        if (j > 0 && __any_sync(0xffffffffu, alpha_pend != 1.f)) {
+          q2_scale_o(lane_base + TM_O + t * HD, alpha_pend);
+          alpha_pend = 1.f;
+        }
+        if (j == 0) {
+          float mraw = -INFINITY;
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(sb + 32 * c, v);
+            tmem_ld_wait_dep(v);
+            if (diag) mask_chunk(v, 32 * c, r);
+            mraw = fmaxf(mraw, chunk_max(v));
+          }
+          m = mraw * sl2;
+        }
+        float bmax, sum;
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          bmax = -INFINITY;
+          sum = q2_exp_row(sb, pdst, r, diag, sl2, m, bmax);
+          if (j == 0 || pass == 1) break;
+          const float mx = bmax * sl2;
+          const bool extreme = mx > m + EXTREME_LOG2;
+          if (!__any_sync(0xffffffffu, extreme)) break;
+          const float a = extreme ? ex2(m - mx) : 1.f;
+          if (extreme) {
+            m = mx;
+            l *= a;
+          }
+          tmem_st_wait();
+          q2_scale_o(lane_base + TM_O + t * HD, a);
+        }
+        l += sum;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+        if (j > 0) {
+          const float mx = bmax * sl2;
+          if (mx > m + RESCALE_LOG2) {
+            const float a = ex2(m - mx);
+            m = mx;
+            l *= a;
+            alpha_pend = a;
+          }
+        }
+      }
+      // item epilogue: this tile's O / l -> bf16, LSE; then O_t back to the MMA warp
+      mbar_wait(&pv_done[t], (cx - 1) & 1);
+      tc_fence_after();
+      const float inv = alpha_pend * __frcp_rn(l);
+      const int tq = (2 * it.qb + t) * BM + r;
+      __nv_bfloat16* orow = p.out + (size_t)(it.b * p.T + tq) * p.ldo + it.h * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(lane_base + TM_O + t * HD + c, v);
+        tmem_ld_wait_dep(v);
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          *reinterpret_cast<uint4*>(orow + c + i) =
+              make_uint4(pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv),
+                         pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv),
+                         pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv),
+                         pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv));
+      }
+      p.lse[((size_t)it.b * p.H + it.h) * p.T + tq] = (m + __log2f(l)) * (1.f / LOG2E);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_free[t]);
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+// hd=64 with T % 256 == 0: the two-query-tile kernel when it has at least one work item per SM
+// (its items are twice as coarse, so fewer of them balance worse: with B=4, T=1024, H=16 it is
+// 3 % faster, at T=4096 9 %, but with 128 items 50 % slower).  SPX_ATTN_Q2=0 / 1 forces it off / on.
+static bool fwd_q2(int items) {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("SPX_ATTN_Q2");
+    v = e ? (e[0] == '1' ? 1 : 0) : -1;
+  }
+  return v == 1 || (v == -1 && items >= num_sms());
+}
+
 template <int HD>
 int launch_fwd(const void* qkv, const FwdParams& p, long long ld_qkv, cudaStream_t s) {
   auto encode = get_tensor_map_encoder();
@@ -534,6 +886,18 @@ int launch_fwd(const void* qkv, const FwdParams& p, long long ld_qkv, cudaStream
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(SPX_ERR_CUDA, "attn_fwd_tc: tensor map encode failed");
+  if (HD == 64 && p.T % (2 * BM) == 0 && fwd_q2((p.T / (2 * BM)) * p.B * p.H)) {
+    static bool setq2 = false;
+    if (!setq2) {
+      cudaError_t e = cudaFuncSetAttribute(attn_fwd_q2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Q2Smem::BYTES);
+      if (e != cudaSuccess) return set_cuda_error(e, "attn_fwd_q2 attr");
+      setq2 = true;
+    }
+    const int items2 = (p.T / (2 * BM)) * p.B * p.H;
+    const int grid2 = items2 < num_sms() ? items2 : num_sms();
+    spx_launch_check(launch_k(attn_fwd_q2_kernel, dim3(grid2), dim3(THREADS), Q2Smem::BYTES, s, map, p));
+    return check_launch("attn_fwd_q2_kernel");
+  }
   auto k = attn_fwd_tc_kernel<HD>;
   static bool set = false;
   if (!set) {

@@ -77,6 +77,45 @@ def test_attention_fwd_bwd(B, T, H, Hkv, hd):
     assert rel(dx[:, :, H + Hkv:].permute(0, 2, 1, 3), v.grad) < 2e-2
 
 
+@pytest.mark.parametrize("q2", ["1", "0"])
+def test_attention_forward_two_query_tiles(q2):
+    """The hd=64 two-query-tile forward (forced on / off with SPX_ATTN_Q2, read once per process)
+    against torch fp32 on shapes below and above its one-item-per-SM threshold, incl. GQA."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import math, torch
+from paper_2502_19913_b200 import native
+worst = 0.0
+for (B, T, H, Hkv) in [(2, 1024, 16, 16), (1, 2048, 8, 2), (1, 512, 4, 4), (4, 1024, 16, 16)]:
+    hd = 64
+    g = torch.Generator().manual_seed(B * T + H)
+    W = (H + 2 * Hkv) * hd
+    qkv = torch.randn(B * T, W, generator=g).to(torch.bfloat16).cuda()
+    o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty(B, H, T, device="cuda")
+    native.attn_fwd(qkv, o, lse, B=B, T=T, H=H, Hkv=Hkv, hd=hd, ld_qkv=W, ld_o=H * hd, scale=1 / math.sqrt(hd))
+    x = qkv.float().view(B, T, H + 2 * Hkv, hd)
+    q = x[:, :, :H].permute(0, 2, 1, 3)
+    k = x[:, :, H:H + Hkv].permute(0, 2, 1, 3).repeat_interleave(H // Hkv, dim=1)
+    v = x[:, :, H + Hkv:].permute(0, 2, 1, 3).repeat_interleave(H // Hkv, dim=1)
+    sc = (q @ k.transpose(-1, -2)) / math.sqrt(hd)
+    sc = sc.masked_fill(torch.ones(T, T, dtype=torch.bool, device="cuda").triu(1), float("-inf"))
+    ref = (torch.softmax(sc, -1) @ v).permute(0, 2, 1, 3).reshape(B * T, H * hd)
+    rel = ((o.float() - ref).norm() / ref.norm()).item()
+    lerr = (lse - torch.logsumexp(sc, -1)).abs().max().item()
+    worst = max(worst, rel, lerr / 10)
+print(worst)
+'''
+    env = dict(os.environ, SPX_ATTN_Q2=q2)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) < 1e-2
+
+
 def test_attention_deterministic():
     B, T, H, hd = 1, 512, 4, 64
     g = torch.Generator().manual_seed(7)
