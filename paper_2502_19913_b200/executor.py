@@ -757,7 +757,15 @@ class Trainer:
         if M != self.M or b != self.b or T1 != self.T + 1:
             raise ValidationError(f"tokens shape {tuple(tokens.shape)} != ({self.M}, {self.b}, {self.T + 1})")
         t = tokens.to(torch.int64).contiguous()
-        return {"tokens": t if t.is_pinned() else t.pin_memory()}
+        if t.is_pinned():
+            return {"tokens": t}
+        # one persistent pinned staging buffer (pinning a fresh tensor every step costs more than
+        # the copy); the previous step's H2D copies from it completed before that step returned
+        # (its loss readback waits for every stream of the step)
+        if getattr(self, "_pinned", None) is None:
+            self._pinned = torch.empty_like(t).pin_memory()
+        self._pinned.copy_(t)
+        return {"tokens": self._pinned}
 
     def h2d_bytes(self, tokens: torch.Tensor) -> int:
         """Bytes of token blocks this rank copies host->device per iteration."""
