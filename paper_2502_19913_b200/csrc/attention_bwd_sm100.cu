@@ -26,6 +26,9 @@ namespace fab {
 #ifndef SPX_FAB_NST64
 #define SPX_FAB_NST64 3
 #endif
+#ifndef SPX_FAB_KVS64
+#define SPX_FAB_KVS64 2
+#endif
 #ifndef SPX_FAB_PT_TMEM
 #define SPX_FAB_PT_TMEM 1
 #endif
@@ -97,9 +100,18 @@ SPX_DEVICE void put_row8p(uint8_t* tile, int r, int c8, const uint32_t* v) {
   *reinterpret_cast<uint4*>(tile + atom * ATOM + r * 128 + ((chunk ^ (r & 7)) << 4)) = make_uint4(v[0], v[1], v[2], v[3]);
 }
 
-// write a 128 x HD accumulator row (TMEM lane) as bf16, optionally through the inverse RoPE
+// write a 128 x HD accumulator row (TMEM lane) as bf16 into this warp's 32-row SWIZZLE_128B
+// staging box(es) -- box a holds columns [64a, 64a+64) -- for a TMA store: one coalesced bulk
+// write per box instead of 32 scattered rows per st.global
 template <int HD>
-SPX_DEVICE void store_grad_row(uint32_t taddr, __nv_bfloat16* dst, float scale, const float* cs, int T, int pos) {
+SPX_DEVICE void stage_grad_row(uint32_t taddr, uint8_t* box0, uint8_t* box1, int row, float scale, const float* cs,
+                               int T, int pos) {
+  auto put = [&](int col, const float* v) {  // 8 columns starting at col (multiple of 8)
+    uint8_t* box = col < 64 ? box0 : box1;
+    const int chunk = (col & 63) >> 3;
+    *reinterpret_cast<uint4*>(box + row * 128 + ((chunk ^ (row & 7)) << 4)) =
+        make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+  };
   if (cs) {
     const float2* c2 = reinterpret_cast<const float2*>(cs);
 #pragma unroll 1
@@ -118,12 +130,8 @@ SPX_DEVICE void store_grad_row(uint32_t taddr, __nv_bfloat16* dst, float scale, 
       }
 #pragma unroll
       for (int j = 0; j < 32; j += 8) {
-        *reinterpret_cast<uint4*>(dst + j0 + j) =
-            make_uint4(pack_bf16(o1[j], o1[j + 1]), pack_bf16(o1[j + 2], o1[j + 3]), pack_bf16(o1[j + 4], o1[j + 5]),
-                       pack_bf16(o1[j + 6], o1[j + 7]));
-        *reinterpret_cast<uint4*>(dst + HD / 2 + j0 + j) =
-            make_uint4(pack_bf16(o2[j], o2[j + 1]), pack_bf16(o2[j + 2], o2[j + 3]), pack_bf16(o2[j + 4], o2[j + 5]),
-                       pack_bf16(o2[j + 6], o2[j + 7]));
+        put(j0 + j, o1 + j);
+        put(HD / 2 + j0 + j, o2 + j);
       }
     }
   } else {
@@ -132,13 +140,11 @@ SPX_DEVICE void store_grad_row(uint32_t taddr, __nv_bfloat16* dst, float scale, 
       uint32_t a[32];
       tmem_ld_32x32b_x32(taddr + c, a);
       tmem_ld_wait();
+      float o[32];
 #pragma unroll
-      for (int j = 0; j < 32; j += 8)
-        *reinterpret_cast<uint4*>(dst + c + j) = make_uint4(
-            pack_bf16(__uint_as_float(a[j]) * scale, __uint_as_float(a[j + 1]) * scale),
-            pack_bf16(__uint_as_float(a[j + 2]) * scale, __uint_as_float(a[j + 3]) * scale),
-            pack_bf16(__uint_as_float(a[j + 4]) * scale, __uint_as_float(a[j + 5]) * scale),
-            pack_bf16(__uint_as_float(a[j + 6]) * scale, __uint_as_float(a[j + 7]) * scale));
+      for (int j = 0; j < 32; ++j) o[j] = __uint_as_float(a[j]) * scale;
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) put(c + j, o + j);
     }
   }
 }
@@ -150,9 +156,12 @@ template <int HD>
 struct DkdvSmem {
   static constexpr int NST = HD == 64 ? SPX_FAB_NST64 : 1;      // Q/dO ring depth
   static constexpr int TILE = (HD / 64) * ATOM;     // 128 x HD bf16
-  static constexpr int OFF_K = 0;
-  static constexpr int OFF_V = OFF_K + TILE;
-  static constexpr int OFF_Q = OFF_V + TILE;        // [NST]
+  // hd=64: K/V double-buffered across items, so the next item's K/V load and its first S/dP
+  // MMAs overlap the current item's last step and dV/dK epilogue (hd=128 has no smem for it)
+  static constexpr int KVS = HD == 64 ? SPX_FAB_KVS64 : 1;
+  static constexpr int OFF_K = 0;                   // [KVS]
+  static constexpr int OFF_V = OFF_K + KVS * TILE;  // [KVS]
+  static constexpr int OFF_Q = OFF_V + KVS * TILE;  // [NST]
   static constexpr int OFF_DO = OFF_Q + NST * TILE; // [NST]
   // hd=64: P^T and dS^T are A operands straight from TMEM (TS MMAs), only dS^T is also staged in
   // shared memory for its TMA store; hd=128 has no spare TMEM columns and stages both in smem
@@ -168,7 +177,8 @@ struct DkdvSmem {
 template <int HD>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
-                            const __grid_constant__ CUtensorMap tmDS, const BwdParams p) {
+                            const __grid_constant__ CUtensorMap tmDS, const __grid_constant__ CUtensorMap tmOut,
+                            const BwdParams p) {
   using L = DkdvSmem<HD>;
   constexpr int NST = L::NST;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -176,15 +186,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   static_assert(NST <= 4, "barrier layout holds up to 4 ring stages");
   uint64_t* full = bars + 0;      // [NST]
   uint64_t* empty = bars + 4;     // [NST]
-  uint64_t* kv_full = bars + 8;
-  uint64_t* kv_empty = bars + 9;
-  uint64_t* sdp_full = bars + 10;
-  uint64_t* p_ready = bars + 11;
-  uint64_t* mma2_done = bars + 12;
-  uint64_t* tmem_free = bars + 13;  // S / dP of the current step copied to registers
-  uint64_t* acc_free = bars + 14;   // dV / dK of the previous item read out of TMEM
-  uint64_t* ds_read = bars + 15;    // the dS^T tile of the step has been read by its TMA store
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  constexpr int KVS = L::KVS;
+  uint64_t* kv_full = bars + 8;     // [KVS]
+  uint64_t* kv_empty = bars + 10;   // [KVS]
+  uint64_t* sdp_full = bars + 12;
+  uint64_t* p_ready = bars + 13;
+  uint64_t* mma2_done = bars + 14;
+  uint64_t* tmem_free = bars + 15;  // S / dP of the current step copied to registers
+  uint64_t* acc_free = bars + 16;   // dV / dK of the previous item read out of TMEM
+  uint64_t* ds_read = bars + 17;    // the dS^T tile of the step has been read by its TMA store
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = p.T / BLK;
@@ -201,8 +212,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmQKV);
     tma_prefetch_desc(&tmDO);
-    mbar_init(kv_full, 1);
-    mbar_init(kv_empty, 1);
+    for (int i = 0; i < KVS; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
     for (int i = 0; i < NST; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -214,6 +227,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(acc_free, EW_WARPS);
     mbar_init(ds_read, 1);
     tma_prefetch_desc(&tmDS);
+    tma_prefetch_desc(&tmOut);
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -235,11 +249,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       int b, kvh, jb;
       item(w, b, kvh, jb);
       const int row0 = b * p.T, nq = nqb - jb;
-      mbar_wait(kv_empty, (n & 1) ^ 1);
-      mbar_expect_tx(kv_full, 2 * L::TILE);
+      const int kv = n % KVS;
+      mbar_wait(&kv_empty[kv], ((n / KVS) & 1) ^ 1);
+      mbar_expect_tx(&kv_full[kv], 2 * L::TILE);
       for (int a = 0; a < HD / 64; ++a) {
-        tma_load_2d(smem + L::OFF_K + a * ATOM, &tmQKV, kv_full, (p.H + kvh) * HD + 64 * a, row0 + jb * BLK);
-        tma_load_2d(smem + L::OFF_V + a * ATOM, &tmQKV, kv_full, (p.H + p.Hkv + kvh) * HD + 64 * a, row0 + jb * BLK);
+        tma_load_2d(smem + L::OFF_K + kv * L::TILE + a * ATOM, &tmQKV, &kv_full[kv], (p.H + kvh) * HD + 64 * a,
+                    row0 + jb * BLK);
+        tma_load_2d(smem + L::OFF_V + kv * L::TILE + a * ATOM, &tmQKV, &kv_full[kv],
+                    (p.H + p.Hkv + kvh) * HD + 64 * a, row0 + jb * BLK);
       }
       for (int it = 0; it < group * nq; ++it, ++gi) {
         const int s = gi % NST;
@@ -260,9 +277,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------- MMA issuer (whole warp; one elected lane issues) ----------------
     constexpr uint32_t ID_S = umma_idesc_bf16(BLK, BLK, false, false);   // K.Q^T, V.dO^T
     constexpr uint32_t ID_G = umma_idesc_bf16(BLK, HD, false, true);     // P^T.dO, dS^T.Q
-    const uint32_t sK = smem_u32(smem + L::OFF_K), sV = smem_u32(smem + L::OFF_V);
     const uint32_t sPT = smem_u32(smem + L::OFF_PT), sDST = smem_u32(smem + L::OFF_DST);
-    auto issue_sdp = [&](int gi) {
+    auto issue_sdp = [&](int gi, int kv) {
+      const uint32_t sK = smem_u32(smem + L::OFF_K + kv * L::TILE), sV = smem_u32(smem + L::OFF_V + kv * L::TILE);
       const int s = gi % NST;
       mbar_wait(&full[s], (gi / NST) & 1);
       tc_fence_after();
@@ -281,24 +298,35 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
     };
     int gi = 0, n = 0;
+    bool issued = false;  // S/dP of step gi already issued (look-ahead from the previous step)
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
       if (w >= n_items) continue;
       int b, kvh, jb;
       item(w, b, kvh, jb);
       const int n_it = group * (nqb - jb);
-      mbar_wait(kv_full, n & 1);
-      bool issued = false;
+      const int kv = n % KVS;
+      // the CTA's next item (rounds past the last valid one hold none)
+      const int w_next = snake(k + 1, blockIdx.x, gridDim.x);
+      const bool has_next = w_next < n_items;
+      mbar_wait(&kv_full[kv], (n / KVS) & 1);
       for (int it = 0; it < n_it; ++it, ++gi) {
         const int s = gi % NST;
-        if (!issued) issue_sdp(gi);
-        // S/dP of this step are in registers: with a 2-deep Q/dO ring the next step's S/dP (same
-        // item: K/V stay) overlap the elementwise math; otherwise they follow this step's dV/dK
+        if (!issued) issue_sdp(gi, kv);
+        // S/dP of this step are in registers: with a 2-deep Q/dO ring the next step's S/dP
+        // overlap the elementwise math -- within the item (K/V stay), and with double-buffered
+        // K/V also across items; otherwise they follow this step's dV/dK
         mbar_wait(tmem_free, gi & 1);
         if (lane == 0) FAB_PROBE(1, gi);
         tc_fence_after();
         issued = false;
         if (NST > 1 && it + 1 < n_it) {
-          issue_sdp(gi + 1);
+          issue_sdp(gi + 1, kv);
+          issued = true;
+        } else if (NST > 1 && KVS > 1 && has_next) {
+          const int kv1 = (n + 1) % KVS;
+          mbar_wait(&kv_full[kv1], ((n + 1) / KVS) & 1);
+          tc_fence_after();
+          issue_sdp(gi + 1, kv1);
           issued = true;
         }
         mbar_wait(p_ready, gi & 1);
@@ -324,7 +352,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           mma_commit(mma2_done);
           mma_commit(&empty[s]);
-          if (it + 1 == n_it) mma_commit(kv_empty);
+          if (it + 1 == n_it) mma_commit(&kv_empty[kv]);
         }
         __syncwarp();
       }
@@ -417,6 +445,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (gi > 0) {
           mbar_wait(mma2_done, (gi - 1) & 1);  // P^T / dS^T tiles free
           mbar_wait(ds_read, (gi - 1) & 1);    // the dS^T store has read its tile
+          if (it == 0) {                       // this warp's dV/dK store has read its staging boxes
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+          }
         }
         if (warp == 4 && lane == 0) FAB_PROBE(5, gi);
         if constexpr (PT_TMEM) {
@@ -440,17 +472,30 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (warp == 4 && lane == 0) FAB_PROBE(6, gi);
         if (lane == 0) mbar_arrive(p_ready);
       }
-      // item outputs: half 0 writes dV, half 1 writes dK (scaled, inverse RoPE)
+      // item outputs: half 0 writes dV, half 1 writes dK (scaled, inverse RoPE), staged in the
+      // warp's own quarter of the P^T / dS^T tiles (free once the last dV/dK MMAs and the last
+      // dS^T store are done; the warp writes the same bytes again first at its next step) and
+      // written by TMA
       mbar_wait(mma2_done, (gi - 1) & 1);
+      mbar_wait(ds_read, (gi - 1) & 1);
       tc_fence_after();
       const int key = jb * BLK + r;
-      __nv_bfloat16* dst = p.dqkv + (size_t)(b * p.T + key) * p.ld;
-      if (half == 0) store_grad_row<HD>(lane_base + TM_DV, dst + (p.H + p.Hkv + kvh) * HD, 1.f, nullptr, p.T, key);
-      else store_grad_row<HD>(lane_base + TM_DK, dst + (p.H + kvh) * HD, p.scale, p.rope_cs, p.T, key);
+      uint8_t* box0 = smem + (L::PT_TMEM ? L::OFF_DST : L::OFF_PT) + half * ATOM + quad * 4096;
+      uint8_t* box1 = smem + L::OFF_DST + half * ATOM + quad * 4096;
+      if (half == 0) stage_grad_row<HD>(lane_base + TM_DV, box0, box1, lane, 1.f, nullptr, p.T, key);
+      else stage_grad_row<HD>(lane_base + TM_DK, box0, box1, lane, p.scale, p.rope_cs, p.T, key);
       tc_fence_before();
+      fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(acc_free);
+      if (lane == 0) {
+        mbar_arrive(acc_free);
+        const int col = (half == 0 ? p.H + p.Hkv + kvh : p.H + kvh) * HD, row = b * p.T + jb * BLK + quad * 32;
+        tma_store_2d(&tmOut, box0, col, row);
+        if (HD == 128) tma_store_2d(&tmOut, box1, col + 64, row);
+        bulk_commit();
+      }
     }
+    if (lane == 0) bulk_wait<0>();
   }
   __syncwarp();
   tc_fence_before();
@@ -472,7 +517,8 @@ struct DqmSmem {
   static constexpr int K_BYTES = (HD / 64) * ATOM;          // 128 keys x HD
   static constexpr int STAGE = DS_BYTES + K_BYTES;
   static constexpr int STAGES = HD == 64 ? 4 : 3;
-  static constexpr int OFF_BAR = STAGES * STAGE;
+  static constexpr int OFF_STG = STAGES * STAGE;            // dQ staging: [HD/64][128 rows][128 B]
+  static constexpr int OFF_BAR = OFF_STG + (HD / 64) * ATOM;
   static constexpr int BYTES = OFF_BAR + 256;
   static constexpr int THREADS = 256;                       // producer, MMA, TMEM, spare, 4 epilogue warps
 };
@@ -480,7 +526,7 @@ struct DqmSmem {
 template <int HD>
 __global__ void __launch_bounds__(DqmSmem<HD>::THREADS, 1)
     attn_bwd_dq_mma_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDS,
-                           const BwdParams p) {
+                           const __grid_constant__ CUtensorMap tmOut, const BwdParams p) {
   using L = DqmSmem<HD>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -506,6 +552,7 @@ __global__ void __launch_bounds__(DqmSmem<HD>::THREADS, 1)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmQKV);
     tma_prefetch_desc(&tmDS);
+    tma_prefetch_desc(&tmOut);
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -581,13 +628,24 @@ __global__ void __launch_bounds__(DqmSmem<HD>::THREADS, 1)
       const int acc = n & 1;
       mbar_wait(&acc_full[acc], (n >> 1) & 1);
       tc_fence_after();
-      const int t = ib * BLK + r;
-      store_grad_row<HD>(tmem + ((uint32_t)(quad * 32) << 16) + acc * HD,
-                         p.dqkv + (size_t)(b * p.T + t) * p.ld + h * HD, p.scale, p.rope_cs, p.T, t);
-      tc_fence_before();
+      if (lane == 0) bulk_wait_read<0>();  // the previous item's store has read the staging boxes
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      const int t = ib * BLK + r;
+      uint8_t* box0 = smem + L::OFF_STG + quad * 4096;
+      stage_grad_row<HD>(tmem + ((uint32_t)(quad * 32) << 16) + acc * HD, box0, box0 + ATOM, lane, p.scale,
+                         p.rope_cs, p.T, t);
+      tc_fence_before();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&acc_empty[acc]);
+        const int row = b * p.T + ib * BLK + quad * 32;
+        tma_store_2d(&tmOut, box0, h * HD, row);
+        if (HD == 128) tma_store_2d(&tmOut, box0 + ATOM, h * HD + 64, row);
+        bulk_commit();
+      }
     }
+    if (lane == 0) bulk_wait<0>();
   }
   __syncwarp();
   tc_fence_before();
@@ -596,13 +654,13 @@ __global__ void __launch_bounds__(DqmSmem<HD>::THREADS, 1)
   if (warp == 2) tmem_dealloc(tmem, TMEM_COLS);
 }
 
-static int make_map(CUtensorMap* m, const void* ptr, long long ld, long long rows) {
-  // 2D bf16 [rows][ld], 64 x 128 boxes, SWIZZLE_128B
+static int make_map(CUtensorMap* m, const void* ptr, long long ld, long long rows, int box_rows = 128) {
+  // 2D bf16 [rows][ld], 64 x box_rows boxes, SWIZZLE_128B
   auto encode = get_tensor_map_encoder();
   if (!encode) return set_error(SPX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -616,6 +674,9 @@ static int launch(const void* qkv, const void* dout, long long ld_o, const BwdPa
   int rc = make_map(&mq, qkv, p.ld, (long long)p.B * p.T);
   if (rc) return rc;
   rc = make_map(&md, dout, ld_o, (long long)p.B * p.T);
+  if (rc) return rc;
+  CUtensorMap mo;  // dQKV, 32-row boxes (one per epilogue warp)
+  rc = make_map(&mo, p.dqkv, p.ld, (long long)p.B * p.T, 32);
   if (rc) return rc;
   static bool set = false;
   if (!set) {
@@ -634,11 +695,11 @@ static int launch(const void* qkv, const void* dout, long long ld_o, const BwdPa
   if (rc) return rc;
   const int items_kv = nqb * p.Hkv * p.B, items_q = nqb * p.H * p.B;
   const int g1 = items_kv < num_sms() ? items_kv : num_sms(), g2 = items_q < num_sms() ? items_q : num_sms();
-  spx_launch_check(launch_k(attn_bwd_dkdv_tc_kernel<HD>, dim3(g1), dim3(THREADS), DkdvSmem<HD>::BYTES, s, mq, md, mds, p));
+  spx_launch_check(launch_k(attn_bwd_dkdv_tc_kernel<HD>, dim3(g1), dim3(THREADS), DkdvSmem<HD>::BYTES, s, mq, md, mds, mo, p));
   rc = check_launch("attn_bwd_dkdv_tc_kernel");
   if (rc) return rc;
   spx_launch_check(launch_k(attn_bwd_dq_mma_kernel<HD>, dim3(g2), dim3(DqmSmem<HD>::THREADS), DqmSmem<HD>::BYTES, s,
-                            mq, mds, p));
+                            mq, mds, mo, p));
   return check_launch("attn_bwd_dq_mma_kernel");
 }
 

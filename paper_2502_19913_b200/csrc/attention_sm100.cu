@@ -208,13 +208,31 @@ struct FwdSmem {
   // row-sum exchange at the end of an item: [half][row]
   static constexpr int OFF_RED = OFF_BAR + 256;
   // >= 116 KB: one CTA per SM (it owns all 512 TMEM columns)
-  static constexpr int RAW = OFF_RED + 6 * BM * 4;
+  // hd=128: O staging for the TMA store, one 32-row x 64-column box per softmax warp
+  static constexpr bool STG = HD == 128;
+  static constexpr int OFF_STG = (OFF_RED + 6 * BM * 4 + 1023) / 1024 * 1024;
+  static constexpr int RAW = OFF_STG + (STG ? 2 * ATOM : 0);
   static constexpr int BYTES = RAW > 116 * 1024 ? RAW : 116 * 1024;
 };
 
+// 32 fp32 accumulator values (columns c0 .. c0+31 of a 64-column box row) * inv -> bf16, into a
+// 32-row SWIZZLE_128B box (the TMA store's layout; conflict-free 16-byte writes)
+SPX_DEVICE void box_put32(uint8_t* box, int row, int c0, const uint32_t* v, float inv) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 8) {
+    const int chunk = (c0 + i) >> 3;
+    *reinterpret_cast<uint4*>(box + row * 128 + ((chunk ^ (row & 7)) << 4)) =
+        make_uint4(pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv),
+                   pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv),
+                   pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv),
+                   pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv));
+  }
+}
+
 template <int HD>
 __global__ void __launch_bounds__(THREADS, 1)
-    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const FwdParams p) {
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmO,
+                       const FwdParams p) {
   using L = FwdSmem<HD>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
@@ -493,26 +511,50 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       const float inv = alpha_pend * __frcp_rn(l);
       const int t = it.qb * BM + r;
-      __nv_bfloat16* orow = p.out + (size_t)(it.b * p.T + t) * p.ldo + it.h * HD + half * HO;
+      if constexpr (L::STG) {
+        // hd=128: this warp's 32 rows x 64 columns through its staging box and one TMA store
+        uint8_t* box = smem + L::OFF_STG + half * L::ATOM + q * 4096;
+        if (lane == 0) bulk_wait_read<0>();  // the previous item's store has read the box
+        __syncwarp();
 #pragma unroll
-      for (int c = 0; c < HO; c += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(lane_base + TM_O + half * HO + c, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          *reinterpret_cast<uint4*>(orow + c + i) =
-              make_uint4(pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv),
-                         pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv),
-                         pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv),
-                         pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv));
+        for (int c = 0; c < HO; c += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(lane_base + TM_O + half * HO + c, v);
+          tmem_ld_wait();
+          box_put32(box, lane, c, v, inv);
         }
+        if (half == 0) p.lse[((size_t)it.b * p.H + it.h) * p.T + t] = (m + __log2f(l)) * (1.f / LOG2E);
+        tc_fence_before();
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(o_free);
+          tma_store_2d(&tmO, box, it.h * HD + half * HO, it.b * p.T + it.qb * BM + q * 32);
+          bulk_commit();
+        }
+      } else {
+        __nv_bfloat16* orow = p.out + (size_t)(it.b * p.T + t) * p.ldo + it.h * HD + half * HO;
+#pragma unroll
+        for (int c = 0; c < HO; c += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(lane_base + TM_O + half * HO + c, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            *reinterpret_cast<uint4*>(orow + c + i) =
+                make_uint4(pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv),
+                           pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv),
+                           pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv),
+                           pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv));
+          }
+        }
+        if (half == 0) p.lse[((size_t)it.b * p.H + it.h) * p.T + t] = (m + __log2f(l)) * (1.f / LOG2E);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_free);
       }
-      if (half == 0) p.lse[((size_t)it.b * p.H + it.h) * p.T + t] = (m + __log2f(l)) * (1.f / LOG2E);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(o_free);
     }
+    if (L::STG && lane == 0) bulk_wait<0>();
   }
   __syncwarp();
   tc_fence_before();
@@ -537,7 +579,8 @@ struct Q2Smem {
   static constexpr int OFF_Q = 0;                       // [2]
   static constexpr int OFF_K = OFF_Q + 2 * TILE;        // [NK]
   static constexpr int OFF_V = OFF_K + NK * TILE;       // [NV]
-  static constexpr int OFF_BAR = OFF_V + NV * TILE;
+  static constexpr int OFF_STG = OFF_V + NV * TILE;     // [tile] O staging, a 32-row box per warp
+  static constexpr int OFF_BAR = OFF_STG + 2 * TILE;
   static constexpr int RAW = OFF_BAR + 256;
   static constexpr int BYTES = RAW > 116 * 1024 ? RAW : 116 * 1024;
 };
@@ -599,7 +642,8 @@ SPX_DEVICE Item q2_item_of(int w, int npair, int BH, int H) {
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
-    attn_fwd_q2_kernel(const __grid_constant__ CUtensorMap tmQKV, const FwdParams p) {
+    attn_fwd_q2_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmO,
+                       const FwdParams p) {
   using L = Q2Smem;
   constexpr int HD = 64;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -834,25 +878,28 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       const float inv = alpha_pend * __frcp_rn(l);
       const int tq = (2 * it.qb + t) * BM + r;
-      __nv_bfloat16* orow = p.out + (size_t)(it.b * p.T + tq) * p.ldo + it.h * HD;
+      // this warp's 32 rows through its staging box and one TMA store
+      uint8_t* box = smem + L::OFF_STG + t * L::TILE + q * 4096;
+      if (lane == 0) bulk_wait_read<0>();  // the previous item's store has read the box
+      __syncwarp();
 #pragma unroll 1
       for (int c = 0; c < HD; c += 32) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(lane_base + TM_O + t * HD + c, v);
         tmem_ld_wait_dep(v);
-#pragma unroll
-        for (int i = 0; i < 32; i += 8)
-          *reinterpret_cast<uint4*>(orow + c + i) =
-              make_uint4(pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv),
-                         pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv),
-                         pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv),
-                         pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv));
+        box_put32(box, lane, c, v, inv);
       }
       p.lse[((size_t)it.b * p.H + it.h) * p.T + tq] = (m + __log2f(l)) * (1.f / LOG2E);
       tc_fence_before();
+      fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&o_free[t]);
+      if (lane == 0) {
+        mbar_arrive(&o_free[t]);
+        tma_store_2d(&tmO, box, it.h * HD, it.b * p.T + (2 * it.qb + t) * BM + q * 32);
+        bulk_commit();
+      }
     }
+    if (lane == 0) bulk_wait<0>();
   }
   __syncwarp();
   tc_fence_before();
@@ -886,6 +933,13 @@ int launch_fwd(const void* qkv, const FwdParams& p, long long ld_qkv, cudaStream
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(SPX_ERR_CUDA, "attn_fwd_tc: tensor map encode failed");
+  CUtensorMap omap;  // O [B*T][ldo], 64 x 32 boxes (one per softmax warp)
+  cuuint64_t odims[2] = {(cuuint64_t)p.ldo, (cuuint64_t)p.B * p.T};
+  cuuint64_t ostrides[1] = {(cuuint64_t)p.ldo * 2};
+  cuuint32_t obox[2] = {64, 32};
+  r = encode(&omap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p.out, odims, ostrides, obox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(SPX_ERR_CUDA, "attn_fwd_tc: output tensor map encode failed");
   if (HD == 64 && p.T % (2 * BM) == 0 && fwd_q2((p.T / (2 * BM)) * p.B * p.H)) {
     static bool setq2 = false;
     if (!setq2) {
@@ -895,7 +949,7 @@ int launch_fwd(const void* qkv, const FwdParams& p, long long ld_qkv, cudaStream
     }
     const int items2 = (p.T / (2 * BM)) * p.B * p.H;
     const int grid2 = items2 < num_sms() ? items2 : num_sms();
-    spx_launch_check(launch_k(attn_fwd_q2_kernel, dim3(grid2), dim3(THREADS), Q2Smem::BYTES, s, map, p));
+    spx_launch_check(launch_k(attn_fwd_q2_kernel, dim3(grid2), dim3(THREADS), Q2Smem::BYTES, s, map, omap, p));
     return check_launch("attn_fwd_q2_kernel");
   }
   auto k = attn_fwd_tc_kernel<HD>;
@@ -907,7 +961,7 @@ int launch_fwd(const void* qkv, const FwdParams& p, long long ld_qkv, cudaStream
   }
   const int items = (p.T / BM) * p.B * p.H;
   const int grid = items < num_sms() ? items : num_sms();
-  spx_launch_check(launch_k(k, dim3(grid), dim3(THREADS), FwdSmem<HD>::BYTES, s, map, p));
+  spx_launch_check(launch_k(k, dim3(grid), dim3(THREADS), FwdSmem<HD>::BYTES, s, map, omap, p));
   return check_launch("attn_fwd_tc_kernel");
 }
 

@@ -389,23 +389,24 @@ def test_gemm_rope_epilogue(hd, H, Hkv):
     assert rel(out.view(B, T, -1, hd), ref) < 1e-2
 
 
-def test_attention_bwd_inverse_rope():
-    B, T, H, hd = 1, 256, 4, 64
+@pytest.mark.parametrize("hd,H,Hkv", [(64, 4, 4), (128, 4, 2)])
+def test_attention_bwd_inverse_rope(hd, H, Hkv):
+    B, T = 1, 256
     g = torch.Generator().manual_seed(11)
-    W = 3 * H * hd
+    W = (H + 2 * Hkv) * hd
     qkv = bf(torch.randn(B * T, W, generator=g)).to(dev)
     do = bf(torch.randn(B * T, H * hd, generator=g)).to(dev)
     cs = rope_table(T, hd).to(dev)
     o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device=dev)
     lse = torch.empty(B, H, T, device=dev)
-    native.attn_fwd(qkv, o, lse, B=B, T=T, H=H, Hkv=H, hd=hd, ld_qkv=W, ld_o=H * hd, scale=0.125)
+    native.attn_fwd(qkv, o, lse, B=B, T=T, H=H, Hkv=Hkv, hd=hd, ld_qkv=W, ld_o=H * hd, scale=0.125)
     plain = torch.zeros_like(qkv)
     fused = torch.zeros_like(qkv)
     delta = torch.empty(native.attn_bwd_ws_floats(B, H, T, hd), device=dev)
-    kw = dict(B=B, T=T, H=H, Hkv=H, hd=hd, ld_qkv=W, ld_o=H * hd, scale=0.125)
+    kw = dict(B=B, T=T, H=H, Hkv=Hkv, hd=hd, ld_qkv=W, ld_o=H * hd, scale=0.125)
     native.attn_bwd(qkv, o, do, lse, delta, plain, **kw)
     native.attn_bwd(qkv, o, do, lse, delta, fused, rope_cs=cs, **kw)
-    native.rope(plain, cs, rows=B * T, T=T, n_heads=2 * H, hd=hd, ld=W, inverse=True)
+    native.rope(plain, cs, rows=B * T, T=T, n_heads=H + Hkv, hd=hd, ld=W, inverse=True)
     torch.cuda.synchronize()
     assert rel(fused, plain) < 1e-2
 
