@@ -137,6 +137,15 @@ int spx_gemm_bf16_rope(const void* A, const void* B, void* C, int64_t M, int64_t
                        int64_t ldb, int64_t ldc, const float* cos_sin, int64_t rope_cols, int64_t T, int64_t head_dim,
                        void* stream);
 
+/* Attention-output dgrad with the attention backward's D pass fused into its epilogue:
+ * dO = A . B (A [M][K] K-major, B [K][N] MN-major: dO = dY . Wo), and for every (row, head) of the
+ * [batch*T][H*head_dim] output D = sum over the head's columns of bf16(dO) * O, written with
+ * lse*log2e into delta_ws (the [2][batch][H][T] prefix of spx_attn_bwd's workspace) -- then call
+ * spx_attn_bwd_ex with SPX_ATTN_DELTA_READY.  head_dim 64 or 128, M = batch * T. */
+int spx_gemm_bf16_attn_delta(const void* A, const void* B, void* dO, const void* O, int64_t ld_o, const float* lse,
+                             float* delta_ws, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
+                             int64_t batch, int64_t T, int64_t head_dim, void* stream);
+
 /* ---- attention (causal, GQA; q/k/v read from the fused QKV buffer) ----
  * qkv [B*T][ld_qkv] bf16 with q heads at column h*hd, k heads at (H+j)*hd, v heads at (H+Hkv+j)*hd.
  * o [B*T][ld_o] bf16, lse [B][H][T] f32 (natural log).  T % 64 == 0, hd in {48, 64, 128}. */
@@ -151,6 +160,12 @@ int64_t spx_attn_bwd_ws_floats(int64_t B, int64_t H, int64_t T, int64_t hd);
 int spx_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, float* delta_ws, void* dqkv,
                  int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv, int64_t ld_o, float scale,
                  const float* rope_cos_sin, void* stream);
+/* spx_attn_bwd with flags: SPX_ATTN_DELTA_READY = the first 2*B*H*T floats of delta_ws already hold
+ * D = rowsum(dO*O) and lse*log2e (written by spx_gemm_bf16_attn_delta), so no D pass runs. */
+#define SPX_ATTN_DELTA_READY 1
+int spx_attn_bwd_ex(const void* qkv, const void* o, const void* dout, const float* lse, float* delta_ws, void* dqkv,
+                    int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv, int64_t ld_o, float scale,
+                    const float* rope_cos_sin, int32_t flags, void* stream);
 
 /* ---- RMSNorm ----
  * fwd: y = x * rsqrt(mean(x^2) + eps) * g ; rstd[rows] saved.

@@ -138,6 +138,7 @@ struct Params {
   long long ldo;        // O / dO row stride
   int B, T, H, Hkv;
   float scale;
+  int delta_ready;      // bwd: the workspace already holds D and lse*log2e (spx_gemm_bf16_attn_delta)
 };
 
 // ----------------------------------------------------------------------------------------
@@ -589,7 +590,7 @@ template <int HD>
 static int run_bwd(const Params& p, cudaStream_t s) {
   constexpr int LD = Tile<HD>::LD;
   constexpr int BQI = (HD > 64) ? 32 : 64;
-  {
+  if (!p.delta_ready) {
     const long long groups = (long long)p.B * p.T * p.H;  // 8 threads each, 4 groups per thread
     const int threads = 256;
     const long long per_block = threads / 8 * 4;
@@ -683,6 +684,14 @@ extern "C" int64_t spx_attn_bwd_ws_floats(int64_t B, int64_t H, int64_t T, int64
 extern "C" int spx_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, float* delta_ws,
                             void* dqkv, int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv,
                             int64_t ld_o, float scale, const float* rope_cos_sin, void* stream) {
+  return spx_attn_bwd_ex(qkv, o, dout, lse, delta_ws, dqkv, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, rope_cos_sin, 0,
+                         stream);
+}
+
+extern "C" int spx_attn_bwd_ex(const void* qkv, const void* o, const void* dout, const float* lse, float* delta_ws,
+                               void* dqkv, int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv,
+                               int64_t ld_o, float scale, const float* rope_cos_sin, int32_t flags, void* stream) {
+  if (flags & ~SPX_ATTN_DELTA_READY) return set_error(SPX_ERR_ARG, "attn_bwd: unknown flags");
   int rc = attn::check_args(B, T, H, Hkv, hd);
   if (rc) return rc;
   if (ld_o % 8 != 0 || (((uintptr_t)o | (uintptr_t)dout) & 15))
@@ -699,6 +708,7 @@ extern "C" int spx_attn_bwd(const void* qkv, const void* o, const void* dout, co
   p.ldo = ld_o;
   p.B = (int)B; p.T = (int)T; p.H = (int)H; p.Hkv = (int)Hkv;
   p.scale = scale;
+  p.delta_ready = (flags & SPX_ATTN_DELTA_READY) ? 1 : 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (hd == 48) return attn::run_bwd<48>(p, s);
   if (hd == 64) return attn::run_bwd<64>(p, s);

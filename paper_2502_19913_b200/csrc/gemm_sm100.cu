@@ -39,6 +39,9 @@ enum GemmEpilogue : int {
   EPI_SWIGLU_BWD = 6,  // D = dh [M, F]; R = gu [M, 2F] (128-col gate/up interleave) -> C2 = dgu [M, 2F]
   EPI_XENT = 7,        // C(bf16) = acc (logits) and C2(f32)[m, 2*(N/128)] = per 128-column block
                        // (max, sum exp(x - max)) of the bf16-rounded logits (cross-entropy partials)
+  EPI_ATTN_DELTA = 8,  // attention-output dgrad: C(bf16) = acc (dO), R = O (bf16, same layout), and per
+                       // (row, head) D = sum_c bf16(acc) * O, written with lse*log2e in the [B, H, T]
+                       // layout of the attention backward's workspace (spx_gemm_bf16_attn_delta)
 };
 
 template <int EPI>
@@ -78,6 +81,11 @@ struct GemmArgs {
               // 4 MMAs only, 5 no output stores, 6 loads only
   int tma_store;  // bf16 outputs leave the staging box by TMA store (SPX_GEMM_TMA_STORE=1) instead of st.global
   int n_major;    // problem 0's tiles walk N first (consecutive units share an A row block; pick_raster)
+  // EPI_ATTN_DELTA: lse [B, H, T] (natural log) in, delta [2][B, H, T] out (D, then lse*log2e)
+  const float* lse;
+  float* delta;
+  int delta_hd, delta_T, delta_H;
+  long long delta_total;  // B * H * T
 };
 
 // Grouped launch (EPI_F32 only, no split-K): up to GEMM_GROUP_MAX independent problems share one
@@ -538,10 +546,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // plain bf16 store, optionally + residual R (read coalesced into the staging box first);
         // EPI_XENT also folds the row's 128 rounded logits into (max, sum exp) partials
         float xm = -INFINITY, xs = 0.f;
+        float dsum = 0.f;  // EPI_ATTN_DELTA: this row's dO . O over the current head
 #pragma unroll 1
         for (int c = cb; c < cb + BN / 2 && n0 + c < args.N; c += 64) {
           box_acquire();
-          if constexpr (EPI == EPI_BF16_RESID) {
+          if constexpr (EPI == EPI_BF16_RESID || EPI == EPI_ATTN_DELTA) {
             const __nv_bfloat16* R = reinterpret_cast<const __nv_bfloat16*>(args.R);
             uint4 rv[8];
 #pragma unroll
@@ -569,6 +578,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 f[8 * j + 4] += a2.x; f[8 * j + 5] += a2.y; f[8 * j + 6] += a3.x; f[8 * j + 7] += a3.y;
               }
             }
+            if constexpr (EPI == EPI_ATTN_DELTA) {
+              // D from dO as stored (bf16-rounded), in column order
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint4 r4 = box_get(lane, 4 * q + j);
+                const uint32_t ow[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 o2 = unpack_bf16(ow[e]);
+                  const float2 d2 = unpack_bf16(pack_bf16(f[8 * j + 2 * e], f[8 * j + 2 * e + 1]));
+                  dsum = fmaf(d2.x, o2.x, dsum);
+                  dsum = fmaf(d2.y, o2.y, dsum);
+                }
+              }
+            }
             if constexpr (EPI == EPI_XENT) {
               // statistics of the values as stored (bf16), online over the 32-column chunks
               float cm = -INFINITY;
@@ -592,6 +616,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             put32(4 * q, f);
           }
           box_out(0, n0 + c, rbase);
+          if constexpr (EPI == EPI_ATTN_DELTA) {
+            if ((n0 + c + 64) % args.delta_hd == 0) {  // the head ends with this 64-column box
+              const int row = rbase + lane;
+              if (row < args.M) {
+                const int b = row / args.delta_T, t = row - b * args.delta_T;
+                const int h = (n0 + c + 64) / args.delta_hd - 1;
+                const long long idx = ((long long)b * args.delta_H + h) * args.delta_T + t;
+                args.delta[idx] = dsum;
+                args.delta[args.delta_total + idx] = args.lse[idx] * 1.4426950408889634f;
+              }
+              dsum = 0.f;
+            }
+          }
         }
         if constexpr (EPI == EPI_XENT) {
           const int row = rbase + lane;
@@ -940,6 +977,30 @@ static int pick_raster(long long M, long long N, long long K, int bn, int cg) {
   const double cost_m = (a > l2 ? a * nn : a) + b;
   const double cost_n = (b > l2 ? b * nm : b) + a;
   return cost_n < cost_m ? 1 : 0;
+}
+
+extern "C" int spx_gemm_bf16_attn_delta(const void* A, const void* B, void* dO, const void* O, int64_t ld_o,
+                                        const float* lse, float* delta_ws, int64_t M, int64_t N, int64_t K, int64_t lda,
+                                        int64_t ldb, int64_t ldc, int64_t batch, int64_t T, int64_t head_dim,
+                                        void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || batch <= 0 || T <= 0) return set_error(SPX_ERR_ARG, "gemm_attn_delta: non-positive shape");
+  if (K % 8 != 0 || lda % 8 != 0 || ldb % 8 != 0 || ldc % 8 != 0 || ld_o % 8 != 0)
+    return set_error(SPX_ERR_ARG, "gemm_attn_delta: K/lda/ldb/ldc/ld_o must be multiples of 8");
+  if (head_dim != 64 && head_dim != 128) return set_error(SPX_ERR_ARG, "gemm_attn_delta: head_dim must be 64 or 128");
+  if (N % head_dim != 0 || M != batch * T) return set_error(SPX_ERR_ARG, "gemm_attn_delta: N = H*head_dim and M = batch*T");
+  if (((uintptr_t)A | (uintptr_t)B | (uintptr_t)O) & 15) return set_error(SPX_ERR_ARG, "gemm_attn_delta: 16-byte alignment");
+  GemmArgs args{(int)M, (int)N, (int)K, dO, O, nullptr, (long long)ldc, (long long)ld_o, 0, 0.f,
+                nullptr, 0, 1, 1, nullptr};
+  args.probe = probe_mode();
+  args.tma_store = tma_store_mode();
+  args.n_major = pick_raster(M, N, K, 256, use_pair((int)M) ? 2 : 1);
+  args.lse = lse;
+  args.delta = delta_ws;
+  args.delta_hd = (int)head_dim;
+  args.delta_T = (int)T;
+  args.delta_H = (int)(N / head_dim);
+  args.delta_total = (long long)M * (N / head_dim);
+  return dispatch_256_fixed<EPI_ATTN_DELTA, false, true>(A, B, lda, ldb, args, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int spx_gemm_bf16(const void* A, const void* B, void* C, const void* R, void* C2, int64_t M, int64_t N,

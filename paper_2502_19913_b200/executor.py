@@ -44,6 +44,9 @@ from .topology import Topology
 
 BF16 = torch.bfloat16
 F32 = torch.float32
+# the attention backward's D = rowsum(dO*O) pass fused into the O-projection dgrad (head_dim 64/128);
+# SPX_ATTN_DELTA_FUSED=0 keeps the separate pass (benchmarking)
+_DELTA_FUSED = os.environ.get("SPX_ATTN_DELTA_FUSED", "1") != "0"
 
 
 @dataclass(frozen=True)
@@ -234,9 +237,15 @@ class StageProgram:
         native.rmsnorm_bwd(a.xmid, ps.w(f"l{i}.mlp_norm"), a.rstd2, sc.dxn, dy, dxm, ps.gv(f"l{i}.mlp_norm"),
                            sc.rms_ws, rows=n, d=d, stream=s)
         # attention; dq, dk leave the attention backward already un-rotated (inverse RoPE fused)
-        native.gemm(dxm, ps.w(f"l{i}.wo"), sc.do, M=n, N=od, K=d, lda=d, ldb=od, ldc=od, b_mn=True, stream=s)
+        fused_delta = hd in (64, 128) and _DELTA_FUSED
+        if fused_delta:  # D = rowsum(dO*O) in the O-projection dgrad's epilogue
+            native.gemm_attn_delta(dxm, ps.w(f"l{i}.wo"), sc.do, a.o, a.lse, sc.delta, M=n, N=od, K=d, lda=d, ldb=od,
+                                   ldc=od, ld_o=od, batch=self.b, T=self.T, head_dim=hd, stream=s)
+        else:
+            native.gemm(dxm, ps.w(f"l{i}.wo"), sc.do, M=n, N=od, K=d, lda=d, ldb=od, ldc=od, b_mn=True, stream=s)
         native.attn_bwd(a.qkv, a.o, sc.do, a.lse, sc.delta, dqkv, B=self.b, T=self.T, H=c.n_heads,
-                        Hkv=c.n_kv_heads, hd=hd, ld_qkv=qd, ld_o=od, scale=self.scale, rope_cs=sc.rope, stream=s)
+                        Hkv=c.n_kv_heads, hd=hd, ld_qkv=qd, ld_o=od, scale=self.scale, rope_cs=sc.rope,
+                        delta_ready=fused_delta, stream=s)
         # weight gradients dW = dY^T X (both operands MN-major), accumulated in fp32
         group = [
             dict(A=dgu, B=a.xn2, C=ps.gv(f"l{i}.wgu"), M=2 * f, N=d, K=n, lda=2 * f, ldb=d, ldc=d, beta=1.0),

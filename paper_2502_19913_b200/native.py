@@ -45,6 +45,9 @@ SIGNATURES: dict[str, list] = {
     "spx_gemm_set_workspace": [_P, _I64],
     "spx_gemm_f32_group": [_I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P],
     "spx_gemm_bf16_rope": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _I64, _I64, _P],
+    "spx_gemm_bf16_attn_delta": [_P, _P, _P, _P, _I64, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
+                                 _P],
+    "spx_attn_bwd_ex": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P, _I32, _P],
     "spx_rmsnorm_fwd": [_P, _P, _P, _P, _I64, _I64, _F, _P],
     "spx_rmsnorm_bwd": [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _P],
     "spx_rmsnorm_ws_floats": [_I64, _I64],
@@ -320,14 +323,30 @@ def attn_bwd_ws_floats(B: int, H: int, T: int, hd: int) -> int:
     return int(load().spx_attn_bwd_ws_floats(B, H, T, hd))
 
 
+ATTN_DELTA_READY = 1
+
+
 def attn_bwd(qkv, o, dout, lse, delta_ws, dqkv, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, rope_cs=None,
-             stream=None) -> None:
-    """delta_ws: fp32 workspace of at least attn_bwd_ws_floats(B, H, T) elements."""
+             delta_ready=False, stream=None) -> None:
+    """delta_ws: fp32 workspace of at least attn_bwd_ws_floats(B, H, T) elements; delta_ready: its D and
+    lse*log2e prefix was written by gemm_attn_delta (spx_attn_bwd_ex with SPX_ATTN_DELTA_READY)."""
     need = attn_bwd_ws_floats(B, H, T, hd)
     if delta_ws.numel() < need:
         raise ValueError(f"attn_bwd: workspace needs {need} floats, got {delta_ws.numel()}")
-    _check(load().spx_attn_bwd(_ptr(qkv), _ptr(o), _ptr(dout), _ptr(lse), _ptr(delta_ws), _ptr(dqkv), B, T, H, Hkv,
-                               hd, ld_qkv, ld_o, float(scale), _ptr(rope_cs), _stream(stream)), "spx_attn_bwd")
+    _check(load().spx_attn_bwd_ex(_ptr(qkv), _ptr(o), _ptr(dout), _ptr(lse), _ptr(delta_ws), _ptr(dqkv), B, T, H,
+                                  Hkv, hd, ld_qkv, ld_o, float(scale), _ptr(rope_cs),
+                                  ATTN_DELTA_READY if delta_ready else 0, _stream(stream)), "spx_attn_bwd_ex")
+
+
+def gemm_attn_delta(A, B, dO, O, lse, delta_ws, *, M, N, K, lda, ldb, ldc, ld_o, batch, T, head_dim,
+                    stream=None) -> None:
+    """dO = A . B (B MN-major) with the attention backward's D = rowsum(dO*O) per head and lse*log2e
+    written into delta_ws's prefix (spx_gemm_bf16_attn_delta); then attn_bwd(..., delta_ready=True)."""
+    if delta_ws.numel() < 2 * M * (N // head_dim):
+        raise ValueError("gemm_attn_delta: workspace too small")
+    _check(load().spx_gemm_bf16_attn_delta(_ptr(A), _ptr(B), _ptr(dO), _ptr(O), ld_o, _ptr(lse), _ptr(delta_ws), M, N,
+                                           K, lda, ldb, ldc, batch, T, head_dim, _stream(stream)),
+           "spx_gemm_bf16_attn_delta")
 
 
 def rmsnorm_fwd(x, g, y, rstd, *, rows, d, eps, stream=None) -> None:

@@ -441,3 +441,38 @@ def test_hop_push_ce_bit_exact():
     torch.cuda.synchronize()
     assert torch.equal(dst, src)
     assert int(flag.item()) == 3
+
+
+@pytest.mark.parametrize("b,T,H,hd,d", [(2, 384, 4, 64, 512), (1, 256, 2, 128, 256), (4, 1024, 16, 64, 1024)])
+def test_gemm_attn_delta_epilogue(b, T, H, hd, d):
+    """spx_gemm_bf16_attn_delta: dO = dY . Wo plus the attention backward's D = rowsum(dO*O) and
+    lse*log2e in the workspace prefix; the backward run with SPX_ATTN_DELTA_READY then matches the
+    backward with its own D pass."""
+    g = torch.Generator().manual_seed(b * T + hd)
+    n, od = b * T, H * hd
+    W = 3 * od
+    dy = bf(torch.randn(n, d, generator=g)).to(dev)
+    wo = bf(torch.randn(d, od, generator=g) / math.sqrt(d)).to(dev)
+    qkv = bf(torch.randn(n, W, generator=g)).to(dev)
+    o = torch.empty(n, od, dtype=torch.bfloat16, device=dev)
+    lse = torch.empty(b, H, T, device=dev)
+    kw = dict(B=b, T=T, H=H, Hkv=H, hd=hd, ld_qkv=W, ld_o=od, scale=1 / math.sqrt(hd))
+    native.attn_fwd(qkv, o, lse, **{k: v for k, v in kw.items()})
+    do_ref = torch.empty(n, od, dtype=torch.bfloat16, device=dev)
+    native.gemm(dy, wo, do_ref, M=n, N=od, K=d, lda=d, ldb=od, ldc=od, b_mn=True)
+    do = torch.empty_like(do_ref)
+    ws = torch.zeros(native.attn_bwd_ws_floats(b, H, T, hd), device=dev)
+    native.gemm_attn_delta(dy, wo, do, o, lse, ws, M=n, N=od, K=d, lda=d, ldb=od, ldc=od, ld_o=od, batch=b, T=T,
+                           head_dim=hd)
+    ws_ref = torch.zeros_like(ws)
+    d_ref, d_fused = torch.zeros_like(qkv), torch.zeros_like(qkv)
+    native.attn_bwd(qkv, o, do_ref, lse, ws_ref, d_ref, **kw)
+    native.attn_bwd(qkv, o, do, lse, ws, d_fused, delta_ready=True, **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(do, do_ref)
+    bht = b * H * T
+    exact = (do.float().view(b, T, H, hd) * o.float().view(b, T, H, hd)).sum(-1).permute(0, 2, 1).reshape(-1)
+    assert rel(ws[:bht], exact) < 1e-5
+    assert rel(ws[:bht], ws_ref[:bht]) < 1e-5
+    assert torch.equal(ws[bht:2 * bht], ws_ref[bht:2 * bht])
+    assert rel(d_fused, d_ref) < 1e-3
