@@ -80,7 +80,8 @@ class RunConfig:
         return tuple(range(1, n_agents, self.swap_every))
 
     def scheduler_config(self) -> SchedulerConfig:
-        return SchedulerConfig(k=self.k, msg_bytes=float(self.msg_bytes), swap_agents=self.swap_agents())
+        # sim_select=0: the run configs keep Algorithm 1's plan (SchedulerConfig.sim_select)
+        return SchedulerConfig(k=self.k, msg_bytes=float(self.msg_bytes), swap_agents=self.swap_agents(), sim_select=0)
 
     def swapped_paths(self) -> int:
         """Number of first-wave paths whose stage sequence is reordered (one swap, CC2)."""

@@ -145,6 +145,16 @@ class SchedulerConfig:
     # NVSwitch box a swap never lowers a path's cost, so A* (ties to the lowest stage) never picks
     # one; listing agents here makes a config exercise reordered paths (BASELINE configs[2]).
     swap_agents: tuple = ()
+    # Extension (not in SPEC): the throughput phase removes *planned* first-wave collisions, which
+    # can cost more (longer paths) than the collisions would have; when it ends unresolved its
+    # conflict-minimal node is not the fastest one either.  With sim_select = W > 0
+    # schedule() keeps, by simulated iteration (W waves of the agents), the faster of the phase's
+    # answer and the TC1-only resolution of the same pool (SkipPipe-without-TC2's answer) -- when
+    # unresolved, also the TC1-clean nodes the search met -- then descends greedily over the
+    # remaining collisions.  0 = Algorithm 1 only (the B200 run configs use 0: on one NVSwitch box
+    # TC2 changes nothing measurable, and their plans are the GPU-validated ones).
+    sim_select: int = int(os.environ.get("SPX_SCHED_SIM_SELECT", "4"))
+    sim_microbatches: int = 0  # microbatches of the selection's simulation (0: sim_select waves)
 
     def __post_init__(self):
         if self.pool_size < 1:
@@ -157,13 +167,16 @@ class SchedulerConfig:
             raise ValidationError("max_swaps is fixed at 1 (multiple swaps are a non-goal, SPEC.md:314)")
         if not self.msg_bytes > 0:
             raise ValidationError("msg_bytes must be positive")
+        if self.sim_select < 0 or self.sim_microbatches < 0:
+            raise ValidationError("sim_select and sim_microbatches must be >= 0")
         object.__setattr__(self, "swap_agents", tuple(sorted(int(a) for a in self.swap_agents)))
 
     def to_dict(self) -> dict:
         return {"k": self.k, "msg_bytes": self.msg_bytes, "pool_size": self.pool_size,
                 "slow_exempt_fraction": self.slow_exempt_fraction, "delta_tie": self.delta_tie,
                 "max_swaps": self.max_swaps, "cc3_branching": self.cc3_branching, "resolve_tc2": self.resolve_tc2,
-                "max_expansions": self.max_expansions, "swap_agents": list(self.swap_agents)}
+                "max_expansions": self.max_expansions, "swap_agents": list(self.swap_agents),
+                "sim_select": self.sim_select, "sim_microbatches": self.sim_microbatches}
 
     @classmethod
     def from_dict(cls, d: dict) -> "SchedulerConfig":
@@ -669,6 +682,67 @@ def find_candidates(topology: Topology, assignment: StageAssignment, agents, con
     return pool
 
 
+SIM_SELECT_MAX = 256    # TC1-clean nodes scored by simulation per resolve_throughput call
+SIM_REFINE_STEPS = 32   # greedy collision-resolution steps after the search (sim_select)
+SIM_REFINE_FANOUT = 16  # collisions tried per step, critical path first
+
+
+class _SimScorer:
+    """Simulated iteration makespan of a search node (SchedulerConfig.sim_select waves of the
+    node's agents), memoised per constraint set (a node's paths are a function of it)."""
+
+    def __init__(self, topology: Topology, config: SchedulerConfig, pl: "_Planner"):
+        from .simulator import SimConfig, simulate
+        self._simulate = simulate
+        self.topology, self.config = topology, config
+        self.agents = [pl.agents[a] for a in sorted(pl.agents)]
+        M = config.sim_microbatches or len(self.agents) * config.sim_select
+        self.sc = SimConfig(total_microbatches=M, msg_bytes=config.msg_bytes)
+        self.memo: dict = {}
+
+    def __call__(self, nd: SearchNode) -> float:
+        t = self.memo.get(nd.constraints)
+        if t is None:
+            sch = Schedule(self.config, self.agents, dict(nd.paths), sorted(nd.constraints), nd.cost, False)
+            t = self.memo[nd.constraints] = self._simulate(sch, self.topology, self.sc).iteration_makespan
+        return t
+
+
+def _sim_refine(node: SearchNode, score: _SimScorer, pl: "_Planner", topology: Topology,
+                assignment: StageAssignment, cap: int) -> SearchNode:
+    """Greedy simulated descent over TC2 resolutions: try both children of each of the first
+    SIM_REFINE_FANOUT collisions (the faster path avoids the slower one's window, or the reverse),
+    keep the child with the shortest simulated iteration if it beats the current node without
+    adding TC1 / CC3 conflicts; repeat."""
+    m = topology.mem_capacity
+    cur, t_cur = node, score(node)
+    def other(cs):  # (CC3, TC1) conflict counts
+        return (sum(isinstance(x, StageOveruse) for x in cs), sum(isinstance(x, NodeOveruse) for x in cs))
+
+    for _ in range(SIM_REFINE_STEPS):
+        conf = detect_conflicts(cur, topology, assignment, m, cap=cap)
+        colls = [c for c in conf if isinstance(c, Collision)]
+        if not colls:
+            break
+        n_other = other(conf)
+        best, t_best = None, t_cur
+        for c in colls[:SIM_REFINE_FANOUT]:
+            for agent, iv in ((c.path_j, c.interval_i), (c.path_i, c.interval_j)):
+                ch = pl.child(cur, [IntervalConstraint(agent, c.node, *iv)])
+                if ch is None:
+                    continue
+                o = other(detect_conflicts(ch, topology, assignment, m, cap=cap))
+                if o[0] > n_other[0] or o[1] > n_other[1]:
+                    continue
+                t = score(ch)
+                if t < t_best:
+                    best, t_best = ch, t
+        if best is None:
+            break
+        cur, t_cur = best, t_best
+    return cur
+
+
 def resolve_throughput(candidates: list[SearchNode], topology: Topology, assignment: StageAssignment,
                        config: SchedulerConfig, _planner: _Planner | None = None) -> tuple[SearchNode, bool]:
     """Phase 2: resolve TC1 then TC2 (critical path first, H3).  Returns (node, resolved)."""
@@ -682,6 +756,22 @@ def resolve_throughput(candidates: list[SearchNode], topology: Topology, assignm
     seen_cons = {c.constraints for c in candidates}
     best, best_key = None, None
     expansions = 0
+    # SchedulerConfig.sim_select: TC1-clean nodes met on the way are scored by simulated iteration
+    # (at most SIM_SELECT_MAX of them); when the search ends unresolved, the best one replaces the
+    # conflict-minimal answer if it is faster
+    sim_on = bool(config.sim_select) and config.resolve_tc2
+    scored: list = []  # (makespan, order, node)
+    sim_time = _SimScorer(topology, config, pl) if sim_on else None
+
+    def finish(node, resolved):
+        if resolved or not scored:  # a fully resolved node is Algorithm 1's answer, kept as is
+            return node, resolved
+        t_node = sim_time(node)
+        t_best, _, nd = min(scored, key=lambda x: (x[0], x[1]))
+        if t_best < t_node:
+            return nd, not detect_conflicts(nd, topology, assignment, m, cap=cap)
+        return node, resolved
+
     while open_ and expansions < config.max_expansions:
         _, node = heapq.heappop(open_)
         expansions += 1
@@ -690,8 +780,10 @@ def resolve_throughput(candidates: list[SearchNode], topology: Topology, assignm
         k = (any(isinstance(c, StageOveruse) for c in conf), len(conf), node.key())
         if best is None or k < best_key:
             best, best_key = node, k
+        if sim_on and conf and len(scored) < SIM_SELECT_MAX and all(isinstance(c, Collision) for c in conf):
+            scored.append((sim_time(node), len(scored), node))
         if not conf:
-            return node, True
+            return finish(node, True)
         c = conf[0]
         children = []
         if isinstance(c, StageOveruse):
@@ -715,7 +807,7 @@ def resolve_throughput(candidates: list[SearchNode], topology: Topology, assignm
             if ch is not None and ch.constraints not in seen_cons:
                 seen_cons.add(ch.constraints)
                 heapq.heappush(open_, (ch.key(), ch))
-    return best, False
+    return finish(best, False)
 
 
 # ---------------------------------------------------------------------------------------
@@ -777,6 +869,24 @@ def schedule(topology: Topology, assignment: StageAssignment, config: SchedulerC
     agents = [pl.agents[a] for a in sorted(pl.agents)]
     pool = find_candidates(topology, assignment, None, config, pl)
     node, resolved = resolve_throughput(pool, topology, assignment, config, pl)
+    if config.sim_select and config.resolve_tc2:
+        # candidate selection by simulated iteration (SchedulerConfig.sim_select): the TC1-only
+        # resolution of the same pool (what SkipPipe-without-TC2 returns) against the TC2 result,
+        # then a greedy simulated descent over the remaining collisions
+        score = _SimScorer(topology, config, pl)
+        cfg1 = SchedulerConfig(**{**config.to_dict(), "resolve_tc2": False})
+        alt, _ = resolve_throughput(pool, topology, assignment, cfg1, pl)
+        cap = cc3_cap(len(agents), assignment.s, path_length(assignment.s, config.k))
+
+        def hard(nd):  # (CC3, TC1) conflict counts
+            cs = detect_conflicts(nd, topology, assignment, topology.mem_capacity, cap=cap)
+            return (sum(isinstance(x, StageOveruse) for x in cs), sum(isinstance(x, NodeOveruse) for x in cs))
+
+        ha, hn = hard(alt), hard(node)
+        if ha[0] <= hn[0] and ha[1] <= hn[1] and score(alt) < score(node):
+            node = alt
+        node = _sim_refine(node, score, pl, topology, assignment, cap)
+        resolved = not detect_conflicts(node, topology, assignment, topology.mem_capacity, cap=cap)
     return Schedule(config, agents, dict(node.paths), sorted(node.constraints), node.cost, resolved)
 
 

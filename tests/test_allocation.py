@@ -127,10 +127,11 @@ def test_compensate_kats():
 
 
 def test_throughput_ordering_sampled():
-    """SPEC.md:536 (reduced for the CPU suite: 6 sampled 9-node topologies, s=4, k=25): SkipPipe
-    beats DT-FM-skip on every run and compensated DT-FM full by >= 30 % on average; against
-    SkipPipe without the throughput phase the mean is not worse (the spec's >= 5 % TC2 gain is not
-    reached at this size -- DESIGN.md §6)."""
+    """SPEC.md:536 (reduced for the CPU suite: 6 sampled 9-node topologies, s=4, k=25; the full
+    50-topology runs per profile are tools/acceptance5.py, profiles/r02_acceptance5_*.jsonl):
+    SkipPipe <= SkipPipe-without-TC2 <= DT-FM-skip on every run (the scheduler's final selection
+    simulates the same M, SchedulerConfig.sim_microbatches) and compensated DT-FM full is >= 30 %
+    slower on average."""
     import math
 
     from paper_2502_19913_b200 import scheduler as S
@@ -144,21 +145,23 @@ def test_throughput_ordering_sampled():
     for seed in range(6):
         T = sample_topology(TopologyProfile(regions=3, nodes_per_region=3, seed=seed))
         A = allocate(T, 4, 25, msg, GAConfig(population=32, generations=40, seed=seed))
-        cfg = S.SchedulerConfig(k=25, msg_bytes=msg)
+        n_sp, n_fa = len(S.make_agents(A, T.mem_capacity)), 2 * T.mem_capacity
+        M = n_sp * n_fa // math.gcd(n_sp, n_fa) * 2
+        cfg = S.SchedulerConfig(k=25, msg_bytes=msg, sim_microbatches=M)
         sp, nt, ds = S.schedule(T, A, cfg), skippipe_no_tc2(T, A, cfg), dtfm_skip(T, A, cfg)
         T8 = T.restrict(list(range(8)))
         full = dtfm_full(T8, 4, msg_bytes=msg)
-        M = len(sp.agents) * len(full.agents) // math.gcd(len(sp.agents), len(full.agents)) * 2
+        assert len(full.agents) == n_fa
         sc = SimConfig(total_microbatches=M, msg_bytes=msg)
         t_sp = simulate(sp, T, sc).iteration_makespan
+        t_nt = simulate(nt, T, sc).iteration_makespan
         t_ds = simulate(ds, T, sc).iteration_makespan
-        assert t_sp < t_ds
+        assert t_sp <= t_nt <= t_ds
         sp_all.append(t_sp)
-        nt_all.append(simulate(nt, T, sc).iteration_makespan)
+        nt_all.append(t_nt)
         full_all.append(compensate(simulate(full, T8, sc).iteration_makespan, 8, 9))
     mean = lambda xs: sum(xs) / len(xs)  # noqa: E731
     assert mean(full_all) / mean(sp_all) >= 1.30
-    assert mean(sp_all) <= 1.01 * mean(nt_all)
 
 
 def test_dtfm_full_matching_equals_bruteforce():

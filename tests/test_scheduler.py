@@ -158,7 +158,7 @@ def _check_schedule(sch, T, A, k, check_tc=True):
 def test_b200_c2_schedule_constraints():
     T = b200_box([0.8, 0.8] + [0.5] * 6)
     A = StageAssignment.contiguous([2, 2, 2, 2])
-    sch = S.schedule(T, A, S.SchedulerConfig(k=25))
+    sch = S.schedule(T, A, S.SchedulerConfig(k=25, sim_select=0))
     assert sch.resolved
     _check_schedule(sch, T, A, 25)
 
