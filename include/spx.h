@@ -163,6 +163,11 @@ int spx_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
 /* spx_attn_bwd with flags: SPX_ATTN_DELTA_READY = the first 2*B*H*T floats of delta_ws already hold
  * D = rowsum(dO*O) and lse*log2e (written by spx_gemm_bf16_attn_delta), so no D pass runs. */
 #define SPX_ATTN_DELTA_READY 1
+/* SPX_ATTN_WS_EX: delta_ws holds spx_attn_bwd_ws_floats_ex(B, H, Hkv, T, hd) floats; with GQA and fewer
+ * (batch, kv head, 128-key block) items than SMs the dK/dV pass then splits each group over several
+ * work items (fp32 partials, summed in a fixed order: still deterministic). */
+#define SPX_ATTN_WS_EX 2
+int64_t spx_attn_bwd_ws_floats_ex(int64_t B, int64_t H, int64_t Hkv, int64_t T, int64_t hd);
 int spx_attn_bwd_ex(const void* qkv, const void* o, const void* dout, const float* lse, float* delta_ws, void* dqkv,
                     int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv, int64_t ld_o, float scale,
                     const float* rope_cos_sin, int32_t flags, void* stream);

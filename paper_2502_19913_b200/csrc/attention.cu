@@ -139,6 +139,7 @@ struct Params {
   int B, T, H, Hkv;
   float scale;
   int delta_ready;      // bwd: the workspace already holds D and lse*log2e (spx_gemm_bf16_attn_delta)
+  int ws_ex;            // bwd: the workspace is sized by spx_attn_bwd_ws_floats_ex (GQA split allowed)
 };
 
 // ----------------------------------------------------------------------------------------
@@ -600,7 +601,7 @@ static int run_bwd(const Params& p, cudaStream_t s) {
   }
   if ((HD == 64 || HD == 128) && p.T % 128 == 0 && !attn_use_legacy())
     return attn_bwd_tcgen05(p.qkv, p.dout, p.lse, p.delta, p.out, p.B, p.T, p.H, p.Hkv, HD, p.ld, p.ldo, p.scale,
-                            p.rope_cs, s);
+                            p.rope_cs, p.ws_ex && attn_gqa_split(p.B, p.H, p.Hkv, p.T, HD), s);
   {
     const int smem = (2 * BK + 2 * BQI) * LD * 2 + 2 * BQI * 4;
     auto k = attn_bwd_dkdv_kernel<HD>;
@@ -670,6 +671,17 @@ bool attn_use_legacy() {
   }();
   return legacy;
 }
+
+// SPX_ATTN_GQA_SPLIT=0 disables the split (A/B comparisons)
+bool attn_gqa_split(int64_t B, int64_t H, int64_t Hkv, int64_t T, int64_t hd) {
+  static const bool enabled = [] {
+    const char* e = getenv("SPX_ATTN_GQA_SPLIT");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!enabled || H <= Hkv || Hkv <= 0 || H % Hkv || (hd != 64 && hd != 128) || T % 128 || attn_use_legacy())
+    return false;
+  return B * Hkv * (T / 128) < num_sms();
+}
 }  // namespace spx
 
 extern "C" int64_t spx_attn_bwd_ws_floats(int64_t B, int64_t H, int64_t T, int64_t hd) {
@@ -678,6 +690,12 @@ extern "C" int64_t spx_attn_bwd_ws_floats(int64_t B, int64_t H, int64_t T, int64
     const int64_t nqb = T / 128;
     n += B * H * (nqb * (nqb + 1) / 2) * 128 * 128 / 2;  // dS^T tiles, bf16
   }
+  return n;
+}
+
+extern "C" int64_t spx_attn_bwd_ws_floats_ex(int64_t B, int64_t H, int64_t Hkv, int64_t T, int64_t hd) {
+  int64_t n = spx_attn_bwd_ws_floats(B, H, T, hd);
+  if (attn_gqa_split(B, H, Hkv, T, hd)) n += B * H * (T / 128) * 2 * hd * 128;  // dV/dK partials, fp32
   return n;
 }
 
@@ -691,7 +709,7 @@ extern "C" int spx_attn_bwd(const void* qkv, const void* o, const void* dout, co
 extern "C" int spx_attn_bwd_ex(const void* qkv, const void* o, const void* dout, const float* lse, float* delta_ws,
                                void* dqkv, int64_t B, int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv,
                                int64_t ld_o, float scale, const float* rope_cos_sin, int32_t flags, void* stream) {
-  if (flags & ~SPX_ATTN_DELTA_READY) return set_error(SPX_ERR_ARG, "attn_bwd: unknown flags");
+  if (flags & ~(SPX_ATTN_DELTA_READY | SPX_ATTN_WS_EX)) return set_error(SPX_ERR_ARG, "attn_bwd: unknown flags");
   int rc = attn::check_args(B, T, H, Hkv, hd);
   if (rc) return rc;
   if (ld_o % 8 != 0 || (((uintptr_t)o | (uintptr_t)dout) & 15))
@@ -709,6 +727,7 @@ extern "C" int spx_attn_bwd_ex(const void* qkv, const void* o, const void* dout,
   p.B = (int)B; p.T = (int)T; p.H = (int)H; p.Hkv = (int)Hkv;
   p.scale = scale;
   p.delta_ready = (flags & SPX_ATTN_DELTA_READY) ? 1 : 0;
+  p.ws_ex = (flags & SPX_ATTN_WS_EX) ? 1 : 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (hd == 48) return attn::run_bwd<48>(p, s);
   if (hd == 64) return attn::run_bwd<64>(p, s);

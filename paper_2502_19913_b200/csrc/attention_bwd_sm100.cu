@@ -86,6 +86,8 @@ struct BwdParams {
   long long ld;
   int B, T, H, Hkv;
   float scale;
+  int gsplit;            // dK/dV items per (batch, kv head, key block): 1, or the GQA group size
+  float* part;           // gsplit > 1: fp32 dV/dK partials [B*Hkv*nqb][gsplit][2][hd][128] (workspace)
 };
 
 // store one 128-column bf16 tile row of P^T / dS^T / dS (K-major SWIZZLE_128B, two 64-col atoms)
@@ -200,13 +202,17 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = p.T / BLK;
   const int group = p.H / p.Hkv;
-  const int BHk = p.B * p.Hkv;
+  const int hpi = group / p.gsplit;  // query heads per item (GQA split: p.gsplit items per key block)
+  const int BHk = p.B * p.Hkv * p.gsplit;
   const int n_items = nqb * BHk;
-  // item w: key block jb = w / (B*Hkv) (early key blocks see the most query blocks: heavy first)
-  auto item = [&](int w, int& b, int& kvh, int& jb) {
+  // item w: key block jb = w / (B*Hkv*gsplit) (early key blocks see the most query blocks: heavy
+  // first), then (batch, kv head, head subset gs)
+  auto item = [&](int w, int& b, int& kvh, int& jb, int& gs) {
     jb = w / BHk;
-    b = (w % BHk) / p.Hkv;
-    kvh = (w % BHk) % p.Hkv;
+    const int bk = (w % BHk) / p.gsplit;
+    gs = (w % BHk) % p.gsplit;
+    b = bk / p.Hkv;
+    kvh = bk % p.Hkv;
   };
 
   if (threadIdx.x == 0) {
@@ -246,8 +252,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     int gi = 0, n = 0;
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
       if (w >= n_items) continue;
-      int b, kvh, jb;
-      item(w, b, kvh, jb);
+      int b, kvh, jb, gs;
+      item(w, b, kvh, jb, gs);
       const int row0 = b * p.T, nq = nqb - jb;
       const int kv = n % KVS;
       mbar_wait(&kv_empty[kv], ((n / KVS) & 1) ^ 1);
@@ -258,9 +264,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma_load_2d(smem + L::OFF_V + kv * L::TILE + a * ATOM, &tmQKV, &kv_full[kv],
                     (p.H + p.Hkv + kvh) * HD + 64 * a, row0 + jb * BLK);
       }
-      for (int it = 0; it < group * nq; ++it, ++gi) {
+      for (int it = 0; it < hpi * nq; ++it, ++gi) {
         const int s = gi % NST;
-        const int h = kvh * group + it / nq, qb = jb + it % nq;
+        const int h = kvh * group + gs * hpi + it / nq, qb = jb + it % nq;
         mbar_wait(&empty[s], ((gi / NST) & 1) ^ 1);
         FAB_PROBE(0, gi);
         mbar_expect_tx(&full[s], 2 * L::TILE + 1024);
@@ -301,9 +307,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     bool issued = false;  // S/dP of step gi already issued (look-ahead from the previous step)
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
       if (w >= n_items) continue;
-      int b, kvh, jb;
-      item(w, b, kvh, jb);
-      const int n_it = group * (nqb - jb);
+      int b, kvh, jb, gs;
+      item(w, b, kvh, jb, gs);
+      const int n_it = hpi * (nqb - jb);
       const int kv = n % KVS;
       // the CTA's next item (rounds past the last valid one hold none)
       const int w_next = snake(k + 1, blockIdx.x, gridDim.x);
@@ -363,11 +369,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int ntri = nqb * (nqb + 1) / 2;
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
       if (w >= n_items) continue;
-      int b, kvh, jb;
-      item(w, b, kvh, jb);
-      const int nq = nqb - jb, n_it = group * nq;
+      int b, kvh, jb, gs;
+      item(w, b, kvh, jb, gs);
+      const int nq = nqb - jb, n_it = hpi * nq;
       for (int it = 0; it < n_it; ++it, ++gi) {
-        const int h = kvh * group + it / nq, qb = jb + it % nq;
+        const int h = kvh * group + gs * hpi + it / nq, qb = jb + it % nq;
         mbar_wait(p_ready, gi & 1);
         const int row = ((b * p.H + h) * ntri + qb * (qb + 1) / 2 + jb) * BLK;
         for (int a = 0; a < 2; ++a) tma_store_2d(&tmDS, smem + L::OFF_DST + a * ATOM, 64 * a, row);
@@ -388,9 +394,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     int gi = 0;
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x)) {
       if (w >= n_items) continue;
-      int b, kvh, jb;
-      item(w, b, kvh, jb);
-      const int nq = nqb - jb, n_it = group * nq;
+      int b, kvh, jb, gs;
+      item(w, b, kvh, jb, gs);
+      const int nq = nqb - jb, n_it = hpi * nq;
       for (int it = 0; it < n_it; ++it, ++gi) {
         const int s = gi % NST;
         const bool diag = (it % nq) == 0;  // query block == key block
@@ -479,6 +485,26 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(mma2_done, (gi - 1) & 1);
       mbar_wait(ds_read, (gi - 1) & 1);
       tc_fence_after();
+      if (p.gsplit > 1) {
+        // GQA split: this item's fp32 dV / dK partial (raw: unscaled, no RoPE) to the workspace,
+        // [tile][gs][dV|dK][column][row] so a warp's 32 rows are one 128-byte store per column;
+        // dkdv_reduce_kernel sums the partials in gs order
+        const size_t tile = ((size_t)(b * p.Hkv + kvh) * nqb + jb) * p.gsplit + gs;
+        float* dst = p.part + (tile * 2 + half) * HD * BLK;
+        const uint32_t ta = lane_base + (half == 0 ? TM_DV : TM_DK);
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(ta + c, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) dst[(size_t)(c + j) * BLK + r] = __uint_as_float(v[j]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_free);
+        continue;
+      }
       const int key = jb * BLK + r;
       uint8_t* box0 = smem + (L::PT_TMEM ? L::OFF_DST : L::OFF_PT) + half * ATOM + quad * 4096;
       uint8_t* box1 = smem + L::OFF_DST + half * ATOM + quad * 4096;
@@ -654,6 +680,60 @@ __global__ void __launch_bounds__(DqmSmem<HD>::THREADS, 1)
   if (warp == 2) tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// GQA split: dK / dV of one (batch, kv head, key block) tile = the sum of its gsplit fp32 partials
+// in gs order (deterministic), scaled (dK), inverse RoPE (dK, when a table is given), bf16 into
+// dQKV.  Block = (tile, dV|dK, 16 rotation pairs (c, c + hd/2)), thread = key row: every partial
+// load is coalesced along the rows and all of a thread's loads are in flight together.
+template <int HD>
+__global__ void __launch_bounds__(BLK) dkdv_reduce_kernel(const BwdParams p) {
+  pdl_wait();
+  constexpr int NP = 16;  // pairs per block
+  const int nqb = p.T / BLK;
+  const int tile = blockIdx.x, which = blockIdx.y, j0 = blockIdx.z * NP;  // which: 0 = dV, 1 = dK
+  const int jb = tile % nqb, kvh = (tile / nqb) % p.Hkv, b = tile / (nqb * p.Hkv);
+  const int r = threadIdx.x, pos = jb * BLK + r;
+  const float* src = p.part + (size_t)tile * p.gsplit * 2 * HD * BLK + (size_t)which * HD * BLK + r;
+  const size_t gstride = (size_t)2 * HD * BLK;
+  float x1[NP], x2[NP];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) x1[j] = x2[j] = 0.f;
+  for (int g = 0; g < p.gsplit; ++g) {
+    const float* sg = src + g * gstride;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      x1[j] += sg[(size_t)(j0 + j) * BLK];
+      x2[j] += sg[(size_t)(HD / 2 + j0 + j) * BLK];
+    }
+  }
+  const float scale = which == 1 ? p.scale : 1.f;
+  float o1[NP], o2[NP];
+  if (which == 1 && p.rope_cs) {
+    const float2* cs = reinterpret_cast<const float2*>(p.rope_cs);
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      const float a = x1[j] * scale, c = x2[j] * scale;
+      const float2 w = cs[(size_t)(j0 + j) * p.T + pos];
+      o1[j] = a * w.x + c * w.y;
+      o2[j] = c * w.x - a * w.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      o1[j] = x1[j] * scale;
+      o2[j] = x2[j] * scale;
+    }
+  }
+  __nv_bfloat16* dst = p.dqkv + (size_t)(b * p.T + pos) * p.ld + (which == 0 ? p.H + p.Hkv + kvh : p.H + kvh) * HD;
+#pragma unroll
+  for (int j = 0; j < NP; j += 8) {
+    *reinterpret_cast<uint4*>(dst + j0 + j) = make_uint4(pack_bf16(o1[j], o1[j + 1]), pack_bf16(o1[j + 2], o1[j + 3]),
+                                                         pack_bf16(o1[j + 4], o1[j + 5]), pack_bf16(o1[j + 6], o1[j + 7]));
+    *reinterpret_cast<uint4*>(dst + HD / 2 + j0 + j) =
+        make_uint4(pack_bf16(o2[j], o2[j + 1]), pack_bf16(o2[j + 2], o2[j + 3]), pack_bf16(o2[j + 4], o2[j + 5]),
+                   pack_bf16(o2[j + 6], o2[j + 7]));
+  }
+}
+
 static int make_map(CUtensorMap* m, const void* ptr, long long ld, long long rows, int box_rows = 128) {
   // 2D bf16 [rows][ld], 64 x box_rows boxes, SWIZZLE_128B
   auto encode = get_tensor_map_encoder();
@@ -693,11 +773,16 @@ static int launch(const void* qkv, const void* dout, long long ld_o, const BwdPa
   const long long ntiles = (long long)p.B * p.H * (nqb * (nqb + 1) / 2);
   rc = make_map(&mds, p.ds, BLK, ntiles * BLK);
   if (rc) return rc;
-  const int items_kv = nqb * p.Hkv * p.B, items_q = nqb * p.H * p.B;
+  const int items_kv = nqb * p.Hkv * p.B * p.gsplit, items_q = nqb * p.H * p.B;
   const int g1 = items_kv < num_sms() ? items_kv : num_sms(), g2 = items_q < num_sms() ? items_q : num_sms();
   spx_launch_check(launch_k(attn_bwd_dkdv_tc_kernel<HD>, dim3(g1), dim3(THREADS), DkdvSmem<HD>::BYTES, s, mq, md, mds, mo, p));
   rc = check_launch("attn_bwd_dkdv_tc_kernel");
   if (rc) return rc;
+  if (p.gsplit > 1) {
+    spx_launch_check(launch_k(dkdv_reduce_kernel<HD>, dim3(p.B * p.Hkv * nqb, 2, HD / 32), dim3(BLK), 0, s, p));
+    rc = check_launch("dkdv_reduce_kernel");
+    if (rc) return rc;
+  }
   spx_launch_check(launch_k(attn_bwd_dq_mma_kernel<HD>, dim3(g2), dim3(DqmSmem<HD>::THREADS), DqmSmem<HD>::BYTES, s,
                             mq, mds, mo, p));
   return check_launch("attn_bwd_dq_mma_kernel");
@@ -708,11 +793,13 @@ static int launch(const void* qkv, const void* dout, long long ld_o, const BwdPa
 // used by spx_attn_bwd (attention.cu) for head_dim 64/128, T % 128 == 0; delta must be computed
 int attn_bwd_tcgen05(const void* qkv, const void* dout, const float* lse, const float* delta, void* dqkv, int64_t B,
                      int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv, int64_t ld_o, float scale,
-                     const float* rope_cs, cudaStream_t s) {
-  // workspace: delta [BHT] | lse*log2e [BHT] | dS^T tiles (bf16)
+                     const float* rope_cs, bool gqa_split, cudaStream_t s) {
+  // workspace: delta [BHT] | lse*log2e [BHT] | dS^T tiles (bf16) | GQA-split dV/dK partials (fp32)
   __nv_bfloat16* ds = reinterpret_cast<__nv_bfloat16*>(const_cast<float*>(delta) + 2 * B * H * T);
+  const int64_t nqb = T / fab::BLK;
+  float* part = const_cast<float*>(delta) + 2 * B * H * T + B * H * (nqb * (nqb + 1) / 2) * fab::BLK * fab::BLK / 2;
   fab::BwdParams p{reinterpret_cast<__nv_bfloat16*>(dqkv), lse, delta, rope_cs, ds, (long long)ld_qkv,
-                   (int)B, (int)T, (int)H, (int)Hkv, scale};
+                   (int)B, (int)T, (int)H, (int)Hkv, scale, gqa_split ? (int)(H / Hkv) : 1, part};
   if (hd == 64) return fab::launch<64>(qkv, dout, ld_o, p, s);
   return fab::launch<128>(qkv, dout, ld_o, p, s);
 }

@@ -77,7 +77,10 @@ int attn_fwd_tcgen05(const void* qkv, void* o, float* lse, int64_t B, int64_t T,
                      int64_t ld_qkv, int64_t ld_o, float scale, cudaStream_t s);
 int attn_bwd_tcgen05(const void* qkv, const void* dout, const float* lse, const float* delta, void* dqkv, int64_t B,
                      int64_t T, int64_t H, int64_t Hkv, int64_t hd, int64_t ld_qkv, int64_t ld_o, float scale,
-                     const float* rope_cs, cudaStream_t s);
+                     const float* rope_cs, bool gqa_split, cudaStream_t s);
 bool attn_use_legacy();
+// the tcgen05 backward splits each GQA group over several dK/dV work items (fp32 partials in the
+// workspace, summed by a reduce pass) when it has fewer (batch, kv head, key block) items than SMs
+bool attn_gqa_split(int64_t B, int64_t H, int64_t Hkv, int64_t T, int64_t hd);
 
 }  // namespace spx

@@ -172,7 +172,8 @@ class Scratch:
         self.dgu2 = [torch.empty(n, 2 * f, **e) for _ in range(2)]
         self.do = torch.empty(n, cfg.n_heads * cfg.head_dim, **e)
         self.dqkv2 = [torch.empty(n, cfg.qkv_dim, **e) for _ in range(2)]
-        self.delta = torch.empty(native.attn_bwd_ws_floats(b, cfg.n_heads, T, cfg.head_dim), dtype=F32, device=device)
+        self.delta = torch.empty(native.attn_bwd_ws_floats(b, cfg.n_heads, T, cfg.head_dim, cfg.n_kv_heads), dtype=F32,
+                                 device=device)
         self.rms_ws = torch.empty(native.rmsnorm_ws_floats(n, d), dtype=F32, device=device)
         self.rope = rope_cos_sin(T, cfg.head_dim, cfg.rope_theta).to(device)
         if with_head:

@@ -41,6 +41,7 @@ SIGNATURES: dict[str, list] = {
     "spx_gemm_bf16": [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _F, _P],
     "spx_attn_fwd": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P],
     "spx_attn_bwd_ws_floats": [_I64, _I64, _I64, _I64],
+    "spx_attn_bwd_ws_floats_ex": [_I64, _I64, _I64, _I64, _I64],
     "spx_attn_bwd": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _P, _P],
     "spx_gemm_set_workspace": [_P, _I64],
     "spx_gemm_f32_group": [_I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P],
@@ -69,6 +70,7 @@ SIGNATURES: dict[str, list] = {
 }
 _RESTYPE = {"spx_last_error": ctypes.c_char_p, "spx_rmsnorm_ws_floats": ctypes.c_int64, "spx_launch_count": ctypes.c_int64,
             "spx_attn_bwd_ws_floats": ctypes.c_int64,
+            "spx_attn_bwd_ws_floats_ex": ctypes.c_int64,
             "spx_sumsq_ws_floats": ctypes.c_int64}
 
 EPI_BF16, EPI_BF16_RESID, EPI_F32, EPI_SWIGLU = 0, 1, 2, 3
@@ -318,12 +320,16 @@ def attn_fwd(qkv, o, lse, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, stream=None)
                                _stream(stream)), "spx_attn_fwd")
 
 
-def attn_bwd_ws_floats(B: int, H: int, T: int, hd: int) -> int:
-    """Workspace of spx_attn_bwd in floats (spx_attn_bwd_ws_floats)."""
+def attn_bwd_ws_floats(B: int, H: int, T: int, hd: int, Hkv: int | None = None) -> int:
+    """Workspace of spx_attn_bwd in floats (spx_attn_bwd_ws_floats); with Hkv, the size that also
+    allows the GQA-split dK/dV pass (spx_attn_bwd_ws_floats_ex)."""
+    if Hkv is not None:
+        return int(load().spx_attn_bwd_ws_floats_ex(B, H, Hkv, T, hd))
     return int(load().spx_attn_bwd_ws_floats(B, H, T, hd))
 
 
 ATTN_DELTA_READY = 1
+ATTN_WS_EX = 2
 
 
 def attn_bwd(qkv, o, dout, lse, delta_ws, dqkv, *, B, T, H, Hkv, hd, ld_qkv, ld_o, scale, rope_cs=None,
@@ -333,9 +339,12 @@ def attn_bwd(qkv, o, dout, lse, delta_ws, dqkv, *, B, T, H, Hkv, hd, ld_qkv, ld_
     need = attn_bwd_ws_floats(B, H, T, hd)
     if delta_ws.numel() < need:
         raise ValueError(f"attn_bwd: workspace needs {need} floats, got {delta_ws.numel()}")
+    flags = ATTN_DELTA_READY if delta_ready else 0
+    if delta_ws.numel() >= attn_bwd_ws_floats(B, H, T, hd, Hkv):
+        flags |= ATTN_WS_EX  # room for the GQA-split dK/dV partials
     _check(load().spx_attn_bwd_ex(_ptr(qkv), _ptr(o), _ptr(dout), _ptr(lse), _ptr(delta_ws), _ptr(dqkv), B, T, H,
-                                  Hkv, hd, ld_qkv, ld_o, float(scale), _ptr(rope_cs),
-                                  ATTN_DELTA_READY if delta_ready else 0, _stream(stream)), "spx_attn_bwd_ex")
+                                  Hkv, hd, ld_qkv, ld_o, float(scale), _ptr(rope_cs), flags, _stream(stream)),
+           "spx_attn_bwd_ex")
 
 
 def gemm_attn_delta(A, B, dO, O, lse, delta_ws, *, M, N, K, lda, ldb, ldc, ld_o, batch, T, head_dim,

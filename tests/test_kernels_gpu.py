@@ -58,7 +58,8 @@ def test_attention_fwd_bwd(B, T, H, Hkv, hd):
     lse = torch.empty(B, H, T, dtype=torch.float32, device=dev)
     native.attn_fwd(qkv, o, lse, B=B, T=T, H=H, Hkv=Hkv, hd=hd, ld_qkv=W, ld_o=H * hd, scale=scale)
     dqkv = torch.zeros_like(qkv)
-    delta = torch.empty(native.attn_bwd_ws_floats(B, H, T, hd), dtype=torch.float32, device=dev)
+    # sized with Hkv: GQA shapes with few kv-head tiles take the split dK/dV pass
+    delta = torch.empty(native.attn_bwd_ws_floats(B, H, T, hd, Hkv), dtype=torch.float32, device=dev)
     native.attn_bwd(qkv, o, do, lse, delta, dqkv, B=B, T=T, H=H, Hkv=Hkv, hd=hd, ld_qkv=W, ld_o=H * hd, scale=scale)
     torch.cuda.synchronize()
 
@@ -476,3 +477,31 @@ def test_gemm_attn_delta_epilogue(b, T, H, hd, d):
     assert rel(ws[:bht], ws_ref[:bht]) < 1e-5
     assert torch.equal(ws[bht:2 * bht], ws_ref[bht:2 * bht])
     assert rel(d_fused, d_ref) < 1e-3
+
+
+@pytest.mark.parametrize("B,T,H,Hkv,hd", [(1, 1024, 32, 8, 128), (1, 512, 8, 2, 64), (2, 256, 8, 2, 128)])
+def test_attention_bwd_gqa_split(B, T, H, Hkv, hd):
+    """GQA backward with fewer (batch, kv head, key block) items than SMs: the split dK/dV pass
+    (workspace sized by attn_bwd_ws_floats(..., Hkv), fp32 partials summed in a fixed order) agrees
+    with the unsplit pass, is deterministic, and keeps dQ bit-identical; inverse RoPE included."""
+    assert native.attn_bwd_ws_floats(B, H, T, hd, Hkv) > native.attn_bwd_ws_floats(B, H, T, hd)
+    g = torch.Generator().manual_seed(T + H + hd)
+    W = (H + 2 * Hkv) * hd
+    qkv = bf(torch.randn(B * T, W, generator=g)).to(dev)
+    do = bf(torch.randn(B * T, H * hd, generator=g)).to(dev)
+    cs = rope_table(T, hd).to(dev)
+    o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device=dev)
+    lse = torch.empty(B, H, T, device=dev)
+    kw = dict(B=B, T=T, H=H, Hkv=Hkv, hd=hd, ld_qkv=W, ld_o=H * hd, scale=1 / math.sqrt(hd), rope_cs=cs)
+    native.attn_fwd(qkv, o, lse, **{k: v for k, v in kw.items() if k != "rope_cs"})
+    outs = []
+    for hkv in (None, Hkv, Hkv):
+        ws = torch.empty(native.attn_bwd_ws_floats(B, H, T, hd, hkv), device=dev)
+        d = torch.zeros_like(qkv)
+        native.attn_bwd(qkv, o, do, lse, ws, d, **kw)
+        outs.append(d)
+    torch.cuda.synchronize()
+    plain, split, split2 = outs
+    assert torch.equal(split, split2)
+    assert torch.equal(split[:, :H * hd], plain[:, :H * hd])  # dQ untouched by the split
+    assert rel(split[:, H * hd:], plain[:, H * hd:]) < 2e-3

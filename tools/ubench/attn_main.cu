@@ -29,7 +29,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&o, n * H * hd * 2);
   cudaMalloc(&dout, n * H * hd * 2);
   cudaMalloc(&lse, (size_t)B * H * T * 4);
-  const long long wsf = spx_attn_bwd_ws_floats(B, H, T, hd);
+  const long long wsf = spx_attn_bwd_ws_floats_ex(B, H, Hkv, T, hd);
   cudaMalloc(&ws, wsf * 4);
   cudaMalloc(&cs, (size_t)hd * T * 4);
   cudaMemset(cs, 0, (size_t)hd * T * 4);
@@ -40,7 +40,7 @@ int main(int argc, char** argv) {
   cudaStreamCreate(&s);
   auto fwd = [&] { return spx_attn_fwd(qkv, o, lse, B, T, H, Hkv, hd, W, H * hd, sc, s); };
   auto bwd = [&] {
-    return spx_attn_bwd(qkv, o, dout, lse, ws, dqkv, B, T, H, Hkv, hd, W, H * hd, sc, nullptr, s);
+    return spx_attn_bwd_ex(qkv, o, dout, lse, ws, dqkv, B, T, H, Hkv, hd, W, H * hd, sc, nullptr, SPX_ATTN_WS_EX, s);
   };
   double fl = 4.0 * B * H * (double)T * T / 2 * hd;
   for (int k = 0; k < 2; ++k) {
