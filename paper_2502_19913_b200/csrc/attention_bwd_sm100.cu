@@ -29,6 +29,9 @@ namespace fab {
 #ifndef SPX_FAB_KVS64
 #define SPX_FAB_KVS64 2
 #endif
+#ifndef SPX_FAB_PT128
+#define SPX_FAB_PT128 1
+#endif
 #ifndef SPX_FAB_PT_TMEM
 #define SPX_FAB_PT_TMEM 1
 #endif
@@ -68,6 +71,7 @@ SPX_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
       "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+SPX_DEVICE void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 SPX_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 SPX_DEVICE void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -107,9 +111,11 @@ SPX_DEVICE void put_row8p(uint8_t* tile, int r, int c8, const uint32_t* v) {
 // write per box instead of 32 scattered rows per st.global
 template <int HD>
 SPX_DEVICE void stage_grad_row(uint32_t taddr, uint8_t* box0, uint8_t* box1, int row, float scale, const float* cs,
-                               int T, int pos) {
+                               int T, int pos, int only = -1) {
+  // only >= 0: write just the columns of box `only` (into box0); the others are skipped
   auto put = [&](int col, const float* v) {  // 8 columns starting at col (multiple of 8)
-    uint8_t* box = col < 64 ? box0 : box1;
+    if (only >= 0 && (col >> 6) != only) return;
+    uint8_t* box = (only >= 0 || col < 64) ? box0 : box1;
     const int chunk = (col & 63) >> 3;
     *reinterpret_cast<uint4*>(box + row * 128 + ((chunk ^ (row & 7)) << 4)) =
         make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
@@ -156,7 +162,11 @@ SPX_DEVICE void stage_grad_row(uint32_t taddr, uint8_t* box0, uint8_t* box1, int
 // ------------------------------------------------------------------------------------------
 template <int HD>
 struct DkdvSmem {
-  static constexpr int NST = HD == 64 ? SPX_FAB_NST64 : 1;      // Q/dO ring depth
+  // hd=128 (ALIAS): P^T / dS^T are written into the TMEM columns of S^T / dP^T once those are read
+  // (TMEM holds S^T, dP^T, dV, dK = 512 columns, nothing spare), which frees the P^T smem tile for a
+  // second Q/dO stage: the next step's loads then overlap this step
+  static constexpr bool ALIAS = HD == 128 && SPX_FAB_PT128;
+  static constexpr int NST = HD == 64 ? SPX_FAB_NST64 : (ALIAS ? 2 : 1);  // Q/dO ring depth
   static constexpr int TILE = (HD / 64) * ATOM;     // 128 x HD bf16
   // hd=64: K/V double-buffered across items, so the next item's K/V load and its first S/dP
   // MMAs overlap the current item's last step and dV/dK epilogue (hd=128 has no smem for it)
@@ -167,13 +177,14 @@ struct DkdvSmem {
   static constexpr int OFF_DO = OFF_Q + NST * TILE; // [NST]
   // hd=64: P^T and dS^T are A operands straight from TMEM (TS MMAs), only dS^T is also staged in
   // shared memory for its TMA store; hd=128 has no spare TMEM columns and stages both in smem
-  static constexpr bool PT_TMEM = HD == 64 && SPX_FAB_PT_TMEM;
+  static constexpr bool PT_TMEM = (HD == 64 && SPX_FAB_PT_TMEM) || ALIAS;
   static constexpr int OFF_PT = OFF_DO + NST * TILE;
   static constexpr int OFF_DST = OFF_PT + (PT_TMEM ? 0 : 2 * ATOM);
   static constexpr int OFF_LSE = OFF_DST + 2 * ATOM;  // [NST][128] f32
   static constexpr int OFF_D = OFF_LSE + NST * 512;   // [NST][128] f32
   static constexpr int OFF_BAR = OFF_D + NST * 512;
   static constexpr int BYTES = OFF_BAR + 256;         // base is __align__(1024)
+  static_assert(BYTES <= 232448, "dK/dV shared memory exceeds the 227 KB opt-in limit");
 };
 
 template <int HD>
@@ -244,8 +255,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // upstream grid complete before any dependent global access
   constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DV = 256, TM_DK = 256 + HD;
-  constexpr bool PT_TMEM = L::PT_TMEM;
-  constexpr uint32_t TM_PT = 384, TM_DST = 448;  // hd=64 only: P^T, dS^T (bf16 pairs along queries)
+  constexpr bool PT_TMEM = L::PT_TMEM, ALIAS = L::ALIAS;
+  // P^T, dS^T (bf16 pairs along queries): hd=64 in spare columns, hd=128 over S^T / dP^T
+  constexpr uint32_t TM_PT = ALIAS ? TM_S : 384, TM_DST = ALIAS ? TM_DP : 448;
 
   if (warp == 0 && lane == 0) {
     // ---------------- producer ----------------
@@ -325,7 +337,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) FAB_PROBE(1, gi);
         tc_fence_after();
         issued = false;
-        if (NST > 1 && it + 1 < n_it) {
+        if (ALIAS) {
+          // S/dP of the next step overwrite P^T / dS^T: issued after this step's dV/dK (below)
+        } else if (NST > 1 && it + 1 < n_it) {
           issue_sdp(gi + 1, kv);
           issued = true;
         } else if (NST > 1 && KVS > 1 && has_next) {
@@ -361,6 +375,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (it + 1 == n_it) mma_commit(&kv_empty[kv]);
         }
         __syncwarp();
+        if (ALIAS && it + 1 < n_it) {  // in issue order after the dV/dK MMAs that read P^T / dS^T
+          issue_sdp(gi + 1, kv);
+          issued = true;
+        }
       }
     }
   } else if (warp == 3 && lane == 0) {
@@ -458,7 +476,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (warp == 4 && lane == 0) FAB_PROBE(5, gi);
         if constexpr (PT_TMEM) {
-          // P^T / dS^T of this thread's key row and 64 query columns -> TMEM (A of the TS MMAs)
+          // P^T / dS^T of this thread's key row and 64 query columns -> TMEM (A of the TS MMAs).
+          // ALIAS: the two warps of a lane quadrant both finished reading S^T / dP^T first (half 1
+          // writes columns half 0 reads)
+          if constexpr (ALIAS) named_bar_sync(1 + quad, 64);
           tmem_st_32x32b_x32(lane_base + TM_PT + (cb >> 1), pk);
           tmem_st_32x32b_x32(lane_base + TM_DST + (cb >> 1), dk);
 #pragma unroll
@@ -506,6 +527,29 @@ __global__ void __launch_bounds__(THREADS, 1)
         continue;
       }
       const int key = jb * BLK + r;
+      if constexpr (ALIAS) {
+        // one 4 KB box per warp (its quarter of the dS^T tile): the two 64-column halves in turn
+        uint8_t* box = smem + L::OFF_DST + half * ATOM + quad * 4096;
+        const int col = (half == 0 ? p.H + p.Hkv + kvh : p.H + kvh) * HD, row = b * p.T + jb * BLK + quad * 32;
+#pragma unroll 1
+        for (int a = 0; a < 2; ++a) {
+          if (a == 1) {
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+          }
+          if (half == 0) stage_grad_row<HD>(lane_base + TM_DV, box, box, lane, 1.f, nullptr, p.T, key, a);
+          else stage_grad_row<HD>(lane_base + TM_DK, box, box, lane, p.scale, p.rope_cs, p.T, key, a);
+          tc_fence_before();
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            if (a == 1) mbar_arrive(acc_free);
+            tma_store_2d(&tmOut, box, col + 64 * a, row);
+            bulk_commit();
+          }
+        }
+        continue;
+      }
       uint8_t* box0 = smem + (L::PT_TMEM ? L::OFF_DST : L::OFF_PT) + half * ATOM + quad * 4096;
       uint8_t* box1 = smem + L::OFF_DST + half * ATOM + quad * 4096;
       if (half == 0) stage_grad_row<HD>(lane_base + TM_DV, box0, box1, lane, 1.f, nullptr, p.T, key);
