@@ -29,6 +29,9 @@ namespace fab {
 #ifndef SPX_FAB_KVS64
 #define SPX_FAB_KVS64 2
 #endif
+#ifndef SPX_FAB_HS
+#define SPX_FAB_HS 1
+#endif
 #ifndef SPX_FAB_PT128
 #define SPX_FAB_PT128 1
 #endif
@@ -69,6 +72,14 @@ SPX_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
       "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
       "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
       "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+SPX_DEVICE void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
 SPX_DEVICE void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -208,7 +219,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tmem_free = bars + 15;  // S / dP of the current step copied to registers
   uint64_t* acc_free = bars + 16;   // dV / dK of the previous item read out of TMEM
   uint64_t* ds_read = bars + 17;    // the dS^T tile of the step has been read by its TMA store
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* sdp_full_b = bars + 18;  // HS: S/dP of the second query half (sdp_full = first half)
+  uint64_t* p_ready_b = bars + 19;   // HS: P^T/dS^T of the second half written (p_ready = first)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = p.T / BLK;
@@ -243,6 +256,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(tmem_free, EW_WARPS);
     mbar_init(acc_free, EW_WARPS);
     mbar_init(ds_read, 1);
+    mbar_init(sdp_full_b, 1);
+    mbar_init(p_ready_b, EW_WARPS);
     tma_prefetch_desc(&tmDS);
     tma_prefetch_desc(&tmOut);
     fence_barrier_init();
@@ -256,6 +271,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   pdl_wait();  // upstream grid complete before any dependent global access
   constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DV = 256, TM_DK = 256 + HD;
   constexpr bool PT_TMEM = L::PT_TMEM, ALIAS = L::ALIAS;
+  // HS (hd=128): each step runs as two 64-query halves, software-pipelined -- the softmax of one
+  // half overlaps the MMAs of the other (dV/dK of the previous half, S/dP of the next)
+  constexpr bool HS = ALIAS && SPX_FAB_HS;
   // P^T, dS^T (bf16 pairs along queries): hd=64 in spare columns, hd=128 over S^T / dP^T
   constexpr uint32_t TM_PT = ALIAS ? TM_S : 384, TM_DST = ALIAS ? TM_DP : 448;
 
@@ -315,6 +333,73 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       __syncwarp();
     };
+    if constexpr (HS) {
+      constexpr uint32_t ID_SH = umma_idesc_bf16(BLK, 64, false, false);  // half the queries
+      // S^T / dP^T of query half hf of step gi -> TMEM columns [64 hf, 64 hf + 64) of S / dP
+      auto issue_sdp_half = [&](int gi, int kv, int hf) {
+        const uint32_t sK = smem_u32(smem + L::OFF_K + kv * L::TILE), sV = smem_u32(smem + L::OFF_V + kv * L::TILE);
+        const int s = gi % NST;
+        mbar_wait(&full[s], (gi / NST) & 1);
+        tc_fence_after();
+        const uint32_t sQ = smem_u32(smem + L::OFF_Q + s * L::TILE) + hf * 64 * 128;
+        const uint32_t sDO = smem_u32(smem + L::OFF_DO + s * L::TILE) + hf * 64 * 128;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t ko = (kk >> 2) * ATOM + (kk & 3) * 32;
+            mma_bf16_ss(tmem + TM_S + 64 * hf, umma_desc_sw128(sK + ko, 16, 1024), umma_desc_sw128(sQ + ko, 16, 1024),
+                        ID_SH, kk > 0);
+            mma_bf16_ss(tmem + TM_DP + 64 * hf, umma_desc_sw128(sV + ko, 16, 1024),
+                        umma_desc_sw128(sDO + ko, 16, 1024), ID_SH, kk > 0);
+          }
+          mma_commit(hf ? sdp_full_b : sdp_full);
+        }
+        __syncwarp();
+      };
+      int gi = 0, n = 0;
+      for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
+        if (w >= n_items) continue;
+        int b, kvh, jb, gs;
+        item(w, b, kvh, jb, gs);
+        const int n_it = hpi * (nqb - jb);
+        const int kv = n % KVS;
+        mbar_wait(&kv_full[kv], (n / KVS) & 1);
+        for (int it = 0; it < n_it; ++it, ++gi) {
+          const int s = gi % NST;
+          if (it == 0) {
+            issue_sdp_half(gi, kv, 0);
+            issue_sdp_half(gi, kv, 1);
+          }
+          const uint32_t sQ = smem_u32(smem + L::OFF_Q + s * L::TILE), sDO = smem_u32(smem + L::OFF_DO + s * L::TILE);
+#pragma unroll 1
+          for (int hf = 0; hf < 2; ++hf) {
+            mbar_wait(hf ? p_ready_b : p_ready, gi & 1);
+            if (it == 0 && hf == 0) mbar_wait(acc_free, (n & 1) ^ 1);  // previous item's dV/dK read out
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+              for (int kq = 0; kq < 4; ++kq) {  // the half's 64 queries, 16 per MMA
+                const int kk = 4 * hf + kq;
+                const uint32_t bo = kk * 2048;
+                const uint32_t acc = (it > 0) || (kk > 0);
+                mma_bf16_ts(tmem + TM_DV, tmem + TM_S + 64 * hf + kq * 8, umma_desc_sw128(sDO + bo, ATOM, 1024), ID_G,
+                            acc);
+                mma_bf16_ts(tmem + TM_DK, tmem + TM_DP + 64 * hf + kq * 8, umma_desc_sw128(sQ + bo, ATOM, 1024),
+                            ID_G, acc);
+              }
+              if (hf == 1) {
+                mma_commit(mma2_done);
+                mma_commit(&empty[s]);
+                if (it + 1 == n_it) mma_commit(&kv_empty[kv]);
+              }
+            }
+            __syncwarp();
+            // the same half of the next step, in issue order after the MMAs that read its P^T / dS^T
+            if (it + 1 < n_it) issue_sdp_half(gi + 1, kv, hf);
+          }
+        }
+      }
+    } else {
     int gi = 0, n = 0;
     bool issued = false;  // S/dP of step gi already issued (look-ahead from the previous step)
     for (int k = 0, w = snake(0, blockIdx.x, gridDim.x); k * (int)gridDim.x < n_items; ++k, w = snake(k, blockIdx.x, gridDim.x), ++n) {
@@ -381,6 +466,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
+    }  // !HS
   } else if (warp == 3 && lane == 0) {
     // ---------------- dS^T tile -> workspace (b, h, qb, jb) for the dQ GEMM ----------------
     int gi = 0;
@@ -392,7 +478,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int nq = nqb - jb, n_it = hpi * nq;
       for (int it = 0; it < n_it; ++it, ++gi) {
         const int h = kvh * group + gs * hpi + it / nq, qb = jb + it % nq;
-        mbar_wait(p_ready, gi & 1);
+        mbar_wait(HS ? p_ready_b : p_ready, gi & 1);
         const int row = ((b * p.H + h) * ntri + qb * (qb + 1) / 2 + jb) * BLK;
         for (int a = 0; a < 2; ++a) tma_store_2d(&tmDS, smem + L::OFF_DST + a * ATOM, 64 * a, row);
         bulk_commit();
@@ -418,6 +504,64 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int it = 0; it < n_it; ++it, ++gi) {
         const int s = gi % NST;
         const bool diag = (it % nq) == 0;  // query block == key block
+        if constexpr (HS) {
+          // two 64-query halves; this warp takes 32 query columns of each (half selects which)
+          mbar_wait(&full[s], (gi / NST) & 1);  // lse / D of this step are in smem
+          const float* lse = reinterpret_cast<const float*>(smem + L::OFF_LSE + s * 512);
+          const float* dd = reinterpret_cast<const float*>(smem + L::OFF_D + s * 512);
+#pragma unroll 1
+          for (int hf = 0; hf < 2; ++hf) {
+            mbar_wait(hf ? sdp_full_b : sdp_full, gi & 1);
+            tc_fence_after();
+            const int c0 = 64 * hf + 32 * half;
+            uint32_t sv[32], dv[32];
+            tmem_ld_32x32b_x32(lane_base + TM_S + c0, sv);
+            tmem_ld_32x32b_x32(lane_base + TM_DP + c0, dv);
+            tmem_ld_wait();
+            uint32_t pk[16], dk[16];
+            auto body = [&](auto diag_c) {
+              constexpr bool DIAG = decltype(diag_c)::value;
+#pragma unroll
+              for (int c8 = 0; c8 < 4; ++c8) {
+                float pv[8], ds[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const int c = c0 + 8 * c8 + j;
+                  float pp = ex2(fmaf(__uint_as_float(sv[8 * c8 + j]), sl2, -lse[c]));
+                  if (DIAG && c < r) pp = 0.f;  // query before key
+                  pv[j] = pp;
+                  ds[j] = pp * (__uint_as_float(dv[8 * c8 + j]) - dd[c]);
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  pk[4 * c8 + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
+                  dk[4 * c8 + e] = pack_bf16(ds[2 * e], ds[2 * e + 1]);
+                }
+              }
+            };
+            if (diag) body(std::true_type{});
+            else body(std::false_type{});
+            if (hf == 0 && gi > 0) {
+              mbar_wait(ds_read, (gi - 1) & 1);  // the previous dS^T tile store has read smem
+              if (it == 0) {                     // this warp's dV/dK store has read its staging box
+                if (lane == 0) bulk_wait_read<0>();
+                __syncwarp();
+              }
+            }
+            // P^T / dS^T over the half's S^T / dP^T columns: both warps of the quadrant have read them
+            named_bar_sync(1 + quad, 64);
+            tmem_st_32x32b_x16(lane_base + TM_S + 64 * hf + 16 * half, pk);
+            tmem_st_32x32b_x16(lane_base + TM_DP + 64 * hf + 16 * half, dk);
+#pragma unroll
+            for (int c8 = 0; c8 < 4; ++c8) put_row8p(sDST, r, (c0 >> 3) + c8, dk + 4 * c8);
+            tmem_st_wait();
+            tc_fence_before();
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(hf ? p_ready_b : p_ready);
+          }
+          continue;
+        }
         mbar_wait(&full[s], (gi / NST) & 1);  // lse / D of this step are in smem
         mbar_wait(sdp_full, gi & 1);
         if (warp == 4 && lane == 0) FAB_PROBE(3, gi);
