@@ -14,6 +14,7 @@
 // applied to dq/dk when a table is given, scale folded in.  D = rowsum(dO*O) comes from
 // attn_bwd_delta_kernel (attention.cu).
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "spx_common.cuh"
