@@ -40,6 +40,10 @@ class SimConfig:
     record_trace: bool = False
     loss_ms: float = 0.0
     bwd_msg_bytes: float | None = None   # backward messages default to msg_bytes
+    # B200 extension (not in SPEC): node -> device.  Logical nodes placed on one GPU share its
+    # compute: a device runs one op at a time, picking B / L before F and then the earliest ready
+    # op over all its nodes.  None = one device per node (the spec's model).
+    device_of: tuple | None = None
 
     def __post_init__(self):
         if self.total_microbatches < 1:
@@ -131,7 +135,13 @@ def simulate(schedule: Schedule, topology: Topology, sim_config: SimConfig) -> S
     cm_b = comm_matrix(topology, sim_config.bwd_msg_bytes or sim_config.msg_bytes)
     loss_ms = float(sim_config.loss_ms)
 
-    running = [False] * n
+    dev = list(sim_config.device_of) if sim_config.device_of is not None else list(range(n))
+    if len(dev) != n:
+        raise ValidationError(f"device_of has {len(dev)} entries for {n} nodes")
+    dev_nodes: dict[int, list[int]] = {}
+    for v in range(n):
+        dev_nodes.setdefault(dev[v], []).append(v)
+    running = {d: False for d in dev_nodes}  # per device
     active = [0] * n
     free_slots = [list(range(m)) for _ in range(n)]
     slot_of: dict[tuple[int, int], int] = {}     # (mb, node) -> slot
@@ -172,7 +182,7 @@ def simulate(schedule: Schedule, topology: Topology, sim_config: SimConfig) -> S
             slot = slot_of[(mb, v)]
             dur = topology.compute_bwd_ms(v) if kind == B else loss_ms
         stats["wait"] += t - ready
-        running[v] = True
+        running[dev[v]] = True
         busy[v] += dur
         record(kind, v, agent, wave, pos, ready, t, t + dur, slot)
         push(t + dur, 0, ("done", v, kind, agent, wave, pos))
@@ -216,7 +226,7 @@ def simulate(schedule: Schedule, topology: Topology, sim_config: SimConfig) -> S
             while events and events[0][0] == t:
                 _, _, _, (what, v, kind, agent, wave, pos) = heapq.heappop(events)
                 if what == "done":
-                    running[v] = False
+                    running[dev[v]] = False
                     complete(t, v, kind, agent, wave, pos)
                 elif kind == L and loss_ms == 0.0:
                     # the spec's cost model has no loss compute: the return passes straight through
@@ -232,15 +242,19 @@ def simulate(schedule: Schedule, topology: Topology, sim_config: SimConfig) -> S
             stats["overrides"] += 1
             start(v, t, queue_f[v].pop(0))
             continue
-        for v in range(n):
-            if running[v]:
+        for d in sorted(dev_nodes):
+            if running[d]:
                 continue
-            if queue_b[v]:
-                queue_b[v].sort()
-                start(v, t, queue_b[v].pop(0))
-            elif queue_f[v] and active[v] < m:
-                queue_f[v].sort()
-                start(v, t, queue_f[v].pop(0))
+            nodes_d = dev_nodes[d]
+            cand = [(min(queue_b[v]), v) for v in nodes_d if queue_b[v]]
+            qs = queue_b
+            if not cand:
+                cand = [(min(queue_f[v]), v) for v in nodes_d if queue_f[v] and active[v] < m]
+                qs = queue_f
+            if cand:
+                entry, v = min(cand)
+                qs[v].remove(entry)
+                start(v, t, entry)
 
     makespan = max((op.end for op in ops), default=0.0)
     return SimReport(
@@ -253,6 +267,41 @@ def simulate(schedule: Schedule, topology: Topology, sim_config: SimConfig) -> S
         cap_overrides=stats["overrides"],
         trace=trace,
     )
+
+
+def replay_makespan(ops, schedule: Schedule, topology: Topology, sim_config: SimConfig, device_of) -> float:
+    """Makespan of executing ``ops`` in exactly this order on devices (node -> device_of[node]):
+    each device runs its ops one at a time in list order, an op starts when its device is free and
+    its input has arrived (the previous op of its path plus the hop).  This is how the executor
+    replays an op list on one stream per GPU, so it scores candidate orders."""
+    cm_f = comm_matrix(topology, sim_config.msg_bytes)
+    cm_b = comm_matrix(topology, sim_config.bwd_msg_bytes or sim_config.msg_bytes)
+    paths = {a: schedule.paths[a].nodes for a in schedule.paths}
+    end: dict = {}
+    free: dict = {}
+    for op in ops:
+        a, w, pos, v = op.agent, op.wave, op.pos, op.node
+        nodes = paths[a]
+        last = len(nodes) - 1
+        if op.kind == F:
+            if pos > 0:
+                r = end[(F, a, w, pos - 1)] + cm_f[nodes[pos - 1], v]
+            else:
+                r = end[(B, a, w - 1, 0)] if w > 0 else 0.0
+            dur = float(topology.compute_fwd_ms[v])
+        elif op.kind == L:
+            r = end[(F, a, w, last)] + (cm_f[nodes[last], v] if nodes[last] != v else 0.0)
+            dur = float(sim_config.loss_ms)
+        else:
+            if pos == last:
+                r = end[(L, a, w, 0)] + (cm_b[nodes[0], v] if nodes[0] != v else 0.0)
+            else:
+                r = end[(B, a, w, pos + 1)] + cm_b[nodes[pos + 1], v]
+            dur = topology.compute_bwd_ms(v)
+        d = device_of[v]
+        t0 = max(free.get(d, 0.0), r)
+        end[(op.kind, a, w, pos)] = free[d] = t0 + dur
+    return max(end.values(), default=0.0)
 
 
 def compare(schedules: dict, topology: Topology, sim_config: SimConfig) -> list[dict]:

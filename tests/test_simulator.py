@@ -163,3 +163,34 @@ def test_compare_identity():
     rc = get_config("C1")
     rows = compare({"a": rc.schedule(), "b": rc.schedule()}, rc.topology(), rc.sim_config())
     assert rows[1]["speedup_vs_first"] == 1.0
+
+
+def test_colocated_devices_and_replay():
+    """B200 extension: SimConfig.device_of shares one device among logical nodes.  Identity devices
+    reproduce the spec's simulation; replay_makespan of the simulator's own order on identity
+    devices is its makespan; a colocated simulation stays causal (every op's path predecessor
+    starts earlier) and, for C3 at 4 GPUs, replays faster than the one-device-per-node order."""
+    from dataclasses import replace
+
+    from paper_2502_19913_b200.configs import get_config
+    from paper_2502_19913_b200.executor import balanced_placement
+    from paper_2502_19913_b200.simulator import replay_makespan
+
+    rc = get_config("C3")
+    T, sch, sc = rc.topology(), rc.schedule(), rc.sim_config()
+    rep = simulate(sch, T, sc)
+    same = simulate(sch, T, replace(sc, device_of=tuple(range(T.n))))
+    assert [(o.kind, o.node, o.agent, o.wave, o.start) for o in same.ops] == \
+           [(o.kind, o.node, o.agent, o.wave, o.start) for o in rep.ops]
+    assert replay_makespan(rep.ops, sch, T, sc, list(range(T.n))) == pytest.approx(rep.iteration_makespan)
+    pl = balanced_placement(rep, T.n, 4)
+    co = simulate(sch, T, replace(sc, device_of=tuple(pl)))
+    start = {(o.kind, o.agent, o.wave, o.pos): o.start for o in co.ops}
+    for o in co.ops:
+        if o.kind == "F" and o.pos > 0:
+            assert start[("F", o.agent, o.wave, o.pos - 1)] < o.start
+        if o.kind == "B" and ("B", o.agent, o.wave, o.pos + 1) in start:
+            assert start[("B", o.agent, o.wave, o.pos + 1)] < o.start
+    busy = [sum(o.end - o.start for o in co.ops if pl[o.node] == r) for r in range(4)]
+    assert co.iteration_makespan >= max(busy) - 1e-9          # a device runs one op at a time
+    assert replay_makespan(co.ops, sch, T, sc, pl) < replay_makespan(rep.ops, sch, T, sc, pl)
