@@ -47,7 +47,9 @@ def attn_ref(q, k, v, scale):  # [B, H, T, hd] fp32, causal, GQA by repeat
 
 
 @pytest.mark.parametrize("B,T,H,Hkv,hd", [(2, 256, 6, 6, 48), (2, 1024, 16, 16, 64), (1, 512, 8, 2, 128),
-                                          (1, 256, 4, 4, 128), (1, 4096, 8, 2, 128), (1, 2048, 4, 4, 64)])
+                                          (1, 256, 4, 4, 128), (1, 4096, 8, 2, 128), (1, 2048, 4, 4, 64),
+                                          (1, 128, 2, 2, 128), (3, 384, 4, 2, 128), (3, 384, 6, 3, 64),
+                                          (1, 128, 2, 1, 64)])
 def test_attention_fwd_bwd(B, T, H, Hkv, hd):
     g = torch.Generator().manual_seed(B * T + H + hd)
     W = (H + 2 * Hkv) * hd
