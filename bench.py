@@ -153,7 +153,7 @@ def run_reference(args, rc):
     c1 = c1_iteration()
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": rc.M * rc.tokens_per_mb / cb["value"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": rc.M * rc.tokens_per_mb / cb["value"] * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": rc.name, "model": rc.model.name, "global_batch": rc.M * rc.b, "seq_len": rc.T,
                        "parallelism": "cpu"},
