@@ -365,6 +365,36 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int m0 = (nmaj ? tile / num_n : tile % pi.num_m) * PAIR_M + (int)rank * GEMM_BM;
       const int n0 = (nmaj ? tile % num_n : tile / pi.num_m) * BN;
       const int rbase = m0 + wq * 32;
+      // residual / attention-delta epilogues: this warp's R rows (32 x BN/2; O for the delta) are
+      // loaded before the accumulator is ready, so their latency hides under the tile's MMAs
+      // instead of lengthening the exposed epilogue
+      constexpr int RCH = (EPI == EPI_BF16_RESID || EPI == EPI_ATTN_DELTA) ? BN / 128 : 0;  // 64-col chunks per warp
+      uint4 rpre[RCH > 0 ? RCH : 1][8];
+      if constexpr (RCH > 0) {
+        const __nv_bfloat16* R = reinterpret_cast<const __nv_bfloat16*>(args.R);
+#pragma unroll
+        for (int ch = 0; ch < RCH; ++ch)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = (lane >> 3) + 4 * i, j = lane & 7;
+            const int grow = rbase + r, gcol = n0 + cb + 64 * ch + 8 * j;
+            rpre[ch][i] = make_uint4(0, 0, 0, 0);
+            if (grow < args.M && gcol < args.N)
+              rpre[ch][i] = *reinterpret_cast<const uint4*>(R + (size_t)grow * args.ldr + gcol);
+          }
+      }
+      // RoPE (head dim 64): the row's 32 (cos, sin) pairs serve every head of the tile; loaded
+      // once, before the accumulator is ready
+      constexpr int RPP = RopeHd<EPI>::value == 64 ? 32 : 1;
+      float2 wpre[RPP];
+      if constexpr (RopeHd<EPI>::value == 64) {
+        const int row = rbase + lane;
+        const float2* cs = reinterpret_cast<const float2*>(args.rope_cs) + (row < args.M ? row : 0) % args.rope_T;
+        if (n0 + cb < args.rope_cols) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) wpre[j] = cs[(size_t)j * args.rope_T];
+        }
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN;
@@ -529,7 +559,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               if (rot) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                  const float2 w = cs[(size_t)(pair0 + j) * T];
+                  const float2 w = HD == 64 ? wpre[j % RPP] : cs[(size_t)(pair0 + j) * T];
                   const float a = x1[j], b = x2[j];
                   x1[j] = second ? (b * w.x + a * w.y) : (a * w.x - b * w.y);
                 }
@@ -550,18 +580,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll 1
         for (int c = cb; c < cb + BN / 2 && n0 + c < args.N; c += 64) {
           box_acquire();
-          if constexpr (EPI == EPI_BF16_RESID || EPI == EPI_ATTN_DELTA) {
-            const __nv_bfloat16* R = reinterpret_cast<const __nv_bfloat16*>(args.R);
-            uint4 rv[8];
+          if constexpr (RCH > 0) {  // the prefetched R / O chunk into the swizzled box
+            const int ch = (c - cb) >> 6;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int r = (lane >> 3) + 4 * i, j = lane & 7;
-              const int grow = rbase + r, gcol = n0 + c + 8 * j;
-              rv[i] = make_uint4(0, 0, 0, 0);
-              if (grow < args.M && gcol < args.N) rv[i] = *reinterpret_cast<const uint4*>(R + (size_t)grow * args.ldr + gcol);
-            }
+            for (int cc = 0; cc < RCH; ++cc)
+              if (cc == ch)
 #pragma unroll
-            for (int i = 0; i < 8; ++i) box_put((lane >> 3) + 4 * i, lane & 7, rv[i]);
+                for (int i = 0; i < 8; ++i) box_put((lane >> 3) + 4 * i, lane & 7, rpre[cc][i]);
             __syncwarp();
           }
 #pragma unroll 1
