@@ -136,6 +136,9 @@ SPX_DEVICE void stage_grad_row(uint32_t taddr, uint8_t* box0, uint8_t* box1, int
     const float2* c2 = reinterpret_cast<const float2*>(cs);
 #pragma unroll 1
     for (int j0 = 0; j0 < HD / 2; j0 += 32) {
+      float2 w[32];  // requested before the TMEM loads, whose wait would serialise them
+#pragma unroll
+      for (int j = 0; j < 32; ++j) w[j] = c2[(size_t)(j0 + j) * T + pos];
       uint32_t a[32], b[32];
       tmem_ld_32x32b_x32(taddr + j0, a);
       tmem_ld_32x32b_x32(taddr + HD / 2 + j0, b);
@@ -143,10 +146,9 @@ SPX_DEVICE void stage_grad_row(uint32_t taddr, uint8_t* box0, uint8_t* box1, int
       float o1[32], o2[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const float2 w = c2[(size_t)(j0 + j) * T + pos];
         const float x1 = __uint_as_float(a[j]) * scale, x2 = __uint_as_float(b[j]) * scale;
-        o1[j] = x1 * w.x + x2 * w.y;
-        o2[j] = x2 * w.x - x1 * w.y;
+        o1[j] = x1 * w[j].x + x2 * w[j].y;
+        o2[j] = x2 * w[j].x - x1 * w[j].y;
       }
 #pragma unroll
       for (int j = 0; j < 32; j += 8) {

@@ -553,13 +553,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               // HD=128: bx selects x1'/x2', q selects pairs 32q..32q+31
               const int pair0 = (HD == 64) ? 0 : 32 * q;
               const bool second = (HD == 64) ? (q == 1) : (bx == 1);
+              // HD=128: this slice's (cos, sin) pairs are requested before the TMEM loads (whose
+              // wait would otherwise serialise them)
+              float2 wq[HD == 64 ? 1 : 32];
+              if constexpr (HD != 64) {
+                if (rot) {
+#pragma unroll
+                  for (int j = 0; j < 32; ++j) wq[j] = cs[(size_t)(pair0 + j) * T];
+                }
+              }
               float x1[32], x2[32];
               ld32(t_row + hb + pair0, x1);
               ld32(t_row + hb + HD / 2 + pair0, x2);
               if (rot) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                  const float2 w = HD == 64 ? wpre[j % RPP] : cs[(size_t)(pair0 + j) * T];
+                  const float2 w = HD == 64 ? wpre[j % RPP] : wq[j % (HD == 64 ? 1 : 32)];
                   const float a = x1[j], b = x2[j];
                   x1[j] = second ? (b * w.x + a * w.y) : (a * w.x - b * w.y);
                 }
