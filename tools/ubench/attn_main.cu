@@ -1,6 +1,6 @@
 // Attention kernel harness (benchmarking only): one translation unit with the libspx attention
 // sources, so variants can be built with -D flags and probed without rebuilding libspx.so.
-//   attn_main B T H Hkv hd iters
+//   attn_main B T H Hkv hd iters [dump]   (ATTN_ROPE=1: backward through the inverse-RoPE epilogues)
 #include "../../paper_2502_19913_b200/csrc/runtime.cu"
 #include "../../paper_2502_19913_b200/csrc/attention.cu"
 #include "../../paper_2502_19913_b200/csrc/attention_sm100.cu"
@@ -36,11 +36,13 @@ int main(int argc, char** argv) {
   cudaMemcpy(qkv, h.data(), n * W * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(dout, h.data(), n * H * hd * 2, cudaMemcpyHostToDevice);
   const float sc = 1.f / sqrtf((float)hd);
+  const bool use_rope = getenv("ATTN_ROPE") != nullptr;  // backward with the inverse-RoPE epilogues
   cudaStream_t s;
   cudaStreamCreate(&s);
   auto fwd = [&] { return spx_attn_fwd(qkv, o, lse, B, T, H, Hkv, hd, W, H * hd, sc, s); };
   auto bwd = [&] {
-    return spx_attn_bwd_ex(qkv, o, dout, lse, ws, dqkv, B, T, H, Hkv, hd, W, H * hd, sc, nullptr, SPX_ATTN_WS_EX, s);
+    return spx_attn_bwd_ex(qkv, o, dout, lse, ws, dqkv, B, T, H, Hkv, hd, W, H * hd, sc, use_rope ? cs : nullptr,
+                           SPX_ATTN_WS_EX, s);
   };
   double fl = 4.0 * B * H * (double)T * T / 2 * hd;
   for (int k = 0; k < 2; ++k) {
